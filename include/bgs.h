@@ -1,0 +1,192 @@
+/* bgs.h -- C ABI of libbgs: the BalanceGS (arXiv 2510.14564) hot path on B200.
+ *
+ * The path is the 3DGS differentiable tile rasterizer that the paper's system
+ * and mapping techniques accelerate ("Gaussian projection ...
+ * color splatting", §II-A l.128-149), one training iteration per view:
+ *
+ *   theta[59n] + camera -> bgs_preprocess -> bgs_sort -> bgs_render_fwd
+ *        -> (dL/dimage from the caller, e.g. bgs_l1_loss_grad)
+ *        -> bgs_render_bwd (grad += ) -> [caller: NCCL all-reduce] -> bgs_adam_step
+ *
+ * Conventions (DESIGN.md §3 lists every reading R1-R27 cited below):
+ *  - Every pointer is a DEVICE pointer unless marked (host).  Every call that
+ *    takes a stream is asynchronous on it; no call allocates, frees or
+ *    synchronises, except bgs_frame_status / bgs_frame_stats, which read a few
+ *    device words back and must be called after the caller synchronised.
+ *  - Ownership: the caller owns theta, grad, exp_avg, exp_avg_sq, images and
+ *    the workspace; the library keeps no global device state.  A bgs_frame is a
+ *    caller-allocated HOST struct describing one view's workspace.
+ *  - Errors: host-side validation happens before any launch; an invalid call
+ *    returns BGS_ERR_INVALID and launches nothing.  A CUDA launch error returns
+ *    BGS_ERR_CUDA (text via bgs_status_string / bgs_last_error).  Key overflow
+ *    (K > max_keys) is detected on the device: later stages of that frame become
+ *    no-ops and bgs_frame_status reports BGS_ERR_CAPACITY with the required K.
+ *  - Concurrency: frames on different streams may share theta read-only; calls
+ *    that accumulate into the same grad must be stream-ordered.  preprocess,
+ *    sort and render_fwd are deterministic (bit-reproducible); render_bwd is not
+ *    (float atomics; BASELINE.json north_star).
+ */
+#ifndef BGS_H
+#define BGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BGS_OK = 0,
+  BGS_ERR_INVALID = -1,
+  BGS_ERR_CAPACITY = -2,
+  BGS_ERR_CUDA = -3,
+  BGS_ERR_UNSUPPORTED = -4
+} bgs_status;
+
+#define BGS_TILE 16            /* "16 x 16 pixel blocks" (§IV-C1) */
+#define BGS_FLOATS_PER_GAUSSIAN 59
+#define BGS_MAX_KEYS_LIMIT ((int64_t)1 << 30)
+
+/* Views into theta[59n] (caller-owned, each segment 16-byte aligned):
+ *   [means 3n | log_scales 3n | quats 4n (w,x,y,z) | opacity_logits n | sh 48n ([n][16][3], k = 0 is DC)]
+ * Raw optimiser parameters; exp / normalise / sigmoid are fused (R5).  The
+ * primitive is G(x) = exp(-1/2 (x-mu)^T Sigma^-1 (x-mu)) with Sigma = R S S^T R^T
+ * (§II-A).  sh_degree = active SH degree 0..3 (R12). */
+typedef struct {
+  int64_t n;
+  int32_t sh_degree;
+  int32_t _pad;
+  const float *means, *log_scales, *quats, *opacity_logits, *sh;
+} bgs_gaussians;
+
+/* Camera (host struct, copied into kernel parameters).  `view` is W of
+ * Sigma' = J W Sigma W^T J^T, world -> camera, column-major
+ * (t_r = sum_k view[r+4k] mu_k + view[12+r]); `proj` = P . view world -> clip,
+ * column-major (R2).  Pixel (x, y) is sampled at integer coordinates (R1). */
+typedef struct {
+  float view[16];
+  float proj[16];
+  float campos[3];
+  float tan_fovx, tan_fovy;
+  int32_t width, height;  /* 1..16384 each; edge tiles may be partial (R1) */
+  float bg[3];            /* background colour: out = C + T_final * bg (R16) */
+  float near_plane;       /* cull iff t_z <= near_plane; 0.2 by default (R3) */
+} bgs_camera;
+
+/* Adam hyper-parameters (R21, PyTorch semantics). lr per group. */
+typedef struct {
+  float lr_means, lr_log_scales, lr_quats, lr_opacity, lr_sh_dc, lr_sh_rest;
+  float beta1, beta2, eps;
+} bgs_adam_hparams;
+
+/* One view's workspace (host struct; fields are library-private).  Sized by
+ * bgs_workspace_bytes, carved by bgs_frame_init out of ONE caller allocation
+ * (>= 256-byte aligned). */
+typedef struct {
+  uint64_t opaque[64];
+} bgs_frame;
+
+/* Device pointers into a frame's workspace, for the parity tests (host struct). */
+typedef struct {
+  int32_t* radius;          /* [n]  0 = culled ("absent")                       */
+  float* depth;             /* [n]  camera-space t_z; its bits are the key low word  */
+  float* record;            /* [n][12] {x, y, A, B, C, opacity, r, g, b, cbits, 0, 0}
+                               with (A, B, C) = (-conic.x/2, -conic.y, -conic.z/2)   */
+  uint32_t* tiles_touched;  /* [n]                                                   */
+  uint32_t* offsets;        /* [n]  exclusive scan of tiles_touched (R13)            */
+  uint64_t* keys_unsorted;  /* [max_keys] (tile << 32 | depth bits), index order     */
+  uint32_t* values_unsorted;/* [max_keys] Gaussian index                             */
+  uint64_t* keys_sorted;    /* [max_keys] stable ascending                           */
+  uint32_t* values_sorted;  /* [max_keys]                                            */
+  uint32_t* ranges;         /* [tiles][2] [start, end) per tile, (0,0) if empty      */
+  float* grad2d;            /* [n][12] per-view blend grads {dx, dy, dconic x,y,z, do,
+                               dr, dg, db, 0, 0, 0}; consumed and zeroed by render_bwd */
+  int64_t n, max_keys;
+  int32_t tiles_x, tiles_y, sort_bits, sort_passes;
+} bgs_frame_views;
+
+/* Per-frame workload counters (bgs_frame_stats; not on the hot path). */
+typedef struct {
+  int64_t visible;      /* V: Gaussians with radius > 0                       */
+  int64_t num_keys;     /* K                                                  */
+  int64_t evals_fwd;    /* E_f: (pixel, list entry) pairs the forward visits  */
+  int64_t evals_bwd;    /* E_b: sum over pixels of n_contrib                  */
+  int64_t evals_slot;   /* E_slot: sum over warps of 32 * max_lane(visits)    */
+  int64_t max_list;     /* longest tile list                                  */
+} bgs_stats;
+
+/* ---------------------------------------------------------------- sizing */
+/* Workspace bytes for n Gaussians, a w x h view and a key capacity max_keys
+ * (1 <= max_keys < BGS_MAX_KEYS_LIMIT = 2^30: the sort's look-back words hold 30-bit
+ * counts; R25).  n < 2^31, 1 <= w, h <= 16384.  Returns 0 on invalid sizes. */
+size_t bgs_workspace_bytes(int64_t n, int32_t w, int32_t h, int64_t max_keys);
+
+/* Carve `workspace` (device, `bytes` >= bgs_workspace_bytes) into frame `f`.
+ * Does not touch device memory.  BGS_ERR_INVALID on bad sizes or alignment. */
+bgs_status bgs_frame_init(bgs_frame* f /*host*/, void* workspace, size_t bytes, int64_t n, int32_t w, int32_t h,
+                          int64_t max_keys);
+
+/* ---------------------------------------------------------------- the hot path */
+/* a1-a3: activations, view transform, near cull, projection, Sigma' = J W Sigma W^T J^T
+ * + 0.3 I, conic, radius, tile rect, SH -> rgb, tiles_touched, and the exclusive scan
+ * into offsets / K (§II-A; P:59 SH colour; readings R1-R13, R22).
+ * Requires g->n == the frame's n and cam->width/height == the frame's w/h.  n = 0 is
+ * valid.  The camera is remembered in the frame for the later calls. */
+bgs_status bgs_preprocess(const bgs_gaussians* g /*host*/, const bgs_camera* cam /*host*/, bgs_frame* f /*host*/,
+                          void* stream);
+
+/* a4-a6: duplicate (tile | depth) keys (values = Gaussian index), stable 64-bit LSD
+ * radix sort on bits [0, 32 + bit_width(tiles - 1)), tile ranges.  Result order =
+ * (tile, depth bits, index): "N ... sorted by depth", ties by index
+ * (R13). */
+bgs_status bgs_sort(bgs_frame* f /*host*/, void* stream);
+
+/* a7: per pixel, front-to-back over its tile's list: alpha = min(0.99, o G), skip
+ * alpha < 1/255, stop before T (1 - alpha) < 1e-4, C += c alpha T (PAPER.md l.143-149,
+ * §II-A; R14-R16).  Outputs planar image[3][h][w], final_T[h][w] and n_contrib[h][w] =
+ * 1-based list position of the last blended Gaussian (0 if none). */
+bgs_status bgs_render_fwd(bgs_frame* f /*host*/, float* image, float* final_T, uint32_t* n_contrib, void* stream);
+
+/* a9-a10: blend backward (back to front, decisions of the forward frozen, R18) and
+ * the chain rule conic -> Sigma' -> Sigma/(s, q) and J -> t -> mu, xy -> mu,
+ * rgb -> SH / view direction -> mu, opacity -> logit.  grad[59n] += dL/dtheta in
+ * theta's layout (the sum over views, R20).  dL_dimage is planar [3][h][w]. */
+bgs_status bgs_render_bwd(const bgs_gaussians* g /*host*/, bgs_frame* f /*host*/, const float* dL_dimage,
+                          const float* final_T, const uint32_t* n_contrib, float* grad, void* stream);
+
+/* a11: fused Adam over theta[59n] (R21, PyTorch semantics: bias-corrected, eps after
+ * sqrt), per-group learning rate, grad zeroed on exit.  step is 1-based. */
+bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
+                         const bgs_adam_hparams* hp /*host*/, int64_t step, void* stream);
+
+/* a8 (caller-side helper): L1 loss gradient against an 8-bit target [3][h][w]
+ * (R19): dL_dimage = scale * sign(image - target/255); loss_sum += sum |image - target/255|
+ * (loss_sum: one device float, accumulated).  scale = 1/(3 h w B) for a batch mean (R20). */
+bgs_status bgs_l1_loss_grad(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale,
+                            float* dL_dimage, float* loss_sum, void* stream);
+
+/* ---------------------------------------------------------------- status / debug */
+/* After the caller synchronised the frame's stream: K (host out) and BGS_OK, or
+ * BGS_ERR_CAPACITY when K > max_keys (re-run with a larger workspace). */
+bgs_status bgs_frame_status(const bgs_frame* f /*host*/, int64_t* num_keys /*host*/);
+bgs_status bgs_frame_debug(const bgs_frame* f /*host*/, bgs_frame_views* out /*host*/);
+/* Workload counters of the last fwd (runs a counting kernel and synchronises). */
+bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contrib, bgs_stats* out /*host*/,
+                           void* stream);
+
+/* Test-only knob: flags & BGS_DEBUG_SKIP_SORT makes bgs_sort stop after the key
+ * duplication (a4), so the unsorted keys/values stay readable via bgs_frame_debug. */
+#define BGS_DEBUG_SKIP_SORT 1
+bgs_status bgs_frame_set_debug(bgs_frame* f /*host*/, int32_t flags);
+
+const char* bgs_status_string(bgs_status s);
+const char* bgs_last_error(void);
+/* Number of kernels this library launched since load (host counter; bench evidence). */
+uint64_t bgs_launch_count(void);
+int32_t bgs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BGS_H */

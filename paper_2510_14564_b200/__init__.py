@@ -1,0 +1,259 @@
+"""Thin Python binding of libbgs (include/bgs.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels of libbgs.so (sm_100a); PyTorch only
+provides device memory, streams and (in bench.py) the NCCL process group.  There is no
+CPU or PyTorch fallback: importing this package without the built library raises.
+
+Names follow the C ABI: bgs_preprocess / bgs_sort / bgs_render_fwd / bgs_render_bwd /
+bgs_adam_step (BASELINE.json north_star), plus the l1 helper, status and debug calls.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbgs.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"libbgs.so not built at {LIB_PATH}: run `python __graft_entry__.py` (build()) first")
+_lib = C.CDLL(LIB_PATH)
+
+BGS_OK, BGS_ERR_INVALID, BGS_ERR_CAPACITY, BGS_ERR_CUDA, BGS_ERR_UNSUPPORTED = 0, -1, -2, -3, -4
+BGS_DEBUG_SKIP_SORT = 1
+
+
+class BgsError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        msg = _lib.bgs_status_string(status).decode()
+        super().__init__(f"{what}: {msg} (status {status})")
+        self.status = status
+
+
+class Gaussians(C.Structure):
+    _fields_ = [("n", C.c_int64), ("sh_degree", C.c_int32), ("_pad", C.c_int32), ("means", C.c_void_p),
+                ("log_scales", C.c_void_p), ("quats", C.c_void_p), ("opacity_logits", C.c_void_p),
+                ("sh", C.c_void_p)]
+
+
+class Camera(C.Structure):
+    _fields_ = [("view", C.c_float * 16), ("proj", C.c_float * 16), ("campos", C.c_float * 3),
+                ("tan_fovx", C.c_float), ("tan_fovy", C.c_float), ("width", C.c_int32), ("height", C.c_int32),
+                ("bg", C.c_float * 3), ("near_plane", C.c_float)]
+
+
+class AdamHParams(C.Structure):
+    _fields_ = [("lr_means", C.c_float), ("lr_log_scales", C.c_float), ("lr_quats", C.c_float),
+                ("lr_opacity", C.c_float), ("lr_sh_dc", C.c_float), ("lr_sh_rest", C.c_float),
+                ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float)]
+
+    def __init__(self, lr_means=1.6e-4, lr_log_scales=5e-3, lr_quats=1e-3, lr_opacity=0.05, lr_sh_dc=2.5e-3,
+                 lr_sh_rest=1.25e-4, beta1=0.9, beta2=0.999, eps=1e-15):
+        # defaults: R21 ([3DGS] learning rates; opacity 0.05, lr_means before the extent scale)
+        super().__init__(lr_means, lr_log_scales, lr_quats, lr_opacity, lr_sh_dc, lr_sh_rest, beta1, beta2, eps)
+
+
+class Frame(C.Structure):
+    _fields_ = [("opaque", C.c_uint64 * 64)]
+
+
+class FrameViews(C.Structure):
+    _fields_ = [("radius", C.c_void_p), ("depth", C.c_void_p), ("record", C.c_void_p),
+                ("tiles_touched", C.c_void_p), ("offsets", C.c_void_p), ("keys_unsorted", C.c_void_p),
+                ("values_unsorted", C.c_void_p), ("keys_sorted", C.c_void_p), ("values_sorted", C.c_void_p),
+                ("ranges", C.c_void_p), ("grad2d", C.c_void_p), ("n", C.c_int64), ("max_keys", C.c_int64),
+                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("sort_bits", C.c_int32), ("sort_passes", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("visible", C.c_int64), ("num_keys", C.c_int64), ("evals_fwd", C.c_int64),
+                ("evals_bwd", C.c_int64), ("evals_slot", C.c_int64), ("max_list", C.c_int64)]
+
+
+_P = C.c_void_p
+_SIGS = {
+    "bgs_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32, C.c_int64]),
+    "bgs_frame_init": (C.c_int, [C.POINTER(Frame), _P, C.c_size_t, C.c_int64, C.c_int32, C.c_int32, C.c_int64]),
+    "bgs_preprocess": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Camera), C.POINTER(Frame), _P]),
+    "bgs_sort": (C.c_int, [C.POINTER(Frame), _P]),
+    "bgs_render_fwd": (C.c_int, [C.POINTER(Frame), _P, _P, _P, _P]),
+    "bgs_render_bwd": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Frame), _P, _P, _P, _P, _P]),
+    "bgs_adam_step": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(AdamHParams), C.c_int64, _P]),
+    "bgs_l1_loss_grad": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_float, _P, _P, _P]),
+    "bgs_frame_status": (C.c_int, [C.POINTER(Frame), C.POINTER(C.c_int64)]),
+    "bgs_frame_debug": (C.c_int, [C.POINTER(Frame), C.POINTER(FrameViews)]),
+    "bgs_frame_stats": (C.c_int, [C.POINTER(Frame), _P, C.POINTER(Stats), _P]),
+    "bgs_frame_set_debug": (C.c_int, [C.POINTER(Frame), C.c_int32]),
+    "bgs_status_string": (C.c_char_p, [C.c_int]),
+    "bgs_last_error": (C.c_char_p, []),
+    "bgs_launch_count": (C.c_uint64, []),
+    "bgs_version": (C.c_int32, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIGS)
+
+
+def _check(st: int, what: str):
+    if st != BGS_OK:
+        raise BgsError(st, what)
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "libbgs takes contiguous CUDA tensors"
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def camera(cam) -> Camera:
+    """Marshal a gen.Camera-like object (view/proj column-major) into bgs_camera."""
+    c = Camera()
+    c.view[:] = [float(x) for x in cam.view]
+    c.proj[:] = [float(x) for x in cam.proj]
+    c.campos[:] = [float(x) for x in cam.campos]
+    c.tan_fovx, c.tan_fovy = float(cam.tan_fovx), float(cam.tan_fovy)
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.bg[:] = [float(x) for x in cam.bg]
+    c.near_plane = float(getattr(cam, "near", 0.2))
+    return c
+
+
+def gaussians(theta: torch.Tensor, n: int, sh_degree: int) -> Gaussians:
+    """Views into theta[59n] (layout: include/bgs.h)."""
+    assert theta.numel() == 59 * n and theta.dtype == torch.float32
+    base = theta.data_ptr()
+    return Gaussians(n, sh_degree, 0, base, base + 4 * 3 * n, base + 4 * 6 * n, base + 4 * 10 * n,
+                     base + 4 * 11 * n)
+
+
+# ------------------------------------------------------------------ the ABI, one call each
+def bgs_workspace_bytes(n, w, h, max_keys) -> int:
+    return int(_lib.bgs_workspace_bytes(n, w, h, max_keys))
+
+
+def bgs_frame_init(frame: Frame, workspace: torch.Tensor, n, w, h, max_keys):
+    _check(_lib.bgs_frame_init(C.byref(frame), _ptr(workspace), workspace.numel(), n, w, h, max_keys),
+           "bgs_frame_init")
+
+
+def bgs_preprocess(g: Gaussians, cam: Camera, frame: Frame, stream=None):
+    _check(_lib.bgs_preprocess(C.byref(g), C.byref(cam), C.byref(frame), _stream(stream)), "bgs_preprocess")
+
+
+def bgs_sort(frame: Frame, stream=None):
+    _check(_lib.bgs_sort(C.byref(frame), _stream(stream)), "bgs_sort")
+
+
+def bgs_render_fwd(frame: Frame, image, final_T, n_contrib, stream=None):
+    _check(_lib.bgs_render_fwd(C.byref(frame), _ptr(image), _ptr(final_T), _ptr(n_contrib), _stream(stream)),
+           "bgs_render_fwd")
+
+
+def bgs_render_bwd(g: Gaussians, frame: Frame, dl_dimage, final_T, n_contrib, grad, stream=None):
+    _check(_lib.bgs_render_bwd(C.byref(g), C.byref(frame), _ptr(dl_dimage), _ptr(final_T), _ptr(n_contrib),
+                               _ptr(grad), _stream(stream)), "bgs_render_bwd")
+
+
+def bgs_adam_step(theta, grad, exp_avg, exp_avg_sq, n, hp: AdamHParams, step: int, stream=None):
+    _check(_lib.bgs_adam_step(_ptr(theta), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), n, C.byref(hp), step,
+                              _stream(stream)), "bgs_adam_step")
+
+
+def bgs_l1_loss_grad(image, target_u8, w, h, scale, dl_dimage, loss_sum, stream=None):
+    _check(_lib.bgs_l1_loss_grad(_ptr(image), _ptr(target_u8), w, h, scale, _ptr(dl_dimage), _ptr(loss_sum),
+                                 _stream(stream)), "bgs_l1_loss_grad")
+
+
+def bgs_frame_status(frame: Frame) -> tuple[int, int]:
+    k = C.c_int64(0)
+    st = _lib.bgs_frame_status(C.byref(frame), C.byref(k))
+    return st, int(k.value)
+
+
+def bgs_frame_debug(frame: Frame) -> FrameViews:
+    v = FrameViews()
+    _check(_lib.bgs_frame_debug(C.byref(frame), C.byref(v)), "bgs_frame_debug")
+    return v
+
+
+def bgs_frame_stats(frame: Frame, n_contrib, stream=None) -> dict:
+    s = Stats()
+    _check(_lib.bgs_frame_stats(C.byref(frame), _ptr(n_contrib), C.byref(s), _stream(stream)), "bgs_frame_stats")
+    return {k: int(getattr(s, k)) for k, _ in Stats._fields_}
+
+
+def bgs_frame_set_debug(frame: Frame, flags: int):
+    _check(_lib.bgs_frame_set_debug(C.byref(frame), flags), "bgs_frame_set_debug")
+
+
+def launch_count() -> int:
+    return int(_lib.bgs_launch_count())
+
+
+def last_error() -> str:
+    return _lib.bgs_last_error().decode()
+
+
+adam_step = bgs_adam_step
+
+
+# ------------------------------------------------------------------ convenience wrapper
+@dataclasses.dataclass
+class Renderer:
+    """One view's workspace (torch-allocated) + frame; forward/backward through the ABI."""
+    n: int
+    width: int
+    height: int
+    max_keys: int = 1 << 24
+    device: torch.device | str = "cuda"
+
+    def __post_init__(self):
+        self.device = torch.device(self.device)
+        self.frame = Frame()
+        self.alloc(self.max_keys)
+        hw = (self.height, self.width)
+        self.image = torch.empty((3, *hw), dtype=torch.float32, device=self.device)
+        self.final_T = torch.empty(hw, dtype=torch.float32, device=self.device)
+        self.n_contrib = torch.empty(hw, dtype=torch.int32, device=self.device)
+
+    def alloc(self, max_keys: int):
+        self.max_keys = int(max_keys)
+        nbytes = bgs_workspace_bytes(self.n, self.width, self.height, self.max_keys)
+        if nbytes == 0:
+            raise BgsError(BGS_ERR_INVALID, "bgs_workspace_bytes")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        bgs_frame_init(self.frame, self.workspace, self.n, self.width, self.height, self.max_keys)
+
+    def forward(self, theta, cam, sh_degree, stream=None, check=True):
+        g = gaussians(theta, self.n, sh_degree)
+        c = camera(cam)
+        bgs_preprocess(g, c, self.frame, stream)
+        bgs_sort(self.frame, stream)
+        bgs_render_fwd(self.frame, self.image, self.final_T, self.n_contrib, stream)
+        if check:
+            torch.cuda.current_stream().synchronize() if stream is None else stream.synchronize()
+            st, k = bgs_frame_status(self.frame)
+            if st == BGS_ERR_CAPACITY:  # grow and redo (R25)
+                self.alloc(max(int(k * 1.25) + 1024, 2 * self.max_keys))
+                return self.forward(theta, cam, sh_degree, stream, check)
+            _check(st, "bgs_frame_status")
+            self.num_keys = k
+        return {"image": self.image, "final_T": self.final_T, "n_contrib": self.n_contrib}
+
+    def backward(self, theta, sh_degree, dl_dimage, out, grad, stream=None):
+        g = gaussians(theta, self.n, sh_degree)
+        bgs_render_bwd(g, self.frame, dl_dimage, out["final_T"], out["n_contrib"], grad, stream)
+
+    def views(self) -> FrameViews:
+        return bgs_frame_debug(self.frame)

@@ -1,0 +1,219 @@
+// adam.cu -- a11 fused Adam (K14), a8 L1 loss gradient (K15), and the workload-count
+// kernel behind bgs_frame_stats (not on the timed path).
+//
+// K14 (R21, PyTorch Adam semantics): m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2;
+// theta -= (lr / bc1) * m / (sqrt(v) / sqrt(bc2) + eps); g = 0.  One pass over the
+// four fp32[59n] buffers with 16-byte vector loads/stores (1888 B per Gaussian, HBM
+// bound: SURVEY §8(d)); the learning-rate group of each element follows from its
+// offset in theta's segment layout (sh_dc = the first 3 of each Gaussian's 48 SH floats).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace bgs {
+
+struct AdamParams {
+  float4* theta;
+  float4* grad;
+  float4* m;
+  float4* v;
+  int64_t n, total4;
+  float lr[6];
+  float b1, b2, eps;
+  float step_size[6];  // lr / bc1
+  float inv_sqrt_bc2;
+};
+
+__device__ __forceinline__ int adam_group(int64_t e, int64_t n) {
+  if (e < 3 * n) return 0;
+  if (e < 6 * n) return 1;
+  if (e < 10 * n) return 2;
+  if (e < 11 * n) return 3;
+  return ((e - 11 * n) % 48) < 3 ? 4 : 5;
+}
+
+__device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v, float ss, const AdamParams& p) {
+  m = fmaf(p.b1, m, (1.0f - p.b1) * g);
+  v = fmaf(p.b2, v, (1.0f - p.b2) * g * g);
+  const float denom = sqrtf(v) * p.inv_sqrt_bc2 + p.eps;
+  th = th - ss * (m / denom);
+  g = 0.0f;
+}
+
+__global__ void __launch_bounds__(256) k_adam(AdamParams p) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.total4; i += stride) {
+    float4 th = p.theta[i], g = p.grad[i], m = p.m[i], v = p.v[i];
+    const int64_t e = 4 * i;
+    const int g0 = adam_group(e, p.n), g3 = adam_group(e + 3, p.n);
+    if (g0 == g3 && g0 < 4) {
+      const float ss = p.step_size[g0];
+      adam_one(th.x, g.x, m.x, v.x, ss, p);
+      adam_one(th.y, g.y, m.y, v.y, ss, p);
+      adam_one(th.z, g.z, m.z, v.z, ss, p);
+      adam_one(th.w, g.w, m.w, v.w, ss, p);
+    } else {
+      adam_one(th.x, g.x, m.x, v.x, p.step_size[adam_group(e, p.n)], p);
+      adam_one(th.y, g.y, m.y, v.y, p.step_size[adam_group(e + 1, p.n)], p);
+      adam_one(th.z, g.z, m.z, v.z, p.step_size[adam_group(e + 2, p.n)], p);
+      adam_one(th.w, g.w, m.w, v.w, p.step_size[adam_group(e + 3, p.n)], p);
+    }
+    p.theta[i] = th;
+    p.grad[i] = g;
+    p.m[i] = m;
+    p.v[i] = v;
+  }
+}
+
+// The scalar tail: the last 59n mod 4 elements.
+__global__ void k_adam_tail(float* theta, float* grad, float* m, float* v, int64_t n, int64_t start, int64_t end,
+                            AdamParams p) {
+  const int64_t e = start + threadIdx.x;
+  if (e >= end) return;
+  adam_one(theta[e], grad[e], m[e], v[e], p.step_size[adam_group(e, n)], p);
+}
+
+bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, const bgs_adam_hparams* hp,
+                       int64_t step, cudaStream_t s) {
+  AdamParams p;
+  p.theta = (float4*)theta;
+  p.grad = (float4*)grad;
+  p.m = (float4*)m;
+  p.v = (float4*)v;
+  p.n = n;
+  p.total4 = 59 * n / 4;  // 59n is a multiple of 4 only if n is; the tail is handled below
+  const float lr[6] = {hp->lr_means, hp->lr_log_scales, hp->lr_quats, hp->lr_opacity, hp->lr_sh_dc, hp->lr_sh_rest};
+  const double bc1 = 1.0 - pow((double)hp->beta1, (double)step);
+  const double bc2 = 1.0 - pow((double)hp->beta2, (double)step);
+  for (int k = 0; k < 6; ++k) {
+    p.lr[k] = lr[k];
+    p.step_size[k] = (float)((double)lr[k] / bc1);
+  }
+  p.b1 = hp->beta1;
+  p.b2 = hp->beta2;
+  p.eps = hp->eps;
+  p.inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+  const int64_t work = p.total4 > 0 ? p.total4 : 1;
+  int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)num_sms() * 8);
+  k_adam<<<blocks, 256, 0, s>>>(p);
+  note_launch();
+  bgs_status st = check_launch("k_adam");
+  if (st != BGS_OK) return st;
+  const int64_t tail = 59 * n - 4 * p.total4;
+  if (tail > 0) {
+    k_adam_tail<<<1, 4, 0, s>>>(theta, grad, m, v, n, 4 * p.total4, 59 * n, p);
+    note_launch();
+    return check_launch("k_adam_tail");
+  }
+  return BGS_OK;
+}
+
+// ---------------------------------------------------------------- K15 L1 loss gradient
+__global__ void __launch_bounds__(256) k_l1(const float* __restrict__ image, const uint8_t* __restrict__ target,
+                                            int64_t count, float scale, float* __restrict__ dl, float* loss_sum) {
+  float acc = 0.0f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    const float d = image[i] - (float)target[i] * (1.0f / 255.0f);
+    dl[i] = d > 0.0f ? scale : (d < 0.0f ? -scale : 0.0f);
+    acc += fabsf(d);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ float s[8];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.0f;
+    for (int w = 0; w < 8; ++w) t += s[w];
+    atomicAdd(loss_sum, t);
+  }
+}
+
+bgs_status launch_l1(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale, float* dl,
+                     float* loss_sum, cudaStream_t s) {
+  const int64_t count = 3ll * w * h;
+  const int blocks = (int)std::min<int64_t>((count + 255) / 256, (int64_t)num_sms() * 4);
+  k_l1<<<blocks, 256, 0, s>>>(image, target, count, scale, dl, loss_sum);
+  note_launch();
+  return check_launch("k_l1");
+}
+
+// ---------------------------------------------------------------- workload counters
+// E_f per pixel is recomputed by re-walking the list with the forward's decisions; not
+// timed (bgs_frame_stats).
+__global__ void __launch_bounds__(kTilePixels) k_stats(const uint2* __restrict__ ranges,
+                                                       const uint32_t* __restrict__ values,
+                                                       const float4* __restrict__ record,
+                                                       const uint32_t* __restrict__ counters, Cam cam,
+                                                       const uint32_t* __restrict__ n_contrib,
+                                                       unsigned long long* out) {
+  const int tile = blockIdx.x;
+  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+  const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+  const bool inside = px < cam.W && py < cam.H;
+  uint2 rg = ranges[tile];
+  if (counters[C_OVERFLOW]) rg = make_uint2(0, 0);
+  uint32_t walked = 0, nc = 0;
+  if (inside) {
+    nc = n_contrib[(int64_t)py * cam.W + px];
+    float T = 1.0f;
+    for (uint32_t j = rg.x; j < rg.y; ++j) {
+      ++walked;
+      const uint32_t id = values[j];
+      const float4 r0 = record[3 * id], r1 = record[3 * id + 1];
+      const float dx = r0.x - (float)px, dy = r0.y - (float)py;
+      const float power = fmaf(r0.z, dx * dx, fmaf(r1.x, dy * dy, r0.w * (dx * dy)));
+      if (power > 0.0f) continue;
+      const float alpha = fminf(0.99f, r1.y * fast_exp(power));
+      if (alpha < (1.0f / 255.0f)) continue;
+      const float tT = T * (1.0f - alpha);
+      if (tT < 1e-4f) break;
+      T = tT;
+    }
+  }
+  const uint32_t wmax = __reduce_max_sync(0xffffffffu, walked);
+  unsigned long long f = walked, b = nc;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    f += __shfl_xor_sync(0xffffffffu, f, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&out[0], f);
+    atomicAdd(&out[1], b);
+    atomicAdd(&out[2], 32ull * wmax);
+  }
+  if (threadIdx.x == 0) atomicMax(&out[3], (unsigned long long)(rg.y - rg.x));
+}
+
+__global__ void k_count_visible(const int32_t* radius, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    c += radius[i] > 0;
+  atomicAdd(&out[4], c);
+}
+
+bgs_status launch_stats(const Frame* F, const uint32_t* n_contrib, bgs_stats* out, cudaStream_t s) {
+  unsigned long long* d = nullptr;
+  if (cudaMallocAsync(&d, 8 * 8, s) != cudaSuccess) return check_launch("stats alloc");
+  cudaMemsetAsync(d, 0, 64, s);
+  k_stats<<<F->num_tiles, kTilePixels, 0, s>>>(F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam,
+                                               n_contrib, d);
+  if (F->n > 0) k_count_visible<<<num_sms() * 4, 256, 0, s>>>(F->radius, F->n, d);
+  unsigned long long h[8];
+  uint32_t c[2];
+  cudaMemcpyAsync(h, d, 64, cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(c, F->counters, 8, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(d, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return check_launch("stats");
+  out->evals_fwd = (int64_t)h[0];
+  out->evals_bwd = (int64_t)h[1];
+  out->evals_slot = (int64_t)h[2];
+  out->max_list = (int64_t)h[3];
+  out->visible = (int64_t)h[4];
+  out->num_keys = (int64_t)(((uint64_t)c[1] << 32) | c[0]);
+  return check_launch("k_stats");
+}
+
+}  // namespace bgs

@@ -1,0 +1,118 @@
+// common.cuh -- internal declarations shared by libbgs's kernels (NOT shared with oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bgs.h"
+
+namespace bgs {
+
+constexpr int kTile = BGS_TILE;       // 16 x 16 pixel tiles
+constexpr int kTilePixels = kTile * kTile;
+
+// counters[] slots (u32 words in the workspace)
+enum : int {
+  C_K_LO = 0, C_K_HI = 1,     // K as u64
+  C_OVERFLOW = 2,             // K > max_keys
+  C_SCAN_TICKET = 3,          // dynamic tile ids for the decoupled-lookback scan
+  C_SORT_TICKET = 4,          // 8 slots: one per radix pass
+  C_VISIBLE = 12,
+  C_NUM = 32
+};
+
+// clamp bits stored in record word 9 (decisions frozen for the backward, R18)
+enum : uint32_t {
+  CB_R = 1u, CB_G = 2u, CB_B = 4u, CB_JX = 8u, CB_JX_NEG = 16u, CB_JY = 32u, CB_JY_NEG = 64u
+};
+
+// Camera as the kernels see it (derived constants computed once on the host with the
+// canonical float expressions of R22: fx = (float)W / (2 tan_fovx), lim = 1.3 tan_fov).
+struct Cam {
+  float V[16], P[16];
+  float campos[3];
+  float fx, fy, limx, limy, near_plane;
+  float bg[3];
+  int32_t W, H, tiles_x, tiles_y;
+};
+
+// Library-private frame layout, stored in bgs_frame::opaque.
+struct Frame {
+  uint64_t magic;
+  int64_t n, max_keys;
+  int32_t W, H, tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
+  int64_t sort_tiles_max;
+  int32_t cam_valid, final_buf, debug_flags, _pad0;
+  Cam cam;
+  int32_t* radius;
+  float* depth;
+  float4* record;          // [n][3]
+  uint32_t* tiles_touched;
+  uint32_t* offsets;
+  uint64_t* keys[2];
+  uint32_t* vals[2];
+  uint2* ranges;
+  unsigned long long* scan_status;  // [scan_tiles]
+  uint32_t* sort_hist;     // [8][256]
+  uint32_t* sort_status;   // [sort_tiles_max][256]
+  uint32_t* counters;      // [C_NUM]
+  float4* grad2d;          // [n][3]
+};
+static_assert(sizeof(Frame) <= sizeof(bgs_frame), "Frame must fit in bgs_frame::opaque");
+constexpr uint64_t kFrameMagic = 0xB6500F7A3E5ull;
+
+inline Frame* frame_of(bgs_frame* f) { return reinterpret_cast<Frame*>(f->opaque); }
+inline const Frame* frame_of(const bgs_frame* f) { return reinterpret_cast<const Frame*>(f->opaque); }
+
+// launch bookkeeping (frame.cu)
+void note_launch(int k = 1);
+bgs_status check_launch(const char* what);
+void set_error(const char* msg);
+
+// stage launchers (one .cu each)
+bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s);
+bgs_status launch_sort(Frame* F, cudaStream_t s);
+bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n_contrib, cudaStream_t s);
+bgs_status launch_render_bwd(const bgs_gaussians* g, Frame* F, const float* dL_dimage, const float* final_T,
+                             const uint32_t* n_contrib, float* grad, cudaStream_t s);
+bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, const bgs_adam_hparams* hp,
+                       int64_t step, cudaStream_t s);
+bgs_status launch_l1(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale, float* dl,
+                     float* loss_sum, cudaStream_t s);
+bgs_status launch_stats(const Frame* F, const uint32_t* n_contrib, bgs_stats* out, cudaStream_t s);
+
+int num_sms();
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ float fast_exp(float x) {
+  // ex2.approx of x*log2(e): MUFU.EX2; differs from a correctly rounded exp by a few
+  // ulp, which only moves decisions inside the R23 near-tie margins.
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x * 1.4426950408889634f));
+  return y;
+}
+
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace bgs

@@ -1,0 +1,302 @@
+// frame.cu -- libbgs C ABI: workspace sizing, frame carving, validation, status, debug.
+// The entry points are declared (with their paper citations) in include/bgs.h.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace bgs {
+
+static std::atomic<uint64_t> g_launches{0};
+static thread_local char g_err[512] = "";
+
+void note_launch(int k) { g_launches.fetch_add((uint64_t)k, std::memory_order_relaxed); }
+void set_error(const char* msg) { snprintf(g_err, sizeof(g_err), "%s", msg); }
+
+bgs_status check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+    return BGS_ERR_CUDA;
+  }
+  return BGS_OK;
+}
+
+int num_sms() {
+  static int sms = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  });
+  return sms;
+}
+
+static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+  size_t radius, depth, record, tiles_touched, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
+      sort_status, counters, grad2d, total;
+  int32_t tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
+  int64_t sort_tiles_max;
+};
+
+constexpr int kScanTile = 2048;
+constexpr int kSortTile = 4096;
+
+static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layout& L) {
+  if (n < 0 || n > ((int64_t)1 << 31) - 1 || w < 1 || h < 1 || w > 16384 || h > 16384 || max_keys < 1 ||
+      max_keys >= BGS_MAX_KEYS_LIMIT)
+    return false;
+  L.tiles_x = (w + kTile - 1) / kTile;
+  L.tiles_y = (h + kTile - 1) / kTile;
+  L.num_tiles = L.tiles_x * L.tiles_y;
+  int b = 0;
+  while (((int64_t)1 << b) < (int64_t)L.num_tiles) ++b;  // bit_width(num_tiles - 1)
+  L.sort_bits = 32 + b;
+  L.sort_passes = (L.sort_bits + 7) / 8;
+  L.scan_tiles = (int32_t)((n + kScanTile - 1) / kScanTile);
+  if (L.scan_tiles < 1) L.scan_tiles = 1;
+  L.sort_tiles_max = (max_keys + kSortTile - 1) / kSortTile;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + (bytes ? bytes : 1));
+    return at;
+  };
+  const size_t N = (size_t)n, K = (size_t)max_keys;
+  L.radius = take(4 * N);
+  L.depth = take(4 * N);
+  L.record = take(48 * N);
+  L.tiles_touched = take(4 * N);
+  L.offsets = take(4 * N);
+  L.keys0 = take(8 * K);
+  L.keys1 = take(8 * K);
+  L.vals0 = take(4 * K);
+  L.vals1 = take(4 * K);
+  L.ranges = take(8 * (size_t)L.num_tiles);
+  L.scan_status = take(8 * (size_t)L.scan_tiles);
+  L.sort_hist = take(4 * 8 * 256);
+  L.sort_status = take(4 * 256 * (size_t)L.sort_tiles_max);
+  L.counters = take(4 * C_NUM);
+  L.grad2d = take(48 * N);
+  L.total = o;
+  return true;
+}
+
+static Cam make_cam(const bgs_camera& c, int32_t tiles_x, int32_t tiles_y) {
+  Cam k;
+  memcpy(k.V, c.view, sizeof(k.V));
+  memcpy(k.P, c.proj, sizeof(k.P));
+  memcpy(k.campos, c.campos, sizeof(k.campos));
+  // canonical float expressions (R22): separately rounded binary32 ops
+  volatile float two_tx = 2.0f * c.tan_fovx, two_ty = 2.0f * c.tan_fovy;
+  k.fx = (float)c.width / two_tx;
+  k.fy = (float)c.height / two_ty;
+  k.limx = 1.3f * c.tan_fovx;
+  k.limy = 1.3f * c.tan_fovy;
+  k.near_plane = c.near_plane;
+  memcpy(k.bg, c.bg, sizeof(k.bg));
+  k.W = c.width;
+  k.H = c.height;
+  k.tiles_x = tiles_x;
+  k.tiles_y = tiles_y;
+  return k;
+}
+
+static bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+static bgs_status validate_camera(const bgs_camera* cam, const Frame* F) {
+  if (!cam) return BGS_ERR_INVALID;
+  if (cam->width != F->W || cam->height != F->H) return BGS_ERR_INVALID;
+  if (!(cam->tan_fovx > 0.0f) || !(cam->tan_fovy > 0.0f) || !(cam->near_plane >= 0.0f)) return BGS_ERR_INVALID;
+  // view 3x3 must be orthonormal, tolerance 1e-5
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) {
+      double d = 0;
+      for (int k = 0; k < 3; ++k) d += (double)cam->view[a + 4 * k] * (double)cam->view[b + 4 * k];
+      if (fabs(d - (a == b ? 1.0 : 0.0)) > 1e-5) return BGS_ERR_INVALID;
+    }
+  for (int k = 0; k < 16; ++k)
+    if (!isfinite(cam->view[k]) || !isfinite(cam->proj[k])) return BGS_ERR_INVALID;
+  return BGS_OK;
+}
+
+static bgs_status validate_gaussians(const bgs_gaussians* g, const Frame* F) {
+  if (!g || g->n != F->n || g->sh_degree < 0 || g->sh_degree > 3) return BGS_ERR_INVALID;
+  if (g->n > 0) {
+    if (!g->means || !g->log_scales || !g->quats || !g->opacity_logits || !g->sh) return BGS_ERR_INVALID;
+    if (!aligned16(g->quats) || !aligned16(g->sh) || !aligned16(g->means) || !aligned16(g->log_scales) ||
+        !aligned16(g->opacity_logits))
+      return BGS_ERR_INVALID;
+  }
+  return BGS_OK;
+}
+
+static bool frame_ok(const bgs_frame* f) { return f && frame_of(f)->magic == kFrameMagic; }
+
+}  // namespace bgs
+
+using namespace bgs;
+
+extern "C" {
+
+int32_t bgs_version(void) { return 1; }
+uint64_t bgs_launch_count(void) { return g_launches.load(); }
+const char* bgs_last_error(void) { return g_err; }
+
+const char* bgs_status_string(bgs_status s) {
+  switch (s) {
+    case BGS_OK: return "ok";
+    case BGS_ERR_INVALID: return "invalid argument";
+    case BGS_ERR_CAPACITY: return "key capacity exceeded (K > max_keys)";
+    case BGS_ERR_CUDA: return g_err[0] ? g_err : "CUDA error";
+    case BGS_ERR_UNSUPPORTED: return "unsupported";
+  }
+  return "unknown status";
+}
+
+size_t bgs_workspace_bytes(int64_t n, int32_t w, int32_t h, int64_t max_keys) {
+  Layout L;
+  return make_layout(n, w, h, max_keys, L) ? L.total : 0;
+}
+
+bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n, int32_t w, int32_t h,
+                          int64_t max_keys) {
+  Layout L;
+  if (!f || !workspace || ((uintptr_t)workspace & 255u) || !make_layout(n, w, h, max_keys, L) || bytes < L.total)
+    return BGS_ERR_INVALID;
+  memset(f, 0, sizeof(*f));
+  Frame* F = frame_of(f);
+  char* base = (char*)workspace;
+  F->magic = kFrameMagic;
+  F->n = n;
+  F->max_keys = max_keys;
+  F->W = w;
+  F->H = h;
+  F->tiles_x = L.tiles_x;
+  F->tiles_y = L.tiles_y;
+  F->num_tiles = L.num_tiles;
+  F->sort_bits = L.sort_bits;
+  F->sort_passes = L.sort_passes;
+  F->scan_tiles = L.scan_tiles;
+  F->sort_tiles_max = L.sort_tiles_max;
+  F->radius = (int32_t*)(base + L.radius);
+  F->depth = (float*)(base + L.depth);
+  F->record = (float4*)(base + L.record);
+  F->tiles_touched = (uint32_t*)(base + L.tiles_touched);
+  F->offsets = (uint32_t*)(base + L.offsets);
+  F->keys[0] = (uint64_t*)(base + L.keys0);
+  F->keys[1] = (uint64_t*)(base + L.keys1);
+  F->vals[0] = (uint32_t*)(base + L.vals0);
+  F->vals[1] = (uint32_t*)(base + L.vals1);
+  F->ranges = (uint2*)(base + L.ranges);
+  F->scan_status = (unsigned long long*)(base + L.scan_status);
+  F->sort_hist = (uint32_t*)(base + L.sort_hist);
+  F->sort_status = (uint32_t*)(base + L.sort_status);
+  F->counters = (uint32_t*)(base + L.counters);
+  F->grad2d = (float4*)(base + L.grad2d);
+  F->final_buf = L.sort_passes & 1;  // pass p reads buf p&1, writes buf (p+1)&1
+  return BGS_OK;
+}
+
+bgs_status bgs_preprocess(const bgs_gaussians* g, const bgs_camera* cam, bgs_frame* f, void* stream) {
+  if (!frame_ok(f)) return BGS_ERR_INVALID;
+  Frame* F = frame_of(f);
+  bgs_status st = validate_gaussians(g, F);
+  if (st != BGS_OK) return st;
+  if ((st = validate_camera(cam, F)) != BGS_OK) return st;
+  F->cam = make_cam(*cam, F->tiles_x, F->tiles_y);
+  F->cam_valid = 1;
+  return launch_preprocess(g, F, (cudaStream_t)stream);
+}
+
+bgs_status bgs_sort(bgs_frame* f, void* stream) {
+  if (!frame_ok(f) || !frame_of(f)->cam_valid) return BGS_ERR_INVALID;
+  return launch_sort(frame_of(f), (cudaStream_t)stream);
+}
+
+bgs_status bgs_render_fwd(bgs_frame* f, float* image, float* final_T, uint32_t* n_contrib, void* stream) {
+  if (!frame_ok(f) || !frame_of(f)->cam_valid || !image || !final_T || !n_contrib) return BGS_ERR_INVALID;
+  return launch_render_fwd(frame_of(f), image, final_T, n_contrib, (cudaStream_t)stream);
+}
+
+bgs_status bgs_render_bwd(const bgs_gaussians* g, bgs_frame* f, const float* dL_dimage, const float* final_T,
+                          const uint32_t* n_contrib, float* grad, void* stream) {
+  if (!frame_ok(f) || !frame_of(f)->cam_valid || !dL_dimage || !final_T || !n_contrib) return BGS_ERR_INVALID;
+  Frame* F = frame_of(f);
+  bgs_status st = validate_gaussians(g, F);
+  if (st != BGS_OK) return st;
+  if (F->n > 0 && (!grad || !aligned16(grad))) return BGS_ERR_INVALID;
+  return launch_render_bwd(g, F, dL_dimage, final_T, n_contrib, grad, (cudaStream_t)stream);
+}
+
+bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
+                         const bgs_adam_hparams* hp, int64_t step, void* stream) {
+  if (n < 0 || !hp || step < 1) return BGS_ERR_INVALID;
+  if (n == 0) return BGS_OK;
+  if (!theta || !grad || !exp_avg || !exp_avg_sq) return BGS_ERR_INVALID;
+  if (!aligned16(theta) || !aligned16(grad) || !aligned16(exp_avg) || !aligned16(exp_avg_sq)) return BGS_ERR_INVALID;
+  if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f && hp->beta2 >= 0.0f && hp->beta2 < 1.0f && hp->eps >= 0.0f))
+    return BGS_ERR_INVALID;
+  return launch_adam(theta, grad, exp_avg, exp_avg_sq, n, hp, step, (cudaStream_t)stream);
+}
+
+bgs_status bgs_l1_loss_grad(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale,
+                            float* dL_dimage, float* loss_sum, void* stream) {
+  if (!image || !target || !dL_dimage || !loss_sum || w < 1 || h < 1 || w > 16384 || h > 16384)
+    return BGS_ERR_INVALID;
+  return launch_l1(image, target, w, h, scale, dL_dimage, loss_sum, (cudaStream_t)stream);
+}
+
+bgs_status bgs_frame_status(const bgs_frame* f, int64_t* num_keys) {
+  if (!frame_ok(f) || !num_keys) return BGS_ERR_INVALID;
+  const Frame* F = frame_of(f);
+  uint32_t c[3];
+  if (cudaMemcpy(c, F->counters, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return check_launch("bgs_frame_status");
+  *num_keys = (int64_t)(((uint64_t)c[C_K_HI] << 32) | c[C_K_LO]);
+  return c[C_OVERFLOW] ? BGS_ERR_CAPACITY : BGS_OK;
+}
+
+bgs_status bgs_frame_debug(const bgs_frame* f, bgs_frame_views* out) {
+  if (!frame_ok(f) || !out) return BGS_ERR_INVALID;
+  const Frame* F = frame_of(f);
+  out->radius = F->radius;
+  out->depth = F->depth;
+  out->record = (float*)F->record;
+  out->tiles_touched = F->tiles_touched;
+  out->offsets = F->offsets;
+  out->keys_unsorted = F->keys[0];
+  out->values_unsorted = F->vals[0];
+  out->keys_sorted = F->keys[F->final_buf];
+  out->values_sorted = F->vals[F->final_buf];
+  out->ranges = (uint32_t*)F->ranges;
+  out->grad2d = (float*)F->grad2d;
+  out->n = F->n;
+  out->max_keys = F->max_keys;
+  out->tiles_x = F->tiles_x;
+  out->tiles_y = F->tiles_y;
+  out->sort_bits = F->sort_bits;
+  out->sort_passes = F->sort_passes;
+  return BGS_OK;
+}
+
+bgs_status bgs_frame_set_debug(bgs_frame* f, int32_t flags) {
+  if (!frame_ok(f)) return BGS_ERR_INVALID;
+  frame_of(f)->debug_flags = flags;
+  return BGS_OK;
+}
+
+bgs_status bgs_frame_stats(const bgs_frame* f, const uint32_t* n_contrib, bgs_stats* out, void* stream) {
+  if (!frame_ok(f) || !n_contrib || !out) return BGS_ERR_INVALID;
+  return launch_stats(frame_of(f), n_contrib, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,305 @@
+// preprocess.cu -- a1-a3: per-Gaussian projection (K7) + exclusive scan of tiles_touched (K8).
+//
+// PAPER.md §II-A l.128-142: G(x) = exp(-1/2 (x-mu)^T Sigma^-1 (x-mu)), Sigma' = J W Sigma W^T J^T;
+// l.59: colour from SH coefficients.  Readings R1-R13 and the canonical expression tree
+// R22: every decision-bearing value (depth, xy, Sigma', conic, radius,
+// rect) is computed with explicit fmaf() and IEEE div/sqrt, and this file is compiled
+// with --fmad=false so nvcc contracts nothing else.  rgb/SH is free-order.
+//
+// Layout: theta segments are read as coalesced vectors (quats float4,
+// SH 12 x float4 per Gaussian, only for Gaussians that survive the culls); outputs are
+// the 48-byte render record {x, y, A, B | C, o, r, g | b, cbits, -, -} that the blend
+// kernels stage through shared memory (the B200 form of the paper's T3 RGB
+// reordering), plus radius, depth and tiles_touched.
+#include "common.cuh"
+
+namespace bgs {
+
+// Real SH constants (R12).
+__constant__ float kC0 = 0.28209479177387814f;
+__constant__ float kC1 = 0.4886025119029199f;
+__constant__ float kC2[5] = {1.0925484305920792f, -1.0925484305920792f, 0.31539156525252005f,
+                             -1.0925484305920792f, 0.5462742152960396f};
+__constant__ float kC3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.4570457994644658f,
+                             0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
+                             -0.5900435899266435f};
+
+struct PreParams {
+  Cam cam;
+  const float* means;
+  const float* log_scales;
+  const float4* quats;
+  const float* ologits;
+  const float4* sh;  // [n][12] float4
+  int64_t n;
+  int32_t deg;
+  int32_t* radius;
+  float* depth;
+  float4* record;
+  uint32_t* tiles_touched;
+  float4* grad2d;
+};
+
+__global__ void __launch_bounds__(256) k_preprocess(PreParams p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  const Cam& c = p.cam;
+  const float mx = p.means[3 * i], my = p.means[3 * i + 1], mz = p.means[3 * i + 2];
+  // camera space (O2) and near cull (R3)
+  const float t0 = fmaf(c.V[8], mz, fmaf(c.V[4], my, fmaf(c.V[0], mx, c.V[12])));
+  const float t1 = fmaf(c.V[9], mz, fmaf(c.V[5], my, fmaf(c.V[1], mx, c.V[13])));
+  const float t2 = fmaf(c.V[10], mz, fmaf(c.V[6], my, fmaf(c.V[2], mx, c.V[14])));
+  p.radius[i] = 0;
+  p.tiles_touched[i] = 0;
+  if (t2 <= c.near_plane) return;
+  // clip, perspective divide (R4), pixel coordinates (R1)
+  const float c0 = fmaf(c.P[8], mz, fmaf(c.P[4], my, fmaf(c.P[0], mx, c.P[12])));
+  const float c1 = fmaf(c.P[9], mz, fmaf(c.P[5], my, fmaf(c.P[1], mx, c.P[13])));
+  const float c3 = fmaf(c.P[11], mz, fmaf(c.P[7], my, fmaf(c.P[3], mx, c.P[15])));
+  const float ndx = __fdiv_rn(c0, c3), ndy = __fdiv_rn(c1, c3);
+  const float px = 0.5f * fmaf(ndx + 1.0f, (float)c.W, -1.0f);
+  const float py = 0.5f * fmaf(ndy + 1.0f, (float)c.H, -1.0f);
+  // activations (R5): double transcendental, rounded once
+  const float s0 = (float)exp((double)p.log_scales[3 * i]);
+  const float s1 = (float)exp((double)p.log_scales[3 * i + 1]);
+  const float s2 = (float)exp((double)p.log_scales[3 * i + 2]);
+  const float o = (float)(1.0 / (1.0 + exp(-(double)p.ologits[i])));
+  float4 q = p.quats[i];
+  const float n2 = fmaf(q.x, q.x, fmaf(q.y, q.y, fmaf(q.z, q.z, q.w * q.w)));
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(n2));
+  const float qw = q.x * inv, qx = q.y * inv, qy = q.z * inv, qz = q.w * inv;
+  // Sigma = (R diag s)(R diag s)^T (R6)
+  const float xx = qx * qx, yy = qy * qy, zz = qz * qz, xy = qx * qy, xz = qx * qz, yz = qy * qz;
+  const float wx = qw * qx, wy = qw * qy, wz = qw * qz;
+  const float M00 = (1.0f - 2.0f * (yy + zz)) * s0, M01 = (2.0f * (xy - wz)) * s1, M02 = (2.0f * (xz + wy)) * s2;
+  const float M10 = (2.0f * (xy + wz)) * s0, M11 = (1.0f - 2.0f * (xx + zz)) * s1, M12 = (2.0f * (yz - wx)) * s2;
+  const float M20 = (2.0f * (xz - wy)) * s0, M21 = (2.0f * (yz + wx)) * s1, M22 = (1.0f - 2.0f * (xx + yy)) * s2;
+  const float S00 = fmaf(M02, M02, fmaf(M01, M01, M00 * M00));
+  const float S01 = fmaf(M02, M12, fmaf(M01, M11, M00 * M10));
+  const float S02 = fmaf(M02, M22, fmaf(M01, M21, M00 * M20));
+  const float S11 = fmaf(M12, M12, fmaf(M11, M11, M10 * M10));
+  const float S12 = fmaf(M12, M22, fmaf(M11, M21, M10 * M20));
+  const float S22 = fmaf(M22, M22, fmaf(M21, M21, M20 * M20));
+  // EWA: T = J W3 (R7 clamp), Sigma' = T Sigma T^T + 0.3 I (R8)
+  uint32_t cb = 0;
+  float u = __fdiv_rn(t0, t2), v = __fdiv_rn(t1, t2);
+  if (u > c.limx) cb |= CB_JX;
+  if (u < -c.limx) cb |= CB_JX | CB_JX_NEG;
+  if (v > c.limy) cb |= CB_JY;
+  if (v < -c.limy) cb |= CB_JY | CB_JY_NEG;
+  u = fminf(c.limx, fmaxf(-c.limx, u));
+  v = fminf(c.limy, fmaxf(-c.limy, v));
+  const float tpx = u * t2, tpy = v * t2;
+  const float tz2 = t2 * t2;
+  const float j00 = __fdiv_rn(c.fx, t2), j02 = -__fdiv_rn(c.fx * tpx, tz2);
+  const float j11 = __fdiv_rn(c.fy, t2), j12 = -__fdiv_rn(c.fy * tpy, tz2);
+  // W_ik = V[i + 4k]
+  const float T00 = fmaf(j02, c.V[2], j00 * c.V[0]);
+  const float T01 = fmaf(j02, c.V[6], j00 * c.V[4]);
+  const float T02 = fmaf(j02, c.V[10], j00 * c.V[8]);
+  const float T10 = fmaf(j12, c.V[2], j11 * c.V[1]);
+  const float T11 = fmaf(j12, c.V[6], j11 * c.V[5]);
+  const float T12 = fmaf(j12, c.V[10], j11 * c.V[9]);
+  // L = T Sigma (row i, column k): L_ik = fma(T_i2, S_2k, fma(T_i1, S_1k, T_i0 S_0k))
+  const float L00 = fmaf(T02, S02, fmaf(T01, S01, T00 * S00));
+  const float L01 = fmaf(T02, S12, fmaf(T01, S11, T00 * S01));
+  const float L02 = fmaf(T02, S22, fmaf(T01, S12, T00 * S02));
+  const float L10 = fmaf(T12, S02, fmaf(T11, S01, T10 * S00));
+  const float L11 = fmaf(T12, S12, fmaf(T11, S11, T10 * S01));
+  const float L12 = fmaf(T12, S22, fmaf(T11, S12, T10 * S02));
+  const float a = fmaf(L02, T02, fmaf(L01, T01, L00 * T00)) + 0.3f;
+  const float b = fmaf(L02, T12, fmaf(L01, T11, L00 * T10));
+  const float cc = fmaf(L12, T12, fmaf(L11, T11, L10 * T10)) + 0.3f;
+  // det, conic (R9), radius (R10)
+  const float det = fmaf(a, cc, -(b * b));
+  if (det <= 0.0f) return;
+  const float idet = __fdiv_rn(1.0f, det);
+  const float conx = cc * idet, cony = -(b * idet), conz = a * idet;
+  const float mid = 0.5f * (a + cc);
+  const float lam = mid + __fsqrt_rn(fmaxf(0.1f, mid * mid - det));
+  const int rad = (int)ceilf(3.0f * __fsqrt_rn(lam));
+  // rect, floor then clamp (R11); culled if empty
+  const float tx = (float)c.tiles_x, ty = (float)c.tiles_y;
+  const int rx0 = (int)fminf(tx, fmaxf(0.0f, floorf((px - (float)rad) * 0.0625f)));
+  const int ry0 = (int)fminf(ty, fmaxf(0.0f, floorf((py - (float)rad) * 0.0625f)));
+  const int rx1 = (int)fminf(tx, fmaxf(0.0f, floorf((px + (float)(rad + 15)) * 0.0625f)));
+  const int ry1 = (int)fminf(ty, fmaxf(0.0f, floorf((py + (float)(rad + 15)) * 0.0625f)));
+  const uint32_t area = (uint32_t)(rx1 - rx0) * (uint32_t)(ry1 - ry0);
+  if (area == 0) return;
+  // SH colour (R12), free order
+  const float dxw = mx - c.campos[0], dyw = my - c.campos[1], dzw = mz - c.campos[2];
+  const float il = rsqrtf(dxw * dxw + dyw * dyw + dzw * dzw);
+  const float x = dxw * il, y = dyw * il, z = dzw * il;
+  const float4* shp = p.sh + 12 * i;
+  float sh[48];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    const float4 f4 = __ldg(shp + k);
+    sh[4 * k] = f4.x; sh[4 * k + 1] = f4.y; sh[4 * k + 2] = f4.z; sh[4 * k + 3] = f4.w;
+  }
+  float rgb[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) rgb[ch] = kC0 * sh[ch];
+  if (p.deg > 0) {
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch)
+      rgb[ch] += -kC1 * y * sh[3 + ch] + kC1 * z * sh[6 + ch] - kC1 * x * sh[9 + ch];
+    if (p.deg > 1) {
+      const float xx_ = x * x, yy_ = y * y, zz_ = z * z;
+      const float b4 = kC2[0] * x * y, b5 = kC2[1] * y * z, b6 = kC2[2] * (2.0f * zz_ - xx_ - yy_);
+      const float b7 = kC2[3] * x * z, b8 = kC2[4] * (xx_ - yy_);
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch)
+        rgb[ch] += b4 * sh[12 + ch] + b5 * sh[15 + ch] + b6 * sh[18 + ch] + b7 * sh[21 + ch] + b8 * sh[24 + ch];
+      if (p.deg > 2) {
+        const float b9 = kC3[0] * y * (3.0f * xx_ - yy_), b10 = kC3[1] * x * y * z;
+        const float b11 = kC3[2] * y * (4.0f * zz_ - xx_ - yy_);
+        const float b12 = kC3[3] * z * (2.0f * zz_ - 3.0f * xx_ - 3.0f * yy_);
+        const float b13 = kC3[4] * x * (4.0f * zz_ - xx_ - yy_), b14 = kC3[5] * z * (xx_ - yy_);
+        const float b15 = kC3[6] * x * (xx_ - 3.0f * yy_);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch)
+          rgb[ch] += b9 * sh[27 + ch] + b10 * sh[30 + ch] + b11 * sh[33 + ch] + b12 * sh[36 + ch] +
+                     b13 * sh[39 + ch] + b14 * sh[42 + ch] + b15 * sh[45 + ch];
+      }
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    rgb[ch] += 0.5f;
+    if (rgb[ch] < 0.0f) {
+      cb |= (1u << ch);
+      rgb[ch] = 0.0f;
+    }
+  }
+  p.radius[i] = rad;
+  p.depth[i] = t2;
+  p.tiles_touched[i] = area;
+  float4* rec = p.record + 3 * i;
+  rec[0] = make_float4(px, py, -0.5f * conx, -cony);
+  rec[1] = make_float4(-0.5f * conz, o, rgb[0], rgb[1]);
+  rec[2] = make_float4(rgb[2], __uint_as_float(cb), 0.0f, 0.0f);
+  // this view's blend-gradient accumulator (render_bwd REDs into it)
+  float4* g2 = p.grad2d + 3 * i;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  g2[0] = z4;
+  g2[1] = z4;
+  g2[2] = z4;
+}
+
+// ---------------------------------------------------------------------------
+// K8: single-pass exclusive scan with decoupled look-back (dynamic tile ids).
+// status word: bits 62-63 = flag (1 aggregate, 2 inclusive prefix), bits 0-61 = value.
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+                                                      int64_t n, unsigned long long* status, uint32_t* counters,
+                                                      int64_t max_keys, int32_t num_tiles) {
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_warp[kScanThreads / 32];
+  __shared__ unsigned long long s_prefix;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_tile = atomicAdd(&counters[C_SCAN_TICKET], 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * kScanTile + (int64_t)tid * kScanItems;
+  uint32_t v[kScanItems];
+  unsigned long long local = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    v[k] = (base + k < n) ? in[base + k] : 0u;
+    local += v[k];
+  }
+  // block exclusive scan of per-thread totals
+  unsigned long long incl = local;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  unsigned long long warp_off = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kScanThreads / 32; ++w) {
+    if (w < warp) warp_off += s_warp[w];
+    total += s_warp[w];
+  }
+  // look-back by warp 0
+  if (warp == 0) {
+    unsigned long long prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st_volatile_u64(&status[0], kFlagP | total);
+    } else {
+      if (lane == 0) st_volatile_u64(&status[tile], kFlagA | total);
+      int64_t j = tile - 1 - lane;  // window of 32 predecessors
+      while (true) {
+        unsigned long long s = 0;
+        if (j >= 0) {
+          do {
+            s = ld_volatile_u64(&status[j]);
+          } while ((s >> 62) == 0);
+        } else {
+          s = kFlagP;  // virtual inclusive prefix 0 before tile 0
+        }
+        const uint32_t pmask = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+        const int stop = pmask ? __ffs(pmask) - 1 : 32;
+        unsigned long long contrib = (lane <= stop) ? (s & kValMask) : 0ull;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
+        prefix += contrib;
+        if (pmask) break;
+        j -= 32;
+      }
+      if (lane == 0) st_volatile_u64(&status[tile], kFlagP | (prefix + total));
+    }
+    if (lane == 0) s_prefix = prefix;
+  }
+  __syncthreads();
+  unsigned long long run = s_prefix + warp_off + (incl - local);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < n) out[base + k] = (uint32_t)(run > 0xffffffffull ? 0xffffffffull : run);
+    run += v[k];
+  }
+  if (tile == num_tiles - 1 && tid == 0) {
+    const unsigned long long K = s_prefix + total;
+    counters[C_K_LO] = (uint32_t)K;
+    counters[C_K_HI] = (uint32_t)(K >> 32);
+    counters[C_OVERFLOW] = K > (unsigned long long)max_keys ? 1u : 0u;
+  }
+}
+
+bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
+  if (cudaMemsetAsync(F->counters, 0, 4 * C_NUM, s) != cudaSuccess) return check_launch("preprocess memset");
+  if (F->n == 0) return BGS_OK;
+  PreParams p;
+  p.cam = F->cam;
+  p.means = g->means;
+  p.log_scales = g->log_scales;
+  p.quats = (const float4*)g->quats;
+  p.ologits = g->opacity_logits;
+  p.sh = (const float4*)g->sh;
+  p.n = F->n;
+  p.deg = g->sh_degree;
+  p.radius = F->radius;
+  p.depth = F->depth;
+  p.record = F->record;
+  p.tiles_touched = F->tiles_touched;
+  p.grad2d = F->grad2d;
+  const int64_t blocks = (F->n + 255) / 256;
+  k_preprocess<<<(unsigned)blocks, 256, 0, s>>>(p);
+  note_launch();
+  bgs_status st = check_launch("k_preprocess");
+  if (st != BGS_OK) return st;
+  if (cudaMemsetAsync(F->scan_status, 0, 8 * (size_t)F->scan_tiles, s) != cudaSuccess)
+    return check_launch("scan memset");
+  k_scan<<<F->scan_tiles, kScanThreads, 0, s>>>(F->tiles_touched, F->offsets, F->n, F->scan_status, F->counters,
+                                                 F->max_keys, F->scan_tiles);
+  note_launch();
+  return check_launch("k_scan");
+}
+
+}  // namespace bgs

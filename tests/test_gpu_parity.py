@@ -1,0 +1,290 @@
+"""GPU vs oracle parity, through the C ABI (libbgs.so), on seeded scenes.
+
+Tolerances (BASELINE.json north_star): bit-exact for depth bits, radius,
+tiles_touched, offsets, K, unsorted/sorted keys and values, ranges, and n_contrib on
+pixels not flagged by the R23 near-tie rule; xy / conic / opacity bit-exact (canonical
+tree R22); rgb <= 1e-6 abs; image <= 1e-4 abs per channel on unflagged pixels;
+final_T <= 1e-5; per-group gradient rel-L2 <= 1e-3; Adam <= 1e-6 rel per element.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def bgs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2510_14564_b200 as m
+
+    return m
+
+
+def scenes():
+    return {
+        "tiny": lambda: gen.tiny(),
+        "ragged": lambda: gen.small_scene(7, 3000, 200, 133, scale_mu=0.04),
+        "dense": lambda: gen.small_scene(8, 6000, 96, 80, scale_mu=0.06, depth=(2.0, 2.5)),
+        "deg1": lambda: gen.small_scene(9, 1500, 120, 72, sh_degree=1),
+        "deg0": lambda: gen.small_scene(10, 1500, 64, 64, sh_degree=0),
+    }
+
+
+def run_gpu(bgs, s, cam, max_keys=1 << 21, skip_sort=False):
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=max_keys, device=dev)
+    if skip_sort:
+        bgs.bgs_frame_set_debug(r.frame, bgs.BGS_DEBUG_SKIP_SORT)
+        g = bgs.gaussians(theta, s.n, s.sh_degree)
+        bgs.bgs_preprocess(g, bgs.camera(cam), r.frame)
+        bgs.bgs_sort(r.frame)
+        torch.cuda.synchronize()
+        return r, theta, None
+    out = r.forward(theta, cam, s.sh_degree)
+    torch.cuda.synchronize()
+    return r, theta, out
+
+
+class _DevPtr:
+    """Zero-copy view of a workspace region through __cuda_array_interface__."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (int(ptr), True),
+                                         "version": 2}
+
+
+def dev_array(ptr, count, dtype):
+    typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.int64: "<i8"}[dtype]
+    if count == 0:
+        return torch.empty(0, dtype=dtype).numpy()
+    torch.cuda.synchronize()
+    return torch.as_tensor(_DevPtr(ptr, count, typestr), device="cuda").cpu().numpy()
+
+
+def views(bgs, r, n, K, ntiles):
+    v = r.views()
+    rec = dev_array(v.record, 12 * n, torch.float32).reshape(n, 12)
+    return dict(radius=dev_array(v.radius, n, torch.int32), depth=dev_array(v.depth, n, torch.float32),
+                record=rec, tiles_touched=dev_array(v.tiles_touched, n, torch.int32).view(np.uint32),
+                offsets=dev_array(v.offsets, n, torch.int32).view(np.uint32),
+                keys_sorted=dev_array(v.keys_sorted, K, torch.int64).view(np.uint64),
+                values_sorted=dev_array(v.values_sorted, K, torch.int32).view(np.uint32),
+                keys_unsorted=dev_array(v.keys_unsorted, K, torch.int64).view(np.uint64),
+                values_unsorted=dev_array(v.values_unsorted, K, torch.int32).view(np.uint32),
+                ranges=dev_array(v.ranges, 2 * ntiles, torch.int32).view(np.uint32).reshape(ntiles, 2))
+
+
+@pytest.mark.parametrize("name", list(scenes()))
+def test_preprocess_parity(bgs, name):
+    s = scenes()[name]()
+    cam = s.cameras[0]
+    r, _, out = run_gpu(bgs, s, cam)
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    pre = ref["pre"]
+    K = ref["srt"]["K"]
+    assert r.num_keys == K
+    v = views(bgs, r, s.n, K, len(ref["srt"]["ranges"]))
+    assert np.array_equal(v["radius"], pre["radius"])
+    assert np.array_equal(v["tiles_touched"], pre["tiles_touched"])
+    assert np.array_equal(v["offsets"].astype(np.uint64), ref["srt"]["offsets"])
+    vis = pre["radius"] > 0
+    assert np.array_equal(v["depth"][vis].view(np.uint32), pre["depth"][vis].view(np.uint32))
+    rec = v["record"][vis]
+    assert np.array_equal(rec[:, 0:2], pre["xy"][vis])
+    conic = np.stack([-2 * rec[:, 2], -rec[:, 3], -2 * rec[:, 4]], 1)
+    assert np.array_equal(conic, pre["conic"][vis])
+    assert np.array_equal(rec[:, 5], pre["opacity"][vis])
+    assert np.abs(rec[:, 6:9] - pre["rgb"][vis]).max() <= 1e-6
+    cb = rec[:, 9].view(np.uint32)
+    assert np.array_equal(cb & 0x78, pre["cbits"][vis] & 0x78)  # J-clamp bits (exact)
+    assert (cb & 7 != pre["cbits"][vis] & 7).sum() <= max(1, vis.sum() // 10000)  # rgb clamp (free-order)
+
+
+@pytest.mark.parametrize("name", ["tiny", "ragged", "dense"])
+def test_unsorted_keys_parity(bgs, name):
+    s = scenes()[name]()
+    cam = s.cameras[0]
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    K = ref["srt"]["K"]
+    r, _, _ = run_gpu(bgs, s, cam, skip_sort=True)
+    v = views(bgs, r, s.n, K, len(ref["srt"]["ranges"]))
+    assert np.array_equal(v["keys_unsorted"], ref["srt"]["keys"])
+    assert np.array_equal(v["values_unsorted"], ref["srt"]["values"])
+
+
+@pytest.mark.parametrize("name", list(scenes()))
+def test_sort_and_ranges_parity(bgs, name):
+    s = scenes()[name]()
+    cam = s.cameras[0]
+    r, _, _ = run_gpu(bgs, s, cam)
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    K = ref["srt"]["K"]
+    v = views(bgs, r, s.n, K, len(ref["srt"]["ranges"]))
+    assert np.array_equal(v["keys_sorted"], ref["srt"]["sorted_keys"])
+    assert np.array_equal(v["values_sorted"], ref["srt"]["sorted_values"])
+    assert np.array_equal(v["ranges"], ref["srt"]["ranges"])
+
+
+@pytest.mark.parametrize("name", list(scenes()))
+def test_render_fwd_parity(bgs, name):
+    s = scenes()[name]()
+    cam = s.cameras[0]
+    _, _, out = run_gpu(bgs, s, cam)
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    ok = ref["flags"] == 0
+    img = out["image"].cpu().numpy()
+    nc = out["n_contrib"].cpu().numpy().view(np.uint32)
+    assert np.abs(img - ref["image"])[:, ok].max() <= IMG_TOL
+    assert np.array_equal(nc[ok], ref["n_contrib"][ok])
+    assert np.abs(out["final_T"].cpu().numpy() - ref["final_T"])[ok].max() <= 1e-5
+    assert (~ok).sum() <= max(4, ok.size // 200), f"{(~ok).sum()} flagged pixels"
+    # flagged pixels still agree loosely (one Gaussian at the alpha or T threshold)
+    assert np.abs(img - ref["image"]).max() <= 2e-2
+
+
+@pytest.mark.parametrize("name", list(scenes()))
+def test_render_bwd_parity(bgs, name):
+    s = scenes()[name]()
+    cam = s.cameras[0]
+    r, theta, out = run_gpu(bgs, s, cam)
+    dl_np = gen.random_dl_dimage(3, cam.width, cam.height)
+    dl = torch.from_numpy(dl_np).cuda()
+    grad = torch.zeros_like(theta)
+    r.backward(theta, s.sh_degree, dl, out, grad)
+    torch.cuda.synchronize()
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    g_ref = oracle.backward(s.theta, s.n, s.sh_degree, cam, ref, dl_np)["grad"]
+    g = grad.cpu().numpy().astype(np.float64)
+    for gname, idx in oracle.group_slices(s.n).items():
+        den = np.linalg.norm(g_ref[idx])
+        if den == 0:
+            assert not g[idx].any(), gname
+            continue
+        err = np.linalg.norm(g[idx] - g_ref[idx]) / den
+        assert err <= GRAD_TOL, (name, gname, err)
+
+
+def test_multi_view_gradients_accumulate(bgs):
+    # R20: grad += over views; equals the sum of the oracle's per-view gradients
+    s = gen.garden(seed=1, n=20000, n_cams=4)
+    cams = s.cameras
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    grad = torch.zeros_like(theta)
+    r = bgs.Renderer(s.n, cams[0].width, cams[0].height, max_keys=1 << 22, device=dev)
+    g_ref = np.zeros(59 * s.n)
+    for i, cam in enumerate(cams[:2]):
+        out = r.forward(theta, cam, 3)
+        dl_np = gen.random_dl_dimage(20 + i, cam.width, cam.height, scale=1e-3)
+        r.backward(theta, 3, torch.from_numpy(dl_np).to(dev), out, grad)
+        ref = oracle.forward(s.theta, s.n, 3, cam)
+        g_ref += oracle.backward(s.theta, s.n, 3, cam, ref, dl_np)["grad"]
+    torch.cuda.synchronize()
+    g = grad.cpu().numpy().astype(np.float64)
+    for gname, idx in oracle.group_slices(s.n).items():
+        err = np.linalg.norm(g[idx] - g_ref[idx]) / np.linalg.norm(g_ref[idx])
+        assert err <= GRAD_TOL, (gname, err)
+
+
+def test_adam_parity(bgs):
+    n = 3001  # 59n not a multiple of 4: exercises the scalar tail
+    r = np.random.default_rng(0)
+    th = r.standard_normal(59 * n).astype(np.float32)
+    m = (0.1 * r.standard_normal(59 * n)).astype(np.float32)
+    v = (0.01 * r.random(59 * n)).astype(np.float32)
+    g = (r.standard_normal(59 * n) * 10.0 ** r.uniform(-6, 0, 59 * n)).astype(np.float32)
+    hp = bgs.AdamHParams()
+    lr6 = [hp.lr_means, hp.lr_log_scales, hp.lr_quats, hp.lr_opacity, hp.lr_sh_dc, hp.lr_sh_rest]
+    T = {k: torch.from_numpy(a.copy()).cuda() for k, a in dict(th=th, m=m, v=v, g=g).items()}
+    bgs.bgs_adam_step(T["th"], T["g"], T["m"], T["v"], n, hp, step=7)
+    torch.cuda.synchronize()
+    th_ref, m_ref, v_ref = oracle.adam(th, g, m, v, n, lr6, b1=float(np.float32(0.9)),
+                                       b2=float(np.float32(0.999)), eps=float(np.float32(1e-15)), step=7)
+    np.testing.assert_allclose(T["m"].cpu().numpy(), m_ref, rtol=1e-6, atol=1e-12)
+    np.testing.assert_allclose(T["v"].cpu().numpy(), v_ref, rtol=1e-6, atol=1e-14)
+    np.testing.assert_allclose(T["th"].cpu().numpy(), th_ref, rtol=1e-6, atol=1e-7)
+    assert not T["g"].any()
+
+
+# ------------------------------------------------------------------ edge cases
+def test_empty_scene(bgs):
+    cam = gen.tiny().cameras[0]
+    s = gen.Scene("empty", 0, np.zeros(0, np.float32), [cam])
+    dev = torch.device("cuda")
+    r = bgs.Renderer(0, cam.width, cam.height, max_keys=1024, device=dev)
+    theta = torch.zeros(0, device=dev)
+    out = r.forward(theta, cam, 3)
+    torch.cuda.synchronize()
+    assert r.num_keys == 0
+    img = out["image"].cpu().numpy()
+    assert (img == cam.bg[:, None, None]).all() and (out["final_T"] == 1).all() and (out["n_contrib"] == 0).all()
+    r.backward(theta, 3, torch.zeros_like(out["image"]), out, theta)
+    torch.cuda.synchronize()
+
+
+def test_all_culled_and_transparent(bgs):
+    s = gen.small_scene(3, 500, 64, 48)
+    seg = gen.segments(s.theta, s.n)
+    seg["opacity_logits"][:] = -100.0
+    cam = s.cameras[0]
+    _, _, out = run_gpu(bgs, s, cam)
+    assert (out["image"].cpu().numpy() == cam.bg[:, None, None]).all()
+    assert (out["n_contrib"] == 0).all()
+    seg["means"][:, 2] = -1.0  # everything behind the camera
+    r, _, out = run_gpu(bgs, s, cam)
+    assert r.num_keys == 0 and (out["final_T"] == 1).all()
+
+
+def test_capacity_overflow_is_reported_and_recovers(bgs):
+    s = scenes()["dense"]()
+    cam = s.cameras[0]
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=1000, device=dev)
+    out = r.forward(theta, cam, s.sh_degree, check=False)
+    torch.cuda.synchronize()
+    st, k = bgs.bgs_frame_status(r.frame)
+    assert st == bgs.BGS_ERR_CAPACITY and k == ref["srt"]["K"]
+    assert (out["image"].cpu().numpy() == cam.bg[:, None, None]).all()  # later stages were no-ops
+    out = r.forward(theta, cam, s.sh_degree)  # grows the workspace and re-runs
+    torch.cuda.synchronize()
+    ok = ref["flags"] == 0
+    assert r.num_keys == ref["srt"]["K"]
+    assert np.abs(out["image"].cpu().numpy() - ref["image"])[:, ok].max() <= IMG_TOL
+
+
+@pytest.mark.parametrize("wh", [(1, 1), (17, 3), (16, 16), (33, 250)])
+def test_odd_image_sizes(bgs, wh):
+    W, H = wh
+    s = gen.small_scene(11, 300, W, H, scale_mu=0.1)
+    cam = s.cameras[0]
+    _, _, out = run_gpu(bgs, s, cam)
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    ok = ref["flags"] == 0
+    assert np.abs(out["image"].cpu().numpy() - ref["image"])[:, ok].max() <= IMG_TOL
+    assert np.array_equal(out["n_contrib"].cpu().numpy().view(np.uint32)[ok], ref["n_contrib"][ok])
+
+
+def test_deterministic_forward(bgs):
+    s = scenes()["ragged"]()
+    cam = s.cameras[0]
+    _, _, a = run_gpu(bgs, s, cam)
+    a = {k: v.clone() for k, v in a.items()}
+    _, _, b = run_gpu(bgs, s, cam)
+    for k in a:
+        assert torch.equal(a[k], b[k]), k
