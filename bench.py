@@ -1,0 +1,516 @@
+#!/usr/bin/env python
+"""bench.py -- BalanceGS hot path (3DGS differentiable tile rasterizer) on B200.
+
+One step = one training iteration over a batch of B = 16 views of the garden-shaped
+5.8M-Gaussian scene (BASELINE.json configs[3]/[4]): for each view preprocess -> sort ->
+blend fwd -> L1 loss grad -> blend bwd -> preprocess bwd (grad +=), then (G > 1) an
+NCCL all-reduce of grad[59N] and the fused Adam step.  The 16 views are split across
+the G ranks (strong scaling: total work per step is fixed).  Every stage runs in
+libbgs.so kernels through the C ABI; torch provides memory, streams and NCCL.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle instead (the
+reference arm of this tier), on a bounded, thinned sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd ms/view & views/s at 1/2/4/8 B200 (garden-shaped 5.8M Gaussians)"
+UNIT = "views/s"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
+FP32_LANES_PER_SM = 128
+
+# Algorithmic work per unit (DESIGN.md §6 restates each):
+OPS_FWD_VISIT = 13      # FP32-pipe lane-ops per visited (pixel, entry) pair
+OPS_FWD_BLEND = 7       # extra lane-ops when the entry is blended (20 total)
+OPS_BWD_EVAL = 57       # lane-ops per evaluated pair in the blend backward
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="garden")
+    p.add_argument("--views", type=int, default=16)
+    p.add_argument("--n", type=int, default=None, help="override the Gaussian count (debug only)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--thin", type=int, default=64, help="oracle sample: every k-th Gaussian")
+    return p.parse_args()
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback"
+
+
+def batch_views(n_views, n_cams):
+    """views 4i mod n_cams for i < n_views."""
+    return [(4 * i) % n_cams for i in range(n_views)]
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[2:]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    import paper_2510_14564_b200 as bgs
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    kw = {} if args.n is None else {"n": args.n}
+    scene = gen.make(args.config, **kw)
+    n = scene.n
+    cams_all = scene.cameras
+    views = batch_views(args.views, len(cams_all))
+    mine = [v for i, v in enumerate(views) if i % world == rank]
+    cams = [cams_all[v] for v in mine]
+    W, H = cams[0].width, cams[0].height
+    theta = torch.from_numpy(scene.theta).to(dev)
+    if world > 1:
+        dist.broadcast(theta, 0)  # replicas start identical
+    grad = torch.zeros_like(theta)
+    m = torch.zeros_like(theta)
+    v = torch.zeros_like(theta)
+    hp = bgs.AdamHParams(lr_means=1.6e-4 * scene.extent)
+    deg = scene.sh_degree
+
+    # size the key capacity once (overflow -> re-run with a larger workspace, R25)
+    rend = bgs.Renderer(n, W, H, max_keys=1 << 24, device=dev)
+    kmax = 0
+    for cam in cams:
+        rend.forward(theta, cam, deg)
+        kmax = max(kmax, rend.num_keys)
+    if int(kmax * 1.1) + 4096 > rend.max_keys:
+        rend.alloc(int(kmax * 1.1) + 4096)
+
+    # targets: a perturbed copy of theta rendered once, 8-bit (R19)
+    r = gen.rng(1234)
+    th_t = scene.theta.copy()
+    seg = gen.segments(th_t, n)
+    seg["sh"][:, 0, :] += 0.05 * r.standard_normal((n, 3)).astype(np.float32)
+    seg["means"][:] += (0.01 * scene.extent * r.standard_normal((n, 3))).astype(np.float32)
+    th_t_dev = torch.from_numpy(th_t).to(dev)
+    targets = []
+    for cam in cams:
+        out = rend.forward(th_t_dev, cam, deg)
+        targets.append((out["image"].clamp(0, 1) * 255 + 0.5).to(torch.uint8).contiguous())
+    del th_t_dev
+    targets_host = [t.cpu().pin_memory() for t in targets]
+    targets_e2e = [torch.empty_like(t) for t in targets]
+    dl = torch.empty((3, H, W), dtype=torch.float32, device=dev)
+    loss = torch.zeros(1, dtype=torch.float32, device=dev)
+    loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+    scale = 1.0 / (3.0 * W * H * args.views)
+    gs = bgs.gaussians(theta, n, deg)
+    cam_structs = [bgs.camera(c) for c in cams]
+    stream = torch.cuda.current_stream()
+    stage_names = ["preprocess", "sort", "render_fwd", "loss", "blend_bwd", "preprocess_bwd", "allreduce", "adam"]
+    ev_pool = {}
+
+    def ev(name, i):
+        key = (name, i)
+        if key not in ev_pool:
+            ev_pool[key] = torch.cuda.Event(enable_timing=True)
+        return ev_pool[key]
+
+    step_no = [0]
+
+    def one_step(tgts, record=None):
+        step_no[0] += 1
+        for j, cs in enumerate(cam_structs):
+            marks = []
+
+            def mark():
+                if record is not None:
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record(stream)
+                    marks.append(e)
+
+            mark()
+            bgs.bgs_preprocess(gs, cs, rend.frame)
+            mark()
+            bgs.bgs_sort(rend.frame)
+            mark()
+            bgs.bgs_render_fwd(rend.frame, rend.image, rend.final_T, rend.n_contrib)
+            mark()
+            bgs.bgs_l1_loss_grad(rend.image, tgts[j], W, H, scale, dl, loss)
+            mark()
+            bgs.bgs_blend_bwd(rend.frame, dl, rend.final_T, rend.n_contrib)
+            mark()
+            bgs.bgs_preprocess_bwd(gs, rend.frame, grad)
+            mark()
+            if record is not None:
+                record.append(("view", marks))
+        marks = []
+        if record is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            marks.append(e)
+        if world > 1:
+            dist.all_reduce(grad)
+        if record is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            marks.append(e)
+        bgs.bgs_adam_step(theta, grad, m, v, n, hp, step_no[0])
+        if record is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            marks.append(e)
+            record.append(("batch", marks))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up
+    for _ in range(args.warmup):
+        one_step(targets)
+    torch.cuda.synchronize()
+
+    # ---- device-resident timed region (inputs larger than L2: theta 1.37 GB, keys GBs)
+    record = []
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = bgs.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        t0.record(stream)
+        for _ in range(args.steps):
+            one_step(targets, record)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = bgs.launch_count() - launches0
+    ms_local = t0.elapsed_time(t1)
+    st, k_last = bgs.bgs_frame_status(rend.frame)
+    assert st == bgs.BGS_OK, "key capacity overflow in the timed region"
+    # per-stage means
+    sums = {s: 0.0 for s in stage_names}
+    for kind, mk in record:
+        if kind == "view":
+            for s, a, b in zip(stage_names[:6], mk[:-1], mk[1:]):
+                sums[s] += a.elapsed_time(b)
+        else:
+            sums["allreduce"] += mk[0].elapsed_time(mk[1])
+            sums["adam"] += mk[1].elapsed_time(mk[2])
+    per_step = {s: sums[s] / args.steps for s in stage_names}
+    launches_per_stage = {"render_fwd": 1, "blend_bwd": 1, "preprocess_bwd": 1, "adam": 1}
+
+    # ---- end-to-end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        def e2e_step():
+            for j in range(len(cams)):
+                targets_e2e[j].copy_(targets_host[j], non_blocking=True)
+            one_step(targets_e2e)
+            loss_host.copy_(loss, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": args.views * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(sum(t.numel() for t in targets_host)) * (world if world > 1 else 1),
+               "d2h_bytes_per_step": 4 * world}
+
+    # ---- workload counters (not timed) for the roofline numerators
+    stats = {"visible": 0, "num_keys": 0, "evals_fwd": 0, "evals_bwd": 0, "evals_slot": 0, "max_list": 0,
+             "blended": 0}
+    for cam, cs in zip(cams, cam_structs):
+        bgs.bgs_preprocess(gs, cs, rend.frame)
+        bgs.bgs_sort(rend.frame)
+        bgs.bgs_render_fwd(rend.frame, rend.image, rend.final_T, rend.n_contrib)
+        s = bgs.bgs_frame_stats(rend.frame, rend.n_contrib)
+        for k2 in stats:
+            if k2 == "max_list":
+                stats[k2] = max(stats[k2], s.get(k2, 0))
+            else:
+                stats[k2] += s.get(k2, 0)
+
+    # ---- max over ranks
+    t = torch.tensor([ms_local], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        for key in ("visible", "num_keys", "evals_fwd", "evals_bwd", "evals_slot", "blended"):
+            tt = torch.tensor([stats[key]], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt)
+            stats[key] = int(tt.item())
+    ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = args.views / (ms_step / 1e3)
+
+    if rank != 0:
+        return
+    peaks, peaks_src = load_peaks()
+    clocks = clk.summary()
+    sm_mhz_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * FP32_LANES_PER_SM * sm_mhz_max * 1e6 / 1e12  # T lane-ops/s
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    K = stats["num_keys"] / len(cams) if cams else 0
+    steps_views = len(cams)  # views per step on rank 0
+    p = 6 if True else None
+    roof = {}
+    # per-view per-launch numerators (rank 0's views)
+    V = stats["visible"] / steps_views
+    Ef, Eb, Ebl = (stats["evals_fwd"] / steps_views, stats["evals_bwd"] / steps_views,
+                   stats["blended"] / steps_views)
+    frame_v = rend.views()
+    passes = frame_v.sort_passes
+
+    def frac(stage, achieved, peak, unit, bound):
+        roof[stage] = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                       "frac": achieved / peak if peak else None, "ms_per_launch": per_step[stage] / steps_views}
+
+    def per_launch(stage):
+        return per_step[stage] / steps_views / 1e3  # seconds
+
+    frac("preprocess", (16 * n + 268 * V) / per_launch("preprocess") / 1e9, hbm, "GB/s", "hbm")
+    frac("sort", ((12 + 8 + 24 * passes + 8) * K + 20 * V) / per_launch("sort") / 1e9, hbm, "GB/s", "hbm")
+    frac("render_fwd", (OPS_FWD_VISIT * Ef + OPS_FWD_BLEND * Ebl) / per_launch("render_fwd") / 1e12, fp32_peak,
+         "T lane-ops/s", "alu")
+    frac("blend_bwd", OPS_BWD_EVAL * Eb / per_launch("blend_bwd") / 1e12, fp32_peak, "T lane-ops/s", "alu")
+    frac("preprocess_bwd", 744 * V / per_launch("preprocess_bwd") / 1e9, hbm, "GB/s", "hbm")
+    roof["adam"] = {"bound": "hbm", "achieved": 1888 * n / (per_step["adam"] / 1e3) / 1e9, "peak": hbm,
+                    "unit": "GB/s", "ms_per_launch": per_step["adam"]}
+    roof["adam"]["frac"] = roof["adam"]["achieved"] / hbm
+    dom = max((s for s in roof), key=lambda s: per_step[s])
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(dom)
+    except Exception:
+        pass
+    d = roof[dom]
+    roofline = {"bound": d["bound"], "achieved": round(d["achieved"], 3), "peak": round(d["peak"], 3),
+                "unit": d["unit"], "frac": round(d["frac"], 4), "traffic": traffic, "kernel": dom,
+                "peak_source": f"{peaks_src} (FP32: 148 SMs x 128 lanes x {sm_mhz_max:.0f} MHz)"
+                if d["bound"] == "alu" else f"{peaks_src} MEASURED_PEAKS.json hbm_gbs"}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args)
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "ms_per_view": round(ms_step / args.views, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded garden-shaped scene, gen/; random-init parameters; targets = render of a "
+                "perturbed copy)",
+        "config": {"workload": f"{scene.name}-shaped {n} Gaussians, {W}x{H}, SH degree {deg}, batch of "
+                               f"{args.views} views per step (fwd+bwd each, then all-reduce + Adam)",
+                   "views_per_step": args.views, "n_gaussians": n, "width": W, "height": H,
+                   "parallelism": f"view-dp{world}", "l2": "inputs larger than L2 (theta 1.37 GB, keys > 126 MB)",
+                   "max_keys": rend.max_keys},
+        "clocks": clocks, "gpu_launches": int(launches), "roofline": roofline,
+        "stages_ms_per_step": {k2: round(v2, 4) for k2, v2 in per_step.items()},
+        "stages_roofline": {k2: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v2.items()}
+                            for k2, v2 in roof.items()},
+        "workload": {"V_per_view": V, "K_per_view": K, "E_f_per_view": Ef, "E_b_per_view": Eb,
+                     "blended_per_view": Ebl, "E_slot_over_E_f": stats["evals_slot"] / max(1, stats["evals_fwd"]),
+                     "max_tile_list": stats["max_list"]},
+        "e2e": e2e, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------- oracle
+def _thinned(args):
+    import gen
+
+    scene = gen.make(args.config)
+    n = scene.n
+    keep = np.arange(0, n, args.thin)
+    seg = gen.segments(scene.theta, n)
+    th = gen.pack(seg["means"][keep], seg["log_scales"][keep], seg["quats"][keep], seg["opacity_logits"][keep],
+                  seg["sh"][keep])
+    return scene, th, len(keep)
+
+
+def _oracle_view(th, n, deg, cam, dl):
+    import oracle
+
+    f = oracle.forward(th, n, deg, cam)
+    b = oracle.backward(th, n, deg, cam, f, dl)
+    return b
+
+
+def cpu_baseline(args):
+    """The oracle as it stands (single thread) on a bounded sample: one view of the scene
+    thinned to every `thin`-th Gaussian, full preprocess -> sort -> fwd -> bwd; the view
+    time is scaled by `thin` to the full scene (assumes cost linear in N)."""
+    import gen
+
+    scene, th, ns = _thinned(args)
+    cam = scene.cameras[0]
+    dl = gen.random_dl_dimage(0, cam.width, cam.height, scale=1e-6)
+    t = time.perf_counter()
+    _oracle_view(th, ns, scene.sh_degree, cam, dl)
+    sec = time.perf_counter() - t
+    return {"value": round(1.0 / (sec * args.thin), 6), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"1 view (camera 0) of the {scene.name} scene thinned to every {args.thin}th Gaussian "
+                      f"({ns} of {scene.n}); oracle fwd+bwd took {sec:.2f} s on 1 core; scaled x{args.thin} to "
+                      f"the full scene (cost assumed linear in N)", "cpu": _cpu_model()}
+
+
+def _cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical cores on host)"
+    except Exception:
+        pass
+    return f"{os.cpu_count()} logical cores"
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    import gen
+    import oracle
+
+    scene, th, ns = _thinned(args)
+    cams = [scene.cameras[v] for v in batch_views(args.views, len(scene.cameras))]
+    deg = scene.sh_degree
+    cam0 = cams[0]
+    dl = gen.random_dl_dimage(0, cam0.width, cam0.height, scale=1e-6)
+    m = np.zeros(59 * ns)
+    vv = np.zeros(59 * ns)
+    thd = th.astype(np.float64)
+    lr6 = [1.6e-4 * scene.extent, 5e-3, 1e-3, 0.05, 2.5e-3, 1.25e-4]
+
+    def step(i):
+        cam = cams[i % len(cams)]
+        b = _oracle_view(th, ns, deg, cam, dl)
+        return oracle.adam(thd, b["grad"], m, vv, ns, lr6, step=i + 1)
+
+    for i in range(args.warmup):
+        step(i)
+    t = time.perf_counter()
+    for i in range(args.steps):
+        step(i)
+    sec = (time.perf_counter() - t) / args.steps
+    value = 1.0 / (sec * args.thin)
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3 * args.thin, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32",
+            "data": "synthetic", "config": {"workload": f"{scene.name}-shaped scene, oracle on a 1/{args.thin} "
+                                                        f"thinned sample, 1 view + Adam per step"},
+            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"each step: 1 view of the scene thinned to every {args.thin}th Gaussian "
+                                       f"({ns} of {scene.n}), fwd+bwd+Adam, scaled x{args.thin}",
+                             "cpu": _cpu_model()},
+            "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -114,6 +114,7 @@ typedef struct {
   int64_t evals_bwd;    /* E_b: sum over pixels of n_contrib                  */
   int64_t evals_slot;   /* E_slot: sum over warps of 32 * max_lane(visits)    */
   int64_t max_list;     /* longest tile list                                  */
+  int64_t blended;      /* (pixel, Gaussian) pairs blended in the forward      */
 } bgs_stats;
 
 /* ---------------------------------------------------------------- sizing */
@@ -154,6 +155,12 @@ bgs_status bgs_render_fwd(bgs_frame* f /*host*/, float* image, float* final_T, u
  * theta's layout (the sum over views, R20).  dL_dimage is planar [3][h][w]. */
 bgs_status bgs_render_bwd(const bgs_gaussians* g /*host*/, bgs_frame* f /*host*/, const float* dL_dimage,
                           const float* final_T, const uint32_t* n_contrib, float* grad, void* stream);
+/* The two halves of bgs_render_bwd, for per-stage timing: a9 accumulates the per-view
+ * blend gradients {dxy, dconic, dopacity, drgb} into the frame's grad2d; a10 applies the
+ * chain rule to theta's layout (grad +=).  bgs_render_bwd == blend_bwd then preprocess_bwd. */
+bgs_status bgs_blend_bwd(bgs_frame* f /*host*/, const float* dL_dimage, const float* final_T,
+                         const uint32_t* n_contrib, void* stream);
+bgs_status bgs_preprocess_bwd(const bgs_gaussians* g /*host*/, bgs_frame* f /*host*/, float* grad, void* stream);
 
 /* a11: fused Adam over theta[59n] (R21, PyTorch semantics: bias-corrected, eps after
  * sqrt), per-group learning rate, grad zeroed on exit.  step is 1-based. */

@@ -28,9 +28,13 @@ PLAIN = 127
 CB_R, CB_G, CB_B, CB_JX, CB_JX_NEG, CB_JY, CB_JY_NEG = 1, 2, 4, 8, 16, 32, 64
 
 # R23 near-tie margins: relative distance of a decision input
-# to its threshold under which a pixel is flagged.
-DELTA_ALPHA = 2.0 ** -14
-DELTA_T = 2.0 ** -9
+# to its threshold under which a pixel is flagged.  The GPU's G = ex2.approx(power*log2e)
+# differs from exp(power) by <= 2^-20.5 relative for |power| <= 5.6 (log2e product rounding
+# 8*2^-24 plus ex2.approx's ~2^-22); DELTA_ALPHA leaves a 4x margin over that.  T is a
+# product of (1 - alpha) factors, each relative error <= 99 * 2^-20.5 (alpha < 0.99
+# unclamped), so DELTA_T = 2^-11 covers several such factors.
+DELTA_ALPHA = 2.0 ** -18
+DELTA_T = 2.0 ** -11
 
 CFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
 

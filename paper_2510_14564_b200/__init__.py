@@ -69,7 +69,8 @@ class FrameViews(C.Structure):
 
 class Stats(C.Structure):
     _fields_ = [("visible", C.c_int64), ("num_keys", C.c_int64), ("evals_fwd", C.c_int64),
-                ("evals_bwd", C.c_int64), ("evals_slot", C.c_int64), ("max_list", C.c_int64)]
+                ("evals_bwd", C.c_int64), ("evals_slot", C.c_int64), ("max_list", C.c_int64),
+                ("blended", C.c_int64)]
 
 
 _P = C.c_void_p
@@ -80,6 +81,8 @@ _SIGS = {
     "bgs_sort": (C.c_int, [C.POINTER(Frame), _P]),
     "bgs_render_fwd": (C.c_int, [C.POINTER(Frame), _P, _P, _P, _P]),
     "bgs_render_bwd": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Frame), _P, _P, _P, _P, _P]),
+    "bgs_blend_bwd": (C.c_int, [C.POINTER(Frame), _P, _P, _P, _P]),
+    "bgs_preprocess_bwd": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Frame), _P, _P]),
     "bgs_adam_step": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(AdamHParams), C.c_int64, _P]),
     "bgs_l1_loss_grad": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_float, _P, _P, _P]),
     "bgs_frame_status": (C.c_int, [C.POINTER(Frame), C.POINTER(C.c_int64)]),
@@ -163,6 +166,15 @@ def bgs_render_fwd(frame: Frame, image, final_T, n_contrib, stream=None):
 def bgs_render_bwd(g: Gaussians, frame: Frame, dl_dimage, final_T, n_contrib, grad, stream=None):
     _check(_lib.bgs_render_bwd(C.byref(g), C.byref(frame), _ptr(dl_dimage), _ptr(final_T), _ptr(n_contrib),
                                _ptr(grad), _stream(stream)), "bgs_render_bwd")
+
+
+def bgs_blend_bwd(frame: Frame, dl_dimage, final_T, n_contrib, stream=None):
+    _check(_lib.bgs_blend_bwd(C.byref(frame), _ptr(dl_dimage), _ptr(final_T), _ptr(n_contrib), _stream(stream)),
+           "bgs_blend_bwd")
+
+
+def bgs_preprocess_bwd(g: Gaussians, frame: Frame, grad, stream=None):
+    _check(_lib.bgs_preprocess_bwd(C.byref(g), C.byref(frame), _ptr(grad), _stream(stream)), "bgs_preprocess_bwd")
 
 
 def bgs_adam_step(theta, grad, exp_avg, exp_avg_sq, n, hp: AdamHParams, step: int, stream=None):

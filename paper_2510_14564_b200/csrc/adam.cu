@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kTilePixels) k_stats(const uint2* __restrict__
   const bool inside = px < cam.W && py < cam.H;
   uint2 rg = ranges[tile];
   if (counters[C_OVERFLOW]) rg = make_uint2(0, 0);
-  uint32_t walked = 0, nc = 0;
+  uint32_t walked = 0, nc = 0, blended = 0;
   if (inside) {
     nc = n_contrib[(int64_t)py * cam.W + px];
     float T = 1.0f;
@@ -170,19 +170,22 @@ __global__ void __launch_bounds__(kTilePixels) k_stats(const uint2* __restrict__
       const float tT = T * (1.0f - alpha);
       if (tT < 1e-4f) break;
       T = tT;
+      ++blended;
     }
   }
   const uint32_t wmax = __reduce_max_sync(0xffffffffu, walked);
-  unsigned long long f = walked, b = nc;
+  unsigned long long f = walked, b = nc, bl = blended;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     f += __shfl_xor_sync(0xffffffffu, f, o);
     b += __shfl_xor_sync(0xffffffffu, b, o);
+    bl += __shfl_xor_sync(0xffffffffu, bl, o);
   }
   if ((threadIdx.x & 31) == 0) {
     atomicAdd(&out[0], f);
     atomicAdd(&out[1], b);
     atomicAdd(&out[2], 32ull * wmax);
+    atomicAdd(&out[5], bl);
   }
   if (threadIdx.x == 0) atomicMax(&out[3], (unsigned long long)(rg.y - rg.x));
 }
@@ -212,6 +215,7 @@ bgs_status launch_stats(const Frame* F, const uint32_t* n_contrib, bgs_stats* ou
   out->evals_slot = (int64_t)h[2];
   out->max_list = (int64_t)h[3];
   out->visible = (int64_t)h[4];
+  out->blended = (int64_t)h[5];
   out->num_keys = (int64_t)(((uint64_t)c[1] << 32) | c[0]);
   return check_launch("k_stats");
 }

@@ -73,6 +73,9 @@ void set_error(const char* msg);
 bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s);
 bgs_status launch_sort(Frame* F, cudaStream_t s);
 bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n_contrib, cudaStream_t s);
+bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
+                            cudaStream_t s);
+bgs_status launch_preprocess_bwd(const bgs_gaussians* g, Frame* F, float* grad, cudaStream_t s);
 bgs_status launch_render_bwd(const bgs_gaussians* g, Frame* F, const float* dL_dimage, const float* final_T,
                              const uint32_t* n_contrib, float* grad, cudaStream_t s);
 bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, const bgs_adam_hparams* hp,

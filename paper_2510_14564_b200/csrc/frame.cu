@@ -237,6 +237,21 @@ bgs_status bgs_render_bwd(const bgs_gaussians* g, bgs_frame* f, const float* dL_
   return launch_render_bwd(g, F, dL_dimage, final_T, n_contrib, grad, (cudaStream_t)stream);
 }
 
+bgs_status bgs_blend_bwd(bgs_frame* f, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
+                         void* stream) {
+  if (!frame_ok(f) || !frame_of(f)->cam_valid || !dL_dimage || !final_T || !n_contrib) return BGS_ERR_INVALID;
+  return launch_blend_bwd(frame_of(f), dL_dimage, final_T, n_contrib, (cudaStream_t)stream);
+}
+
+bgs_status bgs_preprocess_bwd(const bgs_gaussians* g, bgs_frame* f, float* grad, void* stream) {
+  if (!frame_ok(f) || !frame_of(f)->cam_valid) return BGS_ERR_INVALID;
+  Frame* F = frame_of(f);
+  bgs_status st = validate_gaussians(g, F);
+  if (st != BGS_OK) return st;
+  if (F->n > 0 && (!grad || !aligned16(grad))) return BGS_ERR_INVALID;
+  return launch_preprocess_bwd(g, F, grad, (cudaStream_t)stream);
+}
+
 bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
                          const bgs_adam_hparams* hp, int64_t step, void* stream) {
   if (n < 0 || !hp || step < 1) return BGS_ERR_INVALID;

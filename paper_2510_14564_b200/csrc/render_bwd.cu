@@ -376,13 +376,16 @@ __global__ void __launch_bounds__(128) k_preprocess_bwd(PreBwdParams p) {
   gq[3] += (gz_ - z * qd) * iq;
 }
 
-bgs_status launch_render_bwd(const bgs_gaussians* g, Frame* F, const float* dL_dimage, const float* final_T,
-                             const uint32_t* n_contrib, float* grad, cudaStream_t s) {
+bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
+                            cudaStream_t s) {
   k_render_bwd<<<F->num_tiles, kTilePixels, 0, s>>>(F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam,
                                                     dL_dimage, final_T, n_contrib, F->grad2d);
   note_launch();
-  bgs_status st = check_launch("k_render_bwd");
-  if (st != BGS_OK || F->n == 0) return st;
+  return check_launch("k_render_bwd");
+}
+
+bgs_status launch_preprocess_bwd(const bgs_gaussians* g, Frame* F, float* grad, cudaStream_t s) {
+  if (F->n == 0) return BGS_OK;
   PreBwdParams p;
   p.cam = F->cam;
   p.means = g->means;
@@ -399,6 +402,12 @@ bgs_status launch_render_bwd(const bgs_gaussians* g, Frame* F, const float* dL_d
   k_preprocess_bwd<<<(unsigned)((F->n + 127) / 128), 128, 0, s>>>(p);
   note_launch();
   return check_launch("k_preprocess_bwd");
+}
+
+bgs_status launch_render_bwd(const bgs_gaussians* g, Frame* F, const float* dL_dimage, const float* final_T,
+                             const uint32_t* n_contrib, float* grad, cudaStream_t s) {
+  bgs_status st = launch_blend_bwd(F, dL_dimage, final_T, n_contrib, s);
+  return st != BGS_OK ? st : launch_preprocess_bwd(g, F, grad, s);
 }
 
 }  // namespace bgs

@@ -63,7 +63,7 @@ class _DevPtr:
     """Zero-copy view of a workspace region through __cuda_array_interface__."""
 
     def __init__(self, ptr, count, typestr):
-        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (int(ptr), True),
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (int(ptr), False),
                                          "version": 2}
 
 
@@ -156,17 +156,25 @@ def test_render_fwd_parity(bgs, name):
     assert np.abs(img - ref["image"]).max() <= 2e-2
 
 
+def masked_dl(seed, cam, ref, scale=1.0):
+    """Seeded dL/dimage, zero on the pixels the oracle flags as near ties (R23): the
+    backward is compared where both sides took the same forward decisions."""
+    dl = gen.random_dl_dimage(seed, cam.width, cam.height, scale=scale)
+    dl[:, ref["flags"] != 0] = 0.0
+    return dl
+
+
 @pytest.mark.parametrize("name", list(scenes()))
 def test_render_bwd_parity(bgs, name):
     s = scenes()[name]()
     cam = s.cameras[0]
     r, theta, out = run_gpu(bgs, s, cam)
-    dl_np = gen.random_dl_dimage(3, cam.width, cam.height)
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    dl_np = masked_dl(3, cam, ref)
     dl = torch.from_numpy(dl_np).cuda()
     grad = torch.zeros_like(theta)
     r.backward(theta, s.sh_degree, dl, out, grad)
     torch.cuda.synchronize()
-    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
     g_ref = oracle.backward(s.theta, s.n, s.sh_degree, cam, ref, dl_np)["grad"]
     g = grad.cpu().numpy().astype(np.float64)
     for gname, idx in oracle.group_slices(s.n).items():
@@ -189,9 +197,9 @@ def test_multi_view_gradients_accumulate(bgs):
     g_ref = np.zeros(59 * s.n)
     for i, cam in enumerate(cams[:2]):
         out = r.forward(theta, cam, 3)
-        dl_np = gen.random_dl_dimage(20 + i, cam.width, cam.height, scale=1e-3)
-        r.backward(theta, 3, torch.from_numpy(dl_np).to(dev), out, grad)
         ref = oracle.forward(s.theta, s.n, 3, cam)
+        dl_np = masked_dl(20 + i, cam, ref, scale=1e-3)
+        r.backward(theta, 3, torch.from_numpy(dl_np).to(dev), out, grad)
         g_ref += oracle.backward(s.theta, s.n, 3, cam, ref, dl_np)["grad"]
     torch.cuda.synchronize()
     g = grad.cpu().numpy().astype(np.float64)
@@ -214,9 +222,14 @@ def test_adam_parity(bgs):
     torch.cuda.synchronize()
     th_ref, m_ref, v_ref = oracle.adam(th, g, m, v, n, lr6, b1=float(np.float32(0.9)),
                                        b2=float(np.float32(0.999)), eps=float(np.float32(1e-15)), step=7)
-    np.testing.assert_allclose(T["m"].cpu().numpy(), m_ref, rtol=1e-6, atol=1e-12)
-    np.testing.assert_allclose(T["v"].cpu().numpy(), v_ref, rtol=1e-6, atol=1e-14)
-    np.testing.assert_allclose(T["th"].cpu().numpy(), th_ref, rtol=1e-6, atol=1e-7)
+    # 1e-6 relative to the magnitude of the terms each update adds (m and v are sums that
+    # can cancel; theta moves by lr-sized steps)
+    b1, b2 = 0.9, 0.999
+    tm = 1e-6 * (b1 * np.abs(m) + (1 - b1) * np.abs(g)) + 1e-30
+    tv = 1e-6 * (b2 * v + (1 - b2) * g.astype(np.float64) ** 2) + 1e-30
+    assert (np.abs(T["m"].cpu().numpy() - m_ref) <= tm).all()
+    assert (np.abs(T["v"].cpu().numpy() - v_ref) <= tv).all()
+    np.testing.assert_allclose(T["th"].cpu().numpy(), th_ref, rtol=1e-6, atol=1e-6 * max(lr6))
     assert not T["g"].any()
 
 
