@@ -48,7 +48,8 @@ typedef enum {
 #define BGS_FLOATS_PER_GAUSSIAN 59
 #define BGS_MAX_KEYS_LIMIT ((int64_t)1 << 30)
 
-/* Views into theta[59n] (caller-owned, each segment 16-byte aligned):
+/* Views into theta[59n] (caller-owned; segments 4-byte aligned, 16-byte aligned ones take
+ * the vector load paths -- one contiguous buffer with n % 4 == 0 is fully aligned):
  *   [means 3n | log_scales 3n | quats 4n (w,x,y,z) | opacity_logits n | sh 48n ([n][16][3], k = 0 is DC)]
  * Raw optimiser parameters; exp / normalise / sigmoid are fused (R5).  The
  * primitive is G(x) = exp(-1/2 (x-mu)^T Sigma^-1 (x-mu)) with Sigma = R S S^T R^T

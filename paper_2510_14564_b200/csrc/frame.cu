@@ -132,8 +132,10 @@ static bgs_status validate_gaussians(const bgs_gaussians* g, const Frame* F) {
   if (!g || g->n != F->n || g->sh_degree < 0 || g->sh_degree > 3) return BGS_ERR_INVALID;
   if (g->n > 0) {
     if (!g->means || !g->log_scales || !g->quats || !g->opacity_logits || !g->sh) return BGS_ERR_INVALID;
-    if (!aligned16(g->quats) || !aligned16(g->sh) || !aligned16(g->means) || !aligned16(g->log_scales) ||
-        !aligned16(g->opacity_logits))
+    // 4-byte alignment suffices; kernels take their 16-byte vector paths when the
+    // segment pointers allow it (any n with one contiguous theta buffer works)
+    auto a4 = [](const void* q) { return ((uintptr_t)q & 3u) == 0; };
+    if (!a4(g->quats) || !a4(g->sh) || !a4(g->means) || !a4(g->log_scales) || !a4(g->opacity_logits))
       return BGS_ERR_INVALID;
   }
   return BGS_OK;
@@ -233,7 +235,7 @@ bgs_status bgs_render_bwd(const bgs_gaussians* g, bgs_frame* f, const float* dL_
   Frame* F = frame_of(f);
   bgs_status st = validate_gaussians(g, F);
   if (st != BGS_OK) return st;
-  if (F->n > 0 && (!grad || !aligned16(grad))) return BGS_ERR_INVALID;
+  if (F->n > 0 && (!grad || ((uintptr_t)grad & 3u))) return BGS_ERR_INVALID;
   return launch_render_bwd(g, F, dL_dimage, final_T, n_contrib, grad, (cudaStream_t)stream);
 }
 
@@ -248,7 +250,7 @@ bgs_status bgs_preprocess_bwd(const bgs_gaussians* g, bgs_frame* f, float* grad,
   Frame* F = frame_of(f);
   bgs_status st = validate_gaussians(g, F);
   if (st != BGS_OK) return st;
-  if (F->n > 0 && (!grad || !aligned16(grad))) return BGS_ERR_INVALID;
+  if (F->n > 0 && (!grad || ((uintptr_t)grad & 3u))) return BGS_ERR_INVALID;
   return launch_preprocess_bwd(g, F, grad, (cudaStream_t)stream);
 }
 

@@ -28,11 +28,12 @@ struct PreParams {
   Cam cam;
   const float* means;
   const float* log_scales;
-  const float4* quats;
+  const float* quats;
   const float* ologits;
-  const float4* sh;  // [n][12] float4
+  const float* sh;  // [n][16][3]
   int64_t n;
   int32_t deg;
+  bool quat_vec4, sh_vec4;  // 16-byte aligned segments -> vector loads
   int32_t* radius;
   float* depth;
   float4* record;
@@ -64,7 +65,12 @@ __global__ void __launch_bounds__(256) k_preprocess(PreParams p) {
   const float s1 = (float)exp((double)p.log_scales[3 * i + 1]);
   const float s2 = (float)exp((double)p.log_scales[3 * i + 2]);
   const float o = (float)(1.0 / (1.0 + exp(-(double)p.ologits[i])));
-  float4 q = p.quats[i];
+  float4 q;
+  if (p.quat_vec4) {
+    q = __ldg(reinterpret_cast<const float4*>(p.quats) + i);
+  } else {
+    q = make_float4(p.quats[4 * i], p.quats[4 * i + 1], p.quats[4 * i + 2], p.quats[4 * i + 3]);
+  }
   const float n2 = fmaf(q.x, q.x, fmaf(q.y, q.y, fmaf(q.z, q.z, q.w * q.w)));
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(n2));
   const float qw = q.x * inv, qx = q.y * inv, qy = q.z * inv, qz = q.w * inv;
@@ -130,12 +136,17 @@ __global__ void __launch_bounds__(256) k_preprocess(PreParams p) {
   const float dxw = mx - c.campos[0], dyw = my - c.campos[1], dzw = mz - c.campos[2];
   const float il = rsqrtf(dxw * dxw + dyw * dyw + dzw * dzw);
   const float x = dxw * il, y = dyw * il, z = dzw * il;
-  const float4* shp = p.sh + 12 * i;
   float sh[48];
+  if (p.sh_vec4) {
+    const float4* shp = reinterpret_cast<const float4*>(p.sh) + 12 * i;
 #pragma unroll
-  for (int k = 0; k < 12; ++k) {
-    const float4 f4 = __ldg(shp + k);
-    sh[4 * k] = f4.x; sh[4 * k + 1] = f4.y; sh[4 * k + 2] = f4.z; sh[4 * k + 3] = f4.w;
+    for (int k = 0; k < 12; ++k) {
+      const float4 f4 = __ldg(shp + k);
+      sh[4 * k] = f4.x; sh[4 * k + 1] = f4.y; sh[4 * k + 2] = f4.z; sh[4 * k + 3] = f4.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < 48; ++k) sh[k] = __ldg(p.sh + 48 * i + k);
   }
   float rgb[3];
 #pragma unroll
@@ -279,9 +290,11 @@ bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
   p.cam = F->cam;
   p.means = g->means;
   p.log_scales = g->log_scales;
-  p.quats = (const float4*)g->quats;
+  p.quats = g->quats;
   p.ologits = g->opacity_logits;
-  p.sh = (const float4*)g->sh;
+  p.sh = g->sh;
+  p.quat_vec4 = ((uintptr_t)g->quats & 15u) == 0;
+  p.sh_vec4 = ((uintptr_t)g->sh & 15u) == 0;
   p.n = F->n;
   p.deg = g->sh_degree;
   p.radius = F->radius;
