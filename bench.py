@@ -303,7 +303,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- workload counters (not timed) for the roofline numerators
     stats = {"visible": 0, "num_keys": 0, "evals_fwd": 0, "evals_bwd": 0, "evals_slot": 0, "max_list": 0,
-             "blended": 0}
+             "blended": 0, "evals_fwd_culled": 0, "evals_bwd_culled": 0}
     for cam, cs in zip(cams, cam_structs):
         bgs.bgs_preprocess(gs, cs, rend.frame)
         bgs.bgs_sort(rend.frame)
@@ -319,7 +319,8 @@ def run_ours(args, rank, world, local_rank):
     t = torch.tensor([ms_local], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        for key in ("visible", "num_keys", "evals_fwd", "evals_bwd", "evals_slot", "blended"):
+        for key in ("visible", "num_keys", "evals_fwd", "evals_bwd", "evals_slot", "blended", "evals_fwd_culled",
+                    "evals_bwd_culled"):
             tt = torch.tensor([stats[key]], device=dev, dtype=torch.float64)
             dist.all_reduce(tt)
             stats[key] = int(tt.item())
@@ -336,12 +337,14 @@ def run_ours(args, rank, world, local_rank):
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     K = stats["num_keys"] / len(cams) if cams else 0
     steps_views = len(cams)  # views per step on rank 0
-    p = 6 if True else None
     roof = {}
     # per-view per-launch numerators (rank 0's views)
     V = stats["visible"] / steps_views
     Ef, Eb, Ebl = (stats["evals_fwd"] / steps_views, stats["evals_bwd"] / steps_views,
                    stats["blended"] / steps_views)
+    # what the blend kernels must evaluate: list entries whose alpha >= 1/255 box reaches the
+    # pixel's warp block (exact skip of the rest)
+    Efc, Ebc = stats["evals_fwd_culled"] / steps_views, stats["evals_bwd_culled"] / steps_views
     frame_v = rend.views()
     passes = frame_v.sort_passes
 
@@ -354,9 +357,9 @@ def run_ours(args, rank, world, local_rank):
 
     frac("preprocess", (16 * n + 268 * V) / per_launch("preprocess") / 1e9, hbm, "GB/s", "hbm")
     frac("sort", ((12 + 8 + 24 * passes + 8) * K + 20 * V) / per_launch("sort") / 1e9, hbm, "GB/s", "hbm")
-    frac("render_fwd", (OPS_FWD_VISIT * Ef + OPS_FWD_BLEND * Ebl) / per_launch("render_fwd") / 1e12, fp32_peak,
+    frac("render_fwd", (OPS_FWD_VISIT * Efc + OPS_FWD_BLEND * Ebl) / per_launch("render_fwd") / 1e12, fp32_peak,
          "T lane-ops/s", "alu")
-    frac("blend_bwd", OPS_BWD_EVAL * Eb / per_launch("blend_bwd") / 1e12, fp32_peak, "T lane-ops/s", "alu")
+    frac("blend_bwd", OPS_BWD_EVAL * Ebc / per_launch("blend_bwd") / 1e12, fp32_peak, "T lane-ops/s", "alu")
     frac("preprocess_bwd", 744 * V / per_launch("preprocess_bwd") / 1e9, hbm, "GB/s", "hbm")
     roof["adam"] = {"bound": "hbm", "achieved": 1888 * n / (per_step["adam"] / 1e3) / 1e9, "peak": hbm,
                     "unit": "GB/s", "ms_per_launch": per_step["adam"]}
@@ -392,7 +395,8 @@ def run_ours(args, rank, world, local_rank):
         "stages_roofline": {k2: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v2.items()}
                             for k2, v2 in roof.items()},
         "workload": {"V_per_view": V, "K_per_view": K, "E_f_per_view": Ef, "E_b_per_view": Eb,
-                     "blended_per_view": Ebl, "E_slot_over_E_f": stats["evals_slot"] / max(1, stats["evals_fwd"]),
+                     "E_f_culled_per_view": Efc, "E_b_culled_per_view": Ebc, "blended_per_view": Ebl,
+                     "E_slot_over_E_f_culled": stats["evals_slot"] / max(1, stats["evals_fwd_culled"]),
                      "max_tile_list": stats["max_list"]},
         "e2e": e2e, "cpu_baseline": cpu,
     }

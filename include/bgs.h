@@ -113,9 +113,12 @@ typedef struct {
   int64_t num_keys;     /* K                                                  */
   int64_t evals_fwd;    /* E_f: (pixel, list entry) pairs the forward visits  */
   int64_t evals_bwd;    /* E_b: sum over pixels of n_contrib                  */
-  int64_t evals_slot;   /* E_slot: sum over warps of 32 * max_lane(visits)    */
+  int64_t evals_slot;   /* E_slot: sum over 8x4-pixel warps of 32 * max_lane(culled visits) */
   int64_t max_list;     /* longest tile list                                  */
   int64_t blended;      /* (pixel, Gaussian) pairs blended in the forward      */
+  int64_t evals_fwd_culled; /* E_f restricted to entries whose alpha level-set box
+                               reaches the pixel's 8x4 warp block (what the fwd evaluates) */
+  int64_t evals_bwd_culled; /* the same for the backward (positions < n_contrib) */
 } bgs_stats;
 
 /* ---------------------------------------------------------------- sizing */

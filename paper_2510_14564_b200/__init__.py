@@ -70,7 +70,7 @@ class FrameViews(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("visible", C.c_int64), ("num_keys", C.c_int64), ("evals_fwd", C.c_int64),
                 ("evals_bwd", C.c_int64), ("evals_slot", C.c_int64), ("max_list", C.c_int64),
-                ("blended", C.c_int64)]
+                ("blended", C.c_int64), ("evals_fwd_culled", C.c_int64), ("evals_bwd_culled", C.c_int64)]
 
 
 _P = C.c_void_p

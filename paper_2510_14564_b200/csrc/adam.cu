@@ -150,18 +150,25 @@ __global__ void __launch_bounds__(kTilePixels) k_stats(const uint2* __restrict__
                                                        unsigned long long* out) {
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-  const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // the blend kernels' mapping: warp w owns an 8x4 pixel block
+  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7), py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const float bx0 = (float)(tx * kTile + (warp & 1) * 8), by0 = (float)(ty * kTile + (warp >> 1) * 4);
+  const float bx1 = bx0 + 7.0f, by1 = by0 + 3.0f;
   const bool inside = px < cam.W && py < cam.H;
   uint2 rg = ranges[tile];
   if (counters[C_OVERFLOW]) rg = make_uint2(0, 0);
-  uint32_t walked = 0, nc = 0, blended = 0;
+  uint32_t walked = 0, nc = 0, blended = 0, walked_c = 0, bwd_c = 0;
   if (inside) {
     nc = n_contrib[(int64_t)py * cam.W + px];
     float T = 1.0f;
     for (uint32_t j = rg.x; j < rg.y; ++j) {
       ++walked;
       const uint32_t id = values[j];
-      const float4 r0 = record[3 * id], r1 = record[3 * id + 1];
+      const float4 r0 = record[3 * id], r1 = record[3 * id + 1], r2 = record[3 * id + 2];
+      const bool hit = r0.x + r2.z >= bx0 && r0.x - r2.z <= bx1 && r0.y + r2.w >= by0 && r0.y - r2.w <= by1;
+      walked_c += hit;
+      if (hit && j - rg.x < nc) ++bwd_c;
       const float dx = r0.x - (float)px, dy = r0.y - (float)py;
       const float power = fmaf(r0.z, dx * dx, fmaf(r1.x, dy * dy, r0.w * (dx * dy)));
       if (power > 0.0f) continue;
@@ -173,19 +180,23 @@ __global__ void __launch_bounds__(kTilePixels) k_stats(const uint2* __restrict__
       ++blended;
     }
   }
-  const uint32_t wmax = __reduce_max_sync(0xffffffffu, walked);
-  unsigned long long f = walked, b = nc, bl = blended;
+  const uint32_t wmax = __reduce_max_sync(0xffffffffu, walked_c);
+  unsigned long long f = walked, b = nc, bl = blended, fc = walked_c, bc = bwd_c;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     f += __shfl_xor_sync(0xffffffffu, f, o);
     b += __shfl_xor_sync(0xffffffffu, b, o);
     bl += __shfl_xor_sync(0xffffffffu, bl, o);
+    fc += __shfl_xor_sync(0xffffffffu, fc, o);
+    bc += __shfl_xor_sync(0xffffffffu, bc, o);
   }
-  if ((threadIdx.x & 31) == 0) {
+  if (lane == 0) {
     atomicAdd(&out[0], f);
     atomicAdd(&out[1], b);
     atomicAdd(&out[2], 32ull * wmax);
     atomicAdd(&out[5], bl);
+    atomicAdd(&out[6], fc);
+    atomicAdd(&out[7], bc);
   }
   if (threadIdx.x == 0) atomicMax(&out[3], (unsigned long long)(rg.y - rg.x));
 }
@@ -216,6 +227,8 @@ bgs_status launch_stats(const Frame* F, const uint32_t* n_contrib, bgs_stats* ou
   out->max_list = (int64_t)h[3];
   out->visible = (int64_t)h[4];
   out->blended = (int64_t)h[5];
+  out->evals_fwd_culled = (int64_t)h[6];
+  out->evals_bwd_culled = (int64_t)h[7];
   out->num_keys = (int64_t)(((uint64_t)c[1] << 32) | c[0]);
   return check_launch("k_stats");
 }

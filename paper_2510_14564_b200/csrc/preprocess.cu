@@ -189,7 +189,19 @@ __global__ void __launch_bounds__(256) k_preprocess(PreParams p) {
   float4* rec = p.record + 3 * i;
   rec[0] = make_float4(px, py, -0.5f * conx, -cony);
   rec[1] = make_float4(-0.5f * conz, o, rgb[0], rgb[1]);
-  rec[2] = make_float4(rgb[2], __uint_as_float(cb), 0.0f, 0.0f);
+  // Conservative half-extents of the alpha >= 1/255 level set, d^T conic d <= 2 ln(255 o)
+  // (R14): AABB half-widths sqrt(2 tau a), sqrt(2 tau c) with tau raised by 1e-3 (the
+  // threshold lowered by e^-1e-3) and a
+  // 1e-3 relative + 1e-3 px margin, so every pixel outside it gets alpha < 1/255 in the
+  // blend's own float arithmetic (its G error is ~2^-20 relative).  The blend kernels use
+  // it to skip entries per warp block; it never changes a decision.
+  const float tau = logf(255.0f * o) + 1e-3f;
+  float ex = -1e30f, ey = -1e30f;
+  if (tau > 0.0f) {
+    ex = sqrtf(2.0f * tau * a) * 1.001f + 1e-3f;
+    ey = sqrtf(2.0f * tau * cc) * 1.001f + 1e-3f;
+  }
+  rec[2] = make_float4(rgb[2], __uint_as_float(cb), ex, ey);
   // this view's blend-gradient accumulator (render_bwd REDs into it)
   float4* g2 = p.grad2d + 3 * i;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);

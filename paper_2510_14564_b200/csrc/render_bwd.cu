@@ -1,17 +1,20 @@
-// render_bwd.cu -- a9 blend backward (K12) and a10 preprocess backward (K13).
+// render_bwd.cu -- a9 blend backward (K12).
 //
 // The paper has no backward; it inherits 3DGS training.  Reading
 // R18: the gradient of the forward O1-O14 with every discrete decision frozen (cull,
 // rect, power/alpha skips, early stop, the 0.99 alpha clamp -> zero gradient to o and G,
 // the SH clamp, the J-clamp branch).
 //
-// K12: one CTA per tile, one thread per pixel, walking the tile list back to front
-// from the tile's largest n_contrib; T is recovered as T_i = T_{i+1} / (1 - alpha_i)
-// and the colour "behind" accumulates S += c alpha T (S starts at T_final bg).  Per
-// list entry each pixel produces 9 partials {dxy(2), dconic(3), dopacity, drgb(3)};
-// they are summed across the warp with shuffles (skipped when no lane contributes)
-// and lane 0 issues three 16-byte vector REDs into grad2d[id] -- instead of 3DGS's nine
-// scalar atomics per pixel.
+// One CTA per tile, 8 warps each owning an 8x4 pixel block (as the forward); the tile list
+// is walked back to front from the tile's largest n_contrib, in batches of 256 records
+// staged in shared memory.  Each warp compacts a batch to the entries that can reach its
+// block (the same exact alpha-level-set test as the forward, plus position < the warp's
+// largest n_contrib).  Per pixel: T_i = T_{i+1} / (1 - alpha_i), the colour behind
+// accumulates S += c alpha T (S starts at T_final bg), and each evaluated entry yields 9
+// partials {dxy(2), dconic(3), dopacity, drgb(3)}.  They are summed across the warp with
+// shuffles, then across the CTA's 8 warps with shared-memory atomics, and each entry is
+// flushed to grad2d[id] once per tile with two 16-byte vector REDs and one scalar RED --
+// instead of 3DGS's nine scalar global atomics per evaluated (pixel, Gaussian).
 //
 // K13 (the chain rule to theta) is in preprocess_bwd.cu.
 #include "common.cuh"
@@ -39,13 +42,19 @@ __global__ void __launch_bounds__(kTilePixels) k_render_bwd(const uint2* __restr
                                                             const float* __restrict__ final_T,
                                                             const uint32_t* __restrict__ n_contrib,
                                                             float4* __restrict__ grad2d) {
-  __shared__ float4 s_r0[kBatchB], s_r1[kBatchB];
-  __shared__ float s_b[kBatchB];
+  __shared__ float4 s_r0[kBatchB], s_r1[kBatchB], s_r2[kBatchB];
   __shared__ uint32_t s_id[kBatchB];
+  __shared__ float s_g[9][kBatchB];
+  __shared__ uint8_t s_hit[kBatchB];
+  __shared__ uint8_t s_list[kTilePixels / 32][kBatchB];
   __shared__ uint32_t s_max;
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-  const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  const int py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+  const float bx0 = (float)(tx * kTile + (warp & 1) * 8), by0 = (float)(ty * kTile + (warp >> 1) * 4);
+  const float bx1 = bx0 + 7.0f, by1 = by0 + 3.0f;
   const bool inside = px < cam.W && py < cam.H;
   const float pxf = (float)px, pyf = (float)py;
   uint2 rg = ranges[tile];
@@ -64,10 +73,10 @@ __global__ void __launch_bounds__(kTilePixels) k_render_bwd(const uint2* __restr
   if (threadIdx.x == 0) s_max = 0;
   __syncthreads();
   const uint32_t wmax = __reduce_max_sync(0xffffffffu, my_last);
-  if ((threadIdx.x & 31) == 0 && wmax) atomicMax(&s_max, wmax);
+  if (lane == 0 && wmax) atomicMax(&s_max, wmax);
   __syncthreads();
   const int tile_last = (int)min(s_max, rg.y - rg.x);
-  const int lane = threadIdx.x & 31;
+  const uint32_t lt = lanemask_lt();
   for (int end = tile_last; end > 0; end -= kBatchB) {
     const int begin = max(0, end - kBatchB);
     const int cnt = end - begin;
@@ -77,16 +86,38 @@ __global__ void __launch_bounds__(kTilePixels) k_render_bwd(const uint2* __restr
       s_id[threadIdx.x] = id;
       s_r0[threadIdx.x] = __ldg(record + 3 * id);
       s_r1[threadIdx.x] = __ldg(record + 3 * id + 1);
-      s_b[threadIdx.x] = __ldg(record + 3 * id + 2).x;
+      s_r2[threadIdx.x] = __ldg(record + 3 * id + 2);
     }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) s_g[q][threadIdx.x] = 0.0f;
+    s_hit[threadIdx.x] = 0;
     __syncthreads();
-    for (int k = cnt - 1; k >= 0; --k) {
-      const uint32_t pos = (uint32_t)(begin + k);
+    // per-warp compaction: entries that can reach this block, below the warp's largest n_contrib
+    int m = 0;
+    if (wmax > (uint32_t)begin) {
+#pragma unroll
+      for (int r = 0; r < kBatchB / 32; ++r) {
+        const int e = r * 32 + lane;
+        bool hit = false;
+        if (e < cnt && (uint32_t)(begin + e) < wmax) {
+          const float4 a = s_r0[e];
+          const float4 c = s_r2[e];
+          hit = a.x + c.z >= bx0 && a.x - c.z <= bx1 && a.y + c.w >= by0 && a.y - c.w <= by1;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) s_list[warp][m + __popc(bal & lt)] = (uint8_t)e;
+        m += __popc(bal);
+      }
+      __syncwarp();
+    }
+    for (int k = m - 1; k >= 0; --k) {
+      const int e = s_list[warp][k];
+      const uint32_t pos = (uint32_t)(begin + e);
       bool act = pos < my_last;
       float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
       if (act) {
-        const float4 r0 = s_r0[k];
-        const float4 r1 = s_r1[k];
+        const float4 r0 = s_r0[e];
+        const float4 r1 = s_r1[e];
         const float dx = r0.x - pxf, dy = r0.y - pyf;
         const float power = fmaf(r0.z, dx * dx, fmaf(r1.x, dy * dy, r0.w * (dx * dy)));
         const float G = fast_exp(power);
@@ -95,11 +126,10 @@ __global__ void __launch_bounds__(kTilePixels) k_render_bwd(const uint2* __restr
         if (power > 0.0f || alpha < (1.0f / 255.0f)) {
           act = false;
         } else {
-          const float oma = 1.0f - alpha;
-          const float ioma = 1.0f / oma;
+          const float ioma = 1.0f / (1.0f - alpha);
           T = T * ioma;  // transmittance in front of this Gaussian
           const float w = alpha * T;
-          const float cr = r1.z, cg = r1.w, cb = s_b[k];
+          const float cr = r1.z, cg = r1.w, cb = s_r2[e].x;
           g6 = w * dLr;
           g7 = w * dLg;
           g8 = w * dLb;
@@ -123,12 +153,21 @@ __global__ void __launch_bounds__(kTilePixels) k_render_bwd(const uint2* __restr
         g3 = warp_sum(g3); g4 = warp_sum(g4); g5 = warp_sum(g5);
         g6 = warp_sum(g6); g7 = warp_sum(g7); g8 = warp_sum(g8);
         if (lane == 0) {
-          float4* dst = grad2d + 3 * s_id[k];
-          red_add_v4(dst, make_float4(g0, g1, g2, g3));
-          red_add_v4(dst + 1, make_float4(g4, g5, g6, g7));
-          atomicAdd(&dst[2].x, g8);
+          atomicAdd(&s_g[0][e], g0); atomicAdd(&s_g[1][e], g1); atomicAdd(&s_g[2][e], g2);
+          atomicAdd(&s_g[3][e], g3); atomicAdd(&s_g[4][e], g4); atomicAdd(&s_g[5][e], g5);
+          atomicAdd(&s_g[6][e], g6); atomicAdd(&s_g[7][e], g7); atomicAdd(&s_g[8][e], g8);
+          s_hit[e] = 1;
         }
       }
+    }
+    __syncthreads();
+    // one flush per (tile, entry)
+    if ((int)threadIdx.x < cnt && s_hit[threadIdx.x]) {
+      const int e = threadIdx.x;
+      float4* dst = grad2d + 3 * s_id[e];
+      red_add_v4(dst, make_float4(s_g[0][e], s_g[1][e], s_g[2][e], s_g[3][e]));
+      red_add_v4(dst + 1, make_float4(s_g[4][e], s_g[5][e], s_g[6][e], s_g[7][e]));
+      atomicAdd(&dst[2].x, s_g[8][e]);
     }
   }
 }

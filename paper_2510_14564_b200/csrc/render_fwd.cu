@@ -6,16 +6,27 @@
 // Decision-bearing arithmetic is the canonical tree of R22 (explicit fmaf, file built
 // with --fmad=false); G uses MUFU.EX2 (R23 near-tie rule covers the few-ulp difference).
 //
-// Mapping: one CTA per 16x16 tile, one thread per pixel; the tile's list is streamed
-// in batches of 256 render records (48 B each, {x,y,A,B | C,o,r,g | b,..}) staged into
-// shared memory by the whole CTA with 16-byte loads, then every pixel thread walks the
-// batch reading broadcast LDS.128 -- the B200 form of the paper's T3 "batch loading
-// into shared memory" of per-Gaussian contiguous RGB.
+// Mapping (B200): one CTA per 16x16 tile, 8 warps, each warp owns an 8x4 pixel block
+// (one pixel per lane).  The tile list is streamed in batches of 256 render records
+// (48 B: {x,y,A,B | C,o,r,g | b,cbits,ex,ey}) staged into shared memory by the whole CTA
+// with 16-byte loads -- the B200 form of the paper's T3 "batch loading into shared
+// memory" of per-Gaussian contiguous RGB.  Each warp then
+// compacts the batch to the entries whose conservative alpha >= 1/255 bounding box
+// (ex, ey from the preprocess) touches its 8x4 block -- every other entry would be
+// skipped by all 32 of its pixels anyway -- so a pixel walks only those (about a third
+// of the list on the garden workload).  List positions are kept, so n_contrib and every
+// decision are those of the plain per-pixel walk.
 #include "common.cuh"
 
 namespace bgs {
 
 constexpr int kBatch = kTilePixels;
+
+// pixel of (tile, warp, lane): warp w covers columns (w&1)*8..+7, rows (w>>1)*4..+3
+__device__ __forceinline__ void warp_block_pixel(int tx, int ty, int warp, int lane, int& px, int& py) {
+  px = tx * kTile + (warp & 1) * 8 + (lane & 7);
+  py = ty * kTile + (warp >> 1) * 4 + (lane >> 3);
+}
 
 __global__ void __launch_bounds__(kTilePixels) k_render_fwd(const uint2* __restrict__ ranges,
                                                             const uint32_t* __restrict__ values,
@@ -24,16 +35,23 @@ __global__ void __launch_bounds__(kTilePixels) k_render_fwd(const uint2* __restr
                                                             float* __restrict__ image, float* __restrict__ final_T,
                                                             uint32_t* __restrict__ n_contrib) {
   __shared__ float4 s_r0[kBatch], s_r1[kBatch], s_r2[kBatch];
+  __shared__ uint8_t s_list[kTilePixels / 32][kBatch];
   const int tile = blockIdx.x;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-  const int px = tx * kTile + (threadIdx.x & 15), py = ty * kTile + (threadIdx.x >> 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int px, py;
+  warp_block_pixel(tx, ty, warp, lane, px, py);
   const bool inside = px < cam.W && py < cam.H;
   const float pxf = (float)px, pyf = (float)py;
+  // the warp's pixel block, clipped to the image
+  const float bx0 = (float)(tx * kTile + (warp & 1) * 8), by0 = (float)(ty * kTile + (warp >> 1) * 4);
+  const float bx1 = bx0 + 7.0f, by1 = by0 + 3.0f;
   uint2 rg = ranges[tile];
   if (counters[C_OVERFLOW]) rg = make_uint2(0, 0);
   bool done = !inside;
   float T = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f;
   uint32_t last = 0;
+  const uint32_t lt = lanemask_lt();
   for (uint32_t start = rg.x; start < rg.y; start += kBatch) {
     if (__syncthreads_count(done) == kTilePixels) break;
     const uint32_t j = start + threadIdx.x;
@@ -45,10 +63,29 @@ __global__ void __launch_bounds__(kTilePixels) k_render_fwd(const uint2* __restr
     }
     __syncthreads();
     const int cnt = (int)min(rg.y - start, (uint32_t)kBatch);
-    for (int k = 0; k < cnt && !done; ++k) {
-      const float4 r0 = s_r0[k];
+    // per-warp compaction of the batch to the entries that can reach this 8x4 block
+    int m = 0;
+    if (__any_sync(0xffffffffu, !done)) {
+#pragma unroll
+      for (int r = 0; r < kBatch / 32; ++r) {
+        const int e = r * 32 + lane;
+        bool hit = false;
+        if (e < cnt) {
+          const float4 a = s_r0[e];
+          const float4 c = s_r2[e];
+          hit = a.x + c.z >= bx0 && a.x - c.z <= bx1 && a.y + c.w >= by0 && a.y - c.w <= by1;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) s_list[warp][m + __popc(bal & lt)] = (uint8_t)e;
+        m += __popc(bal);
+      }
+      __syncwarp();
+    }
+    for (int k = 0; k < m && !done; ++k) {
+      const int e = s_list[warp][k];
+      const float4 r0 = s_r0[e];
       const float dx = r0.x - pxf, dy = r0.y - pyf;
-      const float4 r1 = s_r1[k];
+      const float4 r1 = s_r1[e];
       const float power = fmaf(r0.z, dx * dx, fmaf(r1.x, dy * dy, r0.w * (dx * dy)));
       if (power > 0.0f) continue;
       const float alpha = fminf(0.99f, r1.y * fast_exp(power));
@@ -61,9 +98,9 @@ __global__ void __launch_bounds__(kTilePixels) k_render_fwd(const uint2* __restr
       const float w = alpha * T;
       Cr = fmaf(r1.z, w, Cr);
       Cg = fmaf(r1.w, w, Cg);
-      Cb = fmaf(s_r2[k].x, w, Cb);
+      Cb = fmaf(s_r2[e].x, w, Cb);
       T = tT;
-      last = start - rg.x + (uint32_t)k + 1u;
+      last = start - rg.x + (uint32_t)e + 1u;
     }
   }
   if (inside) {
