@@ -57,6 +57,10 @@ struct Frame {
   uint32_t* sort_status;   // [sort_tiles_max][256]
   uint32_t* counters;      // [C_NUM]
   float4* grad2d;          // [n][3]
+  uint32_t* tile_count;    // [num_tiles] keys per tile (from the duplication)
+  uint32_t* tile_order;    // [num_tiles] forward CTA -> tile, heavy first
+  uint32_t* tile_order_bwd;// [num_tiles] backward CTA -> tile, heavy first
+  uint32_t* tile_cost;     // [num_tiles] the forward's largest n_contrib per tile
 };
 static_assert(sizeof(Frame) <= sizeof(bgs_frame), "Frame must fit in bgs_frame::opaque");
 constexpr uint64_t kFrameMagic = 0xB6500F7A3E5ull;
@@ -85,6 +89,12 @@ bgs_status launch_l1(const float* image, const uint8_t* target, int32_t w, int32
 bgs_status launch_stats(const Frame* F, const uint32_t* n_contrib, bgs_stats* out, cudaStream_t s);
 
 int num_sms();
+int sort_pass_grid();
+bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* kout, uint32_t* vout,
+                            const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
+                            int shift, cudaStream_t s);
+bgs_status launch_tile_order(const uint32_t* cost, int32_t num_tiles, const uint32_t* counters, uint32_t* order,
+                             cudaStream_t s);
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ float fast_exp(float x) {

@@ -42,7 +42,7 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t radius, depth, record, tiles_touched, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
-      sort_status, counters, grad2d, total;
+      sort_status, counters, grad2d, tile_count, tile_order, tile_order_bwd, tile_cost, total;
   int32_t tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
   int64_t sort_tiles_max;
 };
@@ -86,6 +86,11 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.sort_status = take(4 * 256 * (size_t)L.sort_tiles_max);
   L.counters = take(4 * C_NUM);
   L.grad2d = take(48 * N);
+  const size_t NT = (size_t)L.num_tiles;
+  L.tile_count = take(4 * NT);
+  L.tile_order = take(4 * NT);
+  L.tile_order_bwd = take(4 * NT);
+  L.tile_cost = take(4 * NT);
   L.total = o;
   return true;
 }
@@ -204,6 +209,10 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->sort_status = (uint32_t*)(base + L.sort_status);
   F->counters = (uint32_t*)(base + L.counters);
   F->grad2d = (float4*)(base + L.grad2d);
+  F->tile_count = (uint32_t*)(base + L.tile_count);
+  F->tile_order = (uint32_t*)(base + L.tile_order);
+  F->tile_order_bwd = (uint32_t*)(base + L.tile_order_bwd);
+  F->tile_cost = (uint32_t*)(base + L.tile_cost);
   F->final_buf = L.sort_passes & 1;  // pass p reads buf p&1, writes buf (p+1)&1
   return BGS_OK;
 }

@@ -83,8 +83,6 @@ __global__ void __launch_bounds__(kBwdThreads) k_preprocess_bwd(PreBwdParams p) 
   double Y[16];
   if (valid) {
     const Cam& c = p.cam;
-    const double* none = nullptr;
-    (void)none;
     const float4 ga4 = p.grad2d[3 * i], gb4 = p.grad2d[3 * i + 1], gc4 = p.grad2d[3 * i + 2];
     const double gx = ga4.x, gy = ga4.y, gcx = ga4.z, gcy = ga4.w, gcz = gb4.x, gop = gb4.y;
     const uint32_t cb = __float_as_uint(p.record[3 * i + 2].y);

@@ -1,0 +1,196 @@
+// radix.cu -- a5 (K10): one pass of the stable LSD radix sort of (key, value) pairs,
+// onesweep style (one kernel per 8-bit digit pass; keys read once and written once).
+//
+// "N denotes the set of Gaussians contributing to the pixel, sorted by depth" (PAPER.md
+// l.149, §II-A); ties by Gaussian index (R13): a stable ascending
+// sort of key = tile << 32 | depth bits, fed in index order, yields (tile, depth, index).
+//
+// A 4096-key tile per CTA iteration: warp-level multi-split ranking with
+// __match_any_sync (stable inside a warp's contiguous 512-key slice), warp prefix across
+// the CTA, decoupled look-back across tiles for the digit's global offset, then a
+// shared-memory reorder so the global writes are digit-contiguous (coalesced).  A
+// persistent grid takes tiles in ticket order, so a predecessor tile is always resident
+// when a successor waits on it.  The pass histograms come from the key duplication
+// (depth digits) and the per-tile key counts (tile digits), see sort.cu.
+#include "common.cuh"
+
+namespace bgs {
+
+constexpr int kSortThreads = 256, kSortItems = 16, kSortTile = kSortThreads * kSortItems, kRadix = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr uint32_t kStA = 1u << 30, kStP = 2u << 30, kStMask = (1u << 30) - 1;
+
+__device__ __forceinline__ uint64_t load_k(const uint32_t* counters) {
+  return ((uint64_t)counters[C_K_HI] << 32) | counters[C_K_LO];
+}
+
+// ---------------------------------------------------------------- one onesweep pass
+struct SortSmem {
+  uint64_t keys[kSortTile];
+  uint32_t vals[kSortTile];
+  uint32_t warp_hist[kSortWarps][kRadix];  // counts, then exclusive prefix over warps
+  uint32_t tile_start[kRadix];             // exclusive prefix over digits inside the tile
+  uint32_t global_base[kRadix];            // destination of the digit's first key of this tile
+  uint32_t hist_excl[kRadix];              // exclusive scan of this pass's global histogram
+  uint32_t scan_tmp[kSortWarps];
+  uint32_t tile;
+};
+
+__global__ void __launch_bounds__(kSortThreads) k_sort_pass(const uint64_t* __restrict__ kin,
+                                                            const uint32_t* __restrict__ vin, uint64_t* kout,
+                                                            uint32_t* vout, const uint32_t* __restrict__ hist,
+                                                            uint32_t* status, uint32_t* ticket,
+                                                            const uint32_t* counters, int shift) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
+  if (counters[C_OVERFLOW]) return;
+  const int64_t K = (int64_t)load_k(counters);
+  const int64_t ntiles = (K + kSortTile - 1) / kSortTile;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // exclusive scan of the pass histogram (thread = digit)
+  {
+    const uint32_t h = hist[tid];
+    uint32_t incl = h;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (lane == 31) S.scan_tmp[warp] = incl;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int w = 0; w < warp; ++w) off += S.scan_tmp[w];
+    S.hist_excl[tid] = off + incl - h;
+    __syncthreads();
+  }
+  const uint32_t lt = lanemask_lt();
+  while (true) {
+    if (tid == 0) S.tile = atomicAdd(ticket, 1u);
+    for (int k = tid; k < kSortWarps * kRadix; k += kSortThreads) (&S.warp_hist[0][0])[k] = 0;
+    __syncthreads();
+    const int64_t tile = S.tile;
+    if (tile >= ntiles) break;
+    const int64_t tbase = tile * kSortTile;
+    const int tcount = (int)(K - tbase < kSortTile ? K - tbase : kSortTile);
+    // load: warp w owns the contiguous slice [w*512, (w+1)*512) of the tile
+    uint64_t key[kSortItems];
+    uint32_t val[kSortItems];
+    uint16_t rank[kSortItems];
+    const int wbase = warp * (kSortItems * 32);
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+      const int idx = wbase + k * 32 + lane;
+      if (idx < tcount) {
+        key[k] = kin[tbase + idx];
+        val[k] = vin[tbase + idx];
+      } else {
+        key[k] = ~0ull;
+        val[k] = 0;
+      }
+    }
+    // warp-level multi-split ranking, in input order (stable)
+    uint32_t* wh = S.warp_hist[warp];
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+      const int idx = wbase + k * 32 + lane;
+      const bool valid = idx < tcount;
+      const uint32_t d = valid ? (uint32_t)((key[k] >> shift) & 0xff) : 0x100u + (uint32_t)lane;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      uint32_t base = 0;
+      if (valid) base = wh[d];
+      __syncwarp();
+      if (valid) {
+        const uint32_t before = __popc(peers & lt);
+        if (before == 0) wh[d] = base + __popc(peers);
+        rank[k] = (uint16_t)(base + before);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps, tile count
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int w = 0; w < kSortWarps; ++w) {
+      const uint32_t c = S.warp_hist[w][tid];
+      S.warp_hist[w][tid] = cnt;
+      cnt += c;
+    }
+    // publish the tile aggregate early (decoupled look-back)
+    uint32_t* st = status + tile * kRadix;
+    if (tile == 0) st_volatile_u32(&st[tid], kStP | cnt);
+    else st_volatile_u32(&st[tid], kStA | cnt);
+    // exclusive prefix over digits inside the tile
+    {
+      uint32_t incl = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      if (lane == 31) S.scan_tmp[warp] = incl;
+      __syncthreads();
+      uint32_t off = 0;
+      for (int w = 0; w < warp; ++w) off += S.scan_tmp[w];
+      S.tile_start[tid] = off + incl - cnt;
+    }
+    // look-back for digit tid
+    uint32_t prefix = 0;
+    if (tile > 0) {
+      for (int64_t j = tile - 1; j >= 0; --j) {
+        uint32_t s;
+        do {
+          s = ld_volatile_u32(&status[j * kRadix + tid]);
+        } while ((s >> 30) == 0);
+        prefix += s & kStMask;
+        if ((s >> 30) == 2) break;
+      }
+      st_volatile_u32(&st[tid], kStP | (prefix + cnt));
+    }
+    S.global_base[tid] = S.hist_excl[tid] + prefix;
+    __syncthreads();
+    // reorder through shared memory (digit-contiguous)
+#pragma unroll
+    for (int k = 0; k < kSortItems; ++k) {
+      const int idx = wbase + k * 32 + lane;
+      if (idx < tcount) {
+        const uint32_t d = (uint32_t)((key[k] >> shift) & 0xff);
+        const uint32_t pos = S.tile_start[d] + S.warp_hist[warp][d] + rank[k];
+        S.keys[pos] = key[k];
+        S.vals[pos] = val[k];
+      }
+    }
+    __syncthreads();
+    for (int j = tid; j < tcount; j += kSortThreads) {
+      const uint64_t k2 = S.keys[j];
+      const uint32_t d = (uint32_t)((k2 >> shift) & 0xff);
+      const uint32_t g = S.global_base[d] + (uint32_t)j - S.tile_start[d];
+      kout[g] = k2;
+      vout[g] = S.vals[j];
+    }
+    __syncthreads();
+  }
+}
+
+int sort_pass_grid() {
+  static int grid = 0;
+  if (!grid) {
+    cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem));
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_pass, kSortThreads, sizeof(SortSmem));
+    if (per_sm < 1) per_sm = 1;
+    grid = per_sm * num_sms();
+  }
+  return grid;
+}
+
+
+bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* kout, uint32_t* vout,
+                            const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
+                            int shift, cudaStream_t s) {
+  k_sort_pass<<<sort_pass_grid(), kSortThreads, sizeof(SortSmem), s>>>(kin, vin, kout, vout, hist, status, ticket,
+                                                                        counters, shift);
+  note_launch();
+  return check_launch("k_sort_pass");
+}
+
+}  // namespace bgs

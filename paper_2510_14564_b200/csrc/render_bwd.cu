@@ -38,6 +38,7 @@ __global__ void __launch_bounds__(kTilePixels) k_render_bwd(const uint2* __restr
                                                             const uint32_t* __restrict__ values,
                                                             const float4* __restrict__ record,
                                                             const uint32_t* __restrict__ counters, Cam cam,
+                                                            const uint32_t* __restrict__ tile_order,
                                                             const float* __restrict__ dl_dimage,
                                                             const float* __restrict__ final_T,
                                                             const uint32_t* __restrict__ n_contrib,
@@ -48,7 +49,7 @@ __global__ void __launch_bounds__(kTilePixels) k_render_bwd(const uint2* __restr
   __shared__ uint8_t s_hit[kBatchB];
   __shared__ uint8_t s_list[kTilePixels / 32][kBatchB];
   __shared__ uint32_t s_max;
-  const int tile = blockIdx.x;
+  const int tile = (int)tile_order[blockIdx.x];  // heavy first, by the forward's tile_cost
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int px = tx * kTile + (warp & 1) * 8 + (lane & 7);
@@ -174,8 +175,10 @@ __global__ void __launch_bounds__(kTilePixels) k_render_bwd(const uint2* __restr
 
 bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
                             cudaStream_t s) {
+  bgs_status st = launch_tile_order(F->tile_cost, F->num_tiles, F->counters, F->tile_order_bwd, s);
+  if (st != BGS_OK) return st;
   k_render_bwd<<<F->num_tiles, kTilePixels, 0, s>>>(F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam,
-                                                    dL_dimage, final_T, n_contrib, F->grad2d);
+                                                    F->tile_order_bwd, dL_dimage, final_T, n_contrib, F->grad2d);
   note_launch();
   return check_launch("k_render_bwd");
 }

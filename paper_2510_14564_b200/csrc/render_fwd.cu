@@ -32,11 +32,15 @@ __global__ void __launch_bounds__(kTilePixels) k_render_fwd(const uint2* __restr
                                                             const uint32_t* __restrict__ values,
                                                             const float4* __restrict__ record,
                                                             const uint32_t* __restrict__ counters, Cam cam,
+                                                            const uint32_t* __restrict__ tile_order,
                                                             float* __restrict__ image, float* __restrict__ final_T,
-                                                            uint32_t* __restrict__ n_contrib) {
+                                                            uint32_t* __restrict__ n_contrib,
+                                                            uint32_t* __restrict__ tile_cost) {
   __shared__ float4 s_r0[kBatch], s_r1[kBatch], s_r2[kBatch];
   __shared__ uint8_t s_list[kTilePixels / 32][kBatch];
-  const int tile = blockIdx.x;
+  __shared__ uint32_t s_cost;
+  const int tile = (int)tile_order[blockIdx.x];  // heavy tiles first (k_tile_scan)
+  if (threadIdx.x == 0) s_cost = 0;
   const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int px, py;
@@ -112,11 +116,16 @@ __global__ void __launch_bounds__(kTilePixels) k_render_fwd(const uint2* __restr
     final_T[pix] = T;
     n_contrib[pix] = last;
   }
+  // the tile's largest n_contrib: the backward's cost estimate for its heavy-first order
+  const uint32_t wl = __reduce_max_sync(0xffffffffu, last);
+  if (lane == 0 && wl) atomicMax(&s_cost, wl);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_cost[tile] = s_cost;
 }
 
 bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n_contrib, cudaStream_t s) {
   k_render_fwd<<<F->num_tiles, kTilePixels, 0, s>>>(F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam,
-                                                    image, final_T, n_contrib);
+                                                    F->tile_order, image, final_T, n_contrib, F->tile_cost);
   note_launch();
   return check_launch("k_render_fwd");
 }
