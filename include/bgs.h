@@ -92,8 +92,10 @@ typedef struct {
 typedef struct {
   int32_t* radius;          /* [n]  0 = culled ("absent")                       */
   float* depth;             /* [n]  camera-space t_z; its bits are the key low word  */
-  float* record;            /* [n][12] {x, y, A, B, C, opacity, r, g, b, cbits, 0, 0}
-                               with (A, B, C) = (-conic.x/2, -conic.y, -conic.z/2)   */
+  float* record;            /* [n][12] {x, y, ex, ey | A, B, C, opacity | r, g, b, cbits}
+                               with (A, B, C) = (-conic.x/2, -conic.y, -conic.z/2) and
+                               (ex, ey) conservative half-extents of the alpha >= 1/255
+                               level set (the blend kernels' exact per-block skip test) */
   uint32_t* tiles_touched;  /* [n]                                                   */
   uint32_t* offsets;        /* [n]  exclusive scan of tiles_touched (R13)            */
   uint64_t* keys_unsorted;  /* [max_keys] (tile << 32 | depth bits), index order     */

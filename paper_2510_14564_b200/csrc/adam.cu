@@ -166,13 +166,14 @@ __global__ void __launch_bounds__(kTilePixels) k_stats(const uint2* __restrict__
       ++walked;
       const uint32_t id = values[j];
       const float4 r0 = record[3 * id], r1 = record[3 * id + 1], r2 = record[3 * id + 2];
-      const bool hit = r0.x + r2.z >= bx0 && r0.x - r2.z <= bx1 && r0.y + r2.w >= by0 && r0.y - r2.w <= by1;
+      (void)r2;
+      const bool hit = r0.x + r0.z >= bx0 && r0.x - r0.z <= bx1 && r0.y + r0.w >= by0 && r0.y - r0.w <= by1;
       walked_c += hit;
       if (hit && j - rg.x < nc) ++bwd_c;
       const float dx = r0.x - (float)px, dy = r0.y - (float)py;
-      const float power = fmaf(r0.z, dx * dx, fmaf(r1.x, dy * dy, r0.w * (dx * dy)));
+      const float power = fmaf(r1.x, dx * dx, fmaf(r1.z, dy * dy, r1.y * (dx * dy)));
       if (power > 0.0f) continue;
-      const float alpha = fminf(0.99f, r1.y * fast_exp(power));
+      const float alpha = fminf(0.99f, r1.w * fast_exp(power));
       if (alpha < (1.0f / 255.0f)) continue;
       const float tT = T * (1.0f - alpha);
       if (tT < 1e-4f) break;

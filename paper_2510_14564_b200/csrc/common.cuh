@@ -18,6 +18,8 @@ enum : int {
   C_SCAN_TICKET = 3,          // dynamic tile ids for the decoupled-lookback scan
   C_SORT_TICKET = 4,          // 8 slots: one per radix pass
   C_VISIBLE = 12,
+  C_FWD_TICKET = 13,          // work-item tickets of the warp-persistent blend kernels
+  C_BWD_TICKET = 14,
   C_NUM = 32
 };
 

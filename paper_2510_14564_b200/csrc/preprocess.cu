@@ -8,7 +8,7 @@
 //
 // Layout: theta segments are read as coalesced vectors (quats float4,
 // SH 12 x float4 per Gaussian, only for Gaussians that survive the culls); outputs are
-// the 48-byte render record {x, y, A, B | C, o, r, g | b, cbits, -, -} that the blend
+// the 48-byte render record {x, y, ex, ey | A, B, C, o | r, g, b, cbits} that the blend
 // kernels stage through shared memory (the B200 form of the paper's T3 RGB
 // reordering), plus radius, depth and tiles_touched.
 #include "common.cuh"
@@ -187,8 +187,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PreParams p) {
   p.depth[i] = t2;
   p.tiles_touched[i] = area;
   float4* rec = p.record + 3 * i;
-  rec[0] = make_float4(px, py, -0.5f * conx, -cony);
-  rec[1] = make_float4(-0.5f * conz, o, rgb[0], rgb[1]);
+  rec[1] = make_float4(-0.5f * conx, -cony, -0.5f * conz, o);
   // Conservative half-extents of the alpha >= 1/255 level set, d^T conic d <= 2 ln(255 o)
   // (R14): AABB half-widths sqrt(2 tau a), sqrt(2 tau c) with tau raised by 1e-3 (the
   // threshold lowered by e^-1e-3) and a
@@ -201,7 +200,8 @@ __global__ void __launch_bounds__(256) k_preprocess(PreParams p) {
     ex = sqrtf(2.0f * tau * a) * 1.001f + 1e-3f;
     ey = sqrtf(2.0f * tau * cc) * 1.001f + 1e-3f;
   }
-  rec[2] = make_float4(rgb[2], __uint_as_float(cb), ex, ey);
+  rec[0] = make_float4(px, py, ex, ey);  // everything the per-warp cull test reads
+  rec[2] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(cb));
   // this view's blend-gradient accumulator (render_bwd REDs into it)
   float4* g2 = p.grad2d + 3 * i;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);

@@ -8,7 +8,7 @@
 //
 // Mapping (B200): one CTA per 16x16 tile, 8 warps, each warp owns an 8x4 pixel block
 // (one pixel per lane).  The tile list is streamed in batches of 256 render records
-// (48 B: {x,y,A,B | C,o,r,g | b,cbits,ex,ey}) staged into shared memory by the whole CTA
+// (48 B: {x,y,ex,ey | A,B,C,o | r,g,b,cbits}) staged into shared memory by the whole CTA
 // with 16-byte loads -- the B200 form of the paper's T3 "batch loading into shared
 // memory" of per-Gaussian contiguous RGB.  Each warp then
 // compacts the batch to the entries whose conservative alpha >= 1/255 bounding box
@@ -76,8 +76,7 @@ __global__ void __launch_bounds__(kTilePixels) k_render_fwd(const uint2* __restr
         bool hit = false;
         if (e < cnt) {
           const float4 a = s_r0[e];
-          const float4 c = s_r2[e];
-          hit = a.x + c.z >= bx0 && a.x - c.z <= bx1 && a.y + c.w >= by0 && a.y - c.w <= by1;
+          hit = a.x + a.z >= bx0 && a.x - a.z <= bx1 && a.y + a.w >= by0 && a.y - a.w <= by1;
         }
         const uint32_t bal = __ballot_sync(0xffffffffu, hit);
         if (hit) s_list[warp][m + __popc(bal & lt)] = (uint8_t)e;
@@ -90,9 +89,9 @@ __global__ void __launch_bounds__(kTilePixels) k_render_fwd(const uint2* __restr
       const float4 r0 = s_r0[e];
       const float dx = r0.x - pxf, dy = r0.y - pyf;
       const float4 r1 = s_r1[e];
-      const float power = fmaf(r0.z, dx * dx, fmaf(r1.x, dy * dy, r0.w * (dx * dy)));
+      const float power = fmaf(r1.x, dx * dx, fmaf(r1.z, dy * dy, r1.y * (dx * dy)));
       if (power > 0.0f) continue;
-      const float alpha = fminf(0.99f, r1.y * fast_exp(power));
+      const float alpha = fminf(0.99f, r1.w * fast_exp(power));
       if (alpha < (1.0f / 255.0f)) continue;
       const float tT = T * (1.0f - alpha);
       if (tT < 1e-4f) {
@@ -100,9 +99,10 @@ __global__ void __launch_bounds__(kTilePixels) k_render_fwd(const uint2* __restr
         break;
       }
       const float w = alpha * T;
-      Cr = fmaf(r1.z, w, Cr);
-      Cg = fmaf(r1.w, w, Cg);
-      Cb = fmaf(s_r2[e].x, w, Cb);
+      const float4 r2 = s_r2[e];
+      Cr = fmaf(r2.x, w, Cr);
+      Cg = fmaf(r2.y, w, Cg);
+      Cb = fmaf(r2.z, w, Cb);
       T = tT;
       last = start - rg.x + (uint32_t)e + 1u;
     }

@@ -104,13 +104,20 @@ def test_preprocess_parity(bgs, name):
     assert np.array_equal(v["offsets"].astype(np.uint64), ref["srt"]["offsets"])
     vis = pre["radius"] > 0
     assert np.array_equal(v["depth"][vis].view(np.uint32), pre["depth"][vis].view(np.uint32))
-    rec = v["record"][vis]
+    rec = v["record"][vis]  # {x, y, ex, ey | A, B, C, o | r, g, b, cbits}
     assert np.array_equal(rec[:, 0:2], pre["xy"][vis])
-    conic = np.stack([-2 * rec[:, 2], -rec[:, 3], -2 * rec[:, 4]], 1)
+    conic = np.stack([-2 * rec[:, 4], -rec[:, 5], -2 * rec[:, 6]], 1)
     assert np.array_equal(conic, pre["conic"][vis])
-    assert np.array_equal(rec[:, 5], pre["opacity"][vis])
-    assert np.abs(rec[:, 6:9] - pre["rgb"][vis]).max() <= 1e-6
-    cb = rec[:, 9].view(np.uint32)
+    assert np.array_equal(rec[:, 7], pre["opacity"][vis])
+    assert np.abs(rec[:, 8:11] - pre["rgb"][vis]).max() <= 1e-6
+    # the cull box contains the alpha >= 1/255 level set: d^T conic d <= 2 ln(255 o)
+    tau = np.log(np.maximum(255.0 * pre["opacity"][vis].astype(np.float64), 1e-300))
+    cov = np.stack([pre["conic"][vis][:, 2], pre["conic"][vis][:, 0]], 1) / (
+        pre["conic"][vis][:, 0] * pre["conic"][vis][:, 2] - pre["conic"][vis][:, 1] ** 2)[:, None]
+    live = tau > 0
+    ext = np.sqrt(2 * tau[live, None] * cov[live])
+    assert (rec[live, 2:4] >= ext * (1 - 1e-5)).all()
+    cb = rec[:, 11].view(np.uint32)
     assert np.array_equal(cb & 0x78, pre["cbits"][vis] & 0x78)  # J-clamp bits (exact)
     assert (cb & 7 != pre["cbits"][vis] & 7).sum() <= max(1, vis.sum() // 10000)  # rgb clamp (free-order)
 

@@ -1,0 +1,64 @@
+"""Per-stage timing probe (not the bench): times each ABI call of one garden view in
+isolation, `--reps` back-to-back launches between CUDA events, after a warm-up."""
+import argparse
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import gen  # noqa: E402
+import paper_2510_14564_b200 as bgs  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="garden")
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--view", type=int, default=0)
+    a = ap.parse_args()
+    t0 = time.time()
+    s = gen.make(a.config)
+    print(f"gen {time.time() - t0:.1f}s", flush=True)
+    cam = s.cameras[a.view]
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    grad = torch.zeros_like(theta)
+    r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=1 << 26, device=dev)
+    out = r.forward(theta, cam, s.sh_degree)
+    dl = torch.full((3, cam.height, cam.width), 1e-6, device=dev)
+    g = bgs.gaussians(theta, s.n, s.sh_degree)
+    c = bgs.camera(cam)
+    stages = {
+        "preprocess": lambda: bgs.bgs_preprocess(g, c, r.frame),
+        "sort": lambda: bgs.bgs_sort(r.frame),
+        "render_fwd": lambda: bgs.bgs_render_fwd(r.frame, r.image, r.final_T, r.n_contrib),
+        "blend_bwd": lambda: bgs.bgs_blend_bwd(r.frame, dl, r.final_T, r.n_contrib),
+        "preprocess_bwd": lambda: bgs.bgs_preprocess_bwd(g, r.frame, grad),
+    }
+    for name, fn in stages.items():
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.reps
+        h0 = time.perf_counter()
+        for _ in range(a.reps):
+            fn()
+        host_us = (time.perf_counter() - h0) / a.reps * 1e6
+        torch.cuda.synchronize()
+        print(f"{name:16s} {ms:8.3f} ms/launch-set   host enqueue {host_us:7.1f} us", flush=True)
+    st = bgs.bgs_frame_stats(r.frame, r.n_contrib)
+    print(st)
+
+
+if __name__ == "__main__":
+    main()
