@@ -107,6 +107,8 @@ typedef struct {
                                dr, dg, db, 0, 0, 0}; consumed and zeroed by render_bwd */
   int64_t n, max_keys;
   int32_t tiles_x, tiles_y, sort_bits, sort_passes;
+  int32_t sort_mode;        /* 0 depth-first (keys_* hold 32-bit tile ids), 1 onesweep64 */
+  int32_t _pad;
 } bgs_frame_views;
 
 /* Per-frame workload counters (bgs_frame_stats; not on the hot path). */
@@ -191,6 +193,10 @@ bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contri
 /* Test-only knob: flags & BGS_DEBUG_SKIP_SORT makes bgs_sort stop after the key
  * duplication (a4), so the unsorted keys/values stay readable via bgs_frame_debug. */
 #define BGS_DEBUG_SKIP_SORT 1
+/* Selects the reference sort path: materialised 64-bit (tile | depth) keys and the
+ * onesweep LSD sort over all 32 + bit_width(tiles - 1) bits (keys_sorted is then valid).
+ * The default depth-first path produces bit-identical values and ranges. */
+#define BGS_DEBUG_SORT_ONESWEEP64 2
 bgs_status bgs_frame_set_debug(bgs_frame* f /*host*/, int32_t flags);
 
 const char* bgs_status_string(bgs_status s);

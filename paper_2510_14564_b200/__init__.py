@@ -23,6 +23,7 @@ _lib = C.CDLL(LIB_PATH)
 
 BGS_OK, BGS_ERR_INVALID, BGS_ERR_CAPACITY, BGS_ERR_CUDA, BGS_ERR_UNSUPPORTED = 0, -1, -2, -3, -4
 BGS_DEBUG_SKIP_SORT = 1
+BGS_DEBUG_SORT_ONESWEEP64 = 2
 
 
 class BgsError(RuntimeError):
@@ -64,7 +65,8 @@ class FrameViews(C.Structure):
                 ("tiles_touched", C.c_void_p), ("offsets", C.c_void_p), ("keys_unsorted", C.c_void_p),
                 ("values_unsorted", C.c_void_p), ("keys_sorted", C.c_void_p), ("values_sorted", C.c_void_p),
                 ("ranges", C.c_void_p), ("grad2d", C.c_void_p), ("n", C.c_int64), ("max_keys", C.c_int64),
-                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("sort_bits", C.c_int32), ("sort_passes", C.c_int32)]
+                ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("sort_bits", C.c_int32), ("sort_passes", C.c_int32),
+                ("sort_mode", C.c_int32), ("_pad", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -229,6 +231,7 @@ class Renderer:
     height: int
     max_keys: int = 1 << 24
     device: torch.device | str = "cuda"
+    debug_flags: int = 0
 
     def __post_init__(self):
         self.device = torch.device(self.device)
@@ -246,6 +249,8 @@ class Renderer:
             raise BgsError(BGS_ERR_INVALID, "bgs_workspace_bytes")
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         bgs_frame_init(self.frame, self.workspace, self.n, self.width, self.height, self.max_keys)
+        if self.debug_flags:
+            bgs_frame_set_debug(self.frame, self.debug_flags)
 
     def forward(self, theta, cam, sh_degree, stream=None, check=True):
         g = gaussians(theta, self.n, sh_degree)

@@ -20,6 +20,8 @@ enum : int {
   C_VISIBLE = 12,
   C_FWD_TICKET = 13,          // work-item tickets of the warp-persistent blend kernels
   C_BWD_TICKET = 14,
+  C_SCAN_TOTAL = 15,          // total of a scan that does not define K (depth-first sort)
+  C_SORT32_TICKET = 16,       // 8 slots: the depth-first path's 32-bit passes
   C_NUM = 32
 };
 
@@ -44,7 +46,7 @@ struct Frame {
   int64_t n, max_keys;
   int32_t W, H, tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
   int64_t sort_tiles_max;
-  int32_t cam_valid, final_buf, debug_flags, _pad0;
+  int32_t cam_valid, final_buf, debug_flags, sort_mode;  // sort_mode: 0 depth-first, 1 onesweep64
   Cam cam;
   int32_t* radius;
   float* depth;
@@ -63,6 +65,13 @@ struct Frame {
   uint32_t* tile_order;    // [num_tiles] forward CTA -> tile, heavy first
   uint32_t* tile_order_bwd;// [num_tiles] backward CTA -> tile, heavy first
   uint32_t* tile_cost;     // [num_tiles] the forward's largest n_contrib per tile
+  // depth-first sort path (sort.cu): Gaussians stable-sorted by depth bits, then the
+  // rank-ordered tile items stable-split by tile -- the same order as the 64-bit sort
+  uint32_t* dkey[2];       // [n] depth bits (0xffffffff for culled)
+  uint32_t* dval[2];       // [n] Gaussian index; dval[0] = depth order after 4 passes
+  uint32_t* rank_cnt;      // [n] tiles_touched in depth order
+  uint32_t* item_off;      // [n] exclusive scan of rank_cnt
+  uint2* rank_rect;        // [n] packed tile rect per depth rank
 };
 static_assert(sizeof(Frame) <= sizeof(bgs_frame), "Frame must fit in bgs_frame::opaque");
 constexpr uint64_t kFrameMagic = 0xB6500F7A3E5ull;
@@ -95,6 +104,10 @@ int sort_pass_grid();
 bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* kout, uint32_t* vout,
                             const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                             int shift, cudaStream_t s);
+bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                              const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
+                              int shift, int64_t count, cudaStream_t s);
+bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, bool publish_k, cudaStream_t s);
 bgs_status launch_tile_order(const uint32_t* cost, int32_t num_tiles, const uint32_t* counters, uint32_t* order,
                              cudaStream_t s);
 

@@ -42,7 +42,8 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t radius, depth, record, tiles_touched, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
-      sort_status, counters, grad2d, tile_count, tile_order, tile_order_bwd, tile_cost, total;
+      sort_status, counters, grad2d, tile_count, tile_order, tile_order_bwd, tile_cost, dkey0, dkey1, dval0, dval1,
+      rank_cnt, item_off, rank_rect, total;
   int32_t tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
   int64_t sort_tiles_max;
 };
@@ -63,7 +64,8 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.sort_passes = (L.sort_bits + 7) / 8;
   L.scan_tiles = (int32_t)((n + kScanTile - 1) / kScanTile);
   if (L.scan_tiles < 1) L.scan_tiles = 1;
-  L.sort_tiles_max = (max_keys + kSortTile - 1) / kSortTile;
+  // look-back status words: enough for the K-key passes and the N-key depth passes
+  L.sort_tiles_max = ((max_keys > n ? max_keys : n) + kSortTile - 1) / kSortTile;
   size_t o = 0;
   auto take = [&](size_t bytes) {
     size_t at = o;
@@ -91,6 +93,13 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.tile_order = take(4 * NT);
   L.tile_order_bwd = take(4 * NT);
   L.tile_cost = take(4 * NT);
+  L.dkey0 = take(4 * N);
+  L.dkey1 = take(4 * N);
+  L.dval0 = take(4 * N);
+  L.dval1 = take(4 * N);
+  L.rank_cnt = take(4 * N);
+  L.item_off = take(4 * N);
+  L.rank_rect = take(8 * N);
   L.total = o;
   return true;
 }
@@ -213,6 +222,13 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->tile_order = (uint32_t*)(base + L.tile_order);
   F->tile_order_bwd = (uint32_t*)(base + L.tile_order_bwd);
   F->tile_cost = (uint32_t*)(base + L.tile_cost);
+  F->dkey[0] = (uint32_t*)(base + L.dkey0);
+  F->dkey[1] = (uint32_t*)(base + L.dkey1);
+  F->dval[0] = (uint32_t*)(base + L.dval0);
+  F->dval[1] = (uint32_t*)(base + L.dval1);
+  F->rank_cnt = (uint32_t*)(base + L.rank_cnt);
+  F->item_off = (uint32_t*)(base + L.item_off);
+  F->rank_rect = (uint2*)(base + L.rank_rect);
   F->final_buf = L.sort_passes & 1;  // pass p reads buf p&1, writes buf (p+1)&1
   return BGS_OK;
 }
@@ -311,6 +327,7 @@ bgs_status bgs_frame_debug(const bgs_frame* f, bgs_frame_views* out) {
   out->tiles_y = F->tiles_y;
   out->sort_bits = F->sort_bits;
   out->sort_passes = F->sort_passes;
+  out->sort_mode = F->sort_mode;
   return BGS_OK;
 }
 

@@ -219,12 +219,13 @@ constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask 
 
 __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                       int64_t n, unsigned long long* status, uint32_t* counters,
-                                                      int64_t max_keys, int32_t num_tiles) {
+                                                      uint32_t* ticket, int64_t max_keys, int32_t num_tiles,
+                                                      bool publish_k) {
   __shared__ uint32_t s_tile;
   __shared__ unsigned long long s_warp[kScanThreads / 32];
   __shared__ unsigned long long s_prefix;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = atomicAdd(&counters[C_SCAN_TICKET], 1u);
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const int64_t tile = s_tile;
   const int64_t base = tile * kScanTile + (int64_t)tid * kScanItems;
@@ -289,10 +290,26 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
   }
   if (tile == num_tiles - 1 && tid == 0) {
     const unsigned long long K = s_prefix + total;
-    counters[C_K_LO] = (uint32_t)K;
-    counters[C_K_HI] = (uint32_t)(K >> 32);
-    counters[C_OVERFLOW] = K > (unsigned long long)max_keys ? 1u : 0u;
+    if (publish_k) {
+      counters[C_K_LO] = (uint32_t)K;
+      counters[C_K_HI] = (uint32_t)(K >> 32);
+      counters[C_OVERFLOW] = K > (unsigned long long)max_keys ? 1u : 0u;
+    } else {
+      counters[C_SCAN_TOTAL] = (uint32_t)K;
+    }
   }
+}
+
+bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, bool publish_k, cudaStream_t s) {
+  const int tiles = (int)((n + kScanTile - 1) / kScanTile);
+  if (tiles == 0) return BGS_OK;
+  if (cudaMemsetAsync(F->scan_status, 0, 8 * (size_t)tiles, s) != cudaSuccess ||
+      cudaMemsetAsync(F->counters + C_SCAN_TICKET, 0, 4, s) != cudaSuccess)
+    return check_launch("scan memset");
+  k_scan<<<tiles, kScanThreads, 0, s>>>(in, out, n, F->scan_status, F->counters, F->counters + C_SCAN_TICKET,
+                                        F->max_keys, tiles, publish_k);
+  note_launch();
+  return check_launch("k_scan");
 }
 
 bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
@@ -319,12 +336,7 @@ bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
   note_launch();
   bgs_status st = check_launch("k_preprocess");
   if (st != BGS_OK) return st;
-  if (cudaMemsetAsync(F->scan_status, 0, 8 * (size_t)F->scan_tiles, s) != cudaSuccess)
-    return check_launch("scan memset");
-  k_scan<<<F->scan_tiles, kScanThreads, 0, s>>>(F->tiles_touched, F->offsets, F->n, F->scan_status, F->counters,
-                                                 F->max_keys, F->scan_tiles);
-  note_launch();
-  return check_launch("k_scan");
+  return launch_scan(F->tiles_touched, F->offsets, F->n, F, true, s);
 }
 
 }  // namespace bgs

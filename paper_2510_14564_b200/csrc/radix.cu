@@ -6,7 +6,7 @@
 // sort of key = tile << 32 | depth bits, fed in index order, yields (tile, depth, index).
 //
 // A 4096-key tile per CTA iteration: warp-level multi-split ranking with
-// __match_any_sync (stable inside a warp's contiguous 512-key slice), warp prefix across
+// ballot-based peer detection (stable inside a warp's contiguous 512-key slice), warp prefix across
 // the CTA, decoupled look-back across tiles for the digit's global offset, then a
 // shared-memory reorder so the global writes are digit-contiguous (coalesced).  A
 // persistent grid takes tiles in ticket order, so a predecessor tile is always resident
@@ -25,8 +25,9 @@ __device__ __forceinline__ uint64_t load_k(const uint32_t* counters) {
 }
 
 // ---------------------------------------------------------------- one onesweep pass
+template <typename K>
 struct SortSmem {
-  uint64_t keys[kSortTile];
+  K keys[kSortTile];
   uint32_t vals[kSortTile];
   uint32_t warp_hist[kSortWarps][kRadix];  // counts, then exclusive prefix over warps
   uint32_t tile_start[kRadix];             // exclusive prefix over digits inside the tile
@@ -36,15 +37,18 @@ struct SortSmem {
   uint32_t tile;
 };
 
-__global__ void __launch_bounds__(kSortThreads) k_sort_pass(const uint64_t* __restrict__ kin,
-                                                            const uint32_t* __restrict__ vin, uint64_t* kout,
+// Sorts `count` (key, value) pairs by the digit at `shift`; count < 0 means "read K from
+// counters" (the 64-bit tile|depth keys), otherwise it is the host-known length.
+template <typename KT>
+__global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restrict__ kin,
+                                                            const uint32_t* __restrict__ vin, KT* kout,
                                                             uint32_t* vout, const uint32_t* __restrict__ hist,
                                                             uint32_t* status, uint32_t* ticket,
-                                                            const uint32_t* counters, int shift) {
+                                                            const uint32_t* counters, int shift, int64_t count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SortSmem& S = *reinterpret_cast<SortSmem*>(smem_raw);
+  SortSmem<KT>& S = *reinterpret_cast<SortSmem<KT>*>(smem_raw);
   if (counters[C_OVERFLOW]) return;
-  const int64_t K = (int64_t)load_k(counters);
+  const int64_t K = count >= 0 ? count : (int64_t)load_k(counters);
   const int64_t ntiles = (K + kSortTile - 1) / kSortTile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // exclusive scan of the pass histogram (thread = digit)
@@ -73,7 +77,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const uint64_t* __re
     const int64_t tbase = tile * kSortTile;
     const int tcount = (int)(K - tbase < kSortTile ? K - tbase : kSortTile);
     // load: warp w owns the contiguous slice [w*512, (w+1)*512) of the tile
-    uint64_t key[kSortItems];
+    KT key[kSortItems];
     uint32_t val[kSortItems];
     uint16_t rank[kSortItems];
     const int wbase = warp * (kSortItems * 32);
@@ -84,27 +88,31 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const uint64_t* __re
         key[k] = kin[tbase + idx];
         val[k] = vin[tbase + idx];
       } else {
-        key[k] = ~0ull;
+        key[k] = (KT)~(KT)0;
         val[k] = 0;
       }
     }
-    // warp-level multi-split ranking, in input order (stable)
+    // warp-level multi-split ranking, in input order (stable): peers of a digit from 8
+    // ballots, the lowest peer reserves the slots with one shared-memory atomic and
+    // broadcasts the base by shuffle
     uint32_t* wh = S.warp_hist[warp];
 #pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
       const int idx = wbase + k * 32 + lane;
       const bool valid = idx < tcount;
-      const uint32_t d = valid ? (uint32_t)((key[k] >> shift) & 0xff) : 0x100u + (uint32_t)lane;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      uint32_t base = 0;
-      if (valid) base = wh[d];
-      __syncwarp();
-      if (valid) {
-        const uint32_t before = __popc(peers & lt);
-        if (before == 0) wh[d] = base + __popc(peers);
-        rank[k] = (uint16_t)(base + before);
+      const uint32_t d = (uint32_t)((key[k] >> shift) & 0xff);
+      uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? bal : ~bal;
       }
-      __syncwarp();
+      const int leader = valid ? __ffs(peers) - 1 : lane;
+      uint32_t got = 0;
+      if (valid && leader == lane) got = atomicAdd(&wh[d], (uint32_t)__popc(peers));
+      const uint32_t base = __shfl_sync(0xffffffffu, got, leader);
+      rank[k] = (uint16_t)(base + __popc(peers & lt));
     }
     __syncthreads();
     // per digit: exclusive prefix over warps, tile count
@@ -161,7 +169,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const uint64_t* __re
     }
     __syncthreads();
     for (int j = tid; j < tcount; j += kSortThreads) {
-      const uint64_t k2 = S.keys[j];
+      const KT k2 = S.keys[j];
       const uint32_t d = (uint32_t)((k2 >> shift) & 0xff);
       const uint32_t g = S.global_base[d] + (uint32_t)j - S.tile_start[d];
       kout[g] = k2;
@@ -171,26 +179,37 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_pass(const uint64_t* __re
   }
 }
 
-int sort_pass_grid() {
+template <typename KT>
+static int pass_grid() {
   static int grid = 0;
   if (!grid) {
-    cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem));
+    cudaFuncSetAttribute(k_sort_pass<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SortSmem<KT>));
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_pass, kSortThreads, sizeof(SortSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sort_pass<KT>, kSortThreads, sizeof(SortSmem<KT>));
     if (per_sm < 1) per_sm = 1;
     grid = per_sm * num_sms();
   }
   return grid;
 }
 
+int sort_pass_grid() { return pass_grid<uint64_t>(); }
 
 bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* kout, uint32_t* vout,
                             const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                             int shift, cudaStream_t s) {
-  k_sort_pass<<<sort_pass_grid(), kSortThreads, sizeof(SortSmem), s>>>(kin, vin, kout, vout, hist, status, ticket,
-                                                                        counters, shift);
+  k_sort_pass<uint64_t><<<pass_grid<uint64_t>(), kSortThreads, sizeof(SortSmem<uint64_t>), s>>>(
+      kin, vin, kout, vout, hist, status, ticket, counters, shift, -1);
   note_launch();
-  return check_launch("k_sort_pass");
+  return check_launch("k_sort_pass<u64>");
+}
+
+bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
+                              const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
+                              int shift, int64_t count, cudaStream_t s) {
+  k_sort_pass<uint32_t><<<pass_grid<uint32_t>(), kSortThreads, sizeof(SortSmem<uint32_t>), s>>>(
+      kin, vin, kout, vout, hist, status, ticket, counters, shift, count);
+  note_launch();
+  return check_launch("k_sort_pass<u32>");
 }
 
 }  // namespace bgs

@@ -1,21 +1,26 @@
-// sort.cu -- a4-a6: (tile | depth) key duplication (K9), the radix passes (K10, radix.cu)
-// and tile ranges (K11).
+// sort.cu -- a4-a6: tile/depth ordering of the (tile, Gaussian) pairs (K9-K11).
 //
 // "N denotes the set of Gaussians contributing to the pixel, sorted by depth" (PAPER.md
 // l.149, §II-A); per 16x16 tile; ties by Gaussian index.
-// Reading R13: key = (ty*tiles_x + tx) << 32 | float_bits(t_z), value = Gaussian index,
-// produced in index order with each rect ty-major; a stable ascending sort on bits
-// [0, 32 + bit_width(tiles-1)) then yields the lexicographic (tile, depth bits, index).
+// Reading R13 defines the order as that of a stable ascending sort of the 64-bit keys
+// (ty*tiles_x + tx) << 32 | float_bits(t_z) produced in Gaussian-index order (each rect
+// ty-major): lexicographic (tile, depth bits, index).  Two paths produce it:
 //
-// K9 is load balanced: a warp takes 32 consecutive Gaussians, scans their tiles_touched,
-// and emits the chunk's keys 32 at a time -- lane k finds its Gaussian by a shuffle binary
-// search over the inclusive scan -- so a 4000-tile background Gaussian does not
-// serialise one thread, and the 32 writes of a round are consecutive (coalesced).  The
-// same kernel accumulates, in shared memory, the pass histograms of the depth digits
-// (one atomic per Gaussian, weighted by its key count) and the key count of every tile.
-// K11 then needs no pass over the sorted keys: one CTA scans the tile counts into the
-// ranges, derives the tile-digit pass histograms from them, and orders the tiles heavy
-// first for the blend kernels.
+//  * reference (BGS_DEBUG_SORT_ONESWEEP64): the 64-bit keys are materialised by a
+//    load-balanced duplication (K9) and LSD-sorted on bits [0, 32 + bit_width(tiles-1))
+//    with the onesweep pass of radix.cu (K10): ~8 + 24 p bytes per key (p = 6 passes).
+//  * default, depth first (SURVEY.md §8(a) a5 alternative): (1) stable LSD sort of the N
+//    Gaussians by depth bits (4 passes of 32-bit keys over N, not K; culled Gaussians get
+//    the key 0xffffffff and sort last); (2) scan of their tile counts in that order;
+//    (3) emission of (tile, Gaussian) items in depth order; (4) a stable split of the
+//    items by tile id (ceil(bits/8) 32-bit passes).  A stable split of a depth-ordered
+//    (stable in index) sequence by tile is exactly the (tile, depth, index) order, so the
+//    values and ranges are bit-identical to the reference (tests/test_gpu_parity.py), at
+//    ~40 bytes per key instead of ~152.
+//
+// Both paths count the keys of every tile while emitting them; one CTA (K11) turns the
+// counts into the ranges and the tile-digit pass histograms, and orders the tiles heavy
+// first for the blend kernels -- no pass over the sorted keys is needed.
 #include "common.cuh"
 
 namespace bgs {
@@ -24,20 +29,27 @@ constexpr int kRadixBins = 256;
 constexpr int kDupThreads = 256;
 constexpr int kSmemTiles = 8192;  // tile counts kept in shared memory up to this many tiles
 
-// ---------------------------------------------------------------- K9 duplicate
-__global__ void __launch_bounds__(kDupThreads) k_duplicate(int64_t n, const float4* __restrict__ record,
-                                                           const int32_t* __restrict__ radius,
-                                                           const float* __restrict__ depth,
-                                                           const uint32_t* __restrict__ offsets,
-                                                           const uint32_t* __restrict__ tiles_touched,
-                                                           int32_t tiles_x, int32_t tiles_y, int32_t num_tiles,
-                                                           const uint32_t* counters, uint64_t* keys, uint32_t* vals,
-                                                           uint32_t* tile_count, uint32_t* hist) {
+// ---------------------------------------------------------------- K9: item emission
+// A warp takes 32 consecutive Gaussians (index order) or 32 consecutive depth ranks, scans
+// their tiles_touched and emits their items 32 at a time: lane k finds its Gaussian by a
+// shuffle binary search over the inclusive scan, so a 4000-tile background Gaussian does
+// not serialise one thread and the 32 writes of a round are consecutive.
+template <bool kByRank>
+__global__ void __launch_bounds__(kDupThreads) k_emit(int64_t n, const float4* __restrict__ record,
+                                                      const int32_t* __restrict__ radius,
+                                                      const float* __restrict__ depth,
+                                                      const uint32_t* __restrict__ offsets,  // index or rank order
+                                                      const uint32_t* __restrict__ sigma,    // rank -> Gaussian
+                                                      const uint32_t* __restrict__ tiles_touched, int32_t tiles_x,
+                                                      int32_t tiles_y, int32_t num_tiles, const uint32_t* counters,
+                                                      void* keys_out, uint32_t* vals, uint32_t* tile_count,
+                                                      uint32_t* hist) {
   __shared__ uint32_t s_tc[kSmemTiles];
   __shared__ uint32_t s_h[4][kRadixBins];
   if (counters[C_OVERFLOW]) return;
   const bool smem_tiles = num_tiles <= kSmemTiles;
-  for (int k = threadIdx.x; k < 4 * kRadixBins; k += kDupThreads) (&s_h[0][0])[k] = 0;
+  if (!kByRank)
+    for (int k = threadIdx.x; k < 4 * kRadixBins; k += kDupThreads) (&s_h[0][0])[k] = 0;
   if (smem_tiles)
     for (int k = threadIdx.x; k < num_tiles; k += kDupThreads) s_tc[k] = 0;
   __syncthreads();
@@ -45,23 +57,26 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(int64_t n, const floa
   const int warps = kDupThreads / 32;
   const float ftx = (float)tiles_x, fty = (float)tiles_y;
   for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < n; base += (int64_t)gridDim.x * warps * 32) {
-    const int64_t i = base + lane;
-    uint32_t t = 0, off = 0, dbits = 0;
+    const int64_t r = base + lane;
+    uint32_t t = 0, off = 0, dbits = 0, gid = 0;
     int rx0 = 0, ry0 = 0, w = 1;
-    if (i < n) {
-      off = offsets[i];
-      t = tiles_touched[i];
+    if (r < n) {
+      gid = kByRank ? sigma[r] : (uint32_t)r;
+      off = offsets[r];
+      t = tiles_touched[gid];
       if (t) {
-        const float4 r0 = record[3 * i];
-        const int rad = radius[i];
+        const float4 r0 = record[3 * gid];
+        const int rad = radius[gid];
         // the preprocess's canonical rect expression (R11)
         rx0 = (int)fminf(ftx, fmaxf(0.0f, floorf((r0.x - (float)rad) * 0.0625f)));
         ry0 = (int)fminf(fty, fmaxf(0.0f, floorf((r0.y - (float)rad) * 0.0625f)));
         const int rx1 = (int)fminf(ftx, fmaxf(0.0f, floorf((r0.x + (float)(rad + 15)) * 0.0625f)));
         w = rx1 - rx0;
-        dbits = __float_as_uint(depth[i]);
+        if (!kByRank) {
+          dbits = __float_as_uint(depth[gid]);
 #pragma unroll
-        for (int p = 0; p < 4; ++p) atomicAdd(&s_h[p][(dbits >> (8 * p)) & 0xff], t);
+          for (int p = 0; p < 4; ++p) atomicAdd(&s_h[p][(dbits >> (8 * p)) & 0xff], t);
+        }
       }
     }
     uint32_t incl = t;
@@ -90,24 +105,153 @@ __global__ void __launch_bounds__(kDupThreads) k_duplicate(int64_t n, const floa
       const int g_x0 = __shfl_sync(0xffffffffu, rx0, g);
       const int g_y0 = __shfl_sync(0xffffffffu, ry0, g);
       const uint32_t g_d = __shfl_sync(0xffffffffu, dbits, g);
+      const uint32_t g_id = __shfl_sync(0xffffffffu, gid, g);
       if (valid) {
         const uint32_t local = kk - (g_incl - g_t);
         const uint32_t row = local / (uint32_t)g_w;
         const uint32_t tile = (uint32_t)(g_y0 + (int)row) * (uint32_t)tiles_x + (uint32_t)g_x0 +
                               (local - row * (uint32_t)g_w);
         const uint32_t pos = base_off + kk;
-        keys[pos] = ((uint64_t)tile << 32) | g_d;
-        vals[pos] = (uint32_t)(base + g);
+        if (kByRank) reinterpret_cast<uint32_t*>(keys_out)[pos] = tile;
+        else reinterpret_cast<uint64_t*>(keys_out)[pos] = ((uint64_t)tile << 32) | g_d;
+        vals[pos] = g_id;
         if (smem_tiles) atomicAdd(&s_tc[tile], 1u);
         else atomicAdd(&tile_count[tile], 1u);
       }
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < 4 * kRadixBins; k += kDupThreads) {
-    const uint32_t v = (&s_h[0][0])[k];
+  if (!kByRank)
+    for (int k = threadIdx.x; k < 4 * kRadixBins; k += kDupThreads) {
+      const uint32_t v = (&s_h[0][0])[k];
+      if (v) atomicAdd(&hist[k], v);
+    }
+  if (smem_tiles)
+    for (int k = threadIdx.x; k < num_tiles; k += kDupThreads)
+      if (s_tc[k]) atomicAdd(&tile_count[k], s_tc[k]);
+}
+
+// ---------------------------------------------------------------- depth-first path, step 1
+// 32-bit depth keys (culled: 0xffffffff, sorts last) + the 4 pass histograms.
+__global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const float* __restrict__ depth,
+                                                    const uint32_t* __restrict__ tiles_touched,
+                                                    const uint32_t* counters, uint32_t* dkey, uint32_t* dval,
+                                                    uint32_t* hist) {
+  __shared__ uint32_t s_h[8][4][kRadixBins];  // one copy per warp: conflicts stay inside a warp
+  if (counters[C_OVERFLOW]) return;
+  for (int k = threadIdx.x; k < 8 * 4 * kRadixBins; k += blockDim.x) (&s_h[0][0][0])[k] = 0;
+  __syncthreads();
+  uint32_t(*h)[kRadixBins] = s_h[threadIdx.x >> 5];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t key = tiles_touched[i] ? __float_as_uint(depth[i]) : 0xffffffffu;
+    dkey[i] = key;
+    dval[i] = (uint32_t)i;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(key >> (8 * p)) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 4 * kRadixBins; k += blockDim.x) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) v += (&s_h[w][0][0])[k];
     if (v) atomicAdd(&hist[k], v);
   }
+}
+
+// step 2: per depth rank, gather the Gaussian's tile count and rect once, with every rank
+// independent (full memory-level parallelism), packed as {x0 | y0 << 16, w | h << 16} so
+// the emission reads contiguous data instead of dependent random gathers
+__global__ void __launch_bounds__(256) k_rank_info(int64_t n, const uint32_t* __restrict__ sigma,
+                                                   const uint32_t* __restrict__ tiles_touched,
+                                                   const float4* __restrict__ record,
+                                                   const int32_t* __restrict__ radius, int32_t tiles_x,
+                                                   int32_t tiles_y, const uint32_t* counters, uint32_t* rank_cnt,
+                                                   uint2* rank_rect) {
+  if (counters[C_OVERFLOW]) return;
+  const float ftx = (float)tiles_x, fty = (float)tiles_y;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t g = sigma[r];
+    const uint32_t t = tiles_touched[g];
+    uint2 packed = make_uint2(0u, 0u);
+    if (t) {
+      const float4 r0 = record[3 * g];
+      const int rad = radius[g];
+      // the preprocess's canonical rect expression (R11)
+      const int rx0 = (int)fminf(ftx, fmaxf(0.0f, floorf((r0.x - (float)rad) * 0.0625f)));
+      const int ry0 = (int)fminf(fty, fmaxf(0.0f, floorf((r0.y - (float)rad) * 0.0625f)));
+      const int rx1 = (int)fminf(ftx, fmaxf(0.0f, floorf((r0.x + (float)(rad + 15)) * 0.0625f)));
+      packed = make_uint2((uint32_t)rx0 | ((uint32_t)ry0 << 16), (uint32_t)(rx1 - rx0));
+    }
+    rank_cnt[r] = t;
+    rank_rect[r] = packed;
+  }
+}
+
+// step 3: emission of the (tile, Gaussian) items in depth order, from the packed rank info
+__global__ void __launch_bounds__(kDupThreads) k_emit_ranked(int64_t n, const uint32_t* __restrict__ item_off,
+                                                             const uint32_t* __restrict__ sigma,
+                                                             const uint32_t* __restrict__ rank_cnt,
+                                                             const uint2* __restrict__ rank_rect, int32_t tiles_x,
+                                                             int32_t num_tiles, const uint32_t* counters,
+                                                             uint32_t* keys_out, uint32_t* vals,
+                                                             uint32_t* tile_count) {
+  __shared__ uint32_t s_tc[kSmemTiles];
+  if (counters[C_OVERFLOW]) return;
+  const bool smem_tiles = num_tiles <= kSmemTiles;
+  if (smem_tiles)
+    for (int k = threadIdx.x; k < num_tiles; k += kDupThreads) s_tc[k] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int warps = kDupThreads / 32;
+  for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < n; base += (int64_t)gridDim.x * warps * 32) {
+    const int64_t r = base + lane;
+    uint32_t t = 0, off = 0, gid = 0;
+    uint2 rc = make_uint2(0u, 1u);
+    if (r < n) {
+      t = rank_cnt[r];
+      off = item_off[r];
+      gid = sigma[r];
+      if (t) rc = rank_rect[r];
+    }
+    uint32_t incl = t;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    if (total == 0) continue;
+    const uint32_t base_off = __shfl_sync(0xffffffffu, off, 0);
+    for (uint32_t kb = 0; kb < total; kb += 32) {
+      const uint32_t k = kb + lane;
+      const bool valid = k < total;
+      const uint32_t kk = valid ? k : total - 1;
+      int lo = 0, hi = 31;  // smallest lane g with incl_g > kk
+#pragma unroll
+      for (int it = 0; it < 5; ++it) {
+        const int mid = (lo + hi) >> 1;
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, mid);
+        if (v > kk) hi = mid; else lo = mid + 1;
+      }
+      const int g = lo;
+      const uint32_t g_incl = __shfl_sync(0xffffffffu, incl, g);
+      const uint32_t g_t = __shfl_sync(0xffffffffu, t, g);
+      const uint32_t g_xy = __shfl_sync(0xffffffffu, rc.x, g);
+      const uint32_t g_w = __shfl_sync(0xffffffffu, rc.y, g);
+      const uint32_t g_id = __shfl_sync(0xffffffffu, gid, g);
+      if (valid) {
+        const uint32_t local = kk - (g_incl - g_t);
+        const uint32_t row = local / g_w;
+        const uint32_t tile = ((g_xy >> 16) + row) * (uint32_t)tiles_x + (g_xy & 0xffffu) + (local - row * g_w);
+        const uint32_t pos = base_off + kk;
+        keys_out[pos] = tile;
+        vals[pos] = g_id;
+        if (smem_tiles) atomicAdd(&s_tc[tile], 1u);
+        else atomicAdd(&tile_count[tile], 1u);
+      }
+    }
+  }
+  __syncthreads();
   if (smem_tiles)
     for (int k = threadIdx.x; k < num_tiles; k += kDupThreads)
       if (s_tc[k]) atomicAdd(&tile_count[k], s_tc[k]);
@@ -158,6 +302,8 @@ bgs_status launch_tile_order(const uint32_t* cost, int32_t num_tiles, const uint
 }
 
 // ---------------------------------------------------------------- K11: tile counts -> ranges
+// Also writes the tile-digit pass histograms hist[4 .. passes) (digit p-4 of the tile id)
+// and the heavy-first forward tile order.
 __global__ void __launch_bounds__(kOrderThreads) k_tile_scan(const uint32_t* __restrict__ tile_count, int32_t nt,
                                                               const uint32_t* counters, uint2* ranges, uint32_t* hist,
                                                               int passes, uint32_t* order) {
@@ -197,34 +343,79 @@ __global__ void __launch_bounds__(kOrderThreads) k_tile_scan(const uint32_t* __r
   order_tiles(tile_count, nt, order, s_b);
 }
 
+static bgs_status memset_status(Frame* F, cudaStream_t s) {
+  if (cudaMemsetAsync(F->sort_status, 0, 4 * kRadixBins * (size_t)F->sort_tiles_max, s) != cudaSuccess)
+    return check_launch("sort status memset");
+  return BGS_OK;
+}
+
 bgs_status launch_sort(Frame* F, cudaStream_t s) {
   if (cudaMemsetAsync(F->ranges, 0, 8 * (size_t)F->num_tiles, s) != cudaSuccess ||
       cudaMemsetAsync(F->tile_count, 0, 4 * (size_t)F->num_tiles, s) != cudaSuccess ||
       cudaMemsetAsync(F->sort_hist, 0, 4 * 8 * kRadixBins, s) != cudaSuccess ||
-      cudaMemsetAsync(F->counters + C_SORT_TICKET, 0, 4 * 8, s) != cudaSuccess)
+      cudaMemsetAsync(F->counters + C_SORT_TICKET, 0, 4 * 8, s) != cudaSuccess ||
+      cudaMemsetAsync(F->counters + C_SORT32_TICKET, 0, 4 * 8, s) != cudaSuccess)
     return check_launch("sort memset");
-  if (F->n == 0) {
-    // empty scene: identity tile order, no keys
-    return launch_tile_order(F->tile_count, F->num_tiles, F->counters, F->tile_order, s);
-  }
-  const int grid = 4 * num_sms();
-  k_duplicate<<<grid, kDupThreads, 0, s>>>(F->n, F->record, F->radius, F->depth, F->offsets, F->tiles_touched,
-                                           F->tiles_x, F->tiles_y, F->num_tiles, F->counters, F->keys[0], F->vals[0],
-                                           F->tile_count, F->sort_hist);
-  note_launch();
-  bgs_status st = check_launch("k_duplicate");
-  if (st != BGS_OK) return st;
+  const bool ref64 = (F->debug_flags & (BGS_DEBUG_SORT_ONESWEEP64 | BGS_DEBUG_SKIP_SORT)) != 0;
   const int P = F->sort_passes;
+  F->sort_mode = ref64 ? 1 : 0;
+  F->final_buf = ref64 ? (P & 1) : ((P - 4) & 1);
+  if (F->n == 0) return launch_tile_order(F->tile_count, F->num_tiles, F->counters, F->tile_order, s);
+  const int grid = 4 * num_sms();
+  bgs_status st;
+  if (ref64) {
+    k_emit<false><<<grid, kDupThreads, 0, s>>>(F->n, F->record, F->radius, F->depth, F->offsets, nullptr,
+                                               F->tiles_touched, F->tiles_x, F->tiles_y, F->num_tiles, F->counters,
+                                               F->keys[0], F->vals[0], F->tile_count, F->sort_hist);
+    note_launch();
+    if ((st = check_launch("k_emit<index>")) != BGS_OK) return st;
+    k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, F->num_tiles, F->counters, F->ranges, F->sort_hist, P,
+                                            F->tile_order);
+    note_launch();
+    if ((st = check_launch("k_tile_scan")) != BGS_OK || (F->debug_flags & BGS_DEBUG_SKIP_SORT)) return st;
+    for (int p = 0; p < P; ++p) {
+      if ((st = memset_status(F, s)) != BGS_OK) return st;
+      const int a = p & 1, b = (p + 1) & 1;
+      st = launch_sort_pass(F->keys[a], F->vals[a], F->keys[b], F->vals[b], F->sort_hist + p * kRadixBins,
+                            F->sort_status, F->counters + C_SORT_TICKET + p, F->counters, 8 * p, s);
+      if (st != BGS_OK) return st;
+    }
+    return BGS_OK;
+  }
+  // ---- depth first: (1) stable sort of the Gaussians by depth bits
+  k_depth_keys<<<grid, 256, 0, s>>>(F->n, F->depth, F->tiles_touched, F->counters, F->dkey[0], F->dval[0],
+                                    F->sort_hist);
+  note_launch();
+  if ((st = check_launch("k_depth_keys")) != BGS_OK) return st;
+  for (int p = 0; p < 4; ++p) {
+    if ((st = memset_status(F, s)) != BGS_OK) return st;
+    const int a = p & 1, b = (p + 1) & 1;
+    st = launch_sort_pass32(F->dkey[a], F->dval[a], F->dkey[b], F->dval[b], F->sort_hist + p * kRadixBins,
+                            F->sort_status, F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, F->n, s);
+    if (st != BGS_OK) return st;
+  }
+  // (2) per-rank tile counts and rects, item offsets in depth order
+  k_rank_info<<<grid, 256, 0, s>>>(F->n, F->dval[0], F->tiles_touched, F->record, F->radius, F->tiles_x, F->tiles_y,
+                                   F->counters, F->rank_cnt, F->rank_rect);
+  note_launch();
+  if ((st = check_launch("k_rank_info")) != BGS_OK) return st;
+  if ((st = launch_scan(F->rank_cnt, F->item_off, F->n, F, false, s)) != BGS_OK) return st;
+  // (3) (tile, Gaussian) items in depth order + per-tile counts
+  uint32_t* tkey[2] = {reinterpret_cast<uint32_t*>(F->keys[0]), reinterpret_cast<uint32_t*>(F->keys[1])};
+  k_emit_ranked<<<grid, kDupThreads, 0, s>>>(F->n, F->item_off, F->dval[0], F->rank_cnt, F->rank_rect, F->tiles_x,
+                                             F->num_tiles, F->counters, tkey[0], F->vals[0], F->tile_count);
+  note_launch();
+  if ((st = check_launch("k_emit_ranked")) != BGS_OK) return st;
   k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, F->num_tiles, F->counters, F->ranges, F->sort_hist, P,
                                           F->tile_order);
   note_launch();
-  if ((st = check_launch("k_tile_scan")) != BGS_OK || (F->debug_flags & BGS_DEBUG_SKIP_SORT)) return st;
-  for (int p = 0; p < P; ++p) {
-    if (cudaMemsetAsync(F->sort_status, 0, 4 * kRadixBins * (size_t)F->sort_tiles_max, s) != cudaSuccess)
-      return check_launch("sort status memset");
+  if ((st = check_launch("k_tile_scan")) != BGS_OK) return st;
+  // (4) stable split by tile id
+  for (int p = 0; p < P - 4; ++p) {
+    if ((st = memset_status(F, s)) != BGS_OK) return st;
     const int a = p & 1, b = (p + 1) & 1;
-    st = launch_sort_pass(F->keys[a], F->vals[a], F->keys[b], F->vals[b], F->sort_hist + p * kRadixBins,
-                          F->sort_status, F->counters + C_SORT_TICKET + p, F->counters, 8 * p, s);
+    st = launch_sort_pass32(tkey[a], F->vals[a], tkey[b], F->vals[b], F->sort_hist + (4 + p) * kRadixBins,
+                            F->sort_status, F->counters + C_SORT32_TICKET + 4 + p, F->counters, 8 * p, -1, s);
     if (st != BGS_OK) return st;
   }
   return BGS_OK;

@@ -44,10 +44,10 @@ def scenes():
     }
 
 
-def run_gpu(bgs, s, cam, max_keys=1 << 21, skip_sort=False):
+def run_gpu(bgs, s, cam, max_keys=1 << 21, skip_sort=False, flags=0):
     dev = torch.device("cuda")
     theta = torch.from_numpy(s.theta).to(dev)
-    r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=max_keys, device=dev)
+    r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=max_keys, device=dev, debug_flags=flags)
     if skip_sort:
         bgs.bgs_frame_set_debug(r.frame, bgs.BGS_DEBUG_SKIP_SORT)
         g = bgs.gaussians(theta, s.n, s.sh_degree)
@@ -135,16 +135,41 @@ def test_unsorted_keys_parity(bgs, name):
 
 
 @pytest.mark.parametrize("name", list(scenes()))
-def test_sort_and_ranges_parity(bgs, name):
+@pytest.mark.parametrize("path", ["depth_first", "onesweep64"])
+def test_sort_and_ranges_parity(bgs, name, path):
     s = scenes()[name]()
     cam = s.cameras[0]
-    r, _, _ = run_gpu(bgs, s, cam)
+    flags = bgs.BGS_DEBUG_SORT_ONESWEEP64 if path == "onesweep64" else 0
+    r, _, _ = run_gpu(bgs, s, cam, flags=flags)
     ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
     K = ref["srt"]["K"]
     v = views(bgs, r, s.n, K, len(ref["srt"]["ranges"]))
-    assert np.array_equal(v["keys_sorted"], ref["srt"]["sorted_keys"])
+    assert r.views().sort_mode == (1 if path == "onesweep64" else 0)
+    if path == "onesweep64":
+        assert np.array_equal(v["keys_sorted"], ref["srt"]["sorted_keys"])
     assert np.array_equal(v["values_sorted"], ref["srt"]["sorted_values"])
     assert np.array_equal(v["ranges"], ref["srt"]["ranges"])
+
+
+def test_sort_paths_identical_at_garden_scale(bgs):
+    """The depth-first path and the 64-bit onesweep reference give bit-identical tile lists
+    on a full-size garden view (K ~ 4.8e7), where exact depth ties do occur."""
+    s = gen.garden()
+    cam = s.cameras[8]
+    outs = []
+    for flags in (0, bgs.BGS_DEBUG_SORT_ONESWEEP64):
+        r, _, out = run_gpu(bgs, s, cam, max_keys=1 << 26, flags=flags)
+        K = r.num_keys
+        v = r.views()
+        nt = v.tiles_x * v.tiles_y
+        outs.append((K, torch.as_tensor(_DevPtr(v.values_sorted, K, "<i4"), device="cuda").clone(),
+                     torch.as_tensor(_DevPtr(v.ranges, 2 * nt, "<i4"), device="cuda").clone(),
+                     out["image"].clone(), out["n_contrib"].clone()))
+        del r
+    (K0, v0, r0, i0, n0), (K1, v1, r1, i1, n1) = outs
+    assert K0 == K1 and K0 > 10_000_000
+    assert torch.equal(v0, v1) and torch.equal(r0, r1)
+    assert torch.equal(i0, i1) and torch.equal(n0, n1)
 
 
 @pytest.mark.parametrize("name", list(scenes()))

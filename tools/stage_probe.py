@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--config", default="garden")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--view", type=int, default=0)
+    ap.add_argument("--only", default=None, help="comma-separated stage names")
     a = ap.parse_args()
     t0 = time.time()
     s = gen.make(a.config)
@@ -40,7 +41,10 @@ def main():
         "blend_bwd": lambda: bgs.bgs_blend_bwd(r.frame, dl, r.final_T, r.n_contrib),
         "preprocess_bwd": lambda: bgs.bgs_preprocess_bwd(g, r.frame, grad),
     }
+    only = set(a.only.split(",")) if a.only else None
     for name, fn in stages.items():
+        if only and name not in only:
+            continue
         fn()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
