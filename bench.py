@@ -128,6 +128,7 @@ def run_ours(args, rank, world, local_rank):
 
     import gen
     import paper_2510_14564_b200 as bgs
+    from paper_2510_14564_b200 import dp
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -136,12 +137,11 @@ def run_ours(args, rank, world, local_rank):
     n = scene.n
     cams_all = scene.cameras
     views = batch_views(args.views, len(cams_all))
-    mine = [v for i, v in enumerate(views) if i % world == rank]
+    mine = dp.views_for_rank(views, rank, world)
     cams = [cams_all[v] for v in mine]
     W, H = cams[0].width, cams[0].height
     theta = torch.from_numpy(scene.theta).to(dev)
-    if world > 1:
-        dist.broadcast(theta, 0)  # replicas start identical
+    dp.broadcast_params(theta, world)  # replicas start identical
     grad = torch.zeros_like(theta)
     m = torch.zeros_like(theta)
     v = torch.zeros_like(theta)
@@ -179,59 +179,47 @@ def run_ours(args, rank, world, local_rank):
     cam_structs = [bgs.camera(c) for c in cams]
     stream = torch.cuda.current_stream()
     stage_names = ["preprocess", "sort", "render_fwd", "loss", "blend_bwd", "preprocess_bwd", "allreduce", "adam"]
-    ev_pool = {}
-
-    def ev(name, i):
-        key = (name, i)
-        if key not in ev_pool:
-            ev_pool[key] = torch.cuda.Event(enable_timing=True)
-        return ev_pool[key]
-
+    # all timing events of the timed region are created up front (creating them inside the
+    # loop adds host work between launches)
+    n_marks = args.steps * (7 * len(cam_structs) + 3)
+    pool = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
     step_no = [0]
 
     def one_step(tgts, record=None):
         step_no[0] += 1
+
+        def mark(marks):
+            if record is not None:
+                e = pool[record["next"]]
+                record["next"] += 1
+                e.record(stream)
+                marks.append(e)
+
         for j, cs in enumerate(cam_structs):
             marks = []
-
-            def mark():
-                if record is not None:
-                    e = torch.cuda.Event(enable_timing=True)
-                    e.record(stream)
-                    marks.append(e)
-
-            mark()
+            mark(marks)
             bgs.bgs_preprocess(gs, cs, rend.frame)
-            mark()
+            mark(marks)
             bgs.bgs_sort(rend.frame)
-            mark()
+            mark(marks)
             bgs.bgs_render_fwd(rend.frame, rend.image, rend.final_T, rend.n_contrib)
-            mark()
+            mark(marks)
             bgs.bgs_l1_loss_grad(rend.image, tgts[j], W, H, scale, dl, loss)
-            mark()
+            mark(marks)
             bgs.bgs_blend_bwd(rend.frame, dl, rend.final_T, rend.n_contrib)
-            mark()
+            mark(marks)
             bgs.bgs_preprocess_bwd(gs, rend.frame, grad)
-            mark()
+            mark(marks)
             if record is not None:
-                record.append(("view", marks))
+                record["marks"].append(("view", marks))
         marks = []
-        if record is not None:
-            e = torch.cuda.Event(enable_timing=True)
-            e.record(stream)
-            marks.append(e)
-        if world > 1:
-            dist.all_reduce(grad)
-        if record is not None:
-            e = torch.cuda.Event(enable_timing=True)
-            e.record(stream)
-            marks.append(e)
+        mark(marks)
+        dp.allreduce_grads(grad, world)  # NCCL over NVLink (one exchange per batch)
+        mark(marks)
         bgs.bgs_adam_step(theta, grad, m, v, n, hp, step_no[0])
+        mark(marks)
         if record is not None:
-            e = torch.cuda.Event(enable_timing=True)
-            e.record(stream)
-            marks.append(e)
-            record.append(("batch", marks))
+            record["marks"].append(("batch", marks))
 
     def barrier():
         if world > 1:
@@ -243,7 +231,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     # ---- device-resident timed region (inputs larger than L2: theta 1.37 GB, keys GBs)
-    record = []
+    record = {"next": 0, "marks": []}
     barrier()
     torch.cuda.synchronize()
     launches0 = bgs.launch_count()
@@ -262,7 +250,7 @@ def run_ours(args, rank, world, local_rank):
     assert st == bgs.BGS_OK, "key capacity overflow in the timed region"
     # per-stage means
     sums = {s: 0.0 for s in stage_names}
-    for kind, mk in record:
+    for kind, mk in record["marks"]:
         if kind == "view":
             for s, a, b in zip(stage_names[:6], mk[:-1], mk[1:]):
                 sums[s] += a.elapsed_time(b)
