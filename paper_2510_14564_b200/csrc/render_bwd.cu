@@ -5,16 +5,18 @@
 // rect, power/alpha skips, early stop, the 0.99 alpha clamp -> zero gradient to o and G,
 // the SH clamp, the J-clamp branch).
 //
-// Same workload-balanced mapping as the forward: independent warps of a persistent grid
-// pull (tile, 8x4 block) items heaviest first -- by the forward's per-tile largest
-// n_contrib -- and each walks its tile list back to front from its own block's largest
-// n_contrib, 32 entries at a time, compacted to the entries whose alpha >= 1/255 box
-// reaches the block (exact, as in the forward).  Per pixel: T_i = T_{i+1} / (1 - alpha_i),
-// the colour behind accumulates S += c alpha T (S starts at T_final bg), and each
-// evaluated entry yields 9 partials {dxy(2), dconic(3), dopacity, drgb(3)}, summed across
-// the warp with shuffles; lane 0 then issues two 16-byte vector REDs and one scalar RED
-// into grad2d[id] -- instead of 3DGS's nine scalar global atomics per evaluated
-// (pixel, Gaussian).
+// Workload-balanced mapping: independent warps of a persistent grid pull (tile, 8x4 block)
+// items heaviest first -- by the forward's per-tile largest n_contrib -- so no warp waits
+// on another.  A warp walks its tile list back to front from its own block's largest
+// n_contrib, 32 entries per step, compacted to the entries whose alpha >= 1/255 box
+// reaches the block (exact, as in the forward).  The step loop is software-pipelined:
+// list ids are fetched three steps ahead, the 16-byte cull records {x,y,ex,ey} two steps
+// ahead, and the full records of the hits one step ahead, so the gathers overlap the
+// walk.  Per pixel: T_i = T_{i+1} / (1 - alpha_i), the colour behind accumulates
+// S += c alpha T (S starts at T_final bg), and each evaluated entry yields 9 partials
+// {dxy(2), dconic(3), dopacity, drgb(3)}.  A reduce-scatter butterfly (12 shuffles) leaves
+// the 9 warp totals on 9 lanes, which add them into grad2d[id] with one 9-lane RED
+// instruction -- instead of 3DGS's nine scalar global atomics per evaluated pair.
 //
 // K13 (the chain rule to theta) is in preprocess_bwd.cu.
 #include "common.cuh"
@@ -23,15 +25,39 @@ namespace bgs {
 
 constexpr int kBwdWarpsPerCta = 4;
 
-__device__ __forceinline__ float warp_sum(float v) {
+// Reduce-scatter of 9 per-lane values over the warp: each butterfly step halves the set of
+// values a lane carries (5 -> 3 -> 2 -> 1 -> 1 shuffles: 12 instead of 9 x 5 = 45).  On
+// return lane l holds the warp total of value `idx`, or idx = -1 (padding / duplicate).
+__device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane, int& idx) {
+  const bool a = lane & 16, b = lane & 8, c = lane & 4, d = lane & 2;
+  float s[5];
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-  return v;
+  for (int j = 0; j < 5; ++j) {
+    const float lo = v[j], hi = j < 4 ? v[5 + j] : 0.0f;
+    s[j] = (a ? hi : lo) + __shfl_xor_sync(0xffffffffu, a ? lo : hi, 16);
+  }
+  float t[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const float lo = s[j], hi = j < 2 ? s[3 + j] : 0.0f;
+    t[j] = (b ? hi : lo) + __shfl_xor_sync(0xffffffffu, b ? lo : hi, 8);
+  }
+  float u[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const float lo = t[j], hi = j < 1 ? t[2] : 0.0f;
+    u[j] = (c ? hi : lo) + __shfl_xor_sync(0xffffffffu, c ? lo : hi, 4);
+  }
+  float w = (d ? u[1] : u[0]) + __shfl_xor_sync(0xffffffffu, d ? u[0] : u[1], 2);
+  w += __shfl_xor_sync(0xffffffffu, w, 1);
+  const int slot = (b ? 3 : 0) + (c ? 2 : 0) + (d ? 1 : 0);
+  const bool valid = (b ? !c : !(c && d)) && !(a && slot == 4) && !(lane & 1);
+  idx = valid ? (a ? 5 : 0) + slot : -1;
+  return w;
 }
 
-__device__ __forceinline__ void red_add_v4(float4* addr, float4 v) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
+__device__ __forceinline__ bool box_hits(const float4 a, float bx0, float by0, float bx1, float by1) {
+  return a.x + a.z >= bx0 && a.x - a.z <= bx1 && a.y + a.w >= by0 && a.y - a.w <= by1;
 }
 
 __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
@@ -51,6 +77,7 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
   uint32_t* spos = s_pos[warp];
   uint32_t* sid = s_id[warp];
   const int64_t plane = (int64_t)cam.W * cam.H;
+  const float4 none = make_float4(-1e30f, -1e30f, -1e30f, -1e30f);
   while (true) {
     uint32_t item = 0;
     if (lane == 0) item = atomicAdd(ticket, 1u);
@@ -67,7 +94,7 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     if (overflow) rg = make_uint2(0, 0);
     const int64_t pix = (int64_t)py * cam.W + px;
     const uint32_t my_last = inside ? n_contrib[pix] : 0u;
-    const uint32_t wmax = min(__reduce_max_sync(0xffffffffu, my_last), rg.y - rg.x);
+    const int wmax = (int)min(__reduce_max_sync(0xffffffffu, my_last), rg.y - rg.x);
     if (wmax == 0) continue;
     float T = inside ? final_T[pix] : 1.0f;
     float dLr = 0.f, dLg = 0.f, dLb = 0.f;
@@ -77,27 +104,48 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
       dLb = dl_dimage[2 * plane + pix];
     }
     float Sr = T * cam.bg[0], Sg = T * cam.bg[1], Sb = T * cam.bg[2];
-    for (int end = (int)wmax; end > 0; end -= 32) {
-      const int begin = end - 32;  // may be negative: those lanes are idle
-      const int posl = begin + lane;
-      bool hit = false;
-      uint32_t id = 0;
-      float4 a;
-      if (posl >= 0) {
-        id = __ldg(values + rg.x + (uint32_t)posl);
-        a = __ldg(record + 3 * id);
-        hit = a.x + a.z >= bx0 && a.x - a.z <= bx1 && a.y + a.w >= by0 && a.y - a.w <= by1;
-      }
-      const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-      if (hit) {
+    const int nst = (wmax + 31) / 32;
+    // lane's list position in step s (back to front; negative = no entry)
+    auto pos_of = [&](int s) { return wmax - 32 * (s + 1) + lane; };
+    auto load_id = [&](int s) -> uint32_t {
+      const int p = pos_of(s);
+      return (s < nst && p >= 0) ? __ldg(values + rg.x + (uint32_t)p) : 0xffffffffu;
+    };
+    auto load_cull = [&](uint32_t id) { return id != 0xffffffffu ? __ldg(record + 3 * id) : none; };
+    // pipeline prologue: step 0 fully, step 1 cull record, step 2 id
+    uint32_t id_c = load_id(0);
+    float4 a_c = load_cull(id_c);
+    uint32_t id_n = load_id(1);
+    float4 a_n = load_cull(id_n);
+    uint32_t id_nn = load_id(2);
+    bool h_c = box_hits(a_c, bx0, by0, bx1, by1);
+    float4 r1_c = none, r2_c = none;
+    if (h_c) {
+      r1_c = __ldg(record + 3 * id_c + 1);
+      r2_c = __ldg(record + 3 * id_c + 2);
+    }
+    for (int s = 0; s < nst; ++s) {
+      // (1) commit step s into the warp's shared-memory slice
+      const uint32_t bal = __ballot_sync(0xffffffffu, h_c);
+      if (h_c) {
         const int q = __popc(bal & lt);
-        sr0[q] = a;
-        sr1[q] = __ldg(record + 3 * id + 1);
-        sr2[q] = __ldg(record + 3 * id + 2);
-        spos[q] = (uint32_t)posl;
-        sid[q] = id;
+        sr0[q] = a_c;
+        sr1[q] = r1_c;
+        sr2[q] = r2_c;
+        spos[q] = (uint32_t)pos_of(s);
+        sid[q] = id_c;
       }
       __syncwarp();
+      // (2) step s+1: hit test and its full records; (3) step s+2 cull record, s+3 id
+      const bool h_n = box_hits(a_n, bx0, by0, bx1, by1);
+      float4 r1_n = none, r2_n = none;
+      if (h_n) {
+        r1_n = __ldg(record + 3 * id_n + 1);
+        r2_n = __ldg(record + 3 * id_n + 2);
+      }
+      const float4 a_nn = load_cull(id_nn);
+      const uint32_t id_nnn = load_id(s + 3);
+      // (4) walk step s, back to front
       const int m = __popc(bal);
       for (int k = m - 1; k >= 0; --k) {
         const uint32_t pos = spos[k];
@@ -138,18 +186,23 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
           }
         }
         if (__any_sync(0xffffffffu, act)) {
-          g0 = warp_sum(g0); g1 = warp_sum(g1); g2 = warp_sum(g2);
-          g3 = warp_sum(g3); g4 = warp_sum(g4); g5 = warp_sum(g5);
-          g6 = warp_sum(g6); g7 = warp_sum(g7); g8 = warp_sum(g8);
-          if (lane == 0) {
-            float4* dst = grad2d + 3 * sid[k];
-            red_add_v4(dst, make_float4(g0, g1, g2, g3));
-            red_add_v4(dst + 1, make_float4(g4, g5, g6, g7));
-            atomicAdd(&dst[2].x, g8);
-          }
+          const float gv[9] = {g0, g1, g2, g3, g4, g5, g6, g7, g8};
+          int idx;
+          const float tot = warp_reduce_scatter9(gv, lane, idx);
+          // 9 lanes, 9 consecutive floats of grad2d[id]: one RED instruction
+          if (idx >= 0) atomicAdd(reinterpret_cast<float*>(grad2d + 3 * sid[k]) + idx, tot);
         }
       }
       __syncwarp();
+      // rotate the pipeline
+      id_c = id_n;
+      a_c = a_n;
+      h_c = h_n;
+      r1_c = r1_n;
+      r2_c = r2_n;
+      id_n = id_nn;
+      a_n = a_nn;
+      id_nn = id_nnn;
     }
   }
 }
