@@ -7,129 +7,112 @@
 // with --fmad=false); G uses MUFU.EX2 (R23 near-tie rule covers the few-ulp difference).
 //
 // Workload-balanced mapping (the paper's Challenge-2: with one thread
-// per pixel walking in lock-step over a tile, the slowest pixels set the pace):
-//  * one CTA per 16x16 tile, heaviest tiles first (k_tile_scan orders tiles by list length);
-//  * warp-specialised: a producer warp streams the tile list in 256-entry batches into a
-//    4-slot shared-memory ring -- the B200 form of the paper's T3 batch loading of
-//    per-Gaussian contiguous RGB into shared memory: 48-byte
-//    records {x,y,ex,ey | A,B,C,o | r,g,b,cbits} gathered with 16-byte loads -- and 8
-//    consumer warps, one per 8x4 pixel block, each take the batches at their own pace
-//    (mbarrier full/empty handshakes), so a warp whose pixels are busy never holds up
-//    the others, and the CTA only stops streaming once every warp's pixels are done;
-//  * per batch a consumer warp compacts the entries whose conservative alpha >= 1/255
-//    box (ex, ey) reaches its block -- the rest would be skipped by all 32 of its pixels --
-//    and its pixels walk only those.  List positions are kept, so n_contrib and every
-//    decision are those of the plain per-pixel walk.
+// per pixel walking a tile in lock-step, the slowest pixels and longest tiles set the
+// pace): the unit of work is one warp x one 8x4 pixel block of a tile (one pixel per
+// lane).  A persistent grid of independent warps pulls these (tile, block) items from a
+// global ticket, heaviest tiles first (k_tile_scan orders tiles by list length), so no
+// warp waits on another and a warp leaves its tile as soon as its own 32 pixels are done.
+// A warp streams its tile's list 32 entries per step: each lane gathers one entry's
+// 16-byte cull record {x, y, ex, ey} and tests the conservative alpha >= 1/255 box against
+// the block; the hits (about a fifth of the list on the garden workload) are compacted
+// with a ballot and their 48-byte records {x,y,ex,ey | A,B,C,o | r,g,b,cbits} staged in the
+// warp's slice of shared memory -- the B200 form of the paper's T3 batch loading of
+// per-Gaussian contiguous RGB.  The step loop is
+// software-pipelined (ids three steps ahead, cull records two, hit records one), so the
+// gathers overlap the walk.  List positions are kept, so n_contrib and every decision
+// are those of the plain per-pixel walk.
 #include "common.cuh"
 
 namespace bgs {
 
-constexpr int kBatch = 256;
-constexpr int kRing = 4;
-constexpr int kConsumers = 8;
-constexpr int kFwdThreads = (kConsumers + 1) * 32;
+constexpr int kFwdWarps = 4;
 
-struct FwdSmem {
-  float4 r0[kRing][kBatch];
-  float4 r1[kRing][kBatch];
-  float4 r2[kRing][kBatch];
-  uint32_t cnt[kRing];
-  uint64_t full[kRing];
-  uint64_t empty[kRing];
-  uint8_t list[kConsumers][kBatch];
-  int alive;
-  uint32_t cost;
-};
+__device__ __forceinline__ bool box_hits_f(const float4 a, float bx0, float by0, float bx1, float by1) {
+  return a.x + a.z >= bx0 && a.x - a.z <= bx1 && a.y + a.w >= by0 && a.y - a.w <= by1;
+}
 
-__global__ void __launch_bounds__(kFwdThreads) k_render_fwd(const uint2* __restrict__ ranges,
-                                                             const uint32_t* __restrict__ values,
-                                                             const float4* __restrict__ record,
-                                                             const uint32_t* __restrict__ counters, Cam cam,
-                                                             const uint32_t* __restrict__ tile_order,
-                                                             float* __restrict__ image, float* __restrict__ final_T,
-                                                             uint32_t* __restrict__ n_contrib,
-                                                             uint32_t* __restrict__ tile_cost) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  FwdSmem& S = *reinterpret_cast<FwdSmem*>(smem_raw);
-  const int tile = (int)tile_order[blockIdx.x];
-  const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+__global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const uint2* __restrict__ ranges,
+                                                                const uint32_t* __restrict__ values,
+                                                                const float4* __restrict__ record,
+                                                                const uint32_t* __restrict__ counters, Cam cam,
+                                                                const uint32_t* __restrict__ tile_order,
+                                                                uint32_t n_items, uint32_t* ticket,
+                                                                float* __restrict__ image, float* __restrict__ final_T,
+                                                                uint32_t* __restrict__ n_contrib,
+                                                                uint32_t* __restrict__ tile_cost) {
+  __shared__ float4 s_rec[kFwdWarps][3][32];
+  __shared__ uint32_t s_pos[kFwdWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint2 rg = ranges[tile];
-  if (counters[C_OVERFLOW]) rg = make_uint2(0, 0);
-  const uint32_t len = rg.y - rg.x;
-  const int nb = (int)((len + kBatch - 1) / kBatch);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kRing; ++s) {
-      mbar_init(&S.full[s], 32);         // the producer warp's 32 lanes
-      mbar_init(&S.empty[s], kConsumers);  // one arrive per consumer warp
-    }
-    S.alive = kConsumers;
-    S.cost = 0;
-  }
-  __syncthreads();
-  if (warp == kConsumers) {
-    // ------------------------------------------------ producer warp
-    for (int b = 0; b < nb; ++b) {
-      const int slot = b & (kRing - 1);
-      if (b >= kRing) mbar_wait(&S.empty[slot], (uint32_t)((b / kRing) - 1) & 1u);
-      const int alive = *(volatile int*)&S.alive;
-      const int cnt = alive ? (int)min((uint32_t)kBatch, len - (uint32_t)b * kBatch) : 0;
-      const uint32_t j0 = rg.x + (uint32_t)b * kBatch;
-      for (int e = lane; e < cnt; e += 32) {
-        const uint32_t id = __ldg(values + j0 + e);
-        S.r0[slot][e] = __ldg(record + 3 * id);
-        S.r1[slot][e] = __ldg(record + 3 * id + 1);
-        S.r2[slot][e] = __ldg(record + 3 * id + 2);
-      }
-      if (lane == 0) S.cnt[slot] = (uint32_t)cnt;
-      __syncwarp();
-      mbar_arrive(&S.full[slot]);
-    }
-  } else {
-    // ------------------------------------------------ consumer warp: one 8x4 pixel block
-    const int bx = tx * kTile + (warp & 1) * 8, by = ty * kTile + (warp >> 1) * 4;
+  const uint32_t lt = lanemask_lt();
+  const bool overflow = counters[C_OVERFLOW] != 0;
+  float4* sr0 = s_rec[warp][0];
+  float4* sr1 = s_rec[warp][1];
+  float4* sr2 = s_rec[warp][2];
+  uint32_t* spos = s_pos[warp];
+  const float4 none = make_float4(-1e30f, -1e30f, -1e30f, -1e30f);
+  while (true) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(ticket, 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    const int tile = (int)tile_order[item >> 3], blk = (int)(item & 7);
+    const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
+    const int bx = tx * kTile + (blk & 1) * 8, by = ty * kTile + (blk >> 1) * 4;
     const int px = bx + (lane & 7), py = by + (lane >> 3);
     const float bx0 = (float)bx, by0 = (float)by, bx1 = bx0 + 7.0f, by1 = by0 + 3.0f;
     const bool inside = px < cam.W && py < cam.H;
     const float pxf = (float)px, pyf = (float)py;
-    const uint32_t lt = lanemask_lt();
-    uint8_t* list = S.list[warp];
+    uint2 rg = ranges[tile];
+    if (overflow) rg = make_uint2(0, 0);
+    const int len = (int)(rg.y - rg.x);
+    const int nst = (len + 31) / 32;
     bool done = !inside;
-    bool reported = false;
     float T = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f;
     uint32_t last = 0;
-    for (int b = 0; b < nb; ++b) {
-      const int slot = b & (kRing - 1);
-      mbar_wait(&S.full[slot], (uint32_t)(b / kRing) & 1u);
-      const int cnt = (int)S.cnt[slot];
-      const bool all_done = __all_sync(0xffffffffu, done);
-      if (all_done && !reported) {
-        if (lane == 0) atomicSub(&S.alive, 1);
-        reported = true;
+    auto load_id = [&](int s) -> uint32_t {
+      const int p = 32 * s + lane;
+      return (p < len) ? __ldg(values + rg.x + (uint32_t)p) : 0xffffffffu;
+    };
+    auto load_cull = [&](uint32_t id) { return id != 0xffffffffu ? __ldg(record + 3 * id) : none; };
+    if (nst > 0 && !__all_sync(0xffffffffu, done)) {
+      // pipeline prologue: step 0 fully, step 1 cull record, step 2 id
+      uint32_t id_c = load_id(0);
+      float4 a_c = load_cull(id_c);
+      uint32_t id_n = load_id(1);
+      float4 a_n = load_cull(id_n);
+      uint32_t id_nn = load_id(2);
+      bool h_c = box_hits_f(a_c, bx0, by0, bx1, by1);
+      float4 r1_c = none, r2_c = none;
+      if (h_c) {
+        r1_c = __ldg(record + 3 * id_c + 1);
+        r2_c = __ldg(record + 3 * id_c + 2);
       }
-      if (!all_done && cnt > 0) {
-        const float4* r0s = S.r0[slot];
-        const float4* r1s = S.r1[slot];
-        const float4* r2s = S.r2[slot];
-        int m = 0;
-        for (int r = 0; r * 32 < cnt; ++r) {
-          const int e = r * 32 + lane;
-          bool hit = false;
-          if (e < cnt) {
-            const float4 a = r0s[e];
-            hit = a.x + a.z >= bx0 && a.x - a.z <= bx1 && a.y + a.w >= by0 && a.y - a.w <= by1;
-          }
-          const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-          if (hit) list[m + __popc(bal & lt)] = (uint8_t)e;
-          m += __popc(bal);
+      for (int s = 0; s < nst; ++s) {
+        // (1) commit step s into the warp's shared-memory slice
+        const uint32_t bal = __ballot_sync(0xffffffffu, h_c);
+        if (h_c) {
+          const int q = __popc(bal & lt);
+          sr0[q] = a_c;
+          sr1[q] = r1_c;
+          sr2[q] = r2_c;
+          spos[q] = (uint32_t)(32 * s + lane);
         }
         __syncwarp();
-        const uint32_t pos0 = (uint32_t)b * kBatch + 1u;
+        // (2) step s+1 hit test and records; (3) step s+2 cull record, step s+3 id
+        const bool h_n = box_hits_f(a_n, bx0, by0, bx1, by1);
+        float4 r1_n = none, r2_n = none;
+        if (h_n) {
+          r1_n = __ldg(record + 3 * id_n + 1);
+          r2_n = __ldg(record + 3 * id_n + 2);
+        }
+        const float4 a_nn = load_cull(id_nn);
+        const uint32_t id_nnn = load_id(s + 3);
+        // (4) walk step s
+        const int m = __popc(bal);
         for (int k = 0; k < m && !done; ++k) {
-          const int e = list[k];
-          const float4 r0 = r0s[e];
+          const float4 r0 = sr0[k];
           const float dx = r0.x - pxf, dy = r0.y - pyf;
-          const float4 r1 = r1s[e];
+          const float4 r1 = sr1[k];
           const float power = fmaf(r1.x, dx * dx, fmaf(r1.z, dy * dy, r1.y * (dx * dy)));
           if (power > 0.0f) continue;
           const float alpha = fminf(0.99f, r1.w * fast_exp(power));
@@ -140,16 +123,24 @@ __global__ void __launch_bounds__(kFwdThreads) k_render_fwd(const uint2* __restr
             break;
           }
           const float w = alpha * T;
-          const float4 r2 = r2s[e];
+          const float4 r2 = sr2[k];
           Cr = fmaf(r2.x, w, Cr);
           Cg = fmaf(r2.y, w, Cg);
           Cb = fmaf(r2.z, w, Cb);
           T = tT;
-          last = pos0 + (uint32_t)e;
+          last = spos[k] + 1u;
         }
-        __syncwarp();
+        if (__all_sync(0xffffffffu, done)) break;
+        // rotate the pipeline
+        id_c = id_n;
+        a_c = a_n;
+        h_c = h_n;
+        r1_c = r1_n;
+        r2_c = r2_n;
+        id_n = id_nn;
+        a_n = a_nn;
+        id_nn = id_nnn;
       }
-      if (lane == 0) mbar_arrive(&S.empty[slot]);
     }
     if (inside) {
       const int64_t pix = (int64_t)py * cam.W + px;
@@ -160,23 +151,30 @@ __global__ void __launch_bounds__(kFwdThreads) k_render_fwd(const uint2* __restr
       final_T[pix] = T;
       n_contrib[pix] = last;
     }
-    // the tile's largest n_contrib: the backward's cost estimate for its heavy-first order
+    // the block's largest n_contrib feeds the backward's heavy-first order
     const uint32_t wl = __reduce_max_sync(0xffffffffu, last);
-    if (lane == 0 && wl) atomicMax(&S.cost, wl);
+    if (lane == 0 && wl) atomicMax(&tile_cost[tile], wl);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) tile_cost[tile] = S.cost;
+}
+
+static int fwd_grid() {
+  static int grid = 0;
+  if (!grid) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fwd, kFwdWarps * 32, 0);
+    grid = (per_sm < 1 ? 1 : per_sm) * num_sms();
+  }
+  return grid;
 }
 
 bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n_contrib, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_render_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwdSmem));
-    attr = true;
-  }
-  k_render_fwd<<<F->num_tiles, kFwdThreads, sizeof(FwdSmem), s>>>(F->ranges, F->vals[F->final_buf], F->record,
-                                                                   F->counters, F->cam, F->tile_order, image,
-                                                                   final_T, n_contrib, F->tile_cost);
+  if (cudaMemsetAsync(F->tile_cost, 0, 4 * (size_t)F->num_tiles, s) != cudaSuccess ||
+      cudaMemsetAsync(F->counters + C_FWD_TICKET, 0, 4, s) != cudaSuccess)
+    return check_launch("render_fwd memset");
+  const uint32_t n_items = 8u * (uint32_t)F->num_tiles;
+  k_render_fwd<<<fwd_grid(), kFwdWarps * 32, 0, s>>>(F->ranges, F->vals[F->final_buf], F->record, F->counters,
+                                                     F->cam, F->tile_order, n_items, F->counters + C_FWD_TICKET,
+                                                     image, final_T, n_contrib, F->tile_cost);
   note_launch();
   return check_launch("k_render_fwd");
 }
