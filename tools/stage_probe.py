@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--view", type=int, default=0)
     ap.add_argument("--only", default=None, help="comma-separated stage names")
+    ap.add_argument("--step", type=int, default=0, help="run N full one-view training steps (for ncu)")
     a = ap.parse_args()
     t0 = time.time()
     s = gen.make(a.config)
@@ -41,6 +42,24 @@ def main():
         "blend_bwd": lambda: bgs.bgs_blend_bwd(r.frame, dl, r.final_T, r.n_contrib),
         "preprocess_bwd": lambda: bgs.bgs_preprocess_bwd(g, r.frame, grad),
     }
+    if a.step:
+        # one full training step of one view, repeated: preprocess, sort, fwd, L1, bwd, Adam
+        m = torch.zeros_like(theta)
+        v = torch.zeros_like(theta)
+        tgt = torch.zeros((3, cam.height, cam.width), dtype=torch.uint8, device=dev)
+        loss = torch.zeros(1, device=dev)
+        hp = bgs.AdamHParams()
+        for it in range(a.step):
+            bgs.bgs_preprocess(g, c, r.frame)
+            bgs.bgs_sort(r.frame)
+            bgs.bgs_render_fwd(r.frame, r.image, r.final_T, r.n_contrib)
+            bgs.bgs_l1_loss_grad(r.image, tgt, cam.width, cam.height, 1.0 / (3 * cam.width * cam.height), dl, loss)
+            bgs.bgs_blend_bwd(r.frame, dl, r.final_T, r.n_contrib)
+            bgs.bgs_preprocess_bwd(g, r.frame, grad)
+            bgs.bgs_adam_step(theta, grad, m, v, s.n, hp, it + 1)
+        torch.cuda.synchronize()
+        print("launches per step:", bgs.launch_count())
+        return
     only = set(a.only.split(",")) if a.only else None
     for name, fn in stages.items():
         if only and name not in only:
