@@ -92,10 +92,11 @@ typedef struct {
 typedef struct {
   int32_t* radius;          /* [n]  0 = culled ("absent")                       */
   float* depth;             /* [n]  camera-space t_z; its bits are the key low word  */
-  float* record;            /* [n][12] {x, y, ex, ey | A, B, C, opacity | r, g, b, cbits}
-                               with (A, B, C) = (-conic.x/2, -conic.y, -conic.z/2) and
+  float* record;            /* [n][12] {x, y, ex, ey | A, B, C, opacity | r, g, b, pthr}
+                               with (A, B, C) = (-conic.x/2, -conic.y, -conic.z/2);
                                (ex, ey) conservative half-extents of the alpha >= 1/255
-                               level set (the blend kernels' exact per-block skip test) */
+                               level set and pthr = -(ln(255 o) + 1e-3): the blend kernels'
+                               exact per-block and per-pixel skip tests                 */
   uint32_t* tiles_touched;  /* [n]                                                   */
   uint32_t* offsets;        /* [n]  exclusive scan of tiles_touched (R13)            */
   uint64_t* keys_unsorted;  /* [max_keys] (tile << 32 | depth bits), index order     */
@@ -109,6 +110,8 @@ typedef struct {
   int32_t tiles_x, tiles_y, sort_bits, sort_passes;
   int32_t sort_mode;        /* 0 depth-first (keys_* hold 32-bit tile ids), 1 onesweep64 */
   int32_t _pad;
+  uint8_t* cbits;           /* [n] frozen clamp decisions: rgb clamped (bits 0-2), J clamp
+                               x (bit 3, side bit 4), y (bit 5, side bit 6) (R7, R12, R18) */
 } bgs_frame_views;
 
 /* Per-frame workload counters (bgs_frame_stats; not on the hot path). */

@@ -66,7 +66,7 @@ class FrameViews(C.Structure):
                 ("values_unsorted", C.c_void_p), ("keys_sorted", C.c_void_p), ("values_sorted", C.c_void_p),
                 ("ranges", C.c_void_p), ("grad2d", C.c_void_p), ("n", C.c_int64), ("max_keys", C.c_int64),
                 ("tiles_x", C.c_int32), ("tiles_y", C.c_int32), ("sort_bits", C.c_int32), ("sort_passes", C.c_int32),
-                ("sort_mode", C.c_int32), ("_pad", C.c_int32)]
+                ("sort_mode", C.c_int32), ("_pad", C.c_int32), ("cbits", C.c_void_p)]
 
 
 class Stats(C.Structure):

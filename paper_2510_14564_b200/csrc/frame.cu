@@ -43,7 +43,7 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t radius, depth, record, tiles_touched, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
       sort_status, counters, grad2d, tile_count, tile_order, tile_order_bwd, tile_cost, dkey0, dkey1, dval0, dval1,
-      rank_cnt, item_off, rank_rect, total;
+      rank_cnt, item_off, rank_rect, cbits, total;
   int32_t tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
   int64_t sort_tiles_max;
 };
@@ -100,6 +100,7 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.rank_cnt = take(4 * N);
   L.item_off = take(4 * N);
   L.rank_rect = take(8 * N);
+  L.cbits = take(N);
   L.total = o;
   return true;
 }
@@ -229,6 +230,7 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->rank_cnt = (uint32_t*)(base + L.rank_cnt);
   F->item_off = (uint32_t*)(base + L.item_off);
   F->rank_rect = (uint2*)(base + L.rank_rect);
+  F->cbits = (uint8_t*)(base + L.cbits);
   F->final_buf = L.sort_passes & 1;  // pass p reads buf p&1, writes buf (p+1)&1
   return BGS_OK;
 }
@@ -328,6 +330,7 @@ bgs_status bgs_frame_debug(const bgs_frame* f, bgs_frame_views* out) {
   out->sort_bits = F->sort_bits;
   out->sort_passes = F->sort_passes;
   out->sort_mode = F->sort_mode;
+  out->cbits = F->cbits;
   return BGS_OK;
 }
 

@@ -8,7 +8,7 @@
 //
 // Layout: theta segments are read as coalesced vectors (quats float4,
 // SH 12 x float4 per Gaussian, only for Gaussians that survive the culls); outputs are
-// the 48-byte render record {x, y, ex, ey | A, B, C, o | r, g, b, cbits} that the blend
+// the 48-byte render record {x, y, ex, ey | A, B, C, o | r, g, b, pthr} that the blend
 // kernels stage through shared memory (the B200 form of the paper's T3 RGB
 // reordering), plus radius, depth and tiles_touched.
 #include "common.cuh"
@@ -39,6 +39,7 @@ struct PreParams {
   float4* record;
   uint32_t* tiles_touched;
   float4* grad2d;
+  uint8_t* cbits;
 };
 
 __global__ void __launch_bounds__(256) k_preprocess(PreParams p) {
@@ -195,13 +196,17 @@ __global__ void __launch_bounds__(256) k_preprocess(PreParams p) {
   // blend's own float arithmetic (its G error is ~2^-20 relative).  The blend kernels use
   // it to skip entries per warp block; it never changes a decision.
   const float tau = logf(255.0f * o) + 1e-3f;
-  float ex = -1e30f, ey = -1e30f;
+  float ex = -1e30f, ey = -1e30f, pthr = 3.0e38f;
   if (tau > 0.0f) {
     ex = sqrtf(2.0f * tau * a) * 1.001f + 1e-3f;
     ey = sqrtf(2.0f * tau * cc) * 1.001f + 1e-3f;
+    // the same bound per pixel: power < -tau  =>  o exp(power) < e^-1e-3 / 255, so the
+    // blend's alpha (G within 2^-20 relative) is < 1/255 -- skipped without evaluating G
+    pthr = -tau;
   }
   rec[0] = make_float4(px, py, ex, ey);  // everything the per-warp cull test reads
-  rec[2] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(cb));
+  rec[2] = make_float4(rgb[0], rgb[1], rgb[2], pthr);
+  p.cbits[i] = (uint8_t)cb;
   // this view's blend-gradient accumulator (render_bwd REDs into it)
   float4* g2 = p.grad2d + 3 * i;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -331,6 +336,7 @@ bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
   p.record = F->record;
   p.tiles_touched = F->tiles_touched;
   p.grad2d = F->grad2d;
+  p.cbits = F->cbits;
   const int64_t blocks = (F->n + 255) / 256;
   k_preprocess<<<(unsigned)blocks, 256, 0, s>>>(p);
   note_launch();

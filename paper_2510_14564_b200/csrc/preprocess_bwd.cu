@@ -33,7 +33,7 @@ struct PreBwdParams {
   int32_t deg;
   bool quat_vec4, sh_vec4, gq_vec4, gsh_vec4;  // 16-byte aligned -> vector paths
   const int32_t* radius;
-  const float4* record;
+  const uint8_t* cbits;
   const float4* grad2d;
   float* grad;  // theta layout
 };
@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kBwdThreads) k_preprocess_bwd(PreBwdParams p) 
     const float* P = c.P;
     const float4 ga4 = p.grad2d[3 * i], gb4 = p.grad2d[3 * i + 1], gc4 = p.grad2d[3 * i + 2];
     const float gx = ga4.x, gy = ga4.y, gop = gb4.y;
-    const uint32_t cb = __float_as_uint(p.record[3 * i + 2].w);
+    const uint32_t cb = p.cbits[i];
     const float g_r = (cb & CB_R) ? 0.f : gb4.z, g_g = (cb & CB_G) ? 0.f : gb4.w, g_b = (cb & CB_B) ? 0.f : gc4.x;
     const float mx = p.means[3 * i], my = p.means[3 * i + 1], mz = p.means[3 * i + 2];
     float dmx = 0.f, dmy = 0.f, dmz = 0.f;
@@ -337,7 +337,7 @@ bgs_status launch_preprocess_bwd(const bgs_gaussians* g, Frame* F, float* grad, 
   p.gq_vec4 = al16(grad + 6 * F->n);
   p.gsh_vec4 = al16(grad + 11 * F->n);
   p.radius = F->radius;
-  p.record = F->record;
+  p.cbits = F->cbits;
   p.grad2d = F->grad2d;
   p.grad = grad;
   k_preprocess_bwd<<<(unsigned)((F->n + kBwdThreads - 1) / kBwdThreads), kBwdThreads, 0, s>>>(p);

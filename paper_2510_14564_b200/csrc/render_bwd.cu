@@ -156,12 +156,17 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
           const float4 r1 = sr1[k];
           const float dx = r0.x - pxf, dy = r0.y - pyf;
           const float power = fmaf(r1.x, dx * dx, fmaf(r1.z, dy * dy, r1.y * (dx * dy)));
-          const float G = fast_exp(power);
-          const float og = r1.w * G;
-          const float alpha = fminf(0.99f, og);
-          if (power > 0.0f || alpha < (1.0f / 255.0f)) {
+          float G = 0.0f, og = 0.0f, alpha = 0.0f;
+          // power below the exact alpha < 1/255 bound (pthr): skipped without the MUFU path
+          if (power > 0.0f || power < sr2[k].w) {
             act = false;
           } else {
+            G = fast_exp(power);
+            og = r1.w * G;
+            alpha = fminf(0.99f, og);
+            if (alpha < (1.0f / 255.0f)) act = false;
+          }
+          if (act) {
             const float ioma = 1.0f / (1.0f - alpha);
             T = T * ioma;  // transmittance in front of this Gaussian
             const float w = alpha * T;

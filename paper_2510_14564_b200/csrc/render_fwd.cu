@@ -109,27 +109,31 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const uint2* __re
         const uint32_t id_nnn = load_id(s + 3);
         // (4) walk step s
         const int m = __popc(bal);
-        for (int k = 0; k < m && !done; ++k) {
+        int lastk = -1;
+        for (int k = 0; k < m; ++k) {
           const float4 r0 = sr0[k];
-          const float dx = r0.x - pxf, dy = r0.y - pyf;
           const float4 r1 = sr1[k];
+          const float4 r2 = sr2[k];
+          const float dx = r0.x - pxf, dy = r0.y - pyf;
           const float power = fmaf(r1.x, dx * dx, fmaf(r1.z, dy * dy, r1.y * (dx * dy)));
-          if (power > 0.0f) continue;
+          // one predicate: pixel done, R14's power > 0 guard, or power below the exact
+          // alpha < 1/255 bound (pthr, preprocess) -- the last skips the MUFU path
+          if (done | (power > 0.0f) | (power < r2.w)) continue;
           const float alpha = fminf(0.99f, r1.w * fast_exp(power));
           if (alpha < (1.0f / 255.0f)) continue;
           const float tT = T * (1.0f - alpha);
           if (tT < 1e-4f) {
             done = true;
-            break;
+            continue;
           }
           const float w = alpha * T;
-          const float4 r2 = sr2[k];
           Cr = fmaf(r2.x, w, Cr);
           Cg = fmaf(r2.y, w, Cg);
           Cb = fmaf(r2.z, w, Cb);
           T = tT;
-          last = spos[k] + 1u;
+          lastk = k;
         }
+        if (lastk >= 0) last = spos[lastk] + 1u;
         if (__all_sync(0xffffffffu, done)) break;
         // rotate the pipeline
         id_c = id_n;

@@ -117,7 +117,10 @@ def test_preprocess_parity(bgs, name):
     live = tau > 0
     ext = np.sqrt(2 * tau[live, None] * cov[live])
     assert (rec[live, 2:4] >= ext * (1 - 1e-5)).all()
-    cb = rec[:, 11].view(np.uint32)
+    # per-pixel pre-skip threshold: power < pthr  =>  o exp(power) < 1/255
+    o64 = pre["opacity"][vis].astype(np.float64)
+    assert (o64[live] * np.exp(rec[live, 11].astype(np.float64)) < 1.0 / 255.0).all()
+    cb = torch.as_tensor(_DevPtr(r.views().cbits, s.n, "|u1"), device="cuda").cpu().numpy()[vis].astype(np.uint32)
     assert np.array_equal(cb & 0x78, pre["cbits"][vis] & 0x78)  # J-clamp bits (exact)
     assert (cb & 7 != pre["cbits"][vis] & 7).sum() <= max(1, vis.sum() // 10000)  # rgb clamp (free-order)
 
