@@ -42,7 +42,7 @@ struct PreParams {
   uint8_t* cbits;
 };
 
-__global__ void __launch_bounds__(256) k_preprocess(PreParams p) {
+__global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
   const Cam& c = p.cam;

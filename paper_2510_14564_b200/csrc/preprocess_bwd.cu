@@ -49,7 +49,7 @@ constexpr float kC30 = -0.5900435899266435f, kC31 = 2.890611442640554f, kC32 = -
                 kC33 = 0.3731763325901154f, kC34 = -0.4570457994644658f, kC35 = 1.445305721320277f,
                 kC36 = -0.5900435899266435f;
 
-__global__ void __launch_bounds__(kBwdThreads) k_preprocess_bwd(PreBwdParams p) {
+__global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(PreBwdParams p) {
   __shared__ float s_sh[kBwdThreads / 32][32 * kRow];
   __shared__ int s_vis[kBwdThreads / 32][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
