@@ -48,7 +48,8 @@ def parse():
     p.add_argument("--n", type=int, default=None, help="override the Gaussian count (debug only)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--thin", type=int, default=64, help="oracle sample: every k-th Gaussian")
+    p.add_argument("--thin", type=int, default=None,
+                   help="oracle sample: every k-th Gaussian (default 64 for cpu_baseline, 256 for --impl reference)")
     return p.parse_args()
 
 
@@ -58,6 +59,16 @@ def load_peaks():
             return json.load(f), "measured"
     except Exception:
         return PEAKS_FALLBACK, "fallback"
+
+
+def arm_config(scene, args, world):
+    """The workload description shared by both arms (ours and --impl reference)."""
+    cam = scene.cameras[0]
+    return {"workload": f"{scene.name}-shaped {scene.n} Gaussians, {cam.width}x{cam.height}, SH degree "
+                        f"{scene.sh_degree}, batch of {args.views} views per step (fwd+bwd each, then "
+                        f"all-reduce + Adam)",
+            "views_per_step": args.views, "n_gaussians": scene.n, "width": cam.width, "height": cam.height,
+            "parallelism": f"view-dp{world}", "l2": "inputs larger than L2 (theta 1.37 GB, keys > 126 MB)"}
 
 
 def batch_views(n_views, n_cams):
@@ -379,11 +390,7 @@ def run_ours(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded garden-shaped scene, gen/; random-init parameters; targets = render of a "
                 "perturbed copy)",
-        "config": {"workload": f"{scene.name}-shaped {n} Gaussians, {W}x{H}, SH degree {deg}, batch of "
-                               f"{args.views} views per step (fwd+bwd each, then all-reduce + Adam)",
-                   "views_per_step": args.views, "n_gaussians": n, "width": W, "height": H,
-                   "parallelism": f"view-dp{world}", "l2": "inputs larger than L2 (theta 1.37 GB, keys > 126 MB)",
-                   "max_keys": rend.max_keys},
+        "config": arm_config(scene, args, world),
         "clocks": clocks, "gpu_launches": int(launches), "roofline": roofline,
         "stages_ms_per_step": {k2: round(v2, 4) for k2, v2 in per_step.items()},
         "stages_roofline": {k2: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v2.items()}
@@ -419,6 +426,12 @@ def _oracle_view(th, n, deg, cam, dl):
 
 
 def cpu_baseline(args):
+    if args.thin is None:
+        args.thin = 64
+    return _cpu_baseline(args)
+
+
+def _cpu_baseline(args):
     """The oracle as it stands (single thread) on a bounded sample: one view of the scene
     thinned to every `thin`-th Gaussian, full preprocess -> sort -> fwd -> bwd; the view
     time is scaled by `thin` to the full scene (assumes cost linear in N)."""
@@ -452,6 +465,8 @@ def run_reference(args, rank, world):
     import gen
     import oracle
 
+    if args.thin is None:
+        args.thin = 256
     scene, th, ns = _thinned(args)
     cams = [scene.cameras[v] for v in batch_views(args.views, len(scene.cameras))]
     deg = scene.sh_degree
@@ -477,8 +492,7 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3 * args.thin, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32",
-            "data": "synthetic", "config": {"workload": f"{scene.name}-shaped scene, oracle on a 1/{args.thin} "
-                                                        f"thinned sample, 1 view + Adam per step"},
+            "data": "synthetic", "config": arm_config(scene, args, world),
             "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": f"each step: 1 view of the scene thinned to every {args.thin}th Gaussian "
                                        f"({ns} of {scene.n}), fwd+bwd+Adam, scaled x{args.thin}",
