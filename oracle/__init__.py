@@ -89,6 +89,8 @@ def lib():
                 "orc_render_bwd": [C.c_int64, C.c_int32, P, P, C.c_uint32, P, P, P, P, P, P, P, P, P, P, P, P, P],
                 "orc_preprocess_bwd": [C.c_int64, C.c_int32, P, P, C.c_uint32, P, P, P, P, P, P, P],
                 "orc_adam": [C.c_int64, P, P, P, P, P, C.c_double, C.c_double, C.c_double, C.c_int64],
+                "orc_local_density": [C.c_int64, P, C.c_float, P],
+                "orc_knn_mean": [C.c_int64, P, C.c_int32, P],
             }
             for name, args in sig.items():
                 fn = getattr(l, name)
@@ -222,6 +224,32 @@ def adam(theta, grad, m, v, n, lr6, b1=0.9, b2=0.999, eps=1e-15, step=1):
     lr = np.asarray(lr6, np.float64)
     lib().orc_adam(n, _p(th), _p(gr), _p(mm), _p(vv), _p(lr), b1, b2, eps, step)
     return th, mm, vv
+
+
+def local_density(means, r) -> np.ndarray:
+    """T1 (§III-C1 l.181-183): rho(p) = number of other points within radius r."""
+    m = np.ascontiguousarray(means, np.float32).reshape(-1, 3)
+    out = np.zeros(m.shape[0], np.uint32)
+    lib().orc_local_density(m.shape[0], _p(m), float(np.float32(r)), _p(out))
+    return out
+
+
+def knn_mean_distance(means, k=8) -> np.ndarray:
+    """T1 (§III-C2 l.188-191): d_p = mean distance to the k nearest neighbours."""
+    m = np.ascontiguousarray(means, np.float32).reshape(-1, 3)
+    out = np.zeros(m.shape[0], np.float64)
+    lib().orc_knn_mean(m.shape[0], _p(m), int(k), _p(out))
+    return out
+
+
+def density_thresholds(rho, alpha=1.0, beta=1.0) -> dict:
+    """T1 (§III-C1 l.184-186): rho_low = mu - alpha sigma, rho_high = mu + beta sigma,
+    mu / sigma the mean and (population) standard deviation of all local densities."""
+    r = np.asarray(rho, np.float64)
+    mu = float(r.mean())
+    sd = float(np.sqrt(((r - mu) ** 2).mean()))
+    return {"mu": mu, "sigma": sd, "rho_low": mu - alpha * sd, "rho_high": mu + beta * sd,
+            "below": int((r < mu - alpha * sd).sum()), "above": int((r > mu + beta * sd).sum())}
 
 
 GROUPS = ("means", "log_scales", "quats", "opacity", "sh_dc", "sh_rest")

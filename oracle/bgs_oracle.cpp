@@ -789,6 +789,48 @@ void orc_preprocess_bwd(int64_t n, int32_t deg, const float* theta, const orc_ca
   }
 }
 
+// NEXT-1, T1 statistical density thresholding (§III-C1 l.181-186): "the local
+// density rho is determined as the number of neighboring points within a fixed radius r".
+// Plain O(n^2) definition: rho(p) = #{q != p : |q - p| <= r}, with the squared distance
+// evaluated as ((dx*dx + dy*dy) + dz*dz) in float (separately rounded) and compared with
+// r*r in float -- the same decision the GPU grid kernel takes.
+void orc_local_density(int64_t n, const float* means, float r, uint32_t* counts) {
+  const float r2 = r * r;
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t c = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      const float dx = means[3 * j] - means[3 * i];
+      const float dy = means[3 * j + 1] - means[3 * i + 1];
+      const float dz = means[3 * j + 2] - means[3 * i + 2];
+      const float d2 = (dx * dx + dy * dy) + dz * dz;
+      if (d2 <= r2) ++c;
+    }
+    counts[i] = c;
+  }
+}
+
+// §III-C2 l.190: mean distance to the k nearest neighbours, d_p = (1/k) sum_i d(p, p_i)
+// (double, brute force with std::partial_sort).
+void orc_knn_mean(int64_t n, const float* means, int32_t k, double* out) {
+  std::vector<double> d((size_t)(n > 0 ? n - 1 : 0));
+  for (int64_t i = 0; i < n; ++i) {
+    size_t m = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      if (j == i) continue;
+      const double dx = (double)means[3 * j] - means[3 * i];
+      const double dy = (double)means[3 * j + 1] - means[3 * i + 1];
+      const double dz = (double)means[3 * j + 2] - means[3 * i + 2];
+      d[m++] = std::sqrt(dx * dx + dy * dy + dz * dz);
+    }
+    const size_t kk = std::min<size_t>((size_t)k, m);
+    std::partial_sort(d.begin(), d.begin() + kk, d.begin() + m);
+    double acc = 0.0;
+    for (size_t t = 0; t < kk; ++t) acc += d[t];
+    out[i] = kk ? acc / (double)kk : 0.0;
+  }
+}
+
 // O17: Adam (R21), PyTorch semantics, in double.  lr[6] = means, log_scales,
 // quats, opacity, sh_dc, sh_rest.  grad is zeroed on exit.
 void orc_adam(int64_t n, double* theta, double* grad, double* m, double* v, const double* lr, double b1, double b2,
