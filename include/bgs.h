@@ -184,6 +184,20 @@ bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_a
 bgs_status bgs_l1_loss_grad(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale,
                             float* dL_dimage, float* loss_sum, void* stream);
 
+/* ---------------------------------------------------------------- NEXT-1: T1 density statistics */
+/* Workspace bytes for bgs_local_density over n points (0 on invalid n: 1 <= n < 2^30). */
+size_t bgs_density_workspace_bytes(int64_t n);
+
+/* The paper's statistical density thresholding (§III-C1 l.181-186): for every
+ * point p of means[n][3] (device, e.g. theta's means segment), counts[n] (device, out) =
+ * rho(p) = number of other points q with |q - p| <= r, exact (squared distance evaluated
+ * ((dx*dx + dy*dy) + dz*dz) in float against r*r; hashed uniform grid);
+ * stats[4] (device doubles, out) = {mu_rho, sigma_rho (population), rho_low = mu - alpha
+ * sigma, rho_high = mu + beta sigma}.  workspace: device, >= bgs_density_workspace_bytes(n)
+ * bytes, 256-byte aligned.  BGS_ERR_INVALID on bad arguments (nothing launched). */
+bgs_status bgs_local_density(const float* means, int64_t n, float r, float alpha, float beta, uint32_t* counts,
+                             double* stats, void* workspace, size_t bytes, void* stream);
+
 /* ---------------------------------------------------------------- status / debug */
 /* After the caller synchronised the frame's stream: K (host out) and BGS_OK, or
  * BGS_ERR_CAPACITY when K > max_keys (re-run with a larger workspace). */

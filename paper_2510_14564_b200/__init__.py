@@ -91,6 +91,8 @@ _SIGS = {
     "bgs_frame_debug": (C.c_int, [C.POINTER(Frame), C.POINTER(FrameViews)]),
     "bgs_frame_stats": (C.c_int, [C.POINTER(Frame), _P, C.POINTER(Stats), _P]),
     "bgs_frame_set_debug": (C.c_int, [C.POINTER(Frame), C.c_int32]),
+    "bgs_density_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "bgs_local_density": (C.c_int, [_P, C.c_int64, C.c_float, C.c_float, C.c_float, _P, _P, _P, C.c_size_t, _P]),
     "bgs_status_string": (C.c_char_p, [C.c_int]),
     "bgs_last_error": (C.c_char_p, []),
     "bgs_launch_count": (C.c_uint64, []),
@@ -209,6 +211,23 @@ def bgs_frame_stats(frame: Frame, n_contrib, stream=None) -> dict:
 
 def bgs_frame_set_debug(frame: Frame, flags: int):
     _check(_lib.bgs_frame_set_debug(C.byref(frame), flags), "bgs_frame_set_debug")
+
+
+def bgs_local_density(means, r, alpha=1.0, beta=1.0, counts=None, stats=None, workspace=None, stream=None):
+    """NEXT-1 / T1 (§III-C1): exact fixed-radius neighbour counts + thresholds.
+    means: contiguous CUDA float32 [n, 3] (or the means segment of theta)."""
+    n = means.numel() // 3
+    dev = means.device
+    if counts is None:
+        counts = torch.empty(n, dtype=torch.int32, device=dev)
+    if stats is None:
+        stats = torch.empty(4, dtype=torch.float64, device=dev)
+    nbytes = int(_lib.bgs_density_workspace_bytes(n))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
+    _check(_lib.bgs_local_density(_ptr(means), n, float(r), float(alpha), float(beta), _ptr(counts), _ptr(stats),
+                                  _ptr(workspace), workspace.numel(), _stream(stream)), "bgs_local_density")
+    return counts, stats
 
 
 def launch_count() -> int:
