@@ -48,6 +48,7 @@ def parse():
     p.add_argument("--n", type=int, default=None, help="override the Gaussian count (debug only)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-stage-events", action="store_true", help="diagnostic: no per-stage events in the timed loop")
     p.add_argument("--thin", type=int, default=None,
                    help="oracle sample: every k-th Gaussian (default 64 for cpu_baseline, 256 for --impl reference)")
     return p.parse_args()
@@ -71,6 +72,12 @@ def arm_config(scene, args, world):
             "parallelism": f"view-dp{world}", "l2": "inputs larger than L2 (theta 1.37 GB, keys > 126 MB)"}
 
 
+def _device_index(local_rank):
+    """cuda device of this rank; BGS_FORCE_DEVICE pins every rank to one GPU (test-only)."""
+    forced = os.environ.get("BGS_FORCE_DEVICE")
+    return int(forced) if forced is not None else local_rank
+
+
 def batch_views(n_views, n_cams):
     """views 4i mod n_cams for i < n_views."""
     return [(4 * i) % n_cams for i in range(n_views)]
@@ -91,7 +98,8 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS),
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms",
+                                          os.environ.get("BGS_CLOCK_SAMPLE_MS", "250")],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -141,7 +149,7 @@ def run_ours(args, rank, world, local_rank):
     import paper_2510_14564_b200 as bgs
     from paper_2510_14564_b200 import dp
 
-    dev = torch.device("cuda", local_rank)
+    dev = torch.device("cuda", _device_index(local_rank))
     torch.cuda.set_device(dev)
     kw = {} if args.n is None else {"n": args.n}
     scene = gen.make(args.config, **kw)
@@ -241,6 +249,10 @@ def run_ours(args, rank, world, local_rank):
         one_step(targets)
     torch.cuda.synchronize()
 
+    # the step trains theta (Adam), which changes the workload; the e2e loop restarts from
+    # this snapshot so both loops time the same sequence of training states
+    snap = (theta.clone(), m.clone(), v.clone(), step_no[0]) if not args.no_e2e else None
+
     # ---- device-resident timed region (inputs larger than L2: theta 1.37 GB, keys GBs)
     record = {"next": 0, "marks": []}
     barrier()
@@ -248,10 +260,10 @@ def run_ours(args, rank, world, local_rank):
     launches0 = bgs.launch_count()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(_device_index(local_rank)) as clk:
         t0.record(stream)
         for _ in range(args.steps):
-            one_step(targets, record)
+            one_step(targets, None if args.no_stage_events else record)
         t1.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -280,7 +292,13 @@ def run_ours(args, rank, world, local_rank):
             one_step(targets_e2e)
             loss_host.copy_(loss, non_blocking=True)
 
-        e2e_step()
+        e2e_step()  # warm-up of the copy path
+        theta.copy_(snap[0])
+        m.copy_(snap[1])
+        v.copy_(snap[2])
+        step_no[0] = snap[3]
+        grad.zero_()
+        del snap
         torch.cuda.synchronize()
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -352,7 +370,7 @@ def run_ours(args, rank, world, local_rank):
                        "frac": achieved / peak if peak else None, "ms_per_launch": per_step[stage] / steps_views}
 
     def per_launch(stage):
-        return per_step[stage] / steps_views / 1e3  # seconds
+        return max(per_step[stage] / steps_views / 1e3, 1e-12)  # seconds (0 with --no-stage-events)
 
     frac("preprocess", (16 * n + 268 * V) / per_launch("preprocess") / 1e9, hbm, "GB/s", "hbm")
     if frame_v.sort_mode == 1:  # 64-bit onesweep reference: dup 12 + hist 8 + 24/pass per key, rects 20/visible
@@ -364,7 +382,7 @@ def run_ours(args, rank, world, local_rank):
          "T lane-ops/s", "alu")
     frac("blend_bwd", OPS_BWD_EVAL * Ebc / per_launch("blend_bwd") / 1e12, fp32_peak, "T lane-ops/s", "alu")
     frac("preprocess_bwd", 744 * V / per_launch("preprocess_bwd") / 1e9, hbm, "GB/s", "hbm")
-    roof["adam"] = {"bound": "hbm", "achieved": 1888 * n / (per_step["adam"] / 1e3) / 1e9, "peak": hbm,
+    roof["adam"] = {"bound": "hbm", "achieved": 1888 * n / max(per_step["adam"] / 1e3, 1e-12) / 1e9, "peak": hbm,
                     "unit": "GB/s", "ms_per_launch": per_step["adam"]}
     roof["adam"]["frac"] = roof["adam"]["achieved"] / hbm
     # the dominant KERNEL: stages that are one kernel launch (the sort stage is 13 kernels;
@@ -513,8 +531,12 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("BGS_DIST_BACKEND", "nccl")
+        torch.cuda.set_device(_device_index(local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", _device_index(local_rank)))
+        else:  # test-only: several ranks sharing one GPU (NCCL refuses duplicate GPUs)
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:
