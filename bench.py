@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--n", type=int, default=None, help="override the Gaussian count (debug only)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--one-frame", action="store_true",
+                   help="diagnostic: one frame for all views (no per-view scheduling hint)")
     p.add_argument("--no-stage-events", action="store_true", help="diagnostic: no per-stage events in the timed loop")
     p.add_argument("--thin", type=int, default=None,
                    help="oracle sample: every k-th Gaussian (default 64 for cpu_baseline, 256 for --impl reference)")
@@ -175,6 +177,10 @@ def run_ours(args, rank, world, local_rank):
         kmax = max(kmax, rend.num_keys)
     if int(kmax * 1.1) + 4096 > rend.max_keys:
         rend.alloc(int(kmax * 1.1) + 4096)
+    # one frame per view (as a trainer keeps per-camera state): a frame that re-renders its
+    # view orders the blend work items by its previous forward's per-block costs
+    rends = [rend] + [rend if args.one_frame else bgs.Renderer(n, W, H, max_keys=rend.max_keys, device=dev)
+                      for _ in cams[1:]]
 
     # targets: a perturbed copy of theta rendered once, 8-bit (R19)
     r = gen.rng(1234)
@@ -215,19 +221,20 @@ def run_ours(args, rank, world, local_rank):
                 marks.append(e)
 
         for j, cs in enumerate(cam_structs):
+            rj = rends[j]
             marks = []
             mark(marks)
-            bgs.bgs_preprocess(gs, cs, rend.frame)
+            bgs.bgs_preprocess(gs, cs, rj.frame)
             mark(marks)
-            bgs.bgs_sort(rend.frame)
+            bgs.bgs_sort(rj.frame)
             mark(marks)
-            bgs.bgs_render_fwd(rend.frame, rend.image, rend.final_T, rend.n_contrib)
+            bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
             mark(marks)
-            bgs.bgs_l1_loss_grad(rend.image, tgts[j], W, H, scale, dl, loss)
+            bgs.bgs_l1_loss_grad(rj.image, tgts[j], W, H, scale, dl, loss)
             mark(marks)
-            bgs.bgs_blend_bwd(rend.frame, dl, rend.final_T, rend.n_contrib)
+            bgs.bgs_blend_bwd(rj.frame, dl, rj.final_T, rj.n_contrib)
             mark(marks)
-            bgs.bgs_preprocess_bwd(gs, rend.frame, grad)
+            bgs.bgs_preprocess_bwd(gs, rj.frame, grad)
             mark(marks)
             if record is not None:
                 record["marks"].append(("view", marks))
@@ -269,8 +276,9 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     launches = bgs.launch_count() - launches0
     ms_local = t0.elapsed_time(t1)
-    st, k_last = bgs.bgs_frame_status(rend.frame)
-    assert st == bgs.BGS_OK, "key capacity overflow in the timed region"
+    for rj in rends:
+        st, k_last = bgs.bgs_frame_status(rj.frame)
+        assert st == bgs.BGS_OK, "key capacity overflow in the timed region"
     # per-stage means
     sums = {s: 0.0 for s in stage_names}
     for kind, mk in record["marks"]:
@@ -321,11 +329,11 @@ def run_ours(args, rank, world, local_rank):
     # ---- workload counters (not timed) for the roofline numerators
     stats = {"visible": 0, "num_keys": 0, "evals_fwd": 0, "evals_bwd": 0, "evals_slot": 0, "max_list": 0,
              "blended": 0, "evals_fwd_culled": 0, "evals_bwd_culled": 0}
-    for cam, cs in zip(cams, cam_structs):
-        bgs.bgs_preprocess(gs, cs, rend.frame)
-        bgs.bgs_sort(rend.frame)
-        bgs.bgs_render_fwd(rend.frame, rend.image, rend.final_T, rend.n_contrib)
-        s = bgs.bgs_frame_stats(rend.frame, rend.n_contrib)
+    for rj, cs in zip(rends, cam_structs):
+        bgs.bgs_preprocess(gs, cs, rj.frame)
+        bgs.bgs_sort(rj.frame)
+        bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
+        s = bgs.bgs_frame_stats(rj.frame, rj.n_contrib)
         for k2 in stats:
             if k2 == "max_list":
                 stats[k2] = max(stats[k2], s.get(k2, 0))

@@ -62,9 +62,10 @@ struct Frame {
   uint32_t* counters;      // [C_NUM]
   float4* grad2d;          // [n][3]
   uint32_t* tile_count;    // [num_tiles] keys per tile (from the duplication)
-  uint32_t* tile_order;    // [num_tiles] forward CTA -> tile, heavy first
-  uint32_t* tile_order_bwd;// [num_tiles] backward CTA -> tile, heavy first
-  uint32_t* tile_cost;     // [num_tiles] the forward's largest n_contrib per tile
+  uint32_t* order_fwd;     // [8 tiles] forward work items (tile << 3 | 8x4 block), longest first
+  uint32_t* order_bwd;     // [8 tiles] backward work items, longest first
+  uint32_t* block_cost;    // [8 tiles] each block's largest n_contrib in the last forward
+  int32_t have_cost, _pad1;// block_cost holds this frame's previous forward
   // depth-first sort path (sort.cu): Gaussians stable-sorted by depth bits, then the
   // rank-ordered tile items stable-split by tile -- the same order as the 64-bit sort
   uint32_t* dkey[2];       // [n] depth bits (0xffffffff for culled)
@@ -109,8 +110,8 @@ bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                               int shift, int64_t count, cudaStream_t s);
 bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, bool publish_k, cudaStream_t s);
-bgs_status launch_tile_order(const uint32_t* cost, int32_t num_tiles, const uint32_t* counters, uint32_t* order,
-                             cudaStream_t s);
+bgs_status launch_item_order(const uint32_t* cost, int32_t n_items, int32_t cost_shift, const uint32_t* counters,
+                             uint32_t* order, cudaStream_t s);
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ float fast_exp(float x) {
@@ -121,21 +122,23 @@ __device__ __forceinline__ float fast_exp(float x) {
   return y;
 }
 
-__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
+// look-back status words: relaxed, GPU-scope (L2-coherent; no .sys-scope round trip).  A
+// status word carries its own flag bits, so no ordering with other data is needed.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
-  asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ void st_volatile_u32(uint32_t* p, uint32_t v) {
-  asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // mbarrier (sm_90+) helpers for producer/consumer pipelines in shared memory

@@ -42,7 +42,7 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t radius, depth, record, tiles_touched, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
-      sort_status, counters, grad2d, tile_count, tile_order, tile_order_bwd, tile_cost, dkey0, dkey1, dval0, dval1,
+      sort_status, counters, grad2d, tile_count, order_fwd, order_bwd, block_cost, dkey0, dkey1, dval0, dval1,
       rank_cnt, item_off, rank_rect, cbits, total;
   int32_t tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
   int64_t sort_tiles_max;
@@ -90,9 +90,9 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.grad2d = take(48 * N);
   const size_t NT = (size_t)L.num_tiles;
   L.tile_count = take(4 * NT);
-  L.tile_order = take(4 * NT);
-  L.tile_order_bwd = take(4 * NT);
-  L.tile_cost = take(4 * NT);
+  L.order_fwd = take(4 * 8 * NT);
+  L.order_bwd = take(4 * 8 * NT);
+  L.block_cost = take(4 * 8 * NT);
   L.dkey0 = take(4 * N);
   L.dkey1 = take(4 * N);
   L.dval0 = take(4 * N);
@@ -220,9 +220,10 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->counters = (uint32_t*)(base + L.counters);
   F->grad2d = (float4*)(base + L.grad2d);
   F->tile_count = (uint32_t*)(base + L.tile_count);
-  F->tile_order = (uint32_t*)(base + L.tile_order);
-  F->tile_order_bwd = (uint32_t*)(base + L.tile_order_bwd);
-  F->tile_cost = (uint32_t*)(base + L.tile_cost);
+  F->order_fwd = (uint32_t*)(base + L.order_fwd);
+  F->order_bwd = (uint32_t*)(base + L.order_bwd);
+  F->block_cost = (uint32_t*)(base + L.block_cost);
+  F->have_cost = 0;
   F->dkey[0] = (uint32_t*)(base + L.dkey0);
   F->dkey[1] = (uint32_t*)(base + L.dkey1);
   F->dval[0] = (uint32_t*)(base + L.dval0);

@@ -260,15 +260,15 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
   if (warp == 0) {
     unsigned long long prefix = 0;
     if (tile == 0) {
-      if (lane == 0) st_volatile_u64(&status[0], kFlagP | total);
+      if (lane == 0) st_relaxed_u64(&status[0], kFlagP | total);
     } else {
-      if (lane == 0) st_volatile_u64(&status[tile], kFlagA | total);
+      if (lane == 0) st_relaxed_u64(&status[tile], kFlagA | total);
       int64_t j = tile - 1 - lane;  // window of 32 predecessors
       while (true) {
         unsigned long long s = 0;
         if (j >= 0) {
           do {
-            s = ld_volatile_u64(&status[j]);
+            s = ld_relaxed_u64(&status[j]);
           } while ((s >> 62) == 0);
         } else {
           s = kFlagP;  // virtual inclusive prefix 0 before tile 0
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
         if (pmask) break;
         j -= 32;
       }
-      if (lane == 0) st_volatile_u64(&status[tile], kFlagP | (prefix + total));
+      if (lane == 0) st_relaxed_u64(&status[tile], kFlagP | (prefix + total));
     }
     if (lane == 0) s_prefix = prefix;
   }

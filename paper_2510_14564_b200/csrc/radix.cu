@@ -125,8 +125,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
     }
     // publish the tile aggregate early (decoupled look-back)
     uint32_t* st = status + tile * kRadix;
-    if (tile == 0) st_volatile_u32(&st[tid], kStP | cnt);
-    else st_volatile_u32(&st[tid], kStA | cnt);
+    if (tile == 0) st_relaxed_u32(&st[tid], kStP | cnt);
+    else st_relaxed_u32(&st[tid], kStA | cnt);
     // exclusive prefix over digits inside the tile
     {
       uint32_t incl = cnt;
@@ -147,12 +147,12 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
       for (int64_t j = tile - 1; j >= 0; --j) {
         uint32_t s;
         do {
-          s = ld_volatile_u32(&status[j * kRadix + tid]);
+          s = ld_relaxed_u32(&status[j * kRadix + tid]);
         } while ((s >> 30) == 0);
         prefix += s & kStMask;
         if ((s >> 30) == 2) break;
       }
-      st_volatile_u32(&st[tid], kStP | (prefix + cnt));
+      st_relaxed_u32(&st[tid], kStP | (prefix + cnt));
     }
     S.global_base[tid] = S.hist_excl[tid] + prefix;
     __syncthreads();

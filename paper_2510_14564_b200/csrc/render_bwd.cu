@@ -62,7 +62,7 @@ __device__ __forceinline__ bool box_hits(const float4 a, float bx0, float by0, f
 
 __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ values, const float4* __restrict__ record,
-    const uint32_t* __restrict__ counters, Cam cam, const uint32_t* __restrict__ tile_order, uint32_t n_items,
+    const uint32_t* __restrict__ counters, Cam cam, const uint32_t* __restrict__ item_order, uint32_t n_items,
     uint32_t* ticket, const float* __restrict__ dl_dimage, const float* __restrict__ final_T,
     const uint32_t* __restrict__ n_contrib, float4* __restrict__ grad2d) {
   __shared__ float4 s_rec[kBwdWarpsPerCta][3][32];
@@ -83,7 +83,8 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     if (lane == 0) item = atomicAdd(ticket, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
-    const int tile = (int)tile_order[item >> 3], blk = (int)(item & 7);
+    const uint32_t it = item_order[item];
+    const int tile = (int)(it >> 3), blk = (int)(it & 7);
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int bx = tx * kTile + (blk & 1) * 8, by = ty * kTile + (blk >> 1) * 4;
     const int px = bx + (lane & 7), py = by + (lane >> 3);
@@ -226,11 +227,12 @@ static int bwd_grid() {
 
 bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
                             cudaStream_t s) {
-  bgs_status st = launch_tile_order(F->tile_cost, F->num_tiles, F->counters, F->tile_order_bwd, s);
+  // longest first by each block's largest n_contrib (its back-to-front walk length)
+  bgs_status st = launch_item_order(F->block_cost, 8 * F->num_tiles, 0, F->counters, F->order_bwd, s);
   if (st != BGS_OK) return st;
   if (cudaMemsetAsync(F->counters + C_BWD_TICKET, 0, 4, s) != cudaSuccess) return check_launch("blend_bwd memset");
   k_render_bwd<<<bwd_grid(), kBwdWarpsPerCta * 32, 0, s>>>(
-      F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->tile_order_bwd, 8u * (uint32_t)F->num_tiles,
+      F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, 8u * (uint32_t)F->num_tiles,
       F->counters + C_BWD_TICKET, dL_dimage, final_T, n_contrib, F->grad2d);
   note_launch();
   return check_launch("k_render_bwd");

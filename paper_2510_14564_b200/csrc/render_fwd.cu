@@ -10,12 +10,13 @@
 // per pixel walking a tile in lock-step, the slowest pixels and longest tiles set the
 // pace): the unit of work is one warp x one 8x4 pixel block of a tile (one pixel per
 // lane).  A persistent grid of independent warps pulls these (tile, block) items from a
-// global ticket, heaviest tiles first (k_tile_scan orders tiles by list length), so no
+// global ticket, longest first (by this frame's previous per-block walk lengths when it
+// re-renders a view, else by tile list length), so no
 // warp waits on another and a warp leaves its tile as soon as its own 32 pixels are done.
 // A warp streams its tile's list 32 entries per step: each lane gathers one entry's
 // 16-byte cull record {x, y, ex, ey} and tests the conservative alpha >= 1/255 box against
 // the block; the hits (about a fifth of the list on the garden workload) are compacted
-// with a ballot and their 48-byte records {x,y,ex,ey | A,B,C,o | r,g,b,cbits} staged in the
+// with a ballot and their 48-byte records {x,y,ex,ey | A,B,C,o | r,g,b,pthr} staged in the
 // warp's slice of shared memory -- the B200 form of the paper's T3 batch loading of
 // per-Gaussian contiguous RGB.  The step loop is
 // software-pipelined (ids three steps ahead, cull records two, hit records one), so the
@@ -35,11 +36,11 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const uint2* __re
                                                                 const uint32_t* __restrict__ values,
                                                                 const float4* __restrict__ record,
                                                                 const uint32_t* __restrict__ counters, Cam cam,
-                                                                const uint32_t* __restrict__ tile_order,
+                                                                const uint32_t* __restrict__ item_order,
                                                                 uint32_t n_items, uint32_t* ticket,
                                                                 float* __restrict__ image, float* __restrict__ final_T,
                                                                 uint32_t* __restrict__ n_contrib,
-                                                                uint32_t* __restrict__ tile_cost) {
+                                                                uint32_t* __restrict__ block_cost) {
   __shared__ float4 s_rec[kFwdWarps][3][32];
   __shared__ uint32_t s_pos[kFwdWarps][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -55,7 +56,8 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const uint2* __re
     if (lane == 0) item = atomicAdd(ticket, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_items) break;
-    const int tile = (int)tile_order[item >> 3], blk = (int)(item & 7);
+    const uint32_t it = item_order[item];
+    const int tile = (int)(it >> 3), blk = (int)(it & 7);
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int bx = tx * kTile + (blk & 1) * 8, by = ty * kTile + (blk >> 1) * 4;
     const int px = bx + (lane & 7), py = by + (lane >> 3);
@@ -155,9 +157,9 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const uint2* __re
       final_T[pix] = T;
       n_contrib[pix] = last;
     }
-    // the block's largest n_contrib feeds the backward's heavy-first order
+    // the block's largest n_contrib: the backward's (and this frame's next forward's) cost
     const uint32_t wl = __reduce_max_sync(0xffffffffu, last);
-    if (lane == 0 && wl) atomicMax(&tile_cost[tile], wl);
+    if (lane == 0) block_cost[it] = wl;
   }
 }
 
@@ -172,14 +174,14 @@ static int fwd_grid() {
 }
 
 bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n_contrib, cudaStream_t s) {
-  if (cudaMemsetAsync(F->tile_cost, 0, 4 * (size_t)F->num_tiles, s) != cudaSuccess ||
-      cudaMemsetAsync(F->counters + C_FWD_TICKET, 0, 4, s) != cudaSuccess)
+  if (cudaMemsetAsync(F->counters + C_FWD_TICKET, 0, 4, s) != cudaSuccess)
     return check_launch("render_fwd memset");
   const uint32_t n_items = 8u * (uint32_t)F->num_tiles;
   k_render_fwd<<<fwd_grid(), kFwdWarps * 32, 0, s>>>(F->ranges, F->vals[F->final_buf], F->record, F->counters,
-                                                     F->cam, F->tile_order, n_items, F->counters + C_FWD_TICKET,
-                                                     image, final_T, n_contrib, F->tile_cost);
+                                                     F->cam, F->order_fwd, n_items, F->counters + C_FWD_TICKET,
+                                                     image, final_T, n_contrib, F->block_cost);
   note_launch();
+  F->have_cost = 1;
   return check_launch("k_render_fwd");
 }
 

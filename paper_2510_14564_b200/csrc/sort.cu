@@ -187,7 +187,12 @@ __global__ void __launch_bounds__(256) k_rank_info(int64_t n, const uint32_t* __
   }
 }
 
-// step 3: emission of the (tile, Gaussian) items in depth order, from the packed rank info
+// step 3: emission of the (tile, Gaussian) items in depth order, from the packed rank info.
+// Balanced by items, not ranks: warp w emits the item positions [w L, (w + 1) L) (the nearest
+// Gaussians cover thousands of tiles each, so equal rank ranges would leave a few warps with
+// most of the work).  A warp finds the rank holding its first item with a 32-ary search of
+// item_off, then walks 32-rank windows; each 32-item batch finds its items' ranks with a
+// 5-step shuffle search of the window's inclusive ends.
 __global__ void __launch_bounds__(kDupThreads) k_emit_ranked(int64_t n, const uint32_t* __restrict__ item_off,
                                                              const uint32_t* __restrict__ sigma,
                                                              const uint32_t* __restrict__ rank_cnt,
@@ -201,58 +206,71 @@ __global__ void __launch_bounds__(kDupThreads) k_emit_ranked(int64_t n, const ui
   if (smem_tiles)
     for (int k = threadIdx.x; k < num_tiles; k += kDupThreads) s_tc[k] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int warps = kDupThreads / 32;
-  for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < n; base += (int64_t)gridDim.x * warps * 32) {
-    const int64_t r = base + lane;
-    uint32_t t = 0, off = 0, gid = 0;
-    uint2 rc = make_uint2(0u, 1u);
-    if (r < n) {
-      t = rank_cnt[r];
-      off = item_off[r];
-      gid = sigma[r];
-      if (t) rc = rank_rect[r];
+  const int lane = threadIdx.x & 31;
+  const uint32_t K = counters[C_SCAN_TOTAL];  // sum of rank_cnt (= the key count)
+  const uint32_t n_warps = gridDim.x * (kDupThreads / 32);
+  const uint32_t gw = blockIdx.x * (kDupThreads / 32) + (threadIdx.x >> 5);
+  const uint32_t L = ((K + n_warps - 1) / n_warps + 31) & ~31u;
+  const uint64_t a64 = (uint64_t)gw * L;
+  if (a64 < K) {
+    const uint32_t a = (uint32_t)a64, b = (uint32_t)(a64 + L < K ? a64 + L : K);
+    // largest rank r with item_off[r] <= a (a rank with zero items shares its offset with
+    // the next, so the largest such rank is the one holding item a)
+    int64_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+      const int64_t step = (hi - lo + 31) / 32;
+      const int64_t p = lo + lane * step;
+      const bool ok = p < hi && item_off[p] <= a;
+      const int j = 31 - __clz(__ballot_sync(0xffffffffu, ok));  // lane 0 always ok
+      lo += j * step;
+      hi = min(hi, lo + step);
     }
-    const float inv_w = 1.0f / (float)rc.y;  // once per Gaussian, not per item
-    uint32_t incl = t;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += v;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    if (total == 0) continue;
-    const uint32_t base_off = __shfl_sync(0xffffffffu, off, 0);
-    for (uint32_t kb = 0; kb < total; kb += 32) {
-      const uint32_t k = kb + lane;
-      const bool valid = k < total;
-      const uint32_t kk = valid ? k : total - 1;
-      int lo = 0, hi = 31;  // smallest lane g with incl_g > kk
-#pragma unroll
-      for (int it = 0; it < 5; ++it) {
-        const int mid = (lo + hi) >> 1;
-        const uint32_t v = __shfl_sync(0xffffffffu, incl, mid);
-        if (v > kk) hi = mid; else lo = mid + 1;
+    int64_t rb = lo;
+    uint32_t pos = a;
+    while (pos < b) {
+      const int64_t r = rb + lane;
+      uint32_t t = 0, off = K, gid = 0;
+      uint2 rc = make_uint2(0u, 1u);
+      if (r < n) {
+        t = rank_cnt[r];
+        off = item_off[r];
+        gid = sigma[r];
+        if (t) rc = rank_rect[r];
       }
-      const int g = lo;
-      const uint32_t g_incl = __shfl_sync(0xffffffffu, incl, g);
-      const uint32_t g_t = __shfl_sync(0xffffffffu, t, g);
-      const uint32_t g_xy = __shfl_sync(0xffffffffu, rc.x, g);
-      const uint32_t g_w = __shfl_sync(0xffffffffu, rc.y, g);
-      const float g_iw = __shfl_sync(0xffffffffu, inv_w, g);
-      const uint32_t g_id = __shfl_sync(0xffffffffu, gid, g);
-      if (valid) {
-        const uint32_t local = kk - (g_incl - g_t);
-        // exact: (local + 0.5) / w is >= 1/(2w) away from an integer and its float error is
-        // <= row * 2^-23 < 2^-13 for rows <= 1024 tiles, so truncation gives local / w
-        const uint32_t row = (uint32_t)(((float)local + 0.5f) * g_iw);
-        const uint32_t tile = ((g_xy >> 16) + row) * (uint32_t)tiles_x + (g_xy & 0xffffu) + (local - row * g_w);
-        const uint32_t pos = base_off + kk;
-        keys_out[pos] = tile;
-        vals[pos] = g_id;
-        if (smem_tiles) atomicAdd(&s_tc[tile], 1u);
-        else atomicAdd(&tile_count[tile], 1u);
+      const uint32_t incl = off + t;
+      const float inv_w = 1.0f / (float)rc.y;  // once per Gaussian, not per item
+      const uint32_t end = min(b, __shfl_sync(0xffffffffu, incl, 31));
+      for (uint32_t kb = pos; kb < end; kb += 32) {
+        const uint32_t k = kb + lane;
+        const bool valid = k < end;
+        const uint32_t kk = valid ? k : end - 1;
+        int l = 0, h = 31;  // smallest lane g with incl_g > kk
+#pragma unroll
+        for (int it = 0; it < 5; ++it) {
+          const int mid = (l + h) >> 1;
+          const uint32_t v = __shfl_sync(0xffffffffu, incl, mid);
+          if (v > kk) h = mid; else l = mid + 1;
+        }
+        const int g = l;
+        const uint32_t g_off = __shfl_sync(0xffffffffu, off, g);
+        const uint32_t g_xy = __shfl_sync(0xffffffffu, rc.x, g);
+        const uint32_t g_w = __shfl_sync(0xffffffffu, rc.y, g);
+        const float g_iw = __shfl_sync(0xffffffffu, inv_w, g);
+        const uint32_t g_id = __shfl_sync(0xffffffffu, gid, g);
+        if (valid) {
+          const uint32_t local = kk - g_off;
+          // exact: (local + 0.5) / w is >= 1/(2w) away from an integer and its float error is
+          // <= row * 2^-23 < 2^-13 for rows <= 1024 tiles, so truncation gives local / w
+          const uint32_t row = (uint32_t)(((float)local + 0.5f) * g_iw);
+          const uint32_t tile = ((g_xy >> 16) + row) * (uint32_t)tiles_x + (g_xy & 0xffffu) + (local - row * g_w);
+          keys_out[kk] = tile;
+          vals[kk] = g_id;
+          if (smem_tiles) atomicAdd(&s_tc[tile], 1u);
+          else atomicAdd(&tile_count[tile], 1u);
+        }
       }
+      pos = end;
+      rb += 32;
     }
   }
   __syncthreads();
@@ -261,20 +279,22 @@ __global__ void __launch_bounds__(kDupThreads) k_emit_ranked(int64_t n, const ui
       if (s_tc[k]) atomicAdd(&tile_count[k], s_tc[k]);
 }
 
-// ---------------------------------------------------------------- heavy-first tile order
-// One CTA: bucket the tiles by cost (4 buckets per octave, heaviest bucket first) and
-// scatter them.  Only the CTA scheduling order depends on it, never a result.
+// ---------------------------------------------------------------- longest-first work items
+// The blend kernels' work items are (tile << 3 | 8x4 block).  One CTA buckets them by cost
+// (4 buckets per octave, costliest first) and scatters them; cost[item >> shift] is either
+// a per-tile cost (shift 3: the list length) or a per-block cost (shift 0: the block's
+// largest n_contrib).  Only the scheduling order depends on it, never a result.
 constexpr int kOrderThreads = 1024, kOrderBuckets = 128;
 
-__device__ void order_tiles(const uint32_t* cost, int32_t nt, uint32_t* order, uint32_t* s_b) {
+__device__ void order_items(const uint32_t* cost, int32_t n_items, int32_t shift, uint32_t* order, uint32_t* s_b) {
   for (int k = threadIdx.x; k < kOrderBuckets; k += blockDim.x) s_b[k] = 0;
   __syncthreads();
-  auto bucket = [](uint32_t c) {
-    const float l = log2f((float)c + 1.0f) * 4.0f;
+  auto bucket = [&](int item) {
+    const float l = log2f((float)cost[item >> shift] + 1.0f) * 4.0f;
     const int b = (int)l;
     return kOrderBuckets - 1 - (b < kOrderBuckets - 1 ? b : kOrderBuckets - 1);
   };
-  for (int t = threadIdx.x; t < nt; t += blockDim.x) atomicAdd(&s_b[bucket(cost[t])], 1u);
+  for (int t = threadIdx.x; t < n_items; t += blockDim.x) atomicAdd(&s_b[bucket(t)], 1u);
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t run = 0;
@@ -285,24 +305,24 @@ __device__ void order_tiles(const uint32_t* cost, int32_t nt, uint32_t* order, u
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < nt; t += blockDim.x) order[atomicAdd(&s_b[bucket(cost[t])], 1u)] = (uint32_t)t;
+  for (int t = threadIdx.x; t < n_items; t += blockDim.x) order[atomicAdd(&s_b[bucket(t)], 1u)] = (uint32_t)t;
 }
 
-__global__ void __launch_bounds__(kOrderThreads) k_tile_order(const uint32_t* cost, int32_t nt,
+__global__ void __launch_bounds__(kOrderThreads) k_item_order(const uint32_t* cost, int32_t n_items, int32_t shift,
                                                                const uint32_t* counters, uint32_t* order) {
   __shared__ uint32_t s_b[kOrderBuckets];
   if (counters[C_OVERFLOW]) {
-    for (int t = threadIdx.x; t < nt; t += blockDim.x) order[t] = (uint32_t)t;
+    for (int t = threadIdx.x; t < n_items; t += blockDim.x) order[t] = (uint32_t)t;
     return;
   }
-  order_tiles(cost, nt, order, s_b);
+  order_items(cost, n_items, shift, order, s_b);
 }
 
-bgs_status launch_tile_order(const uint32_t* cost, int32_t num_tiles, const uint32_t* counters, uint32_t* order,
-                             cudaStream_t s) {
-  k_tile_order<<<1, kOrderThreads, 0, s>>>(cost, num_tiles, counters, order);
+bgs_status launch_item_order(const uint32_t* cost, int32_t n_items, int32_t cost_shift, const uint32_t* counters,
+                             uint32_t* order, cudaStream_t s) {
+  k_item_order<<<1, kOrderThreads, 0, s>>>(cost, n_items, cost_shift, counters, order);
   note_launch();
-  return check_launch("k_tile_order");
+  return check_launch("k_item_order");
 }
 
 // ---------------------------------------------------------------- K11: tile counts -> ranges
@@ -310,12 +330,13 @@ bgs_status launch_tile_order(const uint32_t* cost, int32_t num_tiles, const uint
 // and the heavy-first forward tile order.
 __global__ void __launch_bounds__(kOrderThreads) k_tile_scan(const uint32_t* __restrict__ tile_count, int32_t nt,
                                                               const uint32_t* counters, uint2* ranges, uint32_t* hist,
-                                                              int passes, uint32_t* order) {
+                                                              int passes, const uint32_t* block_cost, int use_block_cost,
+                                                              uint32_t* order) {
   __shared__ uint32_t s_warp[kOrderThreads / 32];
   __shared__ uint32_t s_h[4][kRadixBins];
   __shared__ uint32_t s_b[kOrderBuckets];
   if (counters[C_OVERFLOW]) {
-    for (int t = threadIdx.x; t < nt; t += blockDim.x) order[t] = (uint32_t)t;
+    for (int t = threadIdx.x; t < 8 * nt; t += blockDim.x) order[t] = (uint32_t)t;
     return;
   }
   for (int k = threadIdx.x; k < 4 * kRadixBins; k += blockDim.x) (&s_h[0][0])[k] = 0;
@@ -344,7 +365,10 @@ __global__ void __launch_bounds__(kOrderThreads) k_tile_scan(const uint32_t* __r
   __syncthreads();
   for (int k = threadIdx.x; k < (passes - 4) * kRadixBins; k += blockDim.x)
     hist[4 * kRadixBins + k] = (&s_h[0][0])[k];
-  order_tiles(tile_count, nt, order, s_b);
+  // forward work order: this frame's previous per-block costs if it has them (the same
+  // view re-rendered, e.g. in training), else the tile list lengths
+  if (use_block_cost) order_items(block_cost, 8 * nt, 0, order, s_b);
+  else order_items(tile_count, 8 * nt, 3, order, s_b);
 }
 
 static bgs_status memset_status(Frame* F, cudaStream_t s) {
@@ -364,7 +388,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
   const int P = F->sort_passes;
   F->sort_mode = ref64 ? 1 : 0;
   F->final_buf = ref64 ? (P & 1) : ((P - 4) & 1);
-  if (F->n == 0) return launch_tile_order(F->tile_count, F->num_tiles, F->counters, F->tile_order, s);
+  if (F->n == 0) return launch_item_order(F->tile_count, 8 * F->num_tiles, 3, F->counters, F->order_fwd, s);
   const int grid = 4 * num_sms();
   bgs_status st;
   if (ref64) {
@@ -374,7 +398,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
     note_launch();
     if ((st = check_launch("k_emit<index>")) != BGS_OK) return st;
     k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, F->num_tiles, F->counters, F->ranges, F->sort_hist, P,
-                                            F->tile_order);
+                                            F->block_cost, F->have_cost, F->order_fwd);
     note_launch();
     if ((st = check_launch("k_tile_scan")) != BGS_OK || (F->debug_flags & BGS_DEBUG_SKIP_SORT)) return st;
     for (int p = 0; p < P; ++p) {
@@ -411,7 +435,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
   note_launch();
   if ((st = check_launch("k_emit_ranked")) != BGS_OK) return st;
   k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, F->num_tiles, F->counters, F->ranges, F->sort_hist, P,
-                                          F->tile_order);
+                                          F->block_cost, F->have_cost, F->order_fwd);
   note_launch();
   if ((st = check_launch("k_tile_scan")) != BGS_OK) return st;
   // (4) stable split by tile id

@@ -363,3 +363,33 @@ def test_deterministic_forward(bgs):
     _, _, b = run_gpu(bgs, s, cam)
     for k in a:
         assert torch.equal(a[k], b[k]), k
+
+
+def test_schedule_hint_does_not_change_results(bgs):
+    """A frame that re-renders orders its blend work by the previous forward's per-block
+    costs (here: another view's, then its own) -- a scheduling hint only: the forward is
+    bit-identical to a fresh frame's and the backward agrees to float-atomic reordering."""
+    s = scenes()["dense"]()
+    cam_a, cam_b = s.cameras[0], s.cameras[1 % len(s.cameras)]
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    dl = torch.from_numpy(gen.random_dl_dimage(5, cam_a.width, cam_a.height)).to(dev)
+
+    def fwd_bwd(r):
+        out = r.forward(theta, cam_a, s.sh_degree)
+        grad = torch.zeros_like(theta)
+        r.backward(theta, s.sh_degree, dl, out, grad)
+        torch.cuda.synchronize()
+        return {k: v.clone() for k, v in out.items()}, grad
+
+    fresh = bgs.Renderer(s.n, cam_a.width, cam_a.height, max_keys=1 << 21, device=dev)
+    o0, g0 = fwd_bwd(fresh)
+    reused = bgs.Renderer(s.n, cam_a.width, cam_a.height, max_keys=1 << 21, device=dev)
+    reused.forward(theta, cam_b, s.sh_degree)  # costs of another view
+    o1, g1 = fwd_bwd(reused)
+    o2, g2 = fwd_bwd(reused)  # costs of this view
+    for o in (o1, o2):
+        for k in o0:
+            assert torch.equal(o0[k], o[k]), k
+    for g in (g1, g2):
+        assert torch.allclose(g, g0, rtol=1e-4, atol=1e-6 * float(g0.abs().max()))
