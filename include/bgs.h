@@ -85,7 +85,7 @@ typedef struct {
  * bgs_workspace_bytes, carved by bgs_frame_init out of ONE caller allocation
  * (>= 256-byte aligned). */
 typedef struct {
-  uint64_t opaque[64];
+  uint64_t opaque[128];
 } bgs_frame;
 
 /* Device pointers into a frame's workspace, for the parity tests (host struct). */
@@ -215,6 +215,15 @@ bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contri
  * The default depth-first path produces bit-identical values and ranges. */
 #define BGS_DEBUG_SORT_ONESWEEP64 2
 bgs_status bgs_frame_set_debug(bgs_frame* f /*host*/, int32_t flags);
+
+/* Scheduling parameter of the blend kernels (default 4096): a (tile, 8x4 pixel block) work
+ * item whose back-to-front walk is longer than seg_len list entries is split, in the
+ * backward, into segments of seg_len entries processed independently, each starting from
+ * the per-pixel {T, colour behind} the forward recorded at the segment boundary (up to 63
+ * boundaries per item, as many as the frame's checkpoint pool holds; the rest of a walk
+ * stays in its last segment).  Results agree with the unsplit walk to float rounding.
+ * seg_len: multiple of 32 in [32, 65536].  BGS_ERR_INVALID otherwise. */
+bgs_status bgs_frame_set_seg_len(bgs_frame* f /*host*/, int32_t seg_len);
 
 const char* bgs_status_string(bgs_status s);
 const char* bgs_last_error(void);

@@ -57,7 +57,7 @@ class AdamHParams(C.Structure):
 
 
 class Frame(C.Structure):
-    _fields_ = [("opaque", C.c_uint64 * 64)]
+    _fields_ = [("opaque", C.c_uint64 * 128)]
 
 
 class FrameViews(C.Structure):
@@ -91,6 +91,7 @@ _SIGS = {
     "bgs_frame_debug": (C.c_int, [C.POINTER(Frame), C.POINTER(FrameViews)]),
     "bgs_frame_stats": (C.c_int, [C.POINTER(Frame), _P, C.POINTER(Stats), _P]),
     "bgs_frame_set_debug": (C.c_int, [C.POINTER(Frame), C.c_int32]),
+    "bgs_frame_set_seg_len": (C.c_int, [C.POINTER(Frame), C.c_int32]),
     "bgs_density_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "bgs_local_density": (C.c_int, [_P, C.c_int64, C.c_float, C.c_float, C.c_float, _P, _P, _P, C.c_size_t, _P]),
     "bgs_status_string": (C.c_char_p, [C.c_int]),
@@ -211,6 +212,10 @@ def bgs_frame_stats(frame: Frame, n_contrib, stream=None) -> dict:
 
 def bgs_frame_set_debug(frame: Frame, flags: int):
     _check(_lib.bgs_frame_set_debug(C.byref(frame), flags), "bgs_frame_set_debug")
+
+
+def bgs_frame_set_seg_len(frame: Frame, seg_len: int):
+    _check(_lib.bgs_frame_set_seg_len(C.byref(frame), seg_len), "bgs_frame_set_seg_len")
 
 
 def bgs_local_density(means, r, alpha=1.0, beta=1.0, counts=None, stats=None, workspace=None, stream=None):

@@ -10,6 +10,12 @@ namespace bgs {
 
 constexpr int kTile = BGS_TILE;       // 16 x 16 pixel tiles
 constexpr int kTilePixels = kTile * kTile;
+// Long (tile, 8x4 block) walks are split into list segments of seg_len entries: the forward
+// records each block's per-pixel state at every segment boundary b * seg_len (b = 1..kCkMax)
+// it crosses, and the backward processes the segments as independent work units.
+constexpr int kCkMax = 63;
+constexpr int kSegLenDefault = 4096;
+constexpr int kCkPoolSeg = 2048;  // the checkpoint / state pools are sized for seg_len >= this
 
 // counters[] slots (u32 words in the workspace)
 enum : int {
@@ -19,9 +25,12 @@ enum : int {
   C_SORT_TICKET = 4,          // 8 slots: one per radix pass
   C_VISIBLE = 12,
   C_FWD_TICKET = 13,          // work-item tickets of the warp-persistent blend kernels
-  C_BWD_TICKET = 14,
-  C_SCAN_TOTAL = 15,          // total of a scan that does not define K (depth-first sort)
-  C_SORT32_TICKET = 16,       // 8 slots: the depth-first path's 32-bit passes
+  C_CK_BUMP = 14,             // checkpoint slots taken by the forward (reset with C_FWD_TICKET)
+  C_BWD_TICKET = 15,
+  C_SCAN_TOTAL = 16,          // total of a scan that does not define K (depth-first sort)
+  C_SORT32_TICKET = 17,       // 8 slots: the depth-first path's 32-bit passes
+  C_BWD_UNITS = 25,           // number of backward work units (k_bwd_plan)
+  C_FWD_UNITS = 26,           // number of forward work units (k_fwd_plan)
   C_NUM = 32
 };
 
@@ -65,7 +74,15 @@ struct Frame {
   uint32_t* order_fwd;     // [8 tiles] forward work items (tile << 3 | 8x4 block), longest first
   uint32_t* order_bwd;     // [8 tiles] backward work items, longest first
   uint32_t* block_cost;    // [8 tiles] each block's largest n_contrib in the last forward
-  int32_t have_cost, _pad1;// block_cost holds this frame's previous forward
+  int32_t have_cost, seg_len;  // block_cost holds this frame's previous forward; list segment length
+  uint32_t* ck_table;      // [8 tiles][kCkMax] pool slot of boundary b = 1..kCkMax of each block's walk
+  float4* ck_pool;         // [ck_cap][32 lanes] {T, colour behind r, g, b} at a boundary
+  int64_t ck_cap;          // slots of ck_pool, and of spec_state / spec_last
+  uint32_t* spec_base;     // [8 tiles] forward split: first state slot of the item's segments
+  uint32_t* spec_n;        // [8 tiles] forward split: number of segments (1 = not split)
+  uint32_t* arrive;        // [8 tiles] forward split: segments finished
+  float4* spec_state;      // [ck_cap][32] per-segment {T or prod(1 - alpha), C rgb}
+  uint32_t* spec_last;     // [ck_cap][32] per-segment last | stopped << 31
   // depth-first sort path (sort.cu): Gaussians stable-sorted by depth bits, then the
   // rank-ordered tile items stable-split by tile -- the same order as the 64-bit sort
   uint32_t* dkey[2];       // [n] depth bits (0xffffffff for culled)
@@ -110,8 +127,6 @@ bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                               int shift, int64_t count, cudaStream_t s);
 bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, bool publish_k, cudaStream_t s);
-bgs_status launch_item_order(const uint32_t* cost, int32_t n_items, int32_t cost_shift, const uint32_t* counters,
-                             uint32_t* order, cudaStream_t s);
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ float fast_exp(float x) {
@@ -161,6 +176,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// work-unit ordering: bucket of a cost, 4 buckets per octave, costliest first (0..127)
+__device__ __forceinline__ int cost_bucket(uint32_t cost) {
+  const int b = (int)(__float_as_uint((float)cost + 1.0f) >> 21) - (127 << 2);  // 4 log2(cost + 1)
+  return 127 - (b < 127 ? b : 127);
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {

@@ -42,8 +42,10 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t radius, depth, record, tiles_touched, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
-      sort_status, counters, grad2d, tile_count, order_fwd, order_bwd, block_cost, dkey0, dkey1, dval0, dval1,
-      rank_cnt, item_off, rank_rect, cbits, total;
+      sort_status, counters, grad2d, tile_count, order_fwd, order_bwd, block_cost, ck_table, ck_pool, spec_base, spec_n,
+      arrive, spec_state, spec_last, dkey0, dkey1,
+      dval0, dval1, rank_cnt, item_off, rank_rect, cbits, total;
+  int64_t ck_cap;
   int32_t tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
   int64_t sort_tiles_max;
 };
@@ -90,9 +92,19 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.grad2d = take(48 * N);
   const size_t NT = (size_t)L.num_tiles;
   L.tile_count = take(4 * NT);
-  L.order_fwd = take(4 * 8 * NT);
-  L.order_bwd = take(4 * 8 * NT);
+  // checkpoint pool: walks total at most 8 K entries (8 blocks per tile list), so the
+  // segment length kCkPoolSeg needs at most 8 K / kCkPoolSeg boundary slots (+ slack)
+  L.ck_cap = 2 * 8 * (int64_t)NT + 8 * ((max_keys > n ? max_keys : n) / kCkPoolSeg) + 64;
+  L.order_fwd = take(4 * (8 * NT + (size_t)L.ck_cap));  // forward units: items + segments
+  L.order_bwd = take(4 * (8 * NT + (size_t)L.ck_cap));  // backward units: items + boundaries
   L.block_cost = take(4 * 8 * NT);
+  L.ck_table = take(4 * 8 * NT * kCkMax);
+  L.ck_pool = take(512 * (size_t)L.ck_cap);
+  L.spec_base = take(4 * 8 * NT);
+  L.spec_n = take(4 * 8 * NT);
+  L.arrive = take(4 * 8 * NT);
+  L.spec_state = take(512 * (size_t)L.ck_cap);
+  L.spec_last = take(128 * (size_t)L.ck_cap);
   L.dkey0 = take(4 * N);
   L.dkey1 = take(4 * N);
   L.dval0 = take(4 * N);
@@ -224,6 +236,15 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->order_bwd = (uint32_t*)(base + L.order_bwd);
   F->block_cost = (uint32_t*)(base + L.block_cost);
   F->have_cost = 0;
+  F->seg_len = kSegLenDefault;
+  F->ck_table = (uint32_t*)(base + L.ck_table);
+  F->ck_pool = (float4*)(base + L.ck_pool);
+  F->ck_cap = L.ck_cap;
+  F->spec_base = (uint32_t*)(base + L.spec_base);
+  F->spec_n = (uint32_t*)(base + L.spec_n);
+  F->arrive = (uint32_t*)(base + L.arrive);
+  F->spec_state = (float4*)(base + L.spec_state);
+  F->spec_last = (uint32_t*)(base + L.spec_last);
   F->dkey[0] = (uint32_t*)(base + L.dkey0);
   F->dkey[1] = (uint32_t*)(base + L.dkey1);
   F->dval[0] = (uint32_t*)(base + L.dval0);
@@ -338,6 +359,12 @@ bgs_status bgs_frame_debug(const bgs_frame* f, bgs_frame_views* out) {
 bgs_status bgs_frame_set_debug(bgs_frame* f, int32_t flags) {
   if (!frame_ok(f)) return BGS_ERR_INVALID;
   frame_of(f)->debug_flags = flags;
+  return BGS_OK;
+}
+
+bgs_status bgs_frame_set_seg_len(bgs_frame* f, int32_t seg_len) {
+  if (!frame_ok(f) || seg_len < 32 || seg_len > 65536 || (seg_len & 31)) return BGS_ERR_INVALID;
+  frame_of(f)->seg_len = seg_len;
   return BGS_OK;
 }
 

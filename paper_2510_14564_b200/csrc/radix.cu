@@ -145,12 +145,12 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
     uint32_t prefix = 0;
     if (tile > 0) {
       for (int64_t j = tile - 1; j >= 0; --j) {
-        uint32_t s;
+        uint32_t sv;
         do {
-          s = ld_relaxed_u32(&status[j * kRadix + tid]);
-        } while ((s >> 30) == 0);
-        prefix += s & kStMask;
-        if ((s >> 30) == 2) break;
+          sv = ld_relaxed_u32(&status[j * kRadix + tid]);
+        } while ((sv >> 30) == 0);
+        prefix += sv & kStMask;
+        if ((sv >> 30) == 2) break;
       }
       st_relaxed_u32(&st[tid], kStP | (prefix + cnt));
     }

@@ -62,9 +62,10 @@ __device__ __forceinline__ bool box_hits(const float4 a, float bx0, float by0, f
 
 __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ values, const float4* __restrict__ record,
-    const uint32_t* __restrict__ counters, Cam cam, const uint32_t* __restrict__ item_order, uint32_t n_items,
-    uint32_t* ticket, const float* __restrict__ dl_dimage, const float* __restrict__ final_T,
-    const uint32_t* __restrict__ n_contrib, float4* __restrict__ grad2d) {
+    const uint32_t* __restrict__ counters, Cam cam, const uint32_t* __restrict__ units, uint32_t* ticket,
+    const float* __restrict__ dl_dimage, const float* __restrict__ final_T, const uint32_t* __restrict__ n_contrib,
+    float4* __restrict__ grad2d, int32_t seg_len, const uint32_t* __restrict__ ck_table,
+    const float4* __restrict__ ck_pool) {
   __shared__ float4 s_rec[kBwdWarpsPerCta][3][32];
   __shared__ uint32_t s_pos[kBwdWarpsPerCta][32];
   __shared__ uint32_t s_id[kBwdWarpsPerCta][32];
@@ -78,12 +79,17 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
   uint32_t* sid = s_id[warp];
   const int64_t plane = (int64_t)cam.W * cam.H;
   const float4 none = make_float4(-1e30f, -1e30f, -1e30f, -1e30f);
+  const uint32_t n_units = counters[C_BWD_UNITS];
   while (true) {
     uint32_t item = 0;
     if (lane == 0) item = atomicAdd(ticket, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
-    if (item >= n_items) break;
-    const uint32_t it = item_order[item];
+    if (item >= n_units) break;
+    // unit = (tile << 3 | block) | segment k << 25 | last segment << 31
+    const uint32_t code = units[item];
+    const uint32_t it = code & ((1u << 25) - 1u);
+    const int seg = (int)((code >> 25) & 63u);
+    const bool last_seg = (code >> 31) != 0;
     const int tile = (int)(it >> 3), blk = (int)(it & 7);
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
     const int bx = tx * kTile + (blk & 1) * 8, by = ty * kTile + (blk >> 1) * 4;
@@ -96,7 +102,10 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     const int64_t pix = (int64_t)py * cam.W + px;
     const uint32_t my_last = inside ? n_contrib[pix] : 0u;
     const int wmax = (int)min(__reduce_max_sync(0xffffffffu, my_last), rg.y - rg.x);
-    if (wmax == 0) continue;
+    // this unit walks list positions [lo, top): segment seg of the block's walk
+    const int lo = seg * seg_len;
+    const int top = last_seg ? wmax : min(wmax, lo + seg_len);
+    if (top <= lo) continue;
     float T = inside ? final_T[pix] : 1.0f;
     float dLr = 0.f, dLg = 0.f, dLb = 0.f;
     if (inside) {
@@ -105,12 +114,21 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
       dLb = dl_dimage[2 * plane + pix];
     }
     float Sr = T * cam.bg[0], Sg = T * cam.bg[1], Sb = T * cam.bg[2];
-    const int nst = (wmax + 31) / 32;
-    // lane's list position in step s (back to front; negative = no entry)
-    auto pos_of = [&](int s) { return wmax - 32 * (s + 1) + lane; };
+    if (!last_seg && (int)my_last > top) {
+      // the pixel's walk continues past this segment: start from the forward's checkpoint
+      // {T, colour behind} at boundary seg + 1
+      const float4 c = ck_pool[(size_t)ck_table[(size_t)it * kCkMax + seg] * 32 + lane];
+      T = c.x;
+      Sr = c.y;
+      Sg = c.z;
+      Sb = c.w;
+    }
+    const int nst = (top - lo + 31) / 32;
+    // lane's list position in step s (back to front; below lo = no entry)
+    auto pos_of = [&](int s) { return top - 32 * (s + 1) + lane; };
     auto load_id = [&](int s) -> uint32_t {
       const int p = pos_of(s);
-      return (s < nst && p >= 0) ? __ldg(values + rg.x + (uint32_t)p) : 0xffffffffu;
+      return (s < nst && p >= lo) ? __ldg(values + rg.x + (uint32_t)p) : 0xffffffffu;
     };
     auto load_cull = [&](uint32_t id) { return id != 0xffffffffu ? __ldg(record + 3 * id) : none; };
     // pipeline prologue: step 0 fully, step 1 cull record, step 2 id
@@ -225,15 +243,70 @@ static int bwd_grid() {
   return grid;
 }
 
+// Backward work units, longest first: every (tile, 8x4 block) item with a non-empty walk
+// (block_cost = its largest n_contrib, from the forward) contributes one unit per segment:
+// segments [k seg_len, (k + 1) seg_len) for each consecutive recorded boundary, and a last
+// segment up to the walk's end.  One CTA buckets units by length (4 buckets per octave).
+constexpr int kPlanThreads = 1024, kPlanBuckets = 128;
+
+
+__global__ void __launch_bounds__(kPlanThreads) k_bwd_plan(const uint32_t* __restrict__ block_cost, int32_t n_items,
+                                                           const uint32_t* __restrict__ ck_table, uint32_t ck_cap,
+                                                           int32_t seg_len, uint32_t* counters, uint32_t* units) {
+  __shared__ uint32_t s_b[kPlanBuckets];
+  for (int k = threadIdx.x; k < kPlanBuckets; k += blockDim.x) s_b[k] = 0;
+  if (threadIdx.x == 0) counters[C_BWD_TICKET] = 0;
+  __syncthreads();
+  const bool overflow = counters[C_OVERFLOW] != 0;
+  // segments of item t: boundaries b = 1.. with b seg_len < wl and a valid checkpoint slot
+  auto nseg_of = [&](int t, uint32_t wl) {
+    int nb = 0;
+    while (nb < kCkMax && (uint32_t)(nb + 1) * (uint32_t)seg_len < wl && ck_table[(size_t)t * kCkMax + nb] < ck_cap)
+      ++nb;
+    return nb + 1;
+  };
+  for (int t = threadIdx.x; t < n_items; t += blockDim.x) {
+    const uint32_t wl = overflow ? 0u : block_cost[t];
+    if (!wl) continue;
+    const int ns = nseg_of(t, wl);
+    if (ns > 1) atomicAdd(&s_b[cost_bucket((uint32_t)seg_len)], (uint32_t)(ns - 1));
+    atomicAdd(&s_b[cost_bucket(wl - (uint32_t)(ns - 1) * (uint32_t)seg_len)], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t run = 0;
+    for (int b = 0; b < kPlanBuckets; ++b) {
+      const uint32_t c = s_b[b];
+      s_b[b] = run;
+      run += c;
+    }
+    counters[C_BWD_UNITS] = run;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < n_items; t += blockDim.x) {
+    const uint32_t wl = overflow ? 0u : block_cost[t];
+    if (!wl) continue;
+    const int ns = nseg_of(t, wl);
+    if (ns > 1) {
+      const uint32_t base = atomicAdd(&s_b[cost_bucket((uint32_t)seg_len)], (uint32_t)(ns - 1));
+      for (int k = 0; k < ns - 1; ++k) units[base + k] = (uint32_t)t | ((uint32_t)k << 25);
+    }
+    const uint32_t pos = atomicAdd(&s_b[cost_bucket(wl - (uint32_t)(ns - 1) * (uint32_t)seg_len)], 1u);
+    units[pos] = (uint32_t)t | ((uint32_t)(ns - 1) << 25) | (1u << 31);
+  }
+}
+
 bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
                             cudaStream_t s) {
-  // longest first by each block's largest n_contrib (its back-to-front walk length)
-  bgs_status st = launch_item_order(F->block_cost, 8 * F->num_tiles, 0, F->counters, F->order_bwd, s);
+  const uint32_t cap = (uint32_t)(F->ck_cap < 0xffffffffll ? F->ck_cap : 0xffffffffll);
+  k_bwd_plan<<<1, kPlanThreads, 0, s>>>(F->block_cost, 8 * F->num_tiles, F->ck_table, cap, F->seg_len, F->counters,
+                                        F->order_bwd);
+  note_launch();
+  bgs_status st = check_launch("k_bwd_plan");
   if (st != BGS_OK) return st;
-  if (cudaMemsetAsync(F->counters + C_BWD_TICKET, 0, 4, s) != cudaSuccess) return check_launch("blend_bwd memset");
   k_render_bwd<<<bwd_grid(), kBwdWarpsPerCta * 32, 0, s>>>(
-      F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, 8u * (uint32_t)F->num_tiles,
-      F->counters + C_BWD_TICKET, dL_dimage, final_T, n_contrib, F->grad2d);
+      F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,
+      dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool);
   note_launch();
   return check_launch("k_render_bwd");
 }

@@ -279,66 +279,17 @@ __global__ void __launch_bounds__(kDupThreads) k_emit_ranked(int64_t n, const ui
       if (s_tc[k]) atomicAdd(&tile_count[k], s_tc[k]);
 }
 
-// ---------------------------------------------------------------- longest-first work items
-// The blend kernels' work items are (tile << 3 | 8x4 block).  One CTA buckets them by cost
-// (4 buckets per octave, costliest first) and scatters them; cost[item >> shift] is either
-// a per-tile cost (shift 3: the list length) or a per-block cost (shift 0: the block's
-// largest n_contrib).  Only the scheduling order depends on it, never a result.
-constexpr int kOrderThreads = 1024, kOrderBuckets = 128;
-
-__device__ void order_items(const uint32_t* cost, int32_t n_items, int32_t shift, uint32_t* order, uint32_t* s_b) {
-  for (int k = threadIdx.x; k < kOrderBuckets; k += blockDim.x) s_b[k] = 0;
-  __syncthreads();
-  auto bucket = [&](int item) {
-    const float l = log2f((float)cost[item >> shift] + 1.0f) * 4.0f;
-    const int b = (int)l;
-    return kOrderBuckets - 1 - (b < kOrderBuckets - 1 ? b : kOrderBuckets - 1);
-  };
-  for (int t = threadIdx.x; t < n_items; t += blockDim.x) atomicAdd(&s_b[bucket(t)], 1u);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (int b = 0; b < kOrderBuckets; ++b) {
-      const uint32_t c = s_b[b];
-      s_b[b] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < n_items; t += blockDim.x) order[atomicAdd(&s_b[bucket(t)], 1u)] = (uint32_t)t;
-}
-
-__global__ void __launch_bounds__(kOrderThreads) k_item_order(const uint32_t* cost, int32_t n_items, int32_t shift,
-                                                               const uint32_t* counters, uint32_t* order) {
-  __shared__ uint32_t s_b[kOrderBuckets];
-  if (counters[C_OVERFLOW]) {
-    for (int t = threadIdx.x; t < n_items; t += blockDim.x) order[t] = (uint32_t)t;
-    return;
-  }
-  order_items(cost, n_items, shift, order, s_b);
-}
-
-bgs_status launch_item_order(const uint32_t* cost, int32_t n_items, int32_t cost_shift, const uint32_t* counters,
-                             uint32_t* order, cudaStream_t s) {
-  k_item_order<<<1, kOrderThreads, 0, s>>>(cost, n_items, cost_shift, counters, order);
-  note_launch();
-  return check_launch("k_item_order");
-}
-
 // ---------------------------------------------------------------- K11: tile counts -> ranges
+constexpr int kOrderThreads = 1024;
+
 // Also writes the tile-digit pass histograms hist[4 .. passes) (digit p-4 of the tile id)
 // and the heavy-first forward tile order.
 __global__ void __launch_bounds__(kOrderThreads) k_tile_scan(const uint32_t* __restrict__ tile_count, int32_t nt,
                                                               const uint32_t* counters, uint2* ranges, uint32_t* hist,
-                                                              int passes, const uint32_t* block_cost, int use_block_cost,
-                                                              uint32_t* order) {
+                                                              int passes) {
   __shared__ uint32_t s_warp[kOrderThreads / 32];
   __shared__ uint32_t s_h[4][kRadixBins];
-  __shared__ uint32_t s_b[kOrderBuckets];
-  if (counters[C_OVERFLOW]) {
-    for (int t = threadIdx.x; t < 8 * nt; t += blockDim.x) order[t] = (uint32_t)t;
-    return;
-  }
+  if (counters[C_OVERFLOW]) return;
   for (int k = threadIdx.x; k < 4 * kRadixBins; k += blockDim.x) (&s_h[0][0])[k] = 0;
   const int chunk = (nt + kOrderThreads - 1) / kOrderThreads;
   const int t0 = threadIdx.x * chunk, t1 = min(nt, t0 + chunk);
@@ -365,10 +316,6 @@ __global__ void __launch_bounds__(kOrderThreads) k_tile_scan(const uint32_t* __r
   __syncthreads();
   for (int k = threadIdx.x; k < (passes - 4) * kRadixBins; k += blockDim.x)
     hist[4 * kRadixBins + k] = (&s_h[0][0])[k];
-  // forward work order: this frame's previous per-block costs if it has them (the same
-  // view re-rendered, e.g. in training), else the tile list lengths
-  if (use_block_cost) order_items(block_cost, 8 * nt, 0, order, s_b);
-  else order_items(tile_count, 8 * nt, 3, order, s_b);
 }
 
 static bgs_status memset_status(Frame* F, cudaStream_t s) {
@@ -388,7 +335,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
   const int P = F->sort_passes;
   F->sort_mode = ref64 ? 1 : 0;
   F->final_buf = ref64 ? (P & 1) : ((P - 4) & 1);
-  if (F->n == 0) return launch_item_order(F->tile_count, 8 * F->num_tiles, 3, F->counters, F->order_fwd, s);
+  if (F->n == 0) return BGS_OK;
   const int grid = 4 * num_sms();
   bgs_status st;
   if (ref64) {
@@ -397,8 +344,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
                                                F->keys[0], F->vals[0], F->tile_count, F->sort_hist);
     note_launch();
     if ((st = check_launch("k_emit<index>")) != BGS_OK) return st;
-    k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, F->num_tiles, F->counters, F->ranges, F->sort_hist, P,
-                                            F->block_cost, F->have_cost, F->order_fwd);
+    k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, F->num_tiles, F->counters, F->ranges, F->sort_hist, P);
     note_launch();
     if ((st = check_launch("k_tile_scan")) != BGS_OK || (F->debug_flags & BGS_DEBUG_SKIP_SORT)) return st;
     for (int p = 0; p < P; ++p) {
@@ -434,8 +380,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
                                              F->num_tiles, F->counters, tkey[0], F->vals[0], F->tile_count);
   note_launch();
   if ((st = check_launch("k_emit_ranked")) != BGS_OK) return st;
-  k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, F->num_tiles, F->counters, F->ranges, F->sort_hist, P,
-                                          F->block_cost, F->have_cost, F->order_fwd);
+  k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, F->num_tiles, F->counters, F->ranges, F->sort_hist, P);
   note_launch();
   if ((st = check_launch("k_tile_scan")) != BGS_OK) return st;
   // (4) stable split by tile id

@@ -44,10 +44,12 @@ def scenes():
     }
 
 
-def run_gpu(bgs, s, cam, max_keys=1 << 21, skip_sort=False, flags=0):
+def run_gpu(bgs, s, cam, max_keys=1 << 21, skip_sort=False, flags=0, seg_len=None):
     dev = torch.device("cuda")
     theta = torch.from_numpy(s.theta).to(dev)
     r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=max_keys, device=dev, debug_flags=flags)
+    if seg_len is not None:
+        bgs.bgs_frame_set_seg_len(r.frame, seg_len)
     if skip_sort:
         bgs.bgs_frame_set_debug(r.frame, bgs.BGS_DEBUG_SKIP_SORT)
         g = bgs.gaussians(theta, s.n, s.sh_degree)
@@ -222,16 +224,20 @@ def test_render_bwd_parity(bgs, name):
         assert err <= GRAD_TOL, (name, gname, err)
 
 
-@pytest.mark.parametrize("name", ["tiny", "dense", "garden20k"])
-def test_blend_bwd_intermediate_parity(bgs, name):
+@pytest.mark.parametrize("name,seg_len", [("tiny", None), ("dense", None), ("garden20k", None), ("dense", 32),
+                                          ("dense", 96), ("garden20k", 64), ("ragged", 32)])
+def test_blend_bwd_intermediate_parity(bgs, name, seg_len):
     """a9 alone: the per-view blend gradients {dxy, dconic, dopacity, drgb} in grad2d vs
-    the oracle's O15 sums (double)."""
+    the oracle's O15 sums (double).  seg_len: long walks split into list segments that
+    start from the forward's checkpoints (bgs_frame_set_seg_len)."""
     if name == "garden20k":
         s = gen.garden(seed=1, n=20000, n_cams=4)
     else:
         s = scenes()[name]()
     cam = s.cameras[0]
-    r, theta, out = run_gpu(bgs, s, cam, max_keys=1 << 22)
+    r, theta, out = run_gpu(bgs, s, cam, max_keys=1 << 22, seg_len=seg_len)
+    if seg_len is not None:  # the split path is exercised: walks span several segments
+        assert int(out["n_contrib"].max()) > 3 * seg_len
     ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
     dl_np = masked_dl(5, cam, ref)
     bgs.bgs_blend_bwd(r.frame, torch.from_numpy(dl_np).cuda(), out["final_T"], out["n_contrib"])
@@ -393,3 +399,76 @@ def test_schedule_hint_does_not_change_results(bgs):
             assert torch.equal(o0[k], o[k]), k
     for g in (g1, g2):
         assert torch.allclose(g, g0, rtol=1e-4, atol=1e-6 * float(g0.abs().max()))
+
+
+@pytest.mark.parametrize("seg_len", [32, 64, 2048])
+def test_split_backward_matches_unsplit(bgs, seg_len):
+    """The segment split is a scheduling choice: theta gradients of a split backward agree
+    with the default one to float-atomic rounding (garden-shaped scene, long walks)."""
+    s = gen.garden(seed=2, n=30000, n_cams=2)
+    cam = s.cameras[0]
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    dl = torch.from_numpy(gen.random_dl_dimage(7, cam.width, cam.height)).to(dev)
+    grads = []
+    for sl in (65536, seg_len):
+        r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=1 << 22, device=dev)
+        bgs.bgs_frame_set_seg_len(r.frame, sl)
+        out = r.forward(theta, cam, s.sh_degree)
+        g = torch.zeros_like(theta)
+        r.backward(theta, s.sh_degree, dl, out, g)
+        torch.cuda.synchronize()
+        grads.append(g.double())
+    a, b = grads
+    for gname, idx in oracle.group_slices(s.n).items():
+        idx_t = torch.as_tensor(np.arange(59 * s.n)[idx], device=dev)
+        err = float((a[idx_t] - b[idx_t]).norm() / max(float(a[idx_t].norm()), 1e-300))
+        assert err <= 1e-4, (gname, err)
+
+
+def test_seg_len_validation(bgs):
+    s = scenes()["tiny"]()
+    r = bgs.Renderer(s.n, s.cameras[0].width, s.cameras[0].height, max_keys=1 << 16, device="cuda")
+    for bad in (0, 16, 33, 65568, -32):
+        with pytest.raises(bgs.BgsError):
+            bgs.bgs_frame_set_seg_len(r.frame, bad)
+    bgs.bgs_frame_set_seg_len(r.frame, 32)
+
+
+@pytest.mark.parametrize("name,seg_len", [("dense", 32), ("dense", 64), ("garden20k", 64), ("ragged", 32)])
+def test_split_forward_parity(bgs, name, seg_len):
+    """Forward with the segment split (a frame re-rendering its view splits every walk
+    longer than 2 seg_len into speculative segments merged in list order): image, final_T
+    and n_contrib against the oracle on the pixels without an R23 near tie; then the
+    backward from the split forward's checkpoints against the oracle's blend gradients."""
+    s = gen.garden(seed=1, n=20000, n_cams=4) if name == "garden20k" else scenes()[name]()
+    cam = s.cameras[0]
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=1 << 22, device=dev)
+    bgs.bgs_frame_set_seg_len(r.frame, seg_len)
+    out0 = {k: v.clone() for k, v in r.forward(theta, cam, s.sh_degree).items()}  # unsplit, sets the hint
+    assert int(out0["n_contrib"].max()) > 3 * seg_len
+    out = r.forward(theta, cam, s.sh_degree)  # split
+    torch.cuda.synchronize()
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    ok = ref["flags"] == 0
+    img = out["image"].cpu().numpy()
+    nc = out["n_contrib"].cpu().numpy().view(np.uint32)
+    assert np.abs(img - ref["image"])[:, ok].max() <= IMG_TOL
+    assert np.array_equal(nc[ok], ref["n_contrib"][ok])
+    assert np.abs(out["final_T"].cpu().numpy() - ref["final_T"])[ok].max() <= 1e-5
+    assert np.abs(img - ref["image"]).max() <= 2e-2
+    # the split changes only T's rounding order
+    assert torch.allclose(out["image"], out0["image"], atol=1e-5)
+    # backward from the split forward's checkpoints
+    dl_np = masked_dl(5, cam, ref)
+    bgs.bgs_blend_bwd(r.frame, torch.from_numpy(dl_np).cuda(), out["final_T"], out["n_contrib"])
+    torch.cuda.synchronize()
+    g2 = dev_array(r.views().grad2d, 12 * s.n, torch.float32).reshape(s.n, 12).astype(np.float64)
+    g_ref = oracle.backward(s.theta, s.n, s.sh_degree, cam, ref, dl_np)
+    vis = ref["pre"]["radius"] > 0
+    for k, (a, b) in {"xy": (g2[:, 0:2], g_ref["xy"]), "conic": (g2[:, 2:5], g_ref["conic"]),
+                      "opacity": (g2[:, 5], g_ref["opacity"]), "rgb": (g2[:, 6:9], g_ref["rgb"])}.items():
+        err = np.linalg.norm(a[vis] - b[vis]) / max(np.linalg.norm(b[vis]), 1e-300)
+        assert err <= 1e-4, (k, err)

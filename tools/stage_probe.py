@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--view", type=int, default=0)
     ap.add_argument("--only", default=None, help="comma-separated stage names")
     ap.add_argument("--step", type=int, default=0, help="run N full one-view training steps (for ncu)")
+    ap.add_argument("--seg-lens", default=None, help="comma-separated seg_len values: time fwd/bwd for each")
     a = ap.parse_args()
     t0 = time.time()
     s = gen.make(a.config)
@@ -59,6 +60,22 @@ def main():
             bgs.bgs_adam_step(theta, grad, m, v, s.n, hp, it + 1)
         torch.cuda.synchronize()
         print("launches per step:", bgs.launch_count())
+        return
+    if a.seg_lens:
+        for sl in [int(x) for x in a.seg_lens.split(",")]:
+            bgs.bgs_frame_set_seg_len(r.frame, sl)
+            res = {}
+            for name in ("render_fwd", "blend_bwd"):
+                stages["render_fwd"]()  # records this seg_len's checkpoints
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(a.reps):
+                    stages[name]()
+                e1.record()
+                torch.cuda.synchronize()
+                res[name] = e0.elapsed_time(e1) / a.reps
+            print(f"seg_len {sl:6d}: fwd {res['render_fwd']:.3f} ms  bwd {res['blend_bwd']:.3f} ms", flush=True)
         return
     only = set(a.only.split(",")) if a.only else None
     for name, fn in stages.items():
