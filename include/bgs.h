@@ -214,6 +214,9 @@ bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contri
  * onesweep LSD sort over all 32 + bit_width(tiles - 1) bits (keys_sorted is then valid).
  * The default depth-first path produces bit-identical values and ranges. */
 #define BGS_DEBUG_SORT_ONESWEEP64 2
+/* Depth-first path with the radix tile split (two 8-bit onesweep passes over the K items)
+ * instead of the direct chunked split; same values and ranges. */
+#define BGS_DEBUG_SORT_RADIX_SPLIT 4
 bgs_status bgs_frame_set_debug(bgs_frame* f /*host*/, int32_t flags);
 
 /* Scheduling parameter of the blend kernels (default 4096): a (tile, 8x4 pixel block) work

@@ -24,6 +24,7 @@ _lib = C.CDLL(LIB_PATH)
 BGS_OK, BGS_ERR_INVALID, BGS_ERR_CAPACITY, BGS_ERR_CUDA, BGS_ERR_UNSUPPORTED = 0, -1, -2, -3, -4
 BGS_DEBUG_SKIP_SORT = 1
 BGS_DEBUG_SORT_ONESWEEP64 = 2
+BGS_DEBUG_SORT_RADIX_SPLIT = 4
 
 
 class BgsError(RuntimeError):

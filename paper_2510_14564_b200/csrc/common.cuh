@@ -15,7 +15,10 @@ constexpr int kTilePixels = kTile * kTile;
 // it crosses, and the backward processes the segments as independent work units.
 constexpr int kCkMax = 63;
 constexpr int kSegLenDefault = 4096;
-constexpr int kCkPoolSeg = 2048;  // the checkpoint / state pools are sized for seg_len >= this
+constexpr int kCkPoolSeg = 2048;
+// direct tile split (sort.cu): 16384-item chunks; per-warp shared-memory tile counters
+constexpr int kChunkItemsF = 16384;
+constexpr int kDirectMaxCells = 12800;  // (tiles_x + 1)(tiles_y + 1) bound  // the checkpoint / state pools are sized for seg_len >= this
 
 // counters[] slots (u32 words in the workspace)
 enum : int {
@@ -83,6 +86,7 @@ struct Frame {
   uint32_t* arrive;        // [8 tiles] forward split: segments finished
   float4* spec_state;      // [ck_cap][32] per-segment {T or prod(1 - alpha), C rgb}
   uint32_t* spec_last;     // [ck_cap][32] per-segment last | stopped << 31
+  uint32_t* chunk_cnt;     // [max_keys / 16384][tiles] direct tile split (null when the grid is too large)
   // depth-first sort path (sort.cu): Gaussians stable-sorted by depth bits, then the
   // rank-ordered tile items stable-split by tile -- the same order as the 64-bit sort
   uint32_t* dkey[2];       // [n] depth bits (0xffffffff for culled)
@@ -176,6 +180,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+
+// Exact-up-to-margin cull of one list entry against an 8x4 pixel block: can any pixel
+// centre p of [bx0, bx1] x [by0, by1] reach power(p - mu) = A dx^2 + B dx dy + C dy^2 >= thr
+// (the alpha >= 1/255 level set, thr = pthr)?  The power is concave, so its maximum over
+// the rectangle is at mu when mu is inside, else on the edge(s) facing mu, where it is a
+// clamped 1-D vertex.  The margin covers the float error of both this bound and the
+// blend's own per-pixel power (each <= 2^-22 of the terms' magnitude), so no entry the
+// blend would evaluate as power >= thr is ever dropped.
+__device__ __forceinline__ bool ellipse_hits_block(float mx, float my, float A, float B, float C, float thr,
+                                                   float bx0, float by0, float bx1, float by1) {
+  const float lx = bx0 - mx, hx = bx1 - mx, ly = by0 - my, hy = by1 - my;
+  const bool in_x = lx <= 0.0f && hx >= 0.0f, in_y = ly <= 0.0f && hy >= 0.0f;
+  if (in_x && in_y) return true;
+  float best = -3.0e38f;
+  if (!in_x) {
+    const float dx = lx > 0.0f ? lx : hx;
+    const float dy = fminf(fmaxf(__fdividef(-B * dx, 2.0f * C), ly), hy);
+    best = fmaxf(best, A * dx * dx + B * dx * dy + C * dy * dy);
+  }
+  if (!in_y) {
+    const float dy = ly > 0.0f ? ly : hy;
+    const float dx = fminf(fmaxf(__fdividef(-B * dy, 2.0f * A), lx), hx);
+    best = fmaxf(best, A * dx * dx + B * dx * dy + C * dy * dy);
+  }
+  const float ex = fmaxf(-lx, hx), ey = fmaxf(-ly, hy);
+  const float margin = 1e-3f + 1e-5f * (fabsf(A) * ex * ex + fabsf(C) * ey * ey);
+  return best >= thr - margin;
 }
 
 // work-unit ordering: bucket of a cost, 4 buckets per octave, costliest first (0..127)

@@ -43,11 +43,12 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
   size_t radius, depth, record, tiles_touched, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
       sort_status, counters, grad2d, tile_count, order_fwd, order_bwd, block_cost, ck_table, ck_pool, spec_base, spec_n,
-      arrive, spec_state, spec_last, dkey0, dkey1,
+      arrive, spec_state, spec_last, chunk_cnt, dkey0, dkey1,
       dval0, dval1, rank_cnt, item_off, rank_rect, cbits, total;
   int64_t ck_cap;
   int32_t tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
   int64_t sort_tiles_max;
+  bool direct;
 };
 
 constexpr int kScanTile = 2048;
@@ -105,6 +106,8 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.arrive = take(4 * 8 * NT);
   L.spec_state = take(512 * (size_t)L.ck_cap);
   L.spec_last = take(128 * (size_t)L.ck_cap);
+  L.direct = (int64_t)(L.tiles_x + 1) * (L.tiles_y + 1) <= kDirectMaxCells;
+  L.chunk_cnt = L.direct ? take(4 * NT * (size_t)((max_keys + kChunkItemsF - 1) / kChunkItemsF)) : 0;
   L.dkey0 = take(4 * N);
   L.dkey1 = take(4 * N);
   L.dval0 = take(4 * N);
@@ -245,6 +248,7 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->arrive = (uint32_t*)(base + L.arrive);
   F->spec_state = (float4*)(base + L.spec_state);
   F->spec_last = (uint32_t*)(base + L.spec_last);
+  F->chunk_cnt = L.direct ? (uint32_t*)(base + L.chunk_cnt) : nullptr;
   F->dkey[0] = (uint32_t*)(base + L.dkey0);
   F->dkey[1] = (uint32_t*)(base + L.dkey1);
   F->dval[0] = (uint32_t*)(base + L.dval0);

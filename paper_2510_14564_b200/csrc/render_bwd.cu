@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     }
     for (int s = 0; s < nst; ++s) {
       // (1) commit step s into the warp's shared-memory slice
+      // exact ellipse-vs-block cull of the box hits (their full records are loaded)
+      if (h_c) h_c = ellipse_hits_block(a_c.x, a_c.y, r1_c.x, r1_c.y, r1_c.z, r2_c.w, bx0, by0, bx1, by1);
       const uint32_t bal = __ballot_sync(0xffffffffu, h_c);
       if (h_c) {
         const int q = __popc(bal & lt);

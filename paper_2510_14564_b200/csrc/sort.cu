@@ -279,6 +279,271 @@ __global__ void __launch_bounds__(kDupThreads) k_emit_ranked(int64_t n, const ui
       if (s_tc[k]) atomicAdd(&tile_count[k], s_tc[k]);
 }
 
+// ---------------------------------------------------------------- direct tile split
+// Replaces (3)-(4) of the depth-first path when the tile grid is small enough for
+// per-warp shared-memory tile counters: the depth-ordered item sequence is cut into
+// chunks of kChunkItems items; (a) each chunk counts its items per tile (its ranks'
+// rects, clipped to the chunk, added as 2D difference rectangles and prefix-summed);
+// (b) a column scan over chunks gives each (chunk, tile) its offset inside the tile's
+// list; (c) each chunk emits its items in depth order straight to their final positions,
+// a running per-tile counter in shared memory numbering the items of a tile in order (in
+// a 32-item batch, equal tiles are ranked by match_any).  The order is the stable split
+// of the depth-ordered sequence by tile -- the same (tile, depth, index) order -- with no
+// keys materialised and no radix passes over K.
+constexpr int kChunkItems = kChunkItemsF;
+constexpr int kChunkWarps = 4;
+
+// largest rank r with item_off[r] <= a (a rank with zero items shares its offset with the
+// next one, so the largest such rank holds item a); 32-ary search by one warp
+__device__ __forceinline__ int64_t rank_of_item(const uint32_t* __restrict__ item_off, int64_t n, uint32_t a,
+                                                int lane) {
+  int64_t lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const int64_t step = (hi - lo + 31) / 32;
+    const int64_t p = lo + lane * step;
+    const bool ok = p < hi && item_off[p] <= a;
+    const int j = 31 - __clz(__ballot_sync(0xffffffffu, ok));  // lane 0 always ok
+    lo += j * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+// (a) per-(chunk, tile) item counts.  Grid cells: (tiles_y + 1) x (tiles_x + 1) ints per warp.
+__global__ void __launch_bounds__(kChunkWarps * 32) k_chunk_hist(int64_t n, const uint32_t* __restrict__ item_off,
+                                                                 const uint32_t* __restrict__ rank_cnt,
+                                                                 const uint2* __restrict__ rank_rect, int32_t tiles_x,
+                                                                 int32_t tiles_y, const uint32_t* counters,
+                                                                 uint32_t* chunk_cnt) {
+  extern __shared__ int32_t s_grid[];
+  if (counters[C_OVERFLOW]) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = tiles_x + 1, cells = gw * (tiles_y + 1), nt = tiles_x * tiles_y;
+  int32_t* G = s_grid + warp * cells;
+  const uint32_t K = counters[C_SCAN_TOTAL];
+  const uint32_t n_chunks = (K + kChunkItems - 1) / kChunkItems;
+  const uint32_t c = blockIdx.x * kChunkWarps + warp;
+  if (c >= n_chunks) return;
+  for (int k = lane; k < cells; k += 32) G[k] = 0;
+  __syncwarp();
+  const uint32_t a = c * kChunkItems, b = min(K, a + kChunkItems);
+  auto add_rect = [&](int x0, int y0, int x1, int y1) {  // [x0, x1) x [y0, y1), non-empty
+    atomicAdd(&G[y0 * gw + x0], 1);
+    atomicAdd(&G[y0 * gw + x1], -1);
+    atomicAdd(&G[y1 * gw + x0], -1);
+    atomicAdd(&G[y1 * gw + x1], 1);
+  };
+  // the chunk's ranks [r0, r1]: independent loads, 4 windows of 32 per round
+  const int64_t r0 = rank_of_item(item_off, n, a, lane), r1 = rank_of_item(item_off, n, b - 1, lane);
+  for (int64_t rb = r0; rb <= r1; rb += 128) {
+    uint32_t o[4], t[4];
+    uint2 rc[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t r = rb + 32 * q + lane;
+      o[q] = 0;
+      t[q] = 0;
+      rc[q] = make_uint2(0u, 1u);
+      if (r <= r1) {
+        o[q] = item_off[r];
+        t[q] = rank_cnt[r];
+        rc[q] = rank_rect[r];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t s0 = max(a, o[q]), e0 = min(b, o[q] + t[q]);
+      if (t[q] && s0 < e0) {
+        const int w = (int)rc[q].y, x0 = (int)(rc[q].x & 0xffffu), y0 = (int)(rc[q].x >> 16);
+        const int ls = (int)(s0 - o[q]), le = (int)(e0 - o[q]) - 1;  // inclusive local item range
+        const int q1 = ls / w, c1 = ls - q1 * w, q2 = le / w, c2 = le - q2 * w;
+        if (q1 == q2) {
+          add_rect(x0 + c1, y0 + q1, x0 + c2 + 1, y0 + q1 + 1);
+        } else {
+          add_rect(x0 + c1, y0 + q1, x0 + w, y0 + q1 + 1);
+          if (q2 > q1 + 1) add_rect(x0, y0 + q1 + 1, x0 + w, y0 + q2);
+          add_rect(x0, y0 + q2, x0 + c2 + 1, y0 + q2 + 1);
+        }
+      }
+    }
+  }
+  __syncwarp();
+  for (int y = lane; y <= tiles_y; y += 32) {  // prefix along rows
+    int32_t run = 0;
+    for (int x = 0; x <= tiles_x; ++x) run = (G[y * gw + x] += run);
+  }
+  __syncwarp();
+  for (int x = lane; x <= tiles_x; x += 32) {  // then along columns
+    int32_t run = 0;
+    for (int y = 0; y <= tiles_y; ++y) run = (G[y * gw + x] += run);
+  }
+  __syncwarp();
+  uint32_t* row = chunk_cnt + (size_t)c * nt;
+  for (int t = lane; t < nt; t += 32) {
+    const int y = t / tiles_x, x = t - y * tiles_x;
+    row[t] = (uint32_t)G[y * gw + x];
+  }
+}
+
+// (b) exclusive prefix over chunks of each tile's column (in place) and the tile totals.
+// Block = 32 tiles x 32 chunk ranges.
+__global__ void __launch_bounds__(1024) k_chunk_scan(uint32_t* chunk_cnt, int32_t nt, const uint32_t* counters,
+                                                     uint32_t* tile_count) {
+  __shared__ uint32_t s[32][33];
+  if (counters[C_OVERFLOW]) return;
+  const uint32_t K = counters[C_SCAN_TOTAL];
+  const int n_chunks = (int)((K + kChunkItems - 1) / kChunkItems);
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + tx;
+  const int per = (n_chunks + 31) / 32;
+  const int c0 = ty * per, c1 = min(n_chunks, c0 + per);
+  uint32_t sum = 0;
+  if (t < nt)
+    for (int c = c0; c < c1; ++c) sum += chunk_cnt[(size_t)c * nt + t];
+  s[ty][tx] = sum;
+  __syncthreads();
+  if (ty == 0) {
+    uint32_t run = 0;
+    for (int k = 0; k < 32; ++k) {
+      const uint32_t v = s[k][tx];
+      s[k][tx] = run;
+      run += v;
+    }
+    if (t < nt) tile_count[t] = run;
+  }
+  __syncthreads();
+  if (t < nt) {
+    uint32_t run = s[ty][tx];
+    for (int c = c0; c < c1; ++c) {
+      uint32_t* p = chunk_cnt + (size_t)c * nt + t;
+      const uint32_t v = *p;
+      *p = run;
+      run += v;
+    }
+  }
+}
+
+// (c) items of each chunk, in depth order, to their final positions.  Per warp: the next
+// final position of each tile's items (u32) and a per-tile lane scratch (u8) that detects
+// two items of a 32-item batch falling into the same tile.
+constexpr int kEmitWarps = 2;
+
+__global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, const uint32_t* __restrict__ item_off,
+                                                                 const uint32_t* __restrict__ sigma,
+                                                                 const uint32_t* __restrict__ rank_cnt,
+                                                                 const uint2* __restrict__ rank_rect,
+                                                                 int32_t tiles_x, int32_t nt,
+                                                                 const uint32_t* counters,
+                                                                 const uint32_t* __restrict__ chunk_cnt,
+                                                                 const uint2* __restrict__ ranges, uint32_t* vals) {
+  extern __shared__ uint32_t s_dyn[];
+  if (counters[C_OVERFLOW]) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t K = counters[C_SCAN_TOTAL];
+  const uint32_t n_chunks = (K + kChunkItems - 1) / kChunkItems;
+  const uint32_t c = blockIdx.x * kEmitWarps + warp;
+  if (c >= n_chunks) return;
+  const int nt_pad = (nt + 3) & ~3;
+  uint32_t* nxt = s_dyn + warp * (nt_pad + nt_pad / 4);  // nt u32 positions + nt u8 scratch
+  uint8_t* scratch = reinterpret_cast<uint8_t*>(nxt + nt_pad);
+  const uint32_t* row = chunk_cnt + (size_t)c * nt;
+  for (int t = lane; t < nt; t += 32) nxt[t] = ranges[t].x + row[t];
+  __syncwarp();
+  const uint32_t a = c * kChunkItems, b = min(K, a + kChunkItems);
+  int64_t rb = rank_of_item(item_off, n, a, lane);
+  auto load_win = [&](int64_t base, uint32_t& t, uint32_t& off, uint32_t& gid, uint2& rc) {
+    const int64_t r = base + lane;
+    t = 0;
+    off = K;
+    gid = 0;
+    rc = make_uint2(0u, 1u);
+    if (r < n) {
+      t = rank_cnt[r];
+      off = item_off[r];
+      gid = sigma[r];
+      rc = rank_rect[r];
+    }
+  };
+  uint32_t t, off, gid, t_n, off_n, gid_n;
+  uint2 rc, rc_n;
+  load_win(rb, t, off, gid, rc);
+  uint32_t pos = a;
+  while (pos < b) {
+    load_win(rb + 32, t_n, off_n, gid_n, rc_n);  // next window, in flight during this one
+    if (!t) rc = make_uint2(0u, 1u);
+    const uint32_t incl = off + t;
+    const float inv_w = 1.0f / (float)rc.y;
+    const uint32_t end = min(b, __shfl_sync(0xffffffffu, incl, 31));
+    // item kk -> (owning lane g of the window, tile, Gaussian)
+    auto locate = [&](uint32_t kk, int& g, uint32_t& tile, uint32_t& g_id) {
+      int l = 0, h = 31;  // smallest lane g with incl_g > kk
+#pragma unroll
+      for (int it = 0; it < 5; ++it) {
+        const int mid = (l + h) >> 1;
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, mid);
+        if (v > kk) h = mid; else l = mid + 1;
+      }
+      g = l;
+      const uint32_t g_off = __shfl_sync(0xffffffffu, off, g);
+      const uint32_t g_xy = __shfl_sync(0xffffffffu, rc.x, g);
+      const uint32_t g_w = __shfl_sync(0xffffffffu, rc.y, g);
+      const float g_iw = __shfl_sync(0xffffffffu, inv_w, g);
+      g_id = __shfl_sync(0xffffffffu, gid, g);
+      const uint32_t local = kk - g_off;
+      // exact row split: see k_emit_ranked
+      const uint32_t rowi = (uint32_t)(((float)local + 0.5f) * g_iw);
+      tile = ((g_xy >> 16) + rowi) * (uint32_t)tiles_x + (g_xy & 0xffffu) + (local - rowi * g_w);
+    };
+    // commit one 32-item batch in order
+    auto commit = [&](bool valid, int g, uint32_t tile, uint32_t g_id) {
+      // fast path: the batch's items are in distinct tiles
+      if (valid) scratch[tile] = (uint8_t)lane;
+      __syncwarp();
+      const bool clash = valid && scratch[tile] != (uint8_t)lane;
+      if (!__any_sync(0xffffffffu, clash)) {
+        if (valid) {
+          const uint32_t p = nxt[tile];
+          nxt[tile] = p + 1u;
+          vals[p] = g_id;
+        }
+      } else {
+        // a Gaussian's items have distinct tiles, so the batch takes its positions one
+        // Gaussian at a time, in depth order (lanes of a Gaussian are contiguous)
+        uint32_t pending = __ballot_sync(0xffffffffu, valid);
+        while (pending) {
+          const int gcur = __shfl_sync(0xffffffffu, g, __ffs(pending) - 1);
+          const bool mine = valid && g == gcur;
+          pending &= ~__ballot_sync(0xffffffffu, mine);
+          if (mine) {
+            const uint32_t p = nxt[tile];
+            nxt[tile] = p + 1u;
+            vals[p] = g_id;
+          }
+          __syncwarp();
+        }
+      }
+      __syncwarp();
+    };
+    // two batches per round: their lookups are independent (ILP), commits stay in order
+    for (uint32_t kb = pos; kb < end; kb += 64) {
+      const uint32_t k0 = kb + lane, k1 = kb + 32 + lane;
+      const bool v0 = k0 < end, v1 = k1 < end;
+      int g0, g1;
+      uint32_t t0, t1, id0, id1;
+      locate(v0 ? k0 : end - 1, g0, t0, id0);
+      locate(v1 ? k1 : end - 1, g1, t1, id1);
+      commit(v0, g0, t0, id0);
+      if (__any_sync(0xffffffffu, v1)) commit(v1, g1, t1, id1);
+    }
+    pos = end;
+    rb += 32;
+    t = t_n;
+    off = off_n;
+    gid = gid_n;
+    rc = rc_n;
+  }
+}
+
 // ---------------------------------------------------------------- K11: tile counts -> ranges
 constexpr int kOrderThreads = 1024;
 
@@ -318,8 +583,10 @@ __global__ void __launch_bounds__(kOrderThreads) k_tile_scan(const uint32_t* __r
     hist[4 * kRadixBins + k] = (&s_h[0][0])[k];
 }
 
-static bgs_status memset_status(Frame* F, cudaStream_t s) {
-  if (cudaMemsetAsync(F->sort_status, 0, 4 * kRadixBins * (size_t)F->sort_tiles_max, s) != cudaSuccess)
+// look-back status words of a pass over at most `count` keys
+static bgs_status memset_status(Frame* F, cudaStream_t s, int64_t count = -1) {
+  const int64_t tiles = count < 0 ? F->sort_tiles_max : (count + 4095) / 4096;
+  if (cudaMemsetAsync(F->sort_status, 0, 4 * kRadixBins * (size_t)tiles, s) != cudaSuccess)
     return check_launch("sort status memset");
   return BGS_OK;
 }
@@ -362,7 +629,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
   note_launch();
   if ((st = check_launch("k_depth_keys")) != BGS_OK) return st;
   for (int p = 0; p < 4; ++p) {
-    if ((st = memset_status(F, s)) != BGS_OK) return st;
+    if ((st = memset_status(F, s, F->n)) != BGS_OK) return st;
     const int a = p & 1, b = (p + 1) & 1;
     st = launch_sort_pass32(F->dkey[a], F->dval[a], F->dkey[b], F->dval[b], F->sort_hist + p * kRadixBins,
                             F->sort_status, F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, F->n, s);
@@ -374,6 +641,36 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
   note_launch();
   if ((st = check_launch("k_rank_info")) != BGS_OK) return st;
   if ((st = launch_scan(F->rank_cnt, F->item_off, F->n, F, false, s)) != BGS_OK) return st;
+  if (F->chunk_cnt && !(F->debug_flags & BGS_DEBUG_SORT_RADIX_SPLIT)) {
+    // (3') direct tile split: per-(chunk, tile) counts, column scan, ranges, emission
+    F->final_buf = 0;
+    const int gw = F->tiles_x + 1, cells = gw * (F->tiles_y + 1), nt = F->num_tiles;
+    const int64_t max_chunks = (F->max_keys + kChunkItems - 1) / kChunkItems;
+    const int blocks = (int)((max_chunks + kChunkWarps - 1) / kChunkWarps);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_chunk_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_emit_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    k_chunk_hist<<<blocks, kChunkWarps * 32, (size_t)kChunkWarps * cells * 4, s>>>(
+        F->n, F->item_off, F->rank_cnt, F->rank_rect, F->tiles_x, F->tiles_y, F->counters, F->chunk_cnt);
+    note_launch();
+    if ((st = check_launch("k_chunk_hist")) != BGS_OK) return st;
+    k_chunk_scan<<<(nt + 31) / 32, 1024, 0, s>>>(F->chunk_cnt, nt, F->counters, F->tile_count);
+    note_launch();
+    if ((st = check_launch("k_chunk_scan")) != BGS_OK) return st;
+    k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, nt, F->counters, F->ranges, F->sort_hist, 4);
+    note_launch();
+    if ((st = check_launch("k_tile_scan")) != BGS_OK) return st;
+    const int nt_pad = (nt + 3) & ~3;
+    k_emit_direct<<<(int)((max_chunks + kEmitWarps - 1) / kEmitWarps), kEmitWarps * 32,
+                    (size_t)kEmitWarps * 5 * nt_pad, s>>>(
+        F->n, F->item_off, F->dval[0], F->rank_cnt, F->rank_rect, F->tiles_x, nt, F->counters, F->chunk_cnt,
+        F->ranges, F->vals[0]);
+    note_launch();
+    return check_launch("k_emit_direct");
+  }
   // (3) (tile, Gaussian) items in depth order + per-tile counts
   uint32_t* tkey[2] = {reinterpret_cast<uint32_t*>(F->keys[0]), reinterpret_cast<uint32_t*>(F->keys[1])};
   k_emit_ranked<<<grid, kDupThreads, 0, s>>>(F->n, F->item_off, F->dval[0], F->rank_cnt, F->rank_rect, F->tiles_x,

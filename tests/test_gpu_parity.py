@@ -140,11 +140,12 @@ def test_unsorted_keys_parity(bgs, name):
 
 
 @pytest.mark.parametrize("name", list(scenes()))
-@pytest.mark.parametrize("path", ["depth_first", "onesweep64"])
+@pytest.mark.parametrize("path", ["depth_first", "radix_split", "onesweep64"])
 def test_sort_and_ranges_parity(bgs, name, path):
     s = scenes()[name]()
     cam = s.cameras[0]
-    flags = bgs.BGS_DEBUG_SORT_ONESWEEP64 if path == "onesweep64" else 0
+    flags = {"depth_first": 0, "radix_split": bgs.BGS_DEBUG_SORT_RADIX_SPLIT,
+             "onesweep64": bgs.BGS_DEBUG_SORT_ONESWEEP64}[path]
     r, _, _ = run_gpu(bgs, s, cam, flags=flags)
     ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
     K = ref["srt"]["K"]
@@ -157,12 +158,13 @@ def test_sort_and_ranges_parity(bgs, name, path):
 
 
 def test_sort_paths_identical_at_garden_scale(bgs):
-    """The depth-first path and the 64-bit onesweep reference give bit-identical tile lists
+    """The depth-first paths (direct and radix tile split) and the 64-bit onesweep reference
+    give bit-identical tile lists
     on a full-size garden view (K ~ 4.8e7), where exact depth ties do occur."""
     s = gen.garden()
     cam = s.cameras[8]
     outs = []
-    for flags in (0, bgs.BGS_DEBUG_SORT_ONESWEEP64):
+    for flags in (0, bgs.BGS_DEBUG_SORT_ONESWEEP64, bgs.BGS_DEBUG_SORT_RADIX_SPLIT):
         r, _, out = run_gpu(bgs, s, cam, max_keys=1 << 26, flags=flags)
         K = r.num_keys
         v = r.views()
@@ -171,10 +173,11 @@ def test_sort_paths_identical_at_garden_scale(bgs):
                      torch.as_tensor(_DevPtr(v.ranges, 2 * nt, "<i4"), device="cuda").clone(),
                      out["image"].clone(), out["n_contrib"].clone()))
         del r
-    (K0, v0, r0, i0, n0), (K1, v1, r1, i1, n1) = outs
-    assert K0 == K1 and K0 > 10_000_000
-    assert torch.equal(v0, v1) and torch.equal(r0, r1)
-    assert torch.equal(i0, i1) and torch.equal(n0, n1)
+    (K0, v0, r0, i0, n0) = outs[0]
+    for (K1, v1, r1, i1, n1) in outs[1:]:
+        assert K0 == K1 and K0 > 10_000_000
+        assert torch.equal(v0, v1) and torch.equal(r0, r1)
+        assert torch.equal(i0, i1) and torch.equal(n0, n1)
 
 
 @pytest.mark.parametrize("name", list(scenes()))
