@@ -64,6 +64,7 @@ struct Frame {
   float* depth;
   float4* record;          // [n][3]
   uint32_t* tiles_touched;
+  uint2* rect;             // [n] packed tile rect of visible Gaussians
   uint32_t* offsets;
   uint64_t* keys[2];
   uint32_t* vals[2];

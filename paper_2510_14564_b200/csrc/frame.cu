@@ -41,7 +41,7 @@ int num_sms() {
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
-  size_t radius, depth, record, tiles_touched, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
+  size_t radius, depth, record, tiles_touched, rect, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
       sort_status, counters, grad2d, tile_count, order_fwd, order_bwd, block_cost, ck_table, ck_pool, spec_base, spec_n,
       arrive, spec_state, spec_last, chunk_cnt, dkey0, dkey1,
       dval0, dval1, rank_cnt, item_off, rank_rect, cbits, total;
@@ -80,6 +80,7 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.depth = take(4 * N);
   L.record = take(48 * N);
   L.tiles_touched = take(4 * N);
+  L.rect = take(8 * N);
   L.offsets = take(4 * N);
   L.keys0 = take(8 * K);
   L.keys1 = take(8 * K);
@@ -223,6 +224,7 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->depth = (float*)(base + L.depth);
   F->record = (float4*)(base + L.record);
   F->tiles_touched = (uint32_t*)(base + L.tiles_touched);
+  F->rect = (uint2*)(base + L.rect);
   F->offsets = (uint32_t*)(base + L.offsets);
   F->keys[0] = (uint64_t*)(base + L.keys0);
   F->keys[1] = (uint64_t*)(base + L.keys1);

@@ -38,6 +38,7 @@ struct PreParams {
   float* depth;
   float4* record;
   uint32_t* tiles_touched;
+  uint2* rect;              // {x0 | y0 << 16, w | h << 16} of visible Gaussians (depth-first sort)
   float4* grad2d;
   uint8_t* cbits;
 };
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
   p.radius[i] = rad;
   p.depth[i] = t2;
   p.tiles_touched[i] = area;
+  p.rect[i] = make_uint2((uint32_t)rx0 | ((uint32_t)ry0 << 16), (uint32_t)(rx1 - rx0) | ((uint32_t)(ry1 - ry0) << 16));
   float4* rec = p.record + 3 * i;
   rec[1] = make_float4(-0.5f * conx, -cony, -0.5f * conz, o);
   // Conservative half-extents of the alpha >= 1/255 level set, d^T conic d <= 2 ln(255 o)
@@ -299,9 +301,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
       counters[C_K_LO] = (uint32_t)K;
       counters[C_K_HI] = (uint32_t)(K >> 32);
       counters[C_OVERFLOW] = K > (unsigned long long)max_keys ? 1u : 0u;
-    } else {
-      counters[C_SCAN_TOTAL] = (uint32_t)K;
     }
+    counters[C_SCAN_TOTAL] = (uint32_t)K;
   }
 }
 
@@ -335,14 +336,15 @@ bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
   p.depth = F->depth;
   p.record = F->record;
   p.tiles_touched = F->tiles_touched;
+  p.rect = F->rect;
   p.grad2d = F->grad2d;
   p.cbits = F->cbits;
   const int64_t blocks = (F->n + 255) / 256;
   k_preprocess<<<(unsigned)blocks, 256, 0, s>>>(p);
   note_launch();
-  bgs_status st = check_launch("k_preprocess");
-  if (st != BGS_OK) return st;
-  return launch_scan(F->tiles_touched, F->offsets, F->n, F, true, s);
+  // the key count K (and the capacity check) comes from the sort's scan: of tiles_touched
+  // in index order (64-bit reference path), or of the tile counts in depth order
+  return check_launch("k_preprocess");
 }
 
 }  // namespace bgs

@@ -162,25 +162,18 @@ __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const float* __re
 // independent (full memory-level parallelism), packed as {x0 | y0 << 16, w | h << 16} so
 // the emission reads contiguous data instead of dependent random gathers
 __global__ void __launch_bounds__(256) k_rank_info(int64_t n, const uint32_t* __restrict__ sigma,
-                                                   const uint32_t* __restrict__ tiles_touched,
-                                                   const float4* __restrict__ record,
-                                                   const int32_t* __restrict__ radius, int32_t tiles_x,
-                                                   int32_t tiles_y, const uint32_t* counters, uint32_t* rank_cnt,
-                                                   uint2* rank_rect) {
+                                                   const uint32_t* __restrict__ dkey_sorted,
+                                                   const uint2* __restrict__ rect, const uint32_t* counters,
+                                                   uint32_t* rank_cnt, uint2* rank_rect) {
   if (counters[C_OVERFLOW]) return;
-  const float ftx = (float)tiles_x, fty = (float)tiles_y;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t g = sigma[r];
-    const uint32_t t = tiles_touched[g];
+    uint32_t t = 0;
     uint2 packed = make_uint2(0u, 0u);
-    if (t) {
-      const float4 r0 = record[3 * g];
-      const int rad = radius[g];
-      // the preprocess's canonical rect expression (R11)
-      const int rx0 = (int)fminf(ftx, fmaxf(0.0f, floorf((r0.x - (float)rad) * 0.0625f)));
-      const int ry0 = (int)fminf(fty, fmaxf(0.0f, floorf((r0.y - (float)rad) * 0.0625f)));
-      const int rx1 = (int)fminf(ftx, fmaxf(0.0f, floorf((r0.x + (float)(rad + 15)) * 0.0625f)));
-      packed = make_uint2((uint32_t)rx0 | ((uint32_t)ry0 << 16), (uint32_t)(rx1 - rx0));
+    if (dkey_sorted[r] != 0xffffffffu) {  // visible: the preprocess's rect (R11)
+      const uint2 q = rect[sigma[r]];
+      const uint32_t w = q.y & 0xffffu;
+      t = w * (q.y >> 16);
+      packed = make_uint2(q.x, w);
     }
     rank_cnt[r] = t;
     rank_rect[r] = packed;
@@ -606,6 +599,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
   const int grid = 4 * num_sms();
   bgs_status st;
   if (ref64) {
+    if ((st = launch_scan(F->tiles_touched, F->offsets, F->n, F, true, s)) != BGS_OK) return st;  // a3, K
     k_emit<false><<<grid, kDupThreads, 0, s>>>(F->n, F->record, F->radius, F->depth, F->offsets, nullptr,
                                                F->tiles_touched, F->tiles_x, F->tiles_y, F->num_tiles, F->counters,
                                                F->keys[0], F->vals[0], F->tile_count, F->sort_hist);
@@ -636,11 +630,11 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
     if (st != BGS_OK) return st;
   }
   // (2) per-rank tile counts and rects, item offsets in depth order
-  k_rank_info<<<grid, 256, 0, s>>>(F->n, F->dval[0], F->tiles_touched, F->record, F->radius, F->tiles_x, F->tiles_y,
-                                   F->counters, F->rank_cnt, F->rank_rect);
+  k_rank_info<<<grid, 256, 0, s>>>(F->n, F->dval[0], F->dkey[0], F->rect, F->counters, F->rank_cnt, F->rank_rect);
   note_launch();
   if ((st = check_launch("k_rank_info")) != BGS_OK) return st;
-  if ((st = launch_scan(F->rank_cnt, F->item_off, F->n, F, false, s)) != BGS_OK) return st;
+  // K (published with the capacity check) = the total of the depth-order scan
+  if ((st = launch_scan(F->rank_cnt, F->item_off, F->n, F, true, s)) != BGS_OK) return st;
   if (F->chunk_cnt && !(F->debug_flags & BGS_DEBUG_SORT_RADIX_SPLIT)) {
     // (3') direct tile split: per-(chunk, tile) counts, column scan, ranges, emission
     F->final_buf = 0;

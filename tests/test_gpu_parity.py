@@ -62,6 +62,10 @@ def run_gpu(bgs, s, cam, max_keys=1 << 21, skip_sort=False, flags=0, seg_len=Non
     return r, theta, out
 
 
+def ref_K(s, cam):
+    return oracle.forward(s.theta, s.n, s.sh_degree, cam)["srt"]["K"]
+
+
 class _DevPtr:
     """Zero-copy view of a workspace region through __cuda_array_interface__."""
 
@@ -95,7 +99,11 @@ def views(bgs, r, n, K, ntiles):
 def test_preprocess_parity(bgs, name):
     s = scenes()[name]()
     cam = s.cameras[0]
-    r, _, out = run_gpu(bgs, s, cam)
+    # the index-order scan (a3 offsets) runs on the 64-bit reference path; the depth-first
+    # path scans the tile counts in depth order instead (K checked on both)
+    r0, _, _ = run_gpu(bgs, s, cam)
+    assert r0.num_keys == ref_K(s, cam)
+    r, _, out = run_gpu(bgs, s, cam, flags=bgs.BGS_DEBUG_SORT_ONESWEEP64)
     ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
     pre = ref["pre"]
     K = ref["srt"]["K"]
