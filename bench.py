@@ -45,7 +45,11 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="garden")
     p.add_argument("--views", type=int, default=16)
-    p.add_argument("--n", type=int, default=None, help="override the Gaussian count (debug only)")
+    p.add_argument("--num-gaussians", dest="n", type=int, default=None,
+                   help="override the Gaussian count (debug only)")
+    p.add_argument("--update", default="sharded", choices=["sharded", "allreduce"],
+                   help="G > 1: reduce-scatter + Adam on a 1/G shard + all-gather (default), or all-reduce + "
+                        "full Adam on every rank")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--one-frame", action="store_true",
@@ -69,7 +73,7 @@ def arm_config(scene, args, world):
     cam = scene.cameras[0]
     return {"workload": f"{scene.name}-shaped {scene.n} Gaussians, {cam.width}x{cam.height}, SH degree "
                         f"{scene.sh_degree}, batch of {args.views} views per step (fwd+bwd each, then "
-                        f"all-reduce + Adam)",
+                        f"{'reduce-scatter + sharded Adam + all-gather' if world > 1 and args.update == 'sharded' else 'all-reduce + Adam'})",
             "views_per_step": args.views, "n_gaussians": scene.n, "width": cam.width, "height": cam.height,
             "parallelism": f"view-dp{world}", "l2": "inputs larger than L2 (theta 1.37 GB, keys > 126 MB)"}
 
@@ -161,11 +165,22 @@ def run_ours(args, rank, world, local_rank):
     mine = dp.views_for_rank(views, rank, world)
     cams = [cams_all[v] for v in mine]
     W, H = cams[0].width, cams[0].height
-    theta = torch.from_numpy(scene.theta).to(dev)
+    sharded = world > 1 and args.update == "sharded"
+    total = 59 * n
+    if sharded:
+        # reduce-scatter -> Adam on this rank's 1/G shard -> all-gather: theta
+        # and grad padded to G equal 16-byte-aligned shards; Adam moments for the shard only
+        shard, padded = dp.shard_layout(total, world)
+        sh_lo, sh_hi = dp.shard_range(rank, world, total)
+        theta = torch.zeros(padded, dtype=torch.float32, device=dev)
+        theta[:total].copy_(torch.from_numpy(scene.theta))
+        m = torch.zeros(shard, dtype=torch.float32, device=dev)
+    else:
+        theta = torch.from_numpy(scene.theta).to(dev)
+        m = torch.zeros_like(theta)
     dp.broadcast_params(theta, world)  # replicas start identical
     grad = torch.zeros_like(theta)
-    m = torch.zeros_like(theta)
-    v = torch.zeros_like(theta)
+    v = torch.zeros_like(m)
     hp = bgs.AdamHParams(lr_means=1.6e-4 * scene.extent)
     deg = scene.sh_degree
 
@@ -201,12 +216,13 @@ def run_ours(args, rank, world, local_rank):
     loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
     scale = 1.0 / (3.0 * W * H * args.views)
     gs = bgs.gaussians(theta, n, deg)
+    frames = [rj.frame for rj in rends]
     cam_structs = [bgs.camera(c) for c in cams]
     stream = torch.cuda.current_stream()
     stage_names = ["preprocess", "sort", "render_fwd", "loss", "blend_bwd", "preprocess_bwd", "allreduce", "adam"]
     # all timing events of the timed region are created up front (creating them inside the
     # loop adds host work between launches)
-    n_marks = args.steps * (7 * len(cam_structs) + 3)
+    n_marks = args.steps * (7 * len(cam_structs) + 5)
     pool = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
     step_no = [0]
 
@@ -234,15 +250,28 @@ def run_ours(args, rank, world, local_rank):
             mark(marks)
             bgs.bgs_blend_bwd(rj.frame, dl, rj.final_T, rj.n_contrib)
             mark(marks)
-            bgs.bgs_preprocess_bwd(gs, rj.frame, grad)
+            if args.one_frame:  # the frame is reused by the next view: chain rule now
+                bgs.bgs_preprocess_bwd(gs, rj.frame, grad)
             mark(marks)
             if record is not None:
                 record["marks"].append(("view", marks))
         marks = []
         mark(marks)
-        dp.allreduce_grads(grad, world)  # NCCL over NVLink (one exchange per batch)
+        if not args.one_frame:  # a10 once over the batch's views: theta/grad cross HBM once
+            bgs.bgs_preprocess_bwd_batch(gs, frames, grad)
         mark(marks)
-        bgs.bgs_adam_step(theta, grad, m, v, n, hp, step_no[0])
+        if sharded:  # NCCL over NVLink: reduce-scatter, Adam on the shard, all-gather
+            g_shard = dp.reduce_scatter_grads(grad, rank, world)
+            mark(marks)
+            bgs.bgs_adam_step_range(theta[sh_lo:sh_hi], g_shard, m, v, n, sh_lo, sh_hi - sh_lo, hp, step_no[0])
+            bgs.bgs_zero(grad)  # the rest of grad still holds this rank's partial sums
+            mark(marks)
+            dp.all_gather_params(theta, rank, world)
+        else:
+            dp.allreduce_grads(grad, world)  # NCCL over NVLink (one exchange per batch)
+            mark(marks)
+            bgs.bgs_adam_step(theta, grad, m, v, n, hp, step_no[0])
+            mark(marks)
         mark(marks)
         if record is not None:
             record["marks"].append(("batch", marks))
@@ -268,10 +297,12 @@ def run_ours(args, rank, world, local_rank):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(_device_index(local_rank)) as clk:
+        torch.cuda.nvtx.range_push("bench_timed")  # ncu --nvtx --nvtx-include "bench_timed/"
         t0.record(stream)
         for _ in range(args.steps):
             one_step(targets, None if args.no_stage_events else record)
         t1.record(stream)
+        torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
     barrier()
     launches = bgs.launch_count() - launches0
@@ -286,10 +317,11 @@ def run_ours(args, rank, world, local_rank):
             for s, a, b in zip(stage_names[:6], mk[:-1], mk[1:]):
                 sums[s] += a.elapsed_time(b)
         else:
-            sums["allreduce"] += mk[0].elapsed_time(mk[1])
-            sums["adam"] += mk[1].elapsed_time(mk[2])
+            sums["preprocess_bwd"] += mk[0].elapsed_time(mk[1])
+            sums["allreduce"] += mk[1].elapsed_time(mk[2]) + mk[3].elapsed_time(mk[4])
+            sums["adam"] += mk[2].elapsed_time(mk[3])
     per_step = {s: sums[s] / args.steps for s in stage_names}
-    launches_per_stage = {"render_fwd": 1, "blend_bwd": 1, "preprocess_bwd": 1, "adam": 1}
+
 
     # ---- end-to-end through the public API with host buffers
     e2e = None
@@ -389,8 +421,15 @@ def run_ours(args, rank, world, local_rank):
     frac("render_fwd", (OPS_FWD_VISIT * Efc + OPS_FWD_BLEND * Ebl) / per_launch("render_fwd") / 1e12, fp32_peak,
          "T lane-ops/s", "alu")
     frac("blend_bwd", OPS_BWD_EVAL * Ebc / per_launch("blend_bwd") / 1e12, fp32_peak, "T lane-ops/s", "alu")
-    frac("preprocess_bwd", 744 * V / per_launch("preprocess_bwd") / 1e9, hbm, "GB/s", "hbm")
-    roof["adam"] = {"bound": "hbm", "achieved": 1888 * n / max(per_step["adam"] / 1e3, 1e-12) / 1e9, "peak": hbm,
+    if args.one_frame:  # per view: theta 236 + blend grads 36 + grad RMW 472 per visible Gaussian
+        frac("preprocess_bwd", 744 * V / per_launch("preprocess_bwd") / 1e9, hbm, "GB/s", "hbm")
+    else:  # batched over the rank's views: theta 236 + grad RMW 472 per Gaussian once, + per
+        # (view, visible Gaussian) the blend gradients 36 + radius 4 + clamp bits 1; radius 4 per (view, culled)
+        pb_bytes = 708 * n + (37 * V + 4 * n) * steps_views
+        frac("preprocess_bwd", pb_bytes / max(per_step["preprocess_bwd"] / 1e3, 1e-12) / 1e9, hbm, "GB/s", "hbm")
+        roof["preprocess_bwd"]["ms_per_launch"] = per_step["preprocess_bwd"] / -(-steps_views // 16)
+    adam_bytes = 1888 * n / (world if sharded else 1) + (236 * n if sharded else 0)  # + zeroing grad
+    roof["adam"] = {"bound": "hbm", "achieved": adam_bytes / max(per_step["adam"] / 1e3, 1e-12) / 1e9, "peak": hbm,
                     "unit": "GB/s", "ms_per_launch": per_step["adam"]}
     roof["adam"]["frac"] = roof["adam"]["achieved"] / hbm
     # the dominant KERNEL: stages that are one kernel launch (the sort stage is 13 kernels;

@@ -172,11 +172,33 @@ bgs_status bgs_render_bwd(const bgs_gaussians* g /*host*/, bgs_frame* f /*host*/
 bgs_status bgs_blend_bwd(bgs_frame* f /*host*/, const float* dL_dimage, const float* final_T,
                          const uint32_t* n_contrib, void* stream);
 bgs_status bgs_preprocess_bwd(const bgs_gaussians* g /*host*/, bgs_frame* f /*host*/, float* grad, void* stream);
+/* a10 over a batch of views (R20: grad += the sum over views): frames[nframes] (host array
+ * of host frame pointers, 1 <= nframes <= 4096, all of the same n, each after its own
+ * bgs_preprocess + bgs_blend_bwd for this theta) -> grad[59n] +=.  Equal to calling
+ * bgs_preprocess_bwd on each frame up to float summation order, but theta is read and grad
+ * read-modified-written once per 16 views instead of once per view. */
+bgs_status bgs_preprocess_bwd_batch(const bgs_gaussians* g /*host*/, bgs_frame* const* frames /*host*/,
+                                    int32_t nframes, float* grad, void* stream);
 
 /* a11: fused Adam over theta[59n] (R21, PyTorch semantics: bias-corrected, eps after
  * sqrt), per-group learning rate, grad zeroed on exit.  step is 1-based. */
 bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
                          const bgs_adam_hparams* hp /*host*/, int64_t step, void* stream);
+
+/* a11 on a shard (reduce-scatter -> Adam on 1/G of theta -> all-gather):
+ * the same update as bgs_adam_step restricted to theta elements [begin, begin + count) of the
+ * 59n layout.  The four device pointers address element `begin` (shard buffers, or offsets
+ * into the full buffers); the learning-rate group of element i is that of begin + i.
+ * Elements at or past 59n (the caller's shard padding) are not touched.  begin must be a
+ * multiple of 4 and the pointers 16-byte aligned, else BGS_ERR_INVALID (nothing launched). */
+bgs_status bgs_adam_step_range(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
+                               int64_t begin, int64_t count, const bgs_adam_hparams* hp /*host*/, int64_t step,
+                               void* stream);
+
+/* Zero `count` floats at device pointer p (cudaMemsetAsync on `stream`): resets a gradient
+ * buffer whose shard bgs_adam_step_range consumed after a reduce-scatter (the rest of the
+ * buffer still holds this rank's partial sums).  BGS_ERR_INVALID on p = NULL with count > 0. */
+bgs_status bgs_zero(float* p, int64_t count, void* stream);
 
 /* a8 (caller-side helper): L1 loss gradient against an 8-bit target [3][h][w]
  * (R19): dL_dimage = scale * sign(image - target/255); loss_sum += sum |image - target/255|

@@ -86,7 +86,11 @@ _SIGS = {
     "bgs_render_bwd": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Frame), _P, _P, _P, _P, _P]),
     "bgs_blend_bwd": (C.c_int, [C.POINTER(Frame), _P, _P, _P, _P]),
     "bgs_preprocess_bwd": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Frame), _P, _P]),
+    "bgs_preprocess_bwd_batch": (C.c_int, [C.POINTER(Gaussians), C.POINTER(C.POINTER(Frame)), C.c_int32, _P, _P]),
     "bgs_adam_step": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(AdamHParams), C.c_int64, _P]),
+    "bgs_adam_step_range": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.POINTER(AdamHParams),
+                                      C.c_int64, _P]),
+    "bgs_zero": (C.c_int, [_P, C.c_int64, _P]),
     "bgs_l1_loss_grad": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_float, _P, _P, _P]),
     "bgs_frame_status": (C.c_int, [C.POINTER(Frame), C.POINTER(C.c_int64)]),
     "bgs_frame_debug": (C.c_int, [C.POINTER(Frame), C.POINTER(FrameViews)]),
@@ -183,9 +187,26 @@ def bgs_preprocess_bwd(g: Gaussians, frame: Frame, grad, stream=None):
     _check(_lib.bgs_preprocess_bwd(C.byref(g), C.byref(frame), _ptr(grad), _stream(stream)), "bgs_preprocess_bwd")
 
 
+def bgs_preprocess_bwd_batch(g: Gaussians, frames, grad, stream=None):
+    """frames: a sequence of Frame structs (one per view of the batch)."""
+    arr = (C.POINTER(Frame) * len(frames))(*[C.pointer(f) for f in frames])
+    _check(_lib.bgs_preprocess_bwd_batch(C.byref(g), arr, len(frames), _ptr(grad), _stream(stream)),
+           "bgs_preprocess_bwd_batch")
+
+
 def bgs_adam_step(theta, grad, exp_avg, exp_avg_sq, n, hp: AdamHParams, step: int, stream=None):
     _check(_lib.bgs_adam_step(_ptr(theta), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), n, C.byref(hp), step,
                               _stream(stream)), "bgs_adam_step")
+
+
+def bgs_adam_step_range(theta, grad, exp_avg, exp_avg_sq, n, begin, count, hp: AdamHParams, step: int,
+                        stream=None):
+    _check(_lib.bgs_adam_step_range(_ptr(theta), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), n, begin, count,
+                                    C.byref(hp), step, _stream(stream)), "bgs_adam_step_range")
+
+
+def bgs_zero(t, stream=None):
+    _check(_lib.bgs_zero(_ptr(t), t.numel(), _stream(stream)), "bgs_zero")
 
 
 def bgs_l1_loss_grad(image, target_u8, w, h, scale, dl_dimage, loss_sum, stream=None):

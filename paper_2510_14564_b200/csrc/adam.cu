@@ -17,7 +17,7 @@ struct AdamParams {
   float4* grad;
   float4* m;
   float4* v;
-  int64_t n, total4;
+  int64_t n, base, total4;  // element i of the pointers is theta element base + i
   float lr[6];
   float b1, b2, eps;
   float step_size[6];  // lr / bc1
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(256) k_adam(AdamParams p) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.total4; i += stride) {
     float4 th = p.theta[i], g = p.grad[i], m = p.m[i], v = p.v[i];
-    const int64_t e = 4 * i;
+    const int64_t e = p.base + 4 * i;
     const int g0 = adam_group(e, p.n), g3 = adam_group(e + 3, p.n);
     if (g0 == g3 && g0 < 4) {
       const float ss = p.step_size[g0];
@@ -67,23 +67,29 @@ __global__ void __launch_bounds__(256) k_adam(AdamParams p) {
   }
 }
 
-// The scalar tail: the last 59n mod 4 elements.
+// The scalar tail: local elements [start, end) (the last count mod 4).
 __global__ void k_adam_tail(float* theta, float* grad, float* m, float* v, int64_t n, int64_t start, int64_t end,
                             AdamParams p) {
-  const int64_t e = start + threadIdx.x;
-  if (e >= end) return;
-  adam_one(theta[e], grad[e], m[e], v[e], p.step_size[adam_group(e, n)], p);
+  const int64_t i = start + threadIdx.x;
+  if (i >= end) return;
+  adam_one(theta[i], grad[i], m[i], v[i], p.step_size[adam_group(p.base + i, n)], p);
 }
 
-bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, const bgs_adam_hparams* hp,
-                       int64_t step, cudaStream_t s) {
+// Adam over theta elements [begin, begin + count) of the 59n layout; the pointers address
+// element `begin` (a shard of a reduce-scattered update, or begin = 0 for all of theta).
+// Elements at or past 59n (shard padding) are left untouched.
+bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, int64_t begin, int64_t count,
+                       const bgs_adam_hparams* hp, int64_t step, cudaStream_t s) {
+  const int64_t total = std::max<int64_t>(0, std::min<int64_t>(count, 59 * n - begin));
+  if (total == 0) return BGS_OK;
   AdamParams p;
   p.theta = (float4*)theta;
   p.grad = (float4*)grad;
   p.m = (float4*)m;
   p.v = (float4*)v;
   p.n = n;
-  p.total4 = 59 * n / 4;  // 59n is a multiple of 4 only if n is; the tail is handled below
+  p.base = begin;
+  p.total4 = total / 4;  // the tail (total mod 4) is handled below
   const float lr[6] = {hp->lr_means, hp->lr_log_scales, hp->lr_quats, hp->lr_opacity, hp->lr_sh_dc, hp->lr_sh_rest};
   const double bc1 = 1.0 - pow((double)hp->beta1, (double)step);
   const double bc2 = 1.0 - pow((double)hp->beta2, (double)step);
@@ -101,9 +107,9 @@ bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n,
   note_launch();
   bgs_status st = check_launch("k_adam");
   if (st != BGS_OK) return st;
-  const int64_t tail = 59 * n - 4 * p.total4;
+  const int64_t tail = total - 4 * p.total4;
   if (tail > 0) {
-    k_adam_tail<<<1, 4, 0, s>>>(theta, grad, m, v, n, 4 * p.total4, 59 * n, p);
+    k_adam_tail<<<1, 4, 0, s>>>(theta, grad, m, v, n, 4 * p.total4, total, p);
     note_launch();
     return check_launch("k_adam_tail");
   }

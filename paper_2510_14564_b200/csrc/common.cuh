@@ -115,10 +115,13 @@ bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n
 bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
                             cudaStream_t s);
 bgs_status launch_preprocess_bwd(const bgs_gaussians* g, Frame* F, float* grad, cudaStream_t s);
+constexpr int kPreBwdMaxViews = 16;  // views per k_preprocess_bwd launch (kernel-parameter cameras)
+bgs_status launch_preprocess_bwd_batch(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
+                                       cudaStream_t s);
 bgs_status launch_render_bwd(const bgs_gaussians* g, Frame* F, const float* dL_dimage, const float* final_T,
                              const uint32_t* n_contrib, float* grad, cudaStream_t s);
-bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, const bgs_adam_hparams* hp,
-                       int64_t step, cudaStream_t s);
+bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, int64_t begin, int64_t count,
+                       const bgs_adam_hparams* hp, int64_t step, cudaStream_t s);
 bgs_status launch_l1(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale, float* dl,
                      float* loss_sum, cudaStream_t s);
 bgs_status launch_stats(const Frame* F, const uint32_t* n_contrib, bgs_stats* out, cudaStream_t s);

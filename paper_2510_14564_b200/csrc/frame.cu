@@ -309,6 +309,21 @@ bgs_status bgs_preprocess_bwd(const bgs_gaussians* g, bgs_frame* f, float* grad,
   return launch_preprocess_bwd(g, F, grad, (cudaStream_t)stream);
 }
 
+bgs_status bgs_preprocess_bwd_batch(const bgs_gaussians* g, bgs_frame* const* frames, int32_t nframes, float* grad,
+                                    void* stream) {
+  if (!frames || nframes < 1 || nframes > 4096) return BGS_ERR_INVALID;
+  static thread_local Frame* F[4096];
+  for (int v = 0; v < nframes; ++v) {
+    if (!frame_ok(frames[v]) || !frame_of(frames[v])->cam_valid) return BGS_ERR_INVALID;
+    F[v] = frame_of(frames[v]);
+    if (F[v]->n != F[0]->n) return BGS_ERR_INVALID;
+  }
+  bgs_status st = validate_gaussians(g, F[0]);
+  if (st != BGS_OK) return st;
+  if (F[0]->n > 0 && (!grad || ((uintptr_t)grad & 3u))) return BGS_ERR_INVALID;
+  return launch_preprocess_bwd_batch(g, F, nframes, grad, (cudaStream_t)stream);
+}
+
 bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
                          const bgs_adam_hparams* hp, int64_t step, void* stream) {
   if (n < 0 || !hp || step < 1) return BGS_ERR_INVALID;
@@ -317,7 +332,27 @@ bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_a
   if (!aligned16(theta) || !aligned16(grad) || !aligned16(exp_avg) || !aligned16(exp_avg_sq)) return BGS_ERR_INVALID;
   if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f && hp->beta2 >= 0.0f && hp->beta2 < 1.0f && hp->eps >= 0.0f))
     return BGS_ERR_INVALID;
-  return launch_adam(theta, grad, exp_avg, exp_avg_sq, n, hp, step, (cudaStream_t)stream);
+  return launch_adam(theta, grad, exp_avg, exp_avg_sq, n, 0, 59 * n, hp, step, (cudaStream_t)stream);
+}
+
+bgs_status bgs_adam_step_range(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
+                               int64_t begin, int64_t count, const bgs_adam_hparams* hp, int64_t step,
+                               void* stream) {
+  if (n < 0 || begin < 0 || count < 0 || (begin & 3) || !hp || step < 1) return BGS_ERR_INVALID;
+  if (n == 0 || count == 0 || begin >= 59 * n) return BGS_OK;
+  if (!theta || !grad || !exp_avg || !exp_avg_sq) return BGS_ERR_INVALID;
+  if (!aligned16(theta) || !aligned16(grad) || !aligned16(exp_avg) || !aligned16(exp_avg_sq)) return BGS_ERR_INVALID;
+  if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f && hp->beta2 >= 0.0f && hp->beta2 < 1.0f && hp->eps >= 0.0f))
+    return BGS_ERR_INVALID;
+  return launch_adam(theta, grad, exp_avg, exp_avg_sq, n, begin, count, hp, step, (cudaStream_t)stream);
+}
+
+bgs_status bgs_zero(float* p, int64_t count, void* stream) {
+  if (count < 0 || (count > 0 && !p)) return BGS_ERR_INVALID;
+  if (count == 0) return BGS_OK;
+  if (cudaMemsetAsync(p, 0, (size_t)count * sizeof(float), (cudaStream_t)stream) != cudaSuccess)
+    return check_launch("bgs_zero");
+  return BGS_OK;
 }
 
 bgs_status bgs_l1_loss_grad(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale,

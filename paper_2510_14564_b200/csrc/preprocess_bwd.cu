@@ -12,33 +12,41 @@
 // ~1e-3 relative on the log_scales gradient; everything downstream of dL/dSigma' and the
 // SH part are FP32 (B200 runs FP64 at half the FP32 rate; this kernel is HBM-bound).
 //
-// Memory: one thread per Gaussian, 4 warps per CTA.  The 192-byte SH block and the
+// Batching (bgs_preprocess_bwd_batch): the theta-side work and the grad read-modify-write
+// are per Gaussian, the camera-side work per (Gaussian, view); one launch serves up to 16
+// views, so theta and grad cross HBM once per batch instead of once per view.
+//
+// Memory: one thread per Gaussian, 2 warps per CTA.  The 192-byte SH block and the
 // 192-byte SH-gradient block of a warp's 32 Gaussians are contiguous (6 KB each), so the
 // warp reads the SH coefficients and read-modify-writes the SH gradients as coalesced
-// float4 passes staged through shared memory (one padded 49-float row per Gaussian; the
-// SH terms overwrite the row in place with dL/dsh); the per-thread parts (means, scales,
+// float4 passes staged through shared memory (two padded 49-float rows per Gaussian: the
+// coefficients, and dL/dsh summed over the views); the per-thread parts (means, scales,
 // quats, opacity) are naturally coalesced.
 #include "common.cuh"
 
 namespace bgs {
 
-struct PreBwdParams {
+struct PreBwdView {
   Cam cam;
+  const int32_t* radius;
+  const uint8_t* cbits;
+  const float4* grad2d;
+};
+
+struct PreBwdParams {
   const float* means;
   const float* log_scales;
   const float* quats;
   const float* ologits;
   const float* sh;  // [n][16][3]
   int64_t n;
-  int32_t deg;
+  int32_t deg, nviews;
   bool quat_vec4, sh_vec4, gq_vec4, gsh_vec4;  // 16-byte aligned -> vector paths
-  const int32_t* radius;
-  const uint8_t* cbits;
-  const float4* grad2d;
   float* grad;  // theta layout
+  PreBwdView view[kPreBwdMaxViews];
 };
 
-constexpr int kBwdThreads = 128;
+constexpr int kBwdThreads = 64;
 constexpr int kRow = 49;  // padded row stride (floats) of the staged SH block: conflict-free
 
 // Real SH constants (R12).
@@ -49,18 +57,29 @@ constexpr float kC30 = -0.5900435899266435f, kC31 = 2.890611442640554f, kC32 = -
                 kC33 = 0.3731763325901154f, kC34 = -0.4570457994644658f, kC35 = 1.445305721320277f,
                 kC36 = -0.5900435899266435f;
 
-__global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(PreBwdParams p) {
-  __shared__ float s_sh[kBwdThreads / 32][32 * kRow];
+// One thread per Gaussian, looping over the batch's views (one launch per <= 16 views).
+// The view-independent parts -- Sigma = M M^T (FP64), the quaternion/scale chain, the
+// sigmoid, the theta loads and the grad read-modify-write -- are done once per Gaussian;
+// per view only the camera-dependent terms are evaluated, and dL/dSigma, dL/dmu,
+// dL/dopacity and dL/dsh are summed in registers / shared memory across the views.
+__global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_constant__ PreBwdParams p) {
+  __shared__ float s_sh[kBwdThreads / 32][32 * kRow];   // SH coefficients (read-only)
+  __shared__ float s_dsh[kBwdThreads / 32][32 * kRow];  // dL/dsh, summed over the views
   __shared__ int s_vis[kBwdThreads / 32][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = p.n;
   const int64_t wbase = ((int64_t)blockIdx.x * kBwdThreads) + warp * 32;
   const int64_t i = wbase + lane;
-  const bool valid = i < n && p.radius[i] > 0;
+  uint32_t vmask = 0;  // views in which Gaussian i is visible
+  if (i < n)
+    for (int v = 0; v < p.nviews; ++v) vmask |= (p.view[v].radius[i] > 0 ? 1u : 0u) << v;
+  const bool valid = vmask != 0;
   s_vis[warp][lane] = valid;
   float* row = &s_sh[warp][lane * kRow];
+  float* drow = &s_dsh[warp][lane * kRow];
   const int ncoef = (p.deg + 1) * (p.deg + 1);
   const int64_t nvalid = n - wbase < 32 ? n - wbase : 32;
+  for (int k = 0; k < 48; ++k) drow[k] = 0.f;
   __syncwarp();
   // ---- coalesced load of the warp's SH block into shared memory
   if (p.sh_vec4) {
@@ -82,74 +101,7 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(PreBwdParams 
   }
   __syncwarp();
   if (valid) {
-    const Cam& c = p.cam;
-    const float* V = c.V;
-    const float* P = c.P;
-    const float4 ga4 = p.grad2d[3 * i], gb4 = p.grad2d[3 * i + 1], gc4 = p.grad2d[3 * i + 2];
-    const float gx = ga4.x, gy = ga4.y, gop = gb4.y;
-    const uint32_t cb = p.cbits[i];
-    const float g_r = (cb & CB_R) ? 0.f : gb4.z, g_g = (cb & CB_G) ? 0.f : gb4.w, g_b = (cb & CB_B) ? 0.f : gc4.x;
     const float mx = p.means[3 * i], my = p.means[3 * i + 1], mz = p.means[3 * i + 2];
-    float dmx = 0.f, dmy = 0.f, dmz = 0.f;
-    // ---- colour: per SH term, read sh_k from the row, accumulate dL/dd, overwrite the
-    //      row slot with dL/dsh_k = Y_k * dL/drgb (masked by the frozen clamp, R12)
-    {
-      const float dxw = mx - c.campos[0], dyw = my - c.campos[1], dzw = mz - c.campos[2];
-      const float il = rsqrtf(dxw * dxw + dyw * dyw + dzw * dzw);
-      const float x = dxw * il, y = dyw * il, z = dzw * il;
-      const float xx = x * x, yy = y * y, zz = z * z;
-      float ddx = 0.f, ddy = 0.f, ddz = 0.f;
-      auto term = [&](int k, float Y, float dYx, float dYy, float dYz) {
-        const float shg = row[3 * k] * g_r + row[3 * k + 1] * g_g + row[3 * k + 2] * g_b;
-        ddx = fmaf(dYx, shg, ddx);
-        ddy = fmaf(dYy, shg, ddy);
-        ddz = fmaf(dYz, shg, ddz);
-        row[3 * k] = Y * g_r;
-        row[3 * k + 1] = Y * g_g;
-        row[3 * k + 2] = Y * g_b;
-      };
-      term(0, kC0, 0.f, 0.f, 0.f);
-      if (p.deg > 0) {
-        term(1, -kC1 * y, 0.f, -kC1, 0.f);
-        term(2, kC1 * z, 0.f, 0.f, kC1);
-        term(3, -kC1 * x, -kC1, 0.f, 0.f);
-        if (p.deg > 1) {
-          term(4, kC20 * x * y, kC20 * y, kC20 * x, 0.f);
-          term(5, kC21 * y * z, 0.f, kC21 * z, kC21 * y);
-          term(6, kC22 * (2.f * zz - xx - yy), -2.f * kC22 * x, -2.f * kC22 * y, 4.f * kC22 * z);
-          term(7, kC23 * x * z, kC23 * z, 0.f, kC23 * x);
-          term(8, kC24 * (xx - yy), 2.f * kC24 * x, -2.f * kC24 * y, 0.f);
-          if (p.deg > 2) {
-            term(9, kC30 * y * (3.f * xx - yy), 6.f * kC30 * x * y, 3.f * kC30 * (xx - yy), 0.f);
-            term(10, kC31 * x * y * z, kC31 * y * z, kC31 * x * z, kC31 * x * y);
-            term(11, kC32 * y * (4.f * zz - xx - yy), -2.f * kC32 * x * y, kC32 * (4.f * zz - xx - 3.f * yy),
-                 8.f * kC32 * y * z);
-            term(12, kC33 * z * (2.f * zz - 3.f * xx - 3.f * yy), -6.f * kC33 * x * z, -6.f * kC33 * y * z,
-                 kC33 * (6.f * zz - 3.f * xx - 3.f * yy));
-            term(13, kC34 * x * (4.f * zz - xx - yy), kC34 * (4.f * zz - 3.f * xx - yy), -2.f * kC34 * x * y,
-                 8.f * kC34 * x * z);
-            term(14, kC35 * z * (xx - yy), 2.f * kC35 * x * z, -2.f * kC35 * y * z, kC35 * (xx - yy));
-            term(15, kC36 * x * (xx - 3.f * yy), 3.f * kC36 * (xx - yy), -6.f * kC36 * x * y, 0.f);
-          }
-        }
-      }
-      // coefficients above the active degree get no gradient (R12); the float4 RMW chunk
-      // that straddles the last active coefficient must add zeros there
-      for (int k = 3 * ncoef; k < 48; ++k) row[k] = 0.f;
-      const float dot = ddx * x + ddy * y + ddz * z;
-      dmx += (ddx - x * dot) * il;
-      dmy += (ddy - y * dot) * il;
-      dmz += (ddz - z * dot) * il;
-    }
-    // ---- opacity
-    {
-      const float o = 1.0f / (1.0f + expf(-p.ologits[i]));
-      p.grad[10 * n + i] += gop * o * (1.0f - o);
-    }
-    // ---- covariance chain: FP64 through Sigma', det and dL/d(a, b, c)
-    const float t0 = V[0] * mx + V[4] * my + V[8] * mz + V[12];
-    const float t1 = V[1] * mx + V[5] * my + V[9] * mz + V[13];
-    const float t2 = V[2] * mx + V[6] * my + V[10] * mz + V[14];
     const float s[3] = {expf(p.log_scales[3 * i]), expf(p.log_scales[3 * i + 1]), expf(p.log_scales[3 * i + 2])};
     const float4 qh = p.quat_vec4 ? __ldg(reinterpret_cast<const float4*>(p.quats) + i)
                                   : make_float4(p.quats[4 * i], p.quats[4 * i + 1], p.quats[4 * i + 2],
@@ -166,97 +118,167 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(PreBwdParams 
     for (int a = 0; a < 3; ++a)
 #pragma unroll
       for (int k = 0; k < 3; ++k) M[a][k] = R[a][k] * s[k];
-    const float fx = c.fx, fy = c.fy;
-    float u = t0 / t2, v = t1 / t2;
-    if (cb & CB_JX) u = (cb & CB_JX_NEG) ? -c.limx : c.limx;
-    if (cb & CB_JY) v = (cb & CB_JY_NEG) ? -c.limy : c.limy;
-    const float itz = 1.0f / t2, itz2 = itz * itz;
-    const float j00 = fx * itz, j02 = -fx * u * itz, j11 = fy * itz, j12 = -fy * v * itz;
-    float Tm[2][3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      Tm[0][k] = j00 * V[0 + 4 * k] + j02 * V[2 + 4 * k];
-      Tm[1][k] = j11 * V[1 + 4 * k] + j12 * V[2 + 4 * k];
-    }
-    float TS[2][3];
-    double Gp00, Gp01, Gp11;
+    // Sigma (FP64; symmetric, 6 entries)
+    double S00, S01, S02, S11, S12, S22;
     {
-      double Sg[3][3];
-#pragma unroll
-      for (int a = 0; a < 3; ++a)
-#pragma unroll
-        for (int b = a; b < 3; ++b) {
-          Sg[a][b] = (double)M[a][0] * M[b][0] + (double)M[a][1] * M[b][1] + (double)M[a][2] * M[b][2];
-          Sg[b][a] = Sg[a][b];
+      auto sg = [&](int a, int b) {
+        return (double)M[a][0] * M[b][0] + (double)M[a][1] * M[b][1] + (double)M[a][2] * M[b][2];
+      };
+      S00 = sg(0, 0); S01 = sg(0, 1); S02 = sg(0, 2); S11 = sg(1, 1); S12 = sg(1, 2); S22 = sg(2, 2);
+    }
+    float dmx = 0.f, dmy = 0.f, dmz = 0.f, gop = 0.f;
+    float GS00 = 0.f, GS01 = 0.f, GS02 = 0.f, GS11 = 0.f, GS12 = 0.f, GS22 = 0.f;  // dL/dSigma (sym.)
+    for (int vi = 0; vi < p.nviews; ++vi) {
+      if (!((vmask >> vi) & 1u)) continue;
+      const PreBwdView& pv = p.view[vi];
+      const Cam& c = pv.cam;
+      const float* V = c.V;
+      const float* P = c.P;
+      const float4 ga4 = pv.grad2d[3 * i], gb4 = pv.grad2d[3 * i + 1], gc4 = pv.grad2d[3 * i + 2];
+      const float gx = ga4.x, gy = ga4.y;
+      gop += gb4.y;
+      const uint32_t cb = pv.cbits[i];
+      const float g_r = (cb & CB_R) ? 0.f : gb4.z, g_g = (cb & CB_G) ? 0.f : gb4.w, g_b = (cb & CB_B) ? 0.f : gc4.x;
+      // ---- colour: per SH term, dL/dd from the coefficients, dL/dsh_k += Y_k dL/drgb
+      //      (masked by the frozen clamp, R12)
+      {
+        const float dxw = mx - c.campos[0], dyw = my - c.campos[1], dzw = mz - c.campos[2];
+        const float il = rsqrtf(dxw * dxw + dyw * dyw + dzw * dzw);
+        const float x = dxw * il, y = dyw * il, z = dzw * il;
+        const float xx = x * x, yy = y * y, zz = z * z;
+        float ddx = 0.f, ddy = 0.f, ddz = 0.f;
+        auto term = [&](int k, float Y, float dYx, float dYy, float dYz) {
+          const float shg = row[3 * k] * g_r + row[3 * k + 1] * g_g + row[3 * k + 2] * g_b;
+          ddx = fmaf(dYx, shg, ddx);
+          ddy = fmaf(dYy, shg, ddy);
+          ddz = fmaf(dYz, shg, ddz);
+          drow[3 * k] = fmaf(Y, g_r, drow[3 * k]);
+          drow[3 * k + 1] = fmaf(Y, g_g, drow[3 * k + 1]);
+          drow[3 * k + 2] = fmaf(Y, g_b, drow[3 * k + 2]);
+        };
+        term(0, kC0, 0.f, 0.f, 0.f);
+        if (p.deg > 0) {
+          term(1, -kC1 * y, 0.f, -kC1, 0.f);
+          term(2, kC1 * z, 0.f, 0.f, kC1);
+          term(3, -kC1 * x, -kC1, 0.f, 0.f);
+          if (p.deg > 1) {
+            term(4, kC20 * x * y, kC20 * y, kC20 * x, 0.f);
+            term(5, kC21 * y * z, 0.f, kC21 * z, kC21 * y);
+            term(6, kC22 * (2.f * zz - xx - yy), -2.f * kC22 * x, -2.f * kC22 * y, 4.f * kC22 * z);
+            term(7, kC23 * x * z, kC23 * z, 0.f, kC23 * x);
+            term(8, kC24 * (xx - yy), 2.f * kC24 * x, -2.f * kC24 * y, 0.f);
+            if (p.deg > 2) {
+              term(9, kC30 * y * (3.f * xx - yy), 6.f * kC30 * x * y, 3.f * kC30 * (xx - yy), 0.f);
+              term(10, kC31 * x * y * z, kC31 * y * z, kC31 * x * z, kC31 * x * y);
+              term(11, kC32 * y * (4.f * zz - xx - yy), -2.f * kC32 * x * y, kC32 * (4.f * zz - xx - 3.f * yy),
+                   8.f * kC32 * y * z);
+              term(12, kC33 * z * (2.f * zz - 3.f * xx - 3.f * yy), -6.f * kC33 * x * z, -6.f * kC33 * y * z,
+                   kC33 * (6.f * zz - 3.f * xx - 3.f * yy));
+              term(13, kC34 * x * (4.f * zz - xx - yy), kC34 * (4.f * zz - 3.f * xx - yy), -2.f * kC34 * x * y,
+                   8.f * kC34 * x * z);
+              term(14, kC35 * z * (xx - yy), 2.f * kC35 * x * z, -2.f * kC35 * y * z, kC35 * (xx - yy));
+              term(15, kC36 * x * (xx - 3.f * yy), 3.f * kC36 * (xx - yy), -6.f * kC36 * x * y, 0.f);
+            }
+          }
         }
-      double TSd[2][3];
+        const float dot = ddx * x + ddy * y + ddz * z;
+        dmx += (ddx - x * dot) * il;
+        dmy += (ddy - y * dot) * il;
+        dmz += (ddz - z * dot) * il;
+      }
+      // ---- covariance chain: FP64 through Sigma', det and dL/d(a, b, c)
+      const float t0 = V[0] * mx + V[4] * my + V[8] * mz + V[12];
+      const float t1 = V[1] * mx + V[5] * my + V[9] * mz + V[13];
+      const float t2 = V[2] * mx + V[6] * my + V[10] * mz + V[14];
+      const float fx = c.fx, fy = c.fy;
+      float u = t0 / t2, v = t1 / t2;
+      if (cb & CB_JX) u = (cb & CB_JX_NEG) ? -c.limx : c.limx;
+      if (cb & CB_JY) v = (cb & CB_JY_NEG) ? -c.limy : c.limy;
+      const float itz = 1.0f / t2, itz2 = itz * itz;
+      const float j00 = fx * itz, j02 = -fx * u * itz, j11 = fy * itz, j12 = -fy * v * itz;
+      float Tm[2][3];
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int k = 0; k < 3; ++k) {
+        Tm[0][k] = j00 * V[0 + 4 * k] + j02 * V[2 + 4 * k];
+        Tm[1][k] = j11 * V[1 + 4 * k] + j12 * V[2 + 4 * k];
+      }
+      float TS[2][3];
+      double Gp00, Gp01, Gp11;
+      {
+        const double Sg[3][3] = {{S00, S01, S02}, {S01, S11, S12}, {S02, S12, S22}};
+        double TSd[2][3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          TSd[a][k] = (double)Tm[a][0] * Sg[0][k] + (double)Tm[a][1] * Sg[1][k] + (double)Tm[a][2] * Sg[2][k];
-          TS[a][k] = (float)TSd[a][k];
-        }
-      const double A = TSd[0][0] * Tm[0][0] + TSd[0][1] * Tm[0][1] + TSd[0][2] * Tm[0][2] + 0.3;
-      const double B = TSd[0][0] * Tm[1][0] + TSd[0][1] * Tm[1][1] + TSd[0][2] * Tm[1][2];
-      const double Cc = TSd[1][0] * Tm[1][0] + TSd[1][1] * Tm[1][1] + TSd[1][2] * Tm[1][2] + 0.3;
-      const double det = A * Cc - B * B;
-      const double id2 = 1.0 / (det * det);
-      const double gcx = ga4.z, gcy = ga4.w, gcz = gb4.x;
-      Gp00 = (-Cc * Cc * gcx + B * Cc * gcy - B * B * gcz) * id2;
-      Gp01 = 0.5 * (2.0 * B * Cc * gcx - (A * Cc + B * B) * gcy + 2.0 * A * B * gcz) * id2;
-      Gp11 = (-B * B * gcx + A * B * gcy - A * A * gcz) * id2;
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            TSd[a][k] = (double)Tm[a][0] * Sg[0][k] + (double)Tm[a][1] * Sg[1][k] + (double)Tm[a][2] * Sg[2][k];
+            TS[a][k] = (float)TSd[a][k];
+          }
+        const double A = TSd[0][0] * Tm[0][0] + TSd[0][1] * Tm[0][1] + TSd[0][2] * Tm[0][2] + 0.3;
+        const double B = TSd[0][0] * Tm[1][0] + TSd[0][1] * Tm[1][1] + TSd[0][2] * Tm[1][2];
+        const double Cc = TSd[1][0] * Tm[1][0] + TSd[1][1] * Tm[1][1] + TSd[1][2] * Tm[1][2] + 0.3;
+        const double det = A * Cc - B * B;
+        const double id2 = 1.0 / (det * det);
+        const double gcx = ga4.z, gcy = ga4.w, gcz = gb4.x;
+        Gp00 = (-Cc * Cc * gcx + B * Cc * gcy - B * B * gcz) * id2;
+        Gp01 = 0.5 * (2.0 * B * Cc * gcx - (A * Cc + B * B) * gcy + 2.0 * A * B * gcz) * id2;
+        Gp11 = (-B * B * gcx + A * B * gcy - A * A * gcz) * id2;
+      }
+      const float G00 = (float)Gp00, G01 = (float)Gp01, G11 = (float)Gp11;
+      // dL/dSigma += T^T G' T ; dL/dT = 2 G' (T Sigma)
+      auto gs = [&](int r, int q) {
+        return Tm[0][r] * (G00 * Tm[0][q] + G01 * Tm[1][q]) + Tm[1][r] * (G01 * Tm[0][q] + G11 * Tm[1][q]);
+      };
+      GS00 += gs(0, 0); GS01 += gs(0, 1); GS02 += gs(0, 2); GS11 += gs(1, 1); GS12 += gs(1, 2); GS22 += gs(2, 2);
+      float gj00 = 0.f, gj02 = 0.f, gj11 = 0.f, gj12 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float gT0 = 2.f * (G00 * TS[0][k] + G01 * TS[1][k]);
+        const float gT1 = 2.f * (G01 * TS[0][k] + G11 * TS[1][k]);
+        gj00 += gT0 * V[0 + 4 * k];
+        gj02 += gT0 * V[2 + 4 * k];
+        gj11 += gT1 * V[1 + 4 * k];
+        gj12 += gT1 * V[2 + 4 * k];
+      }
+      float gt0 = 0.f, gt1 = 0.f, gt2 = -(gj00 * fx + gj11 * fy) * itz2;
+      if (cb & CB_JX) {
+        gt2 += gj02 * fx * u * itz2;
+      } else {
+        gt0 += -gj02 * fx * itz2;
+        gt2 += gj02 * 2.f * fx * t0 * itz2 * itz;
+      }
+      if (cb & CB_JY) {
+        gt2 += gj12 * fy * v * itz2;
+      } else {
+        gt1 += -gj12 * fy * itz2;
+        gt2 += gj12 * 2.f * fy * t1 * itz2 * itz;
+      }
+      dmx += V[0] * gt0 + V[1] * gt1 + V[2] * gt2;
+      dmy += V[4] * gt0 + V[5] * gt1 + V[6] * gt2;
+      dmz += V[8] * gt0 + V[9] * gt1 + V[10] * gt2;
+      // ---- projected mean (O3)
+      {
+        const float c0 = P[0] * mx + P[4] * my + P[8] * mz + P[12];
+        const float c1 = P[1] * mx + P[5] * my + P[9] * mz + P[13];
+        const float c3 = P[3] * mx + P[7] * my + P[11] * mz + P[15];
+        const float ic3 = 1.0f / c3, ic32 = ic3 * ic3;
+        const float hx = 0.5f * (float)c.W * gx * ic32, hy = 0.5f * (float)c.H * gy * ic32;
+        dmx += hx * (P[0] * c3 - P[3] * c0) + hy * (P[1] * c3 - P[3] * c1);
+        dmy += hx * (P[4] * c3 - P[7] * c0) + hy * (P[5] * c3 - P[7] * c1);
+        dmz += hx * (P[8] * c3 - P[11] * c0) + hy * (P[9] * c3 - P[11] * c1);
+      }
     }
-    const float G00 = (float)Gp00, G01 = (float)Gp01, G11 = (float)Gp11;
-    // dL/dSigma = T^T G' T ; dL/dT = 2 G' (T Sigma)
-    float GS[3][3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r)
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        GS[r][q] = Tm[0][r] * (G00 * Tm[0][q] + G01 * Tm[1][q]) + Tm[1][r] * (G01 * Tm[0][q] + G11 * Tm[1][q]);
-    float gj00 = 0.f, gj02 = 0.f, gj11 = 0.f, gj12 = 0.f;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      const float gT0 = 2.f * (G00 * TS[0][k] + G01 * TS[1][k]);
-      const float gT1 = 2.f * (G01 * TS[0][k] + G11 * TS[1][k]);
-      gj00 += gT0 * V[0 + 4 * k];
-      gj02 += gT0 * V[2 + 4 * k];
-      gj11 += gT1 * V[1 + 4 * k];
-      gj12 += gT1 * V[2 + 4 * k];
-    }
-    float gt0 = 0.f, gt1 = 0.f, gt2 = -(gj00 * fx + gj11 * fy) * itz2;
-    if (cb & CB_JX) {
-      gt2 += gj02 * fx * u * itz2;
-    } else {
-      gt0 += -gj02 * fx * itz2;
-      gt2 += gj02 * 2.f * fx * t0 * itz2 * itz;
-    }
-    if (cb & CB_JY) {
-      gt2 += gj12 * fy * v * itz2;
-    } else {
-      gt1 += -gj12 * fy * itz2;
-      gt2 += gj12 * 2.f * fy * t1 * itz2 * itz;
-    }
-    dmx += V[0] * gt0 + V[1] * gt1 + V[2] * gt2;
-    dmy += V[4] * gt0 + V[5] * gt1 + V[6] * gt2;
-    dmz += V[8] * gt0 + V[9] * gt1 + V[10] * gt2;
-    // ---- projected mean (O3)
+    // ---- opacity
     {
-      const float c0 = P[0] * mx + P[4] * my + P[8] * mz + P[12];
-      const float c1 = P[1] * mx + P[5] * my + P[9] * mz + P[13];
-      const float c3 = P[3] * mx + P[7] * my + P[11] * mz + P[15];
-      const float ic3 = 1.0f / c3, ic32 = ic3 * ic3;
-      const float hx = 0.5f * (float)c.W * gx * ic32, hy = 0.5f * (float)c.H * gy * ic32;
-      dmx += hx * (P[0] * c3 - P[3] * c0) + hy * (P[1] * c3 - P[3] * c1);
-      dmy += hx * (P[4] * c3 - P[7] * c0) + hy * (P[5] * c3 - P[7] * c1);
-      dmz += hx * (P[8] * c3 - P[11] * c0) + hy * (P[9] * c3 - P[11] * c1);
+      const float o = 1.0f / (1.0f + expf(-p.ologits[i]));
+      p.grad[10 * n + i] += gop * o * (1.0f - o);
     }
     float* gm = p.grad + 3 * i;
     gm[0] += dmx;
     gm[1] += dmy;
     gm[2] += dmz;
-    // ---- Sigma = M M^T, M = R diag(s)
+    // ---- Sigma = M M^T, M = R diag(s): the summed dL/dSigma to (s, q) once
+    const float GS[3][3] = {{GS00, GS01, GS02}, {GS01, GS11, GS12}, {GS02, GS12, GS22}};
     float gR[3][3];
     float* gls = p.grad + 3 * n + 3 * i;
 #pragma unroll
@@ -297,12 +319,13 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(PreBwdParams 
   }
   __syncwarp();
   // ---- coalesced read-modify-write of the warp's contiguous SH-gradient block
+  //      (coefficients above the active degree stay zero in the row: no gradient, R12)
   if (p.gsh_vec4) {
     float4* dst = reinterpret_cast<float4*>(p.grad + 11 * n) + 12 * wbase;
     for (int c = lane; c < 12 * nvalid; c += 32) {
       const int g = c / 12, e = 4 * (c % 12);
       if (!s_vis[warp][g] || e >= 3 * ncoef) continue;
-      const float* r = &s_sh[warp][g * kRow + e];
+      const float* r = &s_dsh[warp][g * kRow + e];
       float4 v = dst[c];
       v.x += r[0];
       v.y += r[1];
@@ -315,34 +338,50 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(PreBwdParams 
     for (int c = lane; c < 48 * nvalid; c += 32) {
       const int g = c / 48, e = c % 48;
       if (!s_vis[warp][g] || e >= 3 * ncoef) continue;
-      dst[c] += s_sh[warp][g * kRow + e];
+      dst[c] += s_dsh[warp][g * kRow + e];
     }
   }
 }
 
-bgs_status launch_preprocess_bwd(const bgs_gaussians* g, Frame* F, float* grad, cudaStream_t s) {
-  if (F->n == 0) return BGS_OK;
+// a10 over a batch of views: grad += sum over the frames of each view's chain rule.
+bgs_status launch_preprocess_bwd_batch(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
+                                       cudaStream_t s) {
+  const int64_t n = frames[0]->n;
+  if (n == 0) return BGS_OK;
   PreBwdParams p;
-  p.cam = F->cam;
   p.means = g->means;
   p.log_scales = g->log_scales;
   p.quats = g->quats;
   p.ologits = g->opacity_logits;
   p.sh = g->sh;
-  p.n = F->n;
+  p.n = n;
   p.deg = g->sh_degree;
   auto al16 = [](const void* q) { return ((uintptr_t)q & 15u) == 0; };
   p.quat_vec4 = al16(g->quats);
   p.sh_vec4 = al16(g->sh);
-  p.gq_vec4 = al16(grad + 6 * F->n);
-  p.gsh_vec4 = al16(grad + 11 * F->n);
-  p.radius = F->radius;
-  p.cbits = F->cbits;
-  p.grad2d = F->grad2d;
+  p.gq_vec4 = al16(grad + 6 * n);
+  p.gsh_vec4 = al16(grad + 11 * n);
   p.grad = grad;
-  k_preprocess_bwd<<<(unsigned)((F->n + kBwdThreads - 1) / kBwdThreads), kBwdThreads, 0, s>>>(p);
-  note_launch();
-  return check_launch("k_preprocess_bwd");
+  for (int v0 = 0; v0 < nviews; v0 += kPreBwdMaxViews) {
+    p.nviews = nviews - v0 < kPreBwdMaxViews ? nviews - v0 : kPreBwdMaxViews;
+    for (int v = 0; v < p.nviews; ++v) {
+      const Frame* F = frames[v0 + v];
+      p.view[v].cam = F->cam;
+      p.view[v].radius = F->radius;
+      p.view[v].cbits = F->cbits;
+      p.view[v].grad2d = F->grad2d;
+    }
+    k_preprocess_bwd<<<(unsigned)((n + kBwdThreads - 1) / kBwdThreads), kBwdThreads, 0, s>>>(p);
+    note_launch();
+    bgs_status st = check_launch("k_preprocess_bwd");
+    if (st != BGS_OK) return st;
+  }
+  return BGS_OK;
+}
+
+bgs_status launch_preprocess_bwd(const bgs_gaussians* g, Frame* F, float* grad, cudaStream_t s) {
+  Frame* const frames[1] = {F};
+  return launch_preprocess_bwd_batch(g, frames, 1, grad, s);
 }
 
 }  // namespace bgs

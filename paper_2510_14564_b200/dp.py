@@ -32,3 +32,45 @@ def allreduce_grads(grad: torch.Tensor, world: int) -> None:
     dL/dimage by 1/B, so the sum is the gradient of the batch-mean loss)."""
     if world > 1:
         dist.all_reduce(grad, op=dist.ReduceOp.SUM)
+
+
+# ---------------------------------------------------------------- sharded update (§8(e) 2)
+# reduce-scatter of grad -> Adam on this rank's 1/G of theta -> all-gather of theta: the
+# same link bytes as the all-reduce ((G-1)/G S each way), but each rank runs Adam over S/G
+# elements only and keeps exp_avg / exp_avg_sq for its shard alone.
+
+
+def shard_layout(total: int, world: int, align: int = 4) -> tuple[int, int]:
+    """(shard, padded): each rank owns `shard` consecutive elements (a multiple of `align`,
+    so every shard starts 16-byte aligned for the vectorised Adam); theta and grad are
+    allocated with `padded` = world * shard >= total elements, the tail being padding."""
+    if world < 1 or total < 0:
+        raise ValueError(f"bad layout total={total} world={world}")
+    per = -(-total // world)
+    shard = -(-per // align) * align
+    return shard, shard * world
+
+
+def shard_range(rank: int, world: int, total: int, align: int = 4) -> tuple[int, int]:
+    """[begin, end) of rank's shard in the padded layout."""
+    shard, _ = shard_layout(total, world, align)
+    return rank * shard, (rank + 1) * shard
+
+
+def reduce_scatter_grads(grad_padded: torch.Tensor, rank: int, world: int) -> torch.Tensor:
+    """Sum grad over ranks into this rank's shard, in place (NCCL in-place reduce-scatter:
+    the output is the rank's own slice of the input).  Returns the shard view.  Only the
+    shard is meaningful afterwards; the rest still holds this rank's partial sums."""
+    shard = grad_padded.numel() // world
+    out = grad_padded.narrow(0, rank * shard, shard)
+    if world > 1:
+        dist.reduce_scatter_tensor(out, grad_padded, op=dist.ReduceOp.SUM)
+    return out
+
+
+def all_gather_params(theta_padded: torch.Tensor, rank: int, world: int) -> None:
+    """Every rank's updated shard of theta to every rank, in place (NCCL in-place
+    all-gather), so the replicas are identical again."""
+    if world > 1:
+        shard = theta_padded.numel() // world
+        dist.all_gather_into_tensor(theta_padded, theta_padded.narrow(0, rank * shard, shard))

@@ -87,6 +87,11 @@ def test_invalid_calls_launch_nothing(bgs):
     assert lib.bgs_adam_step(None, None, None, None, -1, C.byref(hp), 1, None) == bgs.BGS_ERR_INVALID
     assert lib.bgs_adam_step(None, None, None, None, 10, C.byref(hp), 0, None) == bgs.BGS_ERR_INVALID
     assert lib.bgs_adam_step(None, None, None, None, 0, C.byref(hp), 1, None) == bgs.BGS_OK  # n = 0: no-op
+    assert lib.bgs_adam_step_range(None, None, None, None, 10, 2, 8, C.byref(hp), 1, None) == bgs.BGS_ERR_INVALID
+    assert lib.bgs_adam_step_range(None, None, None, None, 10, 0, 8, C.byref(hp), 1, None) == bgs.BGS_ERR_INVALID
+    assert lib.bgs_adam_step_range(None, None, None, None, 10, 592, 8, C.byref(hp), 1, None) == bgs.BGS_OK  # past 59n
+    assert lib.bgs_zero(None, 4, None) == bgs.BGS_ERR_INVALID
+    assert lib.bgs_zero(None, 0, None) == bgs.BGS_OK
     # preprocess with a camera whose view is not orthonormal
     fake = C.c_void_p(1 << 40)
     need = bgs.bgs_workspace_bytes(4, 32, 32, 64)

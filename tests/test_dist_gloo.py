@@ -40,6 +40,35 @@ def _view_grad(s, cam, seed):
     return oracle.backward(s.theta, s.n, s.sh_degree, cam, f, dl)["grad"]
 
 
+def _worker_sharded(rank, port, out):
+    """reduce-scatter -> Adam on the rank's shard -> all-gather."""
+    from paper_2510_14564_b200_dp import dp
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    s, cams = _scene()
+    total = 59 * s.n
+    shard, padded = dp.shard_layout(total, WORLD)
+    grad = torch.zeros(padded, dtype=torch.float64)
+    for v in dp.views_for_rank(list(range(N_VIEWS)), rank, WORLD):
+        grad[:total] += torch.from_numpy(_view_grad(s, cams[v], 100 + v))
+    g_shard = dp.reduce_scatter_grads(grad, rank, WORLD)
+    b, e = dp.shard_range(rank, WORLD, total)
+    assert g_shard.data_ptr() == grad[b:].data_ptr() and g_shard.numel() == shard
+    # Adam is elementwise: the oracle's full-layout update, read on this shard only (the
+    # rest of `grad` still holds this rank's partial sums and must not leak into theta)
+    g_full = np.zeros(total)
+    lo, hi = b, min(e, total)
+    g_full[lo:hi] = grad[lo:hi].numpy()
+    th_all, _, _ = oracle.adam(s.theta, g_full, np.zeros(total), np.zeros(total), s.n, LR6, step=1)
+    theta = torch.zeros(padded, dtype=torch.float64)
+    theta[:total] = torch.from_numpy(s.theta.astype(np.float64))
+    theta[lo:hi] = torch.from_numpy(th_all[lo:hi])
+    dp.all_gather_params(theta, rank, WORLD)
+    out[rank] = (g_shard.numpy()[: hi - lo].copy(), theta.numpy().copy(), (lo, hi))
+    dist.destroy_process_group()
+
+
 def _worker(rank, port, out):
     from paper_2510_14564_b200_dp import dp  # loaded without the CUDA library (see below)
 
@@ -86,6 +115,51 @@ def _run_rank(rank, port, q):
     _worker(rank, port, res)
     mine, grad, th = res[rank]
     q.put((rank, mine, grad, th))
+
+
+def _run_rank_sharded(rank, port, q):
+    _load_dp_module()
+    res = {}
+    _worker_sharded(rank, port, res)
+    q.put((rank, *res[rank]))
+
+
+def test_shard_layout():
+    dp = _load_dp_module()
+    for total in (0, 1, 59, 59 * 3001, 59 * 5_800_000):
+        for world in (1, 2, 3, 4, 8):
+            shard, padded = dp.shard_layout(total, world)
+            assert shard % 4 == 0 and padded == shard * world and padded >= total
+            assert padded - total < world * 4 + world  # at most one alignment unit + rounding per rank
+            rs = [dp.shard_range(r, world, total) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == padded
+            assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
+
+
+def test_two_rank_sharded_update_matches_allreduce_path():
+    """Sharded update == all-reduce + full Adam: gradient shards equal the single-process
+    4-view sum, and both replicas end bit-identical to the full update."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_run_rank_sharded, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(WORLD):
+        rank, g_shard, theta, rng = q.get(timeout=300)
+        res[rank] = (g_shard, theta, rng)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    s, cams = _scene()
+    ref = sum(_view_grad(s, cams[v], 100 + v) for v in range(N_VIEWS))
+    th_ref, _, _ = oracle.adam(s.theta, ref, np.zeros(59 * s.n), np.zeros(59 * s.n), s.n, LR6, step=1)
+    for r in range(WORLD):
+        g_shard, theta, (lo, hi) = res[r]
+        np.testing.assert_allclose(g_shard, ref[lo:hi], rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+    assert np.array_equal(res[0][1], res[1][1])  # replicas bit-identical
+    np.testing.assert_allclose(res[0][1][: 59 * s.n], th_ref, rtol=1e-12, atol=1e-15)
 
 
 def test_view_split_round_robin():

@@ -287,6 +287,35 @@ def test_multi_view_gradients_accumulate(bgs):
         assert err <= GRAD_TOL, (gname, err)
 
 
+def test_batched_preprocess_bwd(bgs):
+    """bgs_preprocess_bwd_batch (one chain-rule pass over several views' blend gradients)
+    == the sum of the oracle's per-view gradients (R20); 20 frame entries (4 views x 5)
+    also exercise the split into launches of <= 16 views."""
+    s = gen.garden(seed=2, n=20000, n_cams=4)
+    cams = s.cameras
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    rs = [bgs.Renderer(s.n, cams[0].width, cams[0].height, max_keys=1 << 22, device=dev) for _ in cams]
+    g_ref = np.zeros(59 * s.n)
+    for i, (r, cam) in enumerate(zip(rs, cams)):
+        out = r.forward(theta, cam, 3)
+        ref = oracle.forward(s.theta, s.n, 3, cam)
+        dl_np = masked_dl(40 + i, cam, ref, scale=1e-3)
+        bgs.bgs_blend_bwd(r.frame, torch.from_numpy(dl_np).to(dev), out["final_T"], out["n_contrib"])
+        g_ref += oracle.backward(s.theta, s.n, 3, cam, ref, dl_np)["grad"]
+    g = bgs.gaussians(theta, s.n, 3)
+    grad1 = torch.zeros_like(theta)
+    bgs.bgs_preprocess_bwd_batch(g, [r.frame for r in rs], grad1)
+    grad5 = torch.zeros_like(theta)
+    bgs.bgs_preprocess_bwd_batch(g, [r.frame for r in rs] * 5, grad5)
+    torch.cuda.synchronize()
+    for grad, mult in ((grad1, 1), (grad5, 5)):
+        gg = grad.cpu().numpy().astype(np.float64)
+        for gname, idx in oracle.group_slices(s.n).items():
+            err = np.linalg.norm(gg[idx] - mult * g_ref[idx]) / np.linalg.norm(mult * g_ref[idx])
+            assert err <= GRAD_TOL, (mult, gname, err)
+
+
 def test_adam_parity(bgs):
     n = 3001  # 59n not a multiple of 4: exercises the scalar tail
     r = np.random.default_rng(0)
@@ -310,6 +339,33 @@ def test_adam_parity(bgs):
     assert (np.abs(T["v"].cpu().numpy() - v_ref) <= tv).all()
     np.testing.assert_allclose(T["th"].cpu().numpy(), th_ref, rtol=1e-6, atol=1e-6 * max(lr6))
     assert not T["g"].any()
+
+
+def test_adam_shards_equal_full_update(bgs):
+    """bgs_adam_step_range over the shards of a G-way reduce-scatter layout (incl. the
+    padding past 59n and shards that start inside the SH segment) == bgs_adam_step, bit for bit."""
+    from paper_2510_14564_b200 import dp
+
+    n = 3001
+    total = 59 * n
+    r = np.random.default_rng(5)
+    base = {k: r.standard_normal(total).astype(np.float32) for k in ("th", "m", "g")}
+    base["v"] = r.random(total).astype(np.float32)
+    hp = bgs.AdamHParams()
+    full = {k: torch.from_numpy(a.copy()).cuda() for k, a in base.items()}
+    bgs.bgs_adam_step(full["th"], full["g"], full["m"], full["v"], n, hp, step=3)
+    for world in (2, 3, 8):
+        shard, padded = dp.shard_layout(total, world)
+        T = {k: torch.zeros(padded, device="cuda") for k in base}
+        for k, a in base.items():
+            T[k][:total] = torch.from_numpy(a)
+        for rk in range(world):
+            b, e = dp.shard_range(rk, world, total)
+            bgs.bgs_adam_step_range(T["th"][b:e], T["g"][b:e], T["m"][b:e], T["v"][b:e], n, b, e - b, hp, step=3)
+        torch.cuda.synchronize()
+        for k in base:
+            assert torch.equal(T[k][:total], full[k]), (world, k)
+            assert not T[k][total:].any()  # padding untouched
 
 
 # ------------------------------------------------------------------ edge cases

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--view", type=int, default=0)
     ap.add_argument("--only", default=None, help="comma-separated stage names")
     ap.add_argument("--step", type=int, default=0, help="run N full one-view training steps (for ncu)")
+    ap.add_argument("--views", type=int, default=1, help="--step: views per step (batched chain rule)")
     ap.add_argument("--seg-lens", default=None, help="comma-separated seg_len values: time fwd/bwd for each")
     a = ap.parse_args()
     t0 = time.time()
@@ -50,13 +51,17 @@ def main():
         tgt = torch.zeros((3, cam.height, cam.width), dtype=torch.uint8, device=dev)
         loss = torch.zeros(1, device=dev)
         hp = bgs.AdamHParams()
+        vcams = [s.cameras[(a.view + 4 * j) % len(s.cameras)] for j in range(a.views)]
+        rs = [r] + [bgs.Renderer(s.n, cam.width, cam.height, max_keys=r.max_keys, device=dev) for _ in vcams[1:]]
         for it in range(a.step):
-            bgs.bgs_preprocess(g, c, r.frame)
-            bgs.bgs_sort(r.frame)
-            bgs.bgs_render_fwd(r.frame, r.image, r.final_T, r.n_contrib)
-            bgs.bgs_l1_loss_grad(r.image, tgt, cam.width, cam.height, 1.0 / (3 * cam.width * cam.height), dl, loss)
-            bgs.bgs_blend_bwd(r.frame, dl, r.final_T, r.n_contrib)
-            bgs.bgs_preprocess_bwd(g, r.frame, grad)
+            for rj, cj in zip(rs, vcams):
+                bgs.bgs_preprocess(g, bgs.camera(cj), rj.frame)
+                bgs.bgs_sort(rj.frame)
+                bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
+                bgs.bgs_l1_loss_grad(rj.image, tgt, cam.width, cam.height, 1.0 / (3 * cam.width * cam.height), dl,
+                                     loss)
+                bgs.bgs_blend_bwd(rj.frame, dl, rj.final_T, rj.n_contrib)
+            bgs.bgs_preprocess_bwd_batch(g, [rj.frame for rj in rs], grad)
             bgs.bgs_adam_step(theta, grad, m, v, s.n, hp, it + 1)
         torch.cuda.synchronize()
         print("launches per step:", bgs.launch_count())
