@@ -12,11 +12,13 @@
 // reaches the block (exact, as in the forward).  The step loop is software-pipelined:
 // list ids are fetched three steps ahead, the 16-byte cull records {x,y,ex,ey} two steps
 // ahead, and the full records of the hits one step ahead, so the gathers overlap the
-// walk.  Per pixel: T_i = T_{i+1} / (1 - alpha_i), the colour behind accumulates
-// S += c alpha T (S starts at T_final bg), and each evaluated entry yields 9 partials
-// {dxy(2), dconic(3), dopacity, drgb(3)}.  A reduce-scatter butterfly (12 shuffles) leaves
-// the 9 warp totals on 9 lanes, which add them into grad2d[id] with one 9-lane RED
-// instruction -- instead of 3DGS's nine scalar global atomics per evaluated pair.
+// walk.  Per pixel: T_i = T_{i+1} / (1 - alpha_i), and the colour behind, S += c alpha T
+// (S starts at T_final bg), is carried only as the scalar DS = dL/dC . S it contributes.
+// Each evaluated entry yields 9 partials: dL/dxy (2), dp {dx^2, dx dy, dy^2} (dp =
+// dL/dpower), the opacity part and w dL/dC.  A reduce-scatter butterfly (12 shuffles) leaves
+// the 9 warp totals on 9 lanes, which scale the conic ones and add all 9 into grad2d[id]
+// with one 9-lane RED instruction -- instead of 3DGS's nine scalar global
+// atomics per evaluated pair.
 //
 // K13 (the chain rule to theta) is in preprocess_bwd.cu.
 #include "common.cuh"
@@ -80,6 +82,15 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
   const int64_t plane = (int64_t)cam.W * cam.H;
   const float4 none = make_float4(-1e30f, -1e30f, -1e30f, -1e30f);
   const uint32_t n_units = counters[C_BWD_UNITS];
+  // the factor this lane's reduced value takes (warp_reduce_scatter9's idx depends on the
+  // lane only): the conic partials dp {dx^2, dx dy, dy^2} -> dL/dconic = (-1/2, -1, -1/2) x
+  float red_mul = 1.0f;
+  {
+    int idx;
+    const float zero[9] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    (void)warp_reduce_scatter9(zero, lane, idx);
+    red_mul = idx == 3 ? -1.0f : (idx == 2 || idx == 4) ? -0.5f : 1.0f;
+  }
   while (true) {
     uint32_t item = 0;
     if (lane == 0) item = atomicAdd(ticket, 1u);
@@ -113,15 +124,14 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
       dLg = dl_dimage[plane + pix];
       dLb = dl_dimage[2 * plane + pix];
     }
-    float Sr = T * cam.bg[0], Sg = T * cam.bg[1], Sb = T * cam.bg[2];
+    // the colour behind the current entry enters the gradient only as DS = dL/dC . S
+    float DS = T * (dLr * cam.bg[0] + dLg * cam.bg[1] + dLb * cam.bg[2]);
     if (!last_seg && (int)my_last > top) {
       // the pixel's walk continues past this segment: start from the forward's checkpoint
       // {T, colour behind} at boundary seg + 1
       const float4 c = ck_pool[(size_t)ck_table[(size_t)it * kCkMax + seg] * 32 + lane];
       T = c.x;
-      Sr = c.y;
-      Sg = c.z;
-      Sb = c.w;
+      DS = dLr * c.y + dLg * c.z + dLb * c.w;
     }
     const int nst = (top - lo + 31) / 32;
     // lane's list position in step s (back to front; below lo = no entry)
@@ -166,7 +176,9 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
       }
       const float4 a_nn = load_cull(id_nn);
       const uint32_t id_nnn = load_id(s + 3);
-      // (4) walk step s, back to front
+      // (4) walk step s, back to front.  Per entry and pixel the partials are
+      //   dL/dxy = dp (2A dx + B dy, 2C dy + B dx), dp {dx^2, dx dy, dy^2}, dL/do-part, w dL/dC
+      // (dp = dL/dpower); the conic's factors (-1/2, -1, -1/2) are applied to the warp totals
       const int m = __popc(bal);
       for (int k = m - 1; k >= 0; --k) {
         const uint32_t pos = spos[k];
@@ -177,7 +189,8 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
           const float4 r1 = sr1[k];
           const float4 r2 = sr2[k];
           const float dx = r0.x - pxf, dy = r0.y - pyf;
-          const float power = fmaf(r1.x, dx * dx, fmaf(r1.z, dy * dy, r1.y * (dx * dy)));
+          const float dxx = dx * dx, dyy = dy * dy, dxy = dx * dy;
+          const float power = fmaf(r1.x, dxx, fmaf(r1.z, dyy, r1.y * dxy));
           float G = 0.0f, og = 0.0f, alpha = 0.0f;
           // power below the exact alpha < 1/255 bound (pthr): skipped without the MUFU path
           if (power > 0.0f || power < r2.w) {
@@ -197,19 +210,18 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
             g6 = w * dLr;
             g7 = w * dLg;
             g8 = w * dLb;
-            const float dLda =
-                dLr * (r2.x * T - Sr * ioma) + dLg * (r2.y * T - Sg * ioma) + dLb * (r2.z * T - Sb * ioma);
-            Sr = fmaf(r2.x, w, Sr);
-            Sg = fmaf(r2.y, w, Sg);
-            Sb = fmaf(r2.z, w, Sb);
+            // dL/dalpha = sum_c dL_c (c_c T - S_c / (1 - alpha)) = T (dL . c) - DS / (1 - alpha)
+            const float dLc = fmaf(dLb, r2.z, fmaf(dLg, r2.y, dLr * r2.x));
+            const float dLda = fmaf(T, dLc, -(DS * ioma));
+            DS = fmaf(dLc, w, DS);  // S += c w
             if (og <= 0.99f) {  // unclamped alpha: gradient to opacity and G (R18)
               g5 = dLda * G;
               const float dp = dLda * og;  // dL/dpower
-              g0 = dp * (2.0f * r1.x * dx + r1.y * dy);
-              g1 = dp * (2.0f * r1.z * dy + r1.y * dx);
-              g2 = dp * (-0.5f * dx * dx);
-              g3 = dp * (-dx * dy);
-              g4 = dp * (-0.5f * dy * dy);
+              g0 = dp * fmaf(2.0f * r1.x, dx, r1.y * dy);
+              g1 = dp * fmaf(2.0f * r1.z, dy, r1.y * dx);
+              g2 = dp * dxx;
+              g3 = dp * dxy;
+              g4 = dp * dyy;
             }
           }
         }
@@ -217,8 +229,9 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
           const float gv[9] = {g0, g1, g2, g3, g4, g5, g6, g7, g8};
           int idx;
           const float tot = warp_reduce_scatter9(gv, lane, idx);
-          // 9 lanes, 9 consecutive floats of grad2d[id]: one RED instruction
-          if (idx >= 0) atomicAdd(reinterpret_cast<float*>(grad2d + 3 * sid[k]) + idx, tot);
+          // 9 lanes, 9 consecutive floats of grad2d[id]: one RED instruction (the conic
+          // partials take their constant factor here, once per entry)
+          if (idx >= 0) atomicAdd(reinterpret_cast<float*>(grad2d + 3 * sid[k]) + idx, tot * red_mul);
         }
       }
       __syncwarp();

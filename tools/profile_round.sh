@@ -26,7 +26,7 @@ ncu --set full --clock-control none --import-source on -f -o /tmp/prof_pb_$TAG -
 python tools/ncu_summary.py /tmp/prof_pb_$TAG.ncu-rep $OUT/ncu_summary_pb_$TAG.md --title "$TAG, batched a10 over 16 garden views" \
     --traffic $OUT/ncu_traffic_$TAG.json --stage 'preprocess_bwd=^k_preprocess_bwd$' >> $OUT/ncu_full_$TAG.log 2>&1
 ncu -i /tmp/prof_pb_$TAG.ncu-rep --page source --csv --print-source cuda,sass > $OUT/src_k_preprocess_bwd_$TAG.csv 2>&1
-for k in k_render_fwd k_render_bwd; do
+for k in k_render_fwd k_render_bwd k_emit_direct; do
   ncu -i /tmp/prof_$TAG.ncu-rep --page source --csv --print-source cuda,sass -k regex:$k -s 1 -c 1 \
       > $OUT/src_${k}_$TAG.csv 2>&1
 done
