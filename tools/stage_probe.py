@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--view", type=int, default=0)
     ap.add_argument("--only", default=None, help="comma-separated stage names")
     ap.add_argument("--step", type=int, default=0, help="run N full one-view training steps (for ncu)")
+    ap.add_argument("--debug-flags", type=int, default=0, help="--seg-lens: frame debug flags (timing experiments)")
     ap.add_argument("--views", type=int, default=1, help="--step: views per step (batched chain rule)")
     ap.add_argument("--seg-lens", default=None, help="comma-separated seg_len values: time fwd/bwd for each")
     a = ap.parse_args()
@@ -69,6 +70,7 @@ def main():
     if a.seg_lens:
         for sl in [int(x) for x in a.seg_lens.split(",")]:
             bgs.bgs_frame_set_seg_len(r.frame, sl)
+            bgs.bgs_frame_set_debug(r.frame, a.debug_flags)
             res = {}
             for name in ("render_fwd", "blend_bwd"):
                 stages["render_fwd"]()  # records this seg_len's checkpoints
