@@ -206,6 +206,24 @@ bgs_status bgs_zero(float* p, int64_t count, void* stream);
 bgs_status bgs_l1_loss_grad(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale,
                             float* dL_dimage, float* loss_sum, void* stream);
 
+/* ---------------------------------------------------------------- NEXT-2: the 3DGS training loss */
+/* Workspace bytes for bgs_l1_dssim_loss_grad at w x h (0 on invalid sizes). */
+size_t bgs_loss_workspace_bytes(int32_t w, int32_t h);
+
+/* The 3DGS training loss and its gradient between a7 and a9:
+ *   Loss = (1 - lambda) mean|x - y| + lambda (1 - mean SSIM(x, y)),  lambda = 0.2 in 3DGS,
+ * x = image [3][h][w] (device), y = target [3][h][w] (device, 8-bit, read as t/255), means
+ * over the 3 h w values; SSIM per channel with an 11x11 Gaussian window (sigma 1.5, zero
+ * padding), C1 = 0.01^2, C2 = 0.03^2 (Wang et al. 2004; the paper's quality metric, PAPER.md
+ * §VI-A l.394; window per SPEC.md l.171; readings R28-R30).  Outputs: dL_dimage (device,
+ * [3][h][w], overwritten) = scale * dLoss/dx, and loss_sum (one device float) += scale *
+ * Loss (scale = 1/B gives the batch mean, R20).  workspace: device, 256-byte aligned, >=
+ * bgs_loss_workspace_bytes(w, h); no state is kept in it between calls.  BGS_ERR_INVALID on
+ * null pointers, bad sizes, lambda outside [0, 1] or a short/unaligned workspace. */
+bgs_status bgs_l1_dssim_loss_grad(const float* image, const uint8_t* target, int32_t w, int32_t h, float lambda,
+                                  float scale, float* dL_dimage, float* loss_sum, void* workspace, size_t bytes,
+                                  void* stream);
+
 /* ---------------------------------------------------------------- NEXT-1: T1 density statistics */
 /* Workspace bytes for bgs_local_density over n points (0 on invalid n: 1 <= n < 2^30). */
 size_t bgs_density_workspace_bytes(int64_t n);

@@ -91,6 +91,9 @@ _SIGS = {
     "bgs_adam_step_range": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.POINTER(AdamHParams),
                                       C.c_int64, _P]),
     "bgs_zero": (C.c_int, [_P, C.c_int64, _P]),
+    "bgs_loss_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),
+    "bgs_l1_dssim_loss_grad": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_float, C.c_float, _P, _P, _P, C.c_size_t,
+                                         _P]),
     "bgs_l1_loss_grad": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_float, _P, _P, _P]),
     "bgs_frame_status": (C.c_int, [C.POINTER(Frame), C.POINTER(C.c_int64)]),
     "bgs_frame_debug": (C.c_int, [C.POINTER(Frame), C.POINTER(FrameViews)]),
@@ -155,6 +158,10 @@ def bgs_workspace_bytes(n, w, h, max_keys) -> int:
     return int(_lib.bgs_workspace_bytes(n, w, h, max_keys))
 
 
+def bgs_loss_workspace_bytes(w, h) -> int:
+    return int(_lib.bgs_loss_workspace_bytes(w, h))
+
+
 def bgs_frame_init(frame: Frame, workspace: torch.Tensor, n, w, h, max_keys):
     _check(_lib.bgs_frame_init(C.byref(frame), _ptr(workspace), workspace.numel(), n, w, h, max_keys),
            "bgs_frame_init")
@@ -207,6 +214,13 @@ def bgs_adam_step_range(theta, grad, exp_avg, exp_avg_sq, n, begin, count, hp: A
 
 def bgs_zero(t, stream=None):
     _check(_lib.bgs_zero(_ptr(t), t.numel(), _stream(stream)), "bgs_zero")
+
+
+def bgs_l1_dssim_loss_grad(image, target_u8, w, h, lam, scale, dl_dimage, loss_sum, workspace, stream=None):
+    """workspace: a uint8 CUDA tensor of >= bgs_loss_workspace_bytes(w, h) bytes (256-B aligned)."""
+    _check(_lib.bgs_l1_dssim_loss_grad(_ptr(image), _ptr(target_u8), w, h, lam, scale, _ptr(dl_dimage),
+                                       _ptr(loss_sum), _ptr(workspace), workspace.numel() * workspace.element_size(),
+                                       _stream(stream)), "bgs_l1_dssim_loss_grad")
 
 
 def bgs_l1_loss_grad(image, target_u8, w, h, scale, dl_dimage, loss_sum, stream=None):

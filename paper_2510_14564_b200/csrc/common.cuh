@@ -124,6 +124,9 @@ bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n,
                        const bgs_adam_hparams* hp, int64_t step, cudaStream_t s);
 bgs_status launch_l1(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale, float* dl,
                      float* loss_sum, cudaStream_t s);
+size_t loss_workspace_bytes(int32_t w, int32_t h);
+bgs_status launch_l1_dssim(const float* image, const uint8_t* target, int32_t w, int32_t h, float lam, float scale,
+                           float* dl, float* loss_sum, void* workspace, cudaStream_t s);
 bgs_status launch_stats(const Frame* F, const uint32_t* n_contrib, bgs_stats* out, cudaStream_t s);
 
 int num_sms();

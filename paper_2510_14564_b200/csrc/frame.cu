@@ -362,6 +362,21 @@ bgs_status bgs_l1_loss_grad(const float* image, const uint8_t* target, int32_t w
   return launch_l1(image, target, w, h, scale, dL_dimage, loss_sum, (cudaStream_t)stream);
 }
 
+size_t bgs_loss_workspace_bytes(int32_t w, int32_t h) {
+  if (w < 1 || h < 1 || w > 16384 || h > 16384) return 0;
+  return loss_workspace_bytes(w, h);
+}
+
+bgs_status bgs_l1_dssim_loss_grad(const float* image, const uint8_t* target, int32_t w, int32_t h, float lambda,
+                                  float scale, float* dL_dimage, float* loss_sum, void* workspace, size_t bytes,
+                                  void* stream) {
+  if (!image || !target || !dL_dimage || !loss_sum || !workspace || w < 1 || h < 1 || w > 16384 || h > 16384)
+    return BGS_ERR_INVALID;
+  if (((uintptr_t)workspace & 255u) || bytes < loss_workspace_bytes(w, h)) return BGS_ERR_INVALID;
+  if (!(lambda >= 0.0f && lambda <= 1.0f)) return BGS_ERR_INVALID;
+  return launch_l1_dssim(image, target, w, h, lambda, scale, dL_dimage, loss_sum, workspace, (cudaStream_t)stream);
+}
+
 bgs_status bgs_frame_status(const bgs_frame* f, int64_t* num_keys) {
   if (!frame_ok(f) || !num_keys) return BGS_ERR_INVALID;
   const Frame* F = frame_of(f);

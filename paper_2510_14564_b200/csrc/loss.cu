@@ -1,0 +1,249 @@
+// loss.cu -- NEXT-2: the 3DGS training loss between the blend forward
+// (a7) and backward (a9), fused into two tiled kernels:
+//   Loss = (1 - lam) mean|x - y| + lam (1 - mean SSIM(x, y)),  lam = 0.2 in 3DGS,
+// SSIM per channel with an 11x11 Gaussian window (sigma 1.5, zero padding), C1 = 0.01^2,
+// C2 = 0.03^2 (Wang et al. 2004, the quality metric of PAPER.md §VI-A l.394; window per
+// SPEC.md l.171; readings R28-R30 in DESIGN.md §3).
+//
+// k_ssim_fwd: per (32x16 tile, channel): x and y = target/255 with a 5-pixel halo staged in
+// shared memory, the five window moments {w*x, w*y, w*x^2, w*y^2, w*xy} by a separable
+// 11-tap pass (rows, then columns), then per pixel SSIM, |x - y| and the three partials of
+// SSIM w.r.t. the raw moments (dS/dm, dS/dE, dS/dP) written to the workspace; each block
+// writes its sums of SSIM and |x - y| to its own slot (no same-address atomics).
+// k_ssim_bwd: per tile, the three partial maps (halo 5, zero outside the image) correlated
+// with the (symmetric) window, and dL/dx = scale ((1 - lam) sign(x - y) - lam (w*dS/dm +
+// 2 x w*dS/dE + y w*dS/dP)) / N; block 0 also reduces the per-block sums into the loss.
+// HBM traffic per view: image 12 B + target 3 B + 9 partial maps 2 x 36 B + dL 12 B per
+// pixel, ~100 B per pixel (0.1 GB at 1237 x 822): a few tens of microseconds.
+#include <math.h>
+
+#include "common.cuh"
+
+namespace bgs {
+
+constexpr int kLTx = 32, kLTy = 16, kLR = 5, kLWin = 2 * kLR + 1;
+constexpr int kLHx = kLTx + 2 * kLR, kLHy = kLTy + 2 * kLR;  // tile + halo
+constexpr int kLThreads = 256;
+constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
+
+struct LossWin {
+  float w[kLWin];
+};
+
+__global__ void __launch_bounds__(kLThreads) k_ssim_fwd(const float* __restrict__ img, const uint8_t* __restrict__ tgt,
+                                                        int W, int H, LossWin win, float* __restrict__ part,
+                                                        float* __restrict__ acc) {
+  __shared__ float sx[kLHy][kLHx], sy[kLHy][kLHx];
+  __shared__ float hm[5][kLHy][kLTx];
+  const int ch = blockIdx.z;
+  const int x0 = blockIdx.x * kLTx, y0 = blockIdx.y * kLTy;
+  const size_t plane = (size_t)W * H;
+  const float* xc = img + ch * plane;
+  const uint8_t* yc = tgt + ch * plane;
+  for (int i = threadIdx.x; i < kLHy * kLHx; i += kLThreads) {
+    const int r = i / kLHx, c = i - r * kLHx;
+    const int gx = x0 + c - kLR, gy = y0 + r - kLR;
+    float xv = 0.f, yv = 0.f;
+    if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
+      xv = xc[(size_t)gy * W + gx];
+      yv = (float)yc[(size_t)gy * W + gx] * (1.0f / 255.0f);
+    }
+    sx[r][c] = xv;
+    sy[r][c] = yv;
+  }
+  __syncthreads();
+  // rows: the 11-tap pass along x for every halo row
+  for (int i = threadIdx.x; i < kLHy * kLTx; i += kLThreads) {
+    const int r = i / kLTx, c = i - r * kLTx;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+#pragma unroll
+    for (int k = 0; k < kLWin; ++k) {
+      const float wx = win.w[k], xv = sx[r][c + k], yv = sy[r][c + k];
+      a0 = fmaf(wx, xv, a0);
+      a1 = fmaf(wx, yv, a1);
+      a2 = fmaf(wx, xv * xv, a2);
+      a3 = fmaf(wx, yv * yv, a3);
+      a4 = fmaf(wx, xv * yv, a4);
+    }
+    hm[0][r][c] = a0;
+    hm[1][r][c] = a1;
+    hm[2][r][c] = a2;
+    hm[3][r][c] = a3;
+    hm[4][r][c] = a4;
+  }
+  __syncthreads();
+  // columns, then the per-pixel SSIM and its partials
+  float s_sum = 0.f, l1_sum = 0.f;
+  for (int i = threadIdx.x; i < kLTy * kLTx; i += kLThreads) {
+    const int r = i / kLTx, c = i - r * kLTx;
+    const int gx = x0 + c, gy = y0 + r;
+    if (gx >= W || gy >= H) continue;
+    float mx = 0.f, my = 0.f, exx = 0.f, eyy = 0.f, exy = 0.f;
+#pragma unroll
+    for (int k = 0; k < kLWin; ++k) {
+      const float wy = win.w[k];
+      mx = fmaf(wy, hm[0][r + k][c], mx);
+      my = fmaf(wy, hm[1][r + k][c], my);
+      exx = fmaf(wy, hm[2][r + k][c], exx);
+      eyy = fmaf(wy, hm[3][r + k][c], eyy);
+      exy = fmaf(wy, hm[4][r + k][c], exy);
+    }
+    const float sxx = exx - mx * mx, syy = eyy - my * my, sxy = exy - mx * my;
+    const float a1 = 2.f * mx * my + kC1, a2 = 2.f * sxy + kC2;
+    const float b1 = mx * mx + my * my + kC1, b2 = sxx + syy + kC2;
+    const float ib = 1.0f / (b1 * b2);
+    const float s = a1 * a2 * ib;
+    const float d_e = -s / b2;
+    const float d_p = 2.f * a1 * ib;
+    const float d_m = 2.f * my * a2 * ib - 2.f * mx * s / b1 + 2.f * mx * s / b2 - 2.f * my * a1 * ib;
+    const size_t p = (size_t)gy * W + gx;
+    part[(0 * 3 + ch) * plane + p] = d_m;
+    part[(1 * 3 + ch) * plane + p] = d_e;
+    part[(2 * 3 + ch) * plane + p] = d_p;
+    s_sum += s;
+    l1_sum += fabsf(sx[r + kLR][c + kLR] - sy[r + kLR][c + kLR]);
+  }
+  // block sums -> this block's slot of the partial-sum array (no same-address atomics)
+  __shared__ float s_red[2][kLThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s_sum += __shfl_xor_sync(0xffffffffu, s_sum, o);
+    l1_sum += __shfl_xor_sync(0xffffffffu, l1_sum, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    s_red[0][threadIdx.x >> 5] = l1_sum;
+    s_red[1][threadIdx.x >> 5] = s_sum;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    float t = 0.f;
+    for (int k = 0; k < kLThreads / 32; ++k) t += s_red[threadIdx.x][k];
+    const int b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    acc[2 * b + threadIdx.x] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kLThreads) k_ssim_bwd(const float* __restrict__ img, const uint8_t* __restrict__ tgt,
+                                                        int W, int H, LossWin win, const float* __restrict__ part,
+                                                        float lam, float scale, float* __restrict__ dl,
+                                                        const float* __restrict__ acc, float* loss_sum) {
+  __shared__ float sg[3][kLHy][kLHx];
+  __shared__ float hg[3][kLHy][kLTx];
+  const int ch = blockIdx.z;
+  const int x0 = blockIdx.x * kLTx, y0 = blockIdx.y * kLTy;
+  const size_t plane = (size_t)W * H;
+  const double n = 3.0 * (double)plane;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && ch == 0) {
+    // the loss from k_ssim_fwd's per-block partial sums (in double, fixed order per lane)
+    __shared__ double s_acc[2][kLThreads / 32];
+    const int nb = gridDim.x * gridDim.y * gridDim.z;
+    double l1 = 0.0, ss = 0.0;
+    for (int b = threadIdx.x; b < nb; b += kLThreads) {
+      l1 += (double)acc[2 * b];
+      ss += (double)acc[2 * b + 1];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+      ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_acc[0][threadIdx.x >> 5] = l1;
+      s_acc[1][threadIdx.x >> 5] = ss;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      l1 = ss = 0.0;
+      for (int k = 0; k < kLThreads / 32; ++k) {
+        l1 += s_acc[0][k];
+        ss += s_acc[1][k];
+      }
+      atomicAdd(loss_sum, (float)(scale * ((1.0 - lam) * l1 / n + lam * (1.0 - ss / n))));
+    }
+  }
+  for (int i = threadIdx.x; i < kLHy * kLHx; i += kLThreads) {
+    const int r = i / kLHx, c = i - r * kLHx;
+    const int gx = x0 + c - kLR, gy = y0 + r - kLR;
+    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
+    const size_t p = (size_t)gy * W + gx;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) sg[q][r][c] = in ? part[(q * 3 + ch) * plane + p] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kLHy * kLTx; i += kLThreads) {
+    const int r = i / kLTx, c = i - r * kLTx;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < kLWin; ++k) {
+      const float wx = win.w[k];
+      a0 = fmaf(wx, sg[0][r][c + k], a0);
+      a1 = fmaf(wx, sg[1][r][c + k], a1);
+      a2 = fmaf(wx, sg[2][r][c + k], a2);
+    }
+    hg[0][r][c] = a0;
+    hg[1][r][c] = a1;
+    hg[2][r][c] = a2;
+  }
+  __syncthreads();
+  const float inv_n = (float)(1.0 / n);
+  for (int i = threadIdx.x; i < kLTy * kLTx; i += kLThreads) {
+    const int r = i / kLTx, c = i - r * kLTx;
+    const int gx = x0 + c, gy = y0 + r;
+    if (gx >= W || gy >= H) continue;
+    float cm = 0.f, ce = 0.f, cp = 0.f;
+#pragma unroll
+    for (int k = 0; k < kLWin; ++k) {
+      const float wy = win.w[k];
+      cm = fmaf(wy, hg[0][r + k][c], cm);
+      ce = fmaf(wy, hg[1][r + k][c], ce);
+      cp = fmaf(wy, hg[2][r + k][c], cp);
+    }
+    const size_t p = (size_t)gy * W + gx;
+    const float xv = img[ch * plane + p], yv = (float)tgt[ch * plane + p] * (1.0f / 255.0f);
+    const float d = xv - yv;
+    const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+    const float dssim = cm + 2.f * xv * ce + yv * cp;
+    dl[ch * plane + p] = scale * inv_n * ((1.0f - lam) * sgn - lam * dssim);
+  }
+}
+
+static LossWin make_window() {
+  // R29: g_k ~ exp(-(k - 5)^2 / (2 * 1.5^2)), normalised, in double, rounded once
+  LossWin lw;
+  double g[kLWin], sum = 0.0;
+  for (int k = 0; k < kLWin; ++k) {
+    const double d = (double)(k - kLR);
+    g[k] = exp(-d * d / (2.0 * 1.5 * 1.5));
+    sum += g[k];
+  }
+  for (int k = 0; k < kLWin; ++k) lw.w[k] = (float)(g[k] / sum);
+  return lw;
+}
+
+static size_t loss_blocks(int32_t w, int32_t h) {
+  return (size_t)((w + kLTx - 1) / kLTx) * (size_t)((h + kLTy - 1) / kLTy) * 3;
+}
+
+// [per-block partial sums: 2 floats per k_ssim_fwd block, 256-B padded][9 partial maps]
+static size_t loss_acc_bytes(int32_t w, int32_t h) { return (2 * sizeof(float) * loss_blocks(w, h) + 255) & ~(size_t)255; }
+
+size_t loss_workspace_bytes(int32_t w, int32_t h) {
+  return loss_acc_bytes(w, h) + (size_t)9 * (size_t)w * (size_t)h * sizeof(float);
+}
+
+bgs_status launch_l1_dssim(const float* image, const uint8_t* target, int32_t w, int32_t h, float lam, float scale,
+                           float* dl, float* loss_sum, void* workspace, cudaStream_t s) {
+  static const LossWin win = make_window();
+  float* acc = reinterpret_cast<float*>(workspace);
+  float* part = reinterpret_cast<float*>(static_cast<char*>(workspace) + loss_acc_bytes(w, h));
+  const dim3 grid((w + kLTx - 1) / kLTx, (h + kLTy - 1) / kLTy, 3);
+  k_ssim_fwd<<<grid, kLThreads, 0, s>>>(image, target, w, h, win, part, acc);
+  note_launch();
+  bgs_status st = check_launch("k_ssim_fwd");
+  if (st != BGS_OK) return st;
+  k_ssim_bwd<<<grid, kLThreads, 0, s>>>(image, target, w, h, win, part, lam, scale, dl, acc, loss_sum);
+  note_launch();
+  return check_launch("k_ssim_bwd");
+}
+
+}  // namespace bgs

@@ -92,6 +92,14 @@ def test_invalid_calls_launch_nothing(bgs):
     assert lib.bgs_adam_step_range(None, None, None, None, 10, 592, 8, C.byref(hp), 1, None) == bgs.BGS_OK  # past 59n
     assert lib.bgs_zero(None, 4, None) == bgs.BGS_ERR_INVALID
     assert lib.bgs_zero(None, 0, None) == bgs.BGS_OK
+    assert bgs.bgs_loss_workspace_bytes(0, 10) == 0 and bgs.bgs_loss_workspace_bytes(64, 32) >= 9 * 64 * 32 * 4
+    ws = C.c_void_p(1 << 40)
+    need = bgs.bgs_loss_workspace_bytes(64, 32)
+    assert lib.bgs_l1_dssim_loss_grad(None, ws, 64, 32, 0.2, 1.0, ws, ws, ws, need, None) == bgs.BGS_ERR_INVALID
+    assert lib.bgs_l1_dssim_loss_grad(ws, ws, 64, 32, 0.2, 1.0, ws, ws, ws, need - 1, None) == bgs.BGS_ERR_INVALID
+    assert lib.bgs_l1_dssim_loss_grad(ws, ws, 64, 32, 1.5, 1.0, ws, ws, ws, need, None) == bgs.BGS_ERR_INVALID
+    assert lib.bgs_l1_dssim_loss_grad(ws, ws, 64, 32, 0.2, 1.0, ws, ws, C.c_void_p((1 << 40) + 16), need,
+                                      None) == bgs.BGS_ERR_INVALID  # unaligned workspace
     # preprocess with a camera whose view is not orthonormal
     fake = C.c_void_p(1 << 40)
     need = bgs.bgs_workspace_bytes(4, 32, 32, 64)

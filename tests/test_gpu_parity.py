@@ -539,3 +539,36 @@ def test_split_forward_parity(bgs, name, seg_len):
                       "opacity": (g2[:, 5], g_ref["opacity"]), "rgb": (g2[:, 6:9], g_ref["rgb"])}.items():
         err = np.linalg.norm(a[vis] - b[vis]) / max(np.linalg.norm(b[vis]), 1e-300)
         assert err <= 1e-4, (k, err)
+
+
+# ------------------------------------------------------------------ NEXT-2: L1 + D-SSIM loss
+def _loss_inputs(seed, h, w):
+    r = np.random.default_rng(seed)
+    t = r.integers(0, 256, (3, h, w)).astype(np.uint8)
+    # images near their targets (the training regime), |x - y| kept off the L1 kink
+    x = (t / 255.0 + np.where(r.random(t.shape) < 0.5, -1, 1) * r.uniform(1e-3, 0.15, t.shape)).astype(np.float32)
+    return x, t
+
+
+@pytest.mark.parametrize("hw", [(16, 16), (37, 53), (5, 7), (128, 96), (822, 1237)])
+def test_l1_dssim_loss_parity(bgs, hw):
+    from oracle import ssim as S
+
+    h, w = hw
+    x, t = _loss_inputs(7 + h, h, w)
+    dev = torch.device("cuda")
+    xd, td = torch.from_numpy(x).to(dev), torch.from_numpy(t).to(dev)
+    dl = torch.full_like(xd, float("nan"))
+    loss = torch.zeros(1, device=dev)
+    ws = torch.empty(bgs.bgs_loss_workspace_bytes(w, h), dtype=torch.uint8, device=dev)
+    scale = 0.5
+    for _ in range(2):  # the workspace keeps no state between calls
+        bgs.bgs_l1_dssim_loss_grad(xd, td, w, h, 0.2, scale, dl, loss, ws)
+    torch.cuda.synchronize()
+    ref_loss = S.loss(x.astype(np.float64), t)
+    assert abs(loss.item() - 2 * scale * ref_loss) <= 1e-5 * abs(2 * scale * ref_loss)
+    g = dl.cpu().numpy().astype(np.float64)
+    g_ref = scale * S.loss_grad(x.astype(np.float64), t)
+    err = np.linalg.norm(g - g_ref) / np.linalg.norm(g_ref)
+    assert err <= 1e-4, err
+    assert np.abs(g - g_ref).max() <= 1e-3 * np.abs(g_ref).max()
