@@ -144,9 +144,14 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const FwdArgs a, 
           r1_c = __ldg(a.record + 3 * id_c + 1);
           r2_c = __ldg(a.record + 3 * id_c + 2);
         }
+        // the next segment boundary this (exact) walk records, or -1
+        int ck_step = (exact && nck < kCkMax) ? (nck + 1) * seg_steps : -1;
         for (int s = s_lo; s < s_hi; ++s) {
           // (0) segment boundary: record {T, C} before it
-          if (exact && s == (nck + 1) * seg_steps && nck < kCkMax) record_ck();
+          if (s == ck_step) {
+            record_ck();
+            ck_step = nck < kCkMax ? (nck + 1) * seg_steps : -1;
+          }
           // (1) commit step s into the warp's shared-memory slice
           const uint32_t bal = __ballot_sync(0xffffffffu, h_c);
           if (h_c) {
