@@ -238,6 +238,48 @@ size_t bgs_density_workspace_bytes(int64_t n);
 bgs_status bgs_local_density(const float* means, int64_t n, float r, float alpha, float beta, uint32_t* counts,
                              double* stats, void* workspace, size_t bytes, void* stream);
 
+/* ---------------------------------------------------------------- NEXT-1: the density-control step */
+/* PAPER.md §III-C2-C4 (l.188-228): merge dense pairs, densify sparse points, every few
+ * thousand iterations (l.228).  Readings R31-R36. */
+typedef struct {
+  float r;            /* local-density radius (world units, > 0) */
+  float alpha, beta;  /* rho_low / rho_high factors */
+  float gamma;        /* d_merge = mu_d + gamma sigma_d */
+  float alpha_sigma;  /* densification spread sigma_p = alpha_sigma d_bar_p (> 1) */
+  float delta;        /* jitter half-width */
+  int32_t k;          /* neighbours for d_bar_p and mu_d / sigma_d (1..16; 8) */
+  int32_t max_new;    /* children per sparse point cap (0..64; 4) */
+} bgs_density_params;
+
+typedef struct {      /* filled on the device by bgs_density_plan */
+  int64_t n_in, n_out, n_pairs, n_children;
+  double mu_rho, sigma_rho, rho_low, rho_high, mu_d, sigma_d, d_merge;
+} bgs_density_report;
+
+/* Workspace bytes for the density step over n Gaussians (0 on invalid n: 1 <= n < 2^30). */
+size_t bgs_density_step_workspace_bytes(int64_t n);
+/* Plan (asynchronous): on theta[59n] (device; the means segment is read): rho and the k
+ * nearest neighbours per point (exact; rings of grid cells), the statistics and d_merge
+ * (R31-R32; neighbour distances truncated at 6 r), mutual-nearest dense pairs within d_merge (R33), the children of sparse points
+ * (R35), the output offsets and n_out -- all kept in the workspace (device, 256-byte
+ * aligned, >= bgs_density_step_workspace_bytes(n)). */
+bgs_status bgs_density_plan(const float* theta, int64_t n, const bgs_density_params* p /*host*/, void* workspace,
+                            size_t bytes, void* stream);
+/* After the caller synchronised the plan's stream: the report (host out; n_out and
+ * n_children size the apply call's buffers) and the number of points with fewer than k
+ * neighbours within 6 r (their missing distances count as 6 r, R32). */
+bgs_status bgs_density_result(const void* workspace, int64_t n, bgs_density_report* out /*host*/,
+                              uint32_t* short_knn /*host, may be NULL*/);
+/* Apply (asynchronous): theta_out / exp_avg_out / exp_avg_sq_out [59 n_out] (device) =
+ * survivors in index order (a merged pair's result at its lower index, R34), then the
+ * children in (parent, j) order (R35); Adam moments kept for unmerged survivors, zero for
+ * merged Gaussians and children (R36).  normals / uniforms: device [n_children][3] N(0,1)
+ * and U(-1,1) variates (the method's random draws, supplied by the caller). */
+bgs_status bgs_density_apply(const float* theta, const float* exp_avg, const float* exp_avg_sq, int64_t n,
+                             const void* workspace, const bgs_density_params* p /*host*/, const float* normals,
+                             const float* uniforms, int64_t n_children, float* theta_out, float* exp_avg_out,
+                             float* exp_avg_sq_out, int64_t n_out, void* stream);
+
 /* ---------------------------------------------------------------- status / debug */
 /* After the caller synchronised the frame's stream: K (host out) and BGS_OK, or
  * BGS_ERR_CAPACITY when K > max_keys (re-run with a larger workspace). */

@@ -57,6 +57,21 @@ class AdamHParams(C.Structure):
         super().__init__(lr_means, lr_log_scales, lr_quats, lr_opacity, lr_sh_dc, lr_sh_rest, beta1, beta2, eps)
 
 
+class DensityParams(C.Structure):
+    """bgs_density_params (include/bgs.h); defaults per DESIGN.md R31-R36 / SPEC's ledger."""
+    _fields_ = [("r", C.c_float), ("alpha", C.c_float), ("beta", C.c_float), ("gamma", C.c_float),
+                ("alpha_sigma", C.c_float), ("delta", C.c_float), ("k", C.c_int32), ("max_new", C.c_int32)]
+
+    def __init__(self, r, alpha=1.0, beta=1.0, gamma=1.0, alpha_sigma=1.5, delta=None, k=8, max_new=4):
+        super().__init__(r, alpha, beta, gamma, alpha_sigma, 0.1 * r if delta is None else delta, k, max_new)
+
+
+class DensityReport(C.Structure):
+    _fields_ = [("n_in", C.c_int64), ("n_out", C.c_int64), ("n_pairs", C.c_int64), ("n_children", C.c_int64),
+                ("mu_rho", C.c_double), ("sigma_rho", C.c_double), ("rho_low", C.c_double),
+                ("rho_high", C.c_double), ("mu_d", C.c_double), ("sigma_d", C.c_double), ("d_merge", C.c_double)]
+
+
 class Frame(C.Structure):
     _fields_ = [("opaque", C.c_uint64 * 128)]
 
@@ -102,6 +117,11 @@ _SIGS = {
     "bgs_frame_set_seg_len": (C.c_int, [C.POINTER(Frame), C.c_int32]),
     "bgs_density_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "bgs_local_density": (C.c_int, [_P, C.c_int64, C.c_float, C.c_float, C.c_float, _P, _P, _P, C.c_size_t, _P]),
+    "bgs_density_step_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "bgs_density_plan": (C.c_int, [_P, C.c_int64, C.POINTER(DensityParams), _P, C.c_size_t, _P]),
+    "bgs_density_result": (C.c_int, [_P, C.c_int64, C.POINTER(DensityReport), C.POINTER(C.c_uint32)]),
+    "bgs_density_apply": (C.c_int, [_P, _P, _P, C.c_int64, _P, C.POINTER(DensityParams), _P, _P, C.c_int64, _P, _P,
+                                    _P, C.c_int64, _P]),
     "bgs_status_string": (C.c_char_p, [C.c_int]),
     "bgs_last_error": (C.c_char_p, []),
     "bgs_launch_count": (C.c_uint64, []),
@@ -269,6 +289,34 @@ def bgs_local_density(means, r, alpha=1.0, beta=1.0, counts=None, stats=None, wo
     _check(_lib.bgs_local_density(_ptr(means), n, float(r), float(alpha), float(beta), _ptr(counts), _ptr(stats),
                                   _ptr(workspace), workspace.numel(), _stream(stream)), "bgs_local_density")
     return counts, stats
+
+
+def density_control(theta, exp_avg, exp_avg_sq, n, params: DensityParams, generator=None, stream=None):
+    """One NEXT-1 density-control step (§III-C2-C4): plan on the device, one host
+    read of the report (n_out sizes the new buffers), the method's random draws
+    (N(0,1) / U(-1,1) variates, torch generator on the device), apply.  Returns
+    (theta', exp_avg', exp_avg_sq', n', report, short_knn, (normals, uniforms)), short_knn =
+    points with fewer than k neighbours within 6 r (R32)."""
+    dev = theta.device
+    nbytes = int(_lib.bgs_density_step_workspace_bytes(n))
+    if nbytes == 0:
+        raise BgsError(BGS_ERR_INVALID, "bgs_density_step_workspace_bytes")
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    _check(_lib.bgs_density_plan(_ptr(theta), n, C.byref(params), _ptr(ws), nbytes, _stream(stream)),
+           "bgs_density_plan")
+    rep = DensityReport()
+    short = C.c_uint32(0)
+    torch.cuda.current_stream(dev).synchronize() if stream is None else stream.synchronize()
+    _check(_lib.bgs_density_result(_ptr(ws), n, C.byref(rep), C.byref(short)), "bgs_density_result")
+    nc, n_out = int(rep.n_children), int(rep.n_out)
+    normals = torch.randn((max(nc, 1), 3), generator=generator, device=dev)
+    uniforms = torch.rand((max(nc, 1), 3), generator=generator, device=dev) * 2.0 - 1.0
+    th2 = torch.empty(59 * n_out, dtype=torch.float32, device=dev)
+    m2, v2 = torch.empty_like(th2), torch.empty_like(th2)
+    _check(_lib.bgs_density_apply(_ptr(theta), _ptr(exp_avg), _ptr(exp_avg_sq), n, _ptr(ws), C.byref(params),
+                                  _ptr(normals), _ptr(uniforms), nc, _ptr(th2), _ptr(m2), _ptr(v2), n_out,
+                                  _stream(stream)), "bgs_density_apply")
+    return th2, m2, v2, n_out, rep, int(short.value), (normals[:nc], uniforms[:nc])
 
 
 def launch_count() -> int:

@@ -158,6 +158,367 @@ __global__ void k_density_finish(int64_t n, const unsigned long long* sums, floa
   out[3] = mu + (double)beta * sd;
 }
 
+
+// ============================================================================ density step
+// NEXT-1, the rest of T1 (§III-C2-C4 l.188-228; readings R31-R36 in DESIGN.md §3):
+// per point rho (as above) and its k nearest neighbours within 6 r (rings of grid cells are
+// added until the k-th candidate lies within the searched radius, at most 6 rings; distances
+// beyond 6 r count as 6 r, R32),
+// the pooled neighbour-distance statistics and d_merge, mutual-nearest dense pairs within
+// d_merge, the densification deficit of sparse points, and the compaction of the new
+// theta / Adam moments.  Distances for kNN and merging are squared in double from the float
+// coordinates ((dx^2 + dy^2) + dz^2, dx exact), with ties by the lower index -- the oracle's
+// (oracle/density.py) decisions.
+constexpr int kKnnMax = 16, kMaxRing = 6, kStepThreads = 256;
+
+struct StepWs {
+  DensityWs g;                  // the hashed grid (cell size r * 1.0001)
+  uint32_t* rho;                // [n]
+  double* dbar;                 // [n] mean distance to the k nearest
+  int32_t* nn;                  // [n] nearest dense neighbour within d_merge, or -1
+  unsigned long long* packed;   // [n] (keep << 32 | children), then its exclusive scan
+  unsigned long long* blk;      // [scan blocks] block totals
+  double* part;                 // [stat blocks][4] {sum rho, sum rho^2, sum d, sum d^2}
+  uint32_t* flags;              // [4] {points with < k neighbours within 6 r, ...}
+  bgs_density_report* rep;      // device copy of the report
+  int64_t stat_blocks, scan_blocks;
+};
+
+static bool step_layout(int64_t n, char* base, StepWs* w, size_t* total) {
+  size_t gtotal = 0;
+  if (!dens_layout(n, nullptr, nullptr, &gtotal)) return false;
+  const int64_t stat_blocks = 4 * 148, scan_blocks = (n + 1023) / 1024;
+  size_t o = dens_align(gtotal);
+  auto take = [&](size_t b) {
+    size_t at = o;
+    o = dens_align(o + b);
+    return at;
+  };
+  const size_t a_rho = take(4 * (size_t)n), a_dbar = take(8 * (size_t)n), a_nn = take(4 * (size_t)n),
+               a_pk = take(8 * (size_t)n), a_blk = take(8 * (size_t)(scan_blocks + 1)),
+               a_part = take(32 * (size_t)stat_blocks), a_fl = take(16), a_rep = take(sizeof(bgs_density_report));
+  if (total) *total = o;
+  if (w && base) {
+    dens_layout(n, base, &w->g, nullptr);
+    w->rho = (uint32_t*)(base + a_rho);
+    w->dbar = (double*)(base + a_dbar);
+    w->nn = (int32_t*)(base + a_nn);
+    w->packed = (unsigned long long*)(base + a_pk);
+    w->blk = (unsigned long long*)(base + a_blk);
+    w->part = (double*)(base + a_part);
+    w->flags = (uint32_t*)(base + a_fl);
+    w->rep = (bgs_density_report*)(base + a_rep);
+    w->stat_blocks = stat_blocks;
+    w->scan_blocks = scan_blocks;
+  }
+  return true;
+}
+
+__device__ __forceinline__ double sqd(const float* means, int64_t p, int64_t q) {
+  const double dx = (double)means[3 * q] - (double)means[3 * p];
+  const double dy = (double)means[3 * q + 1] - (double)means[3 * p + 1];
+  const double dz = (double)means[3 * q + 2] - (double)means[3 * p + 2];
+  return (dx * dx + dy * dy) + dz * dz;
+}
+
+// rho (27 cells, float decision) + the k nearest (double, rings until exact) per point;
+// per-block partial sums of rho, rho^2, the k distances and their squares.
+__global__ void __launch_bounds__(kStepThreads) k_rho_knn(int64_t n, const float* __restrict__ means, float inv_cs,
+                                                          float cs, float r2, float r_param, uint32_t mask, int k,
+                                                          const uint32_t* __restrict__ sval,
+                                                          const uint32_t* __restrict__ start,
+                                                          const uint32_t* __restrict__ end, uint32_t* rho_out,
+                                                          double* dbar, double* part, uint32_t* flags) {
+  double s_r = 0, s_r2 = 0, s_d = 0, s_d2 = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int cx, cy, cz;
+    cell_of(means, i, inv_cs, cx, cy, cz);
+    const float px = means[3 * i], py = means[3 * i + 1], pz = means[3 * i + 2];
+    // rho: the 27 neighbour buckets, each distinct bucket once
+    uint32_t seen[27];
+    int nseen = 0;
+    uint32_t c = 0;
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          const uint32_t h = cell_hash(cx + dx, cy + dy, cz + dz, mask);
+          bool dup = false;
+          for (int t = 0; t < nseen; ++t) dup |= seen[t] == h;
+          if (dup) continue;
+          seen[nseen++] = h;
+          const uint32_t e = end[h];
+          for (uint32_t j = start[h]; j < e; ++j) {
+            const uint32_t q = sval[j];
+            if (q == (uint32_t)i) continue;
+            const float ddx = means[3 * (int64_t)q] - px;
+            const float ddy = means[3 * (int64_t)q + 1] - py;
+            const float ddz = means[3 * (int64_t)q + 2] - pz;
+            if ((ddx * ddx + ddy * ddy) + ddz * ddz <= r2) ++c;
+          }
+        }
+    rho_out[i] = c;
+    s_r += (double)c;
+    s_r2 += (double)c * (double)c;
+    // kNN: sorted (d2, q) lists; a point reached through two colliding cells is inserted once
+    double bd[kKnnMax];
+    uint32_t bq[kKnnMax];
+    int nb = 0;
+    const int kk = (int)((int64_t)k < n - 1 ? (int64_t)k : n - 1);
+    bool exact = kk == 0;
+    for (int R = 0; R <= kMaxRing && !exact; ++R) {
+      for (int dz = -R; dz <= R; ++dz)
+        for (int dy = -R; dy <= R; ++dy)
+          for (int dx = -R; dx <= R; ++dx) {
+            if (max(abs(dx), max(abs(dy), abs(dz))) != R) continue;  // the shell of ring R
+            const uint32_t h = cell_hash(cx + dx, cy + dy, cz + dz, mask);
+            const uint32_t e = end[h];
+            for (uint32_t j = start[h]; j < e; ++j) {
+              const uint32_t q = sval[j];
+              if (q == (uint32_t)i) continue;
+              const double d2 = sqd(means, i, q);
+              if (nb == kk && (d2 > bd[kk - 1] || (d2 == bd[kk - 1] && q >= bq[kk - 1]))) continue;
+              bool dup = false;
+              for (int t = 0; t < nb; ++t) dup |= bq[t] == q;
+              if (dup) continue;
+              int pos = nb < kk ? nb++ : kk - 1;
+              while (pos > 0 && (bd[pos - 1] > d2 || (bd[pos - 1] == d2 && bq[pos - 1] > q))) {
+                bd[pos] = bd[pos - 1];
+                bq[pos] = bq[pos - 1];
+                --pos;
+              }
+              bd[pos] = d2;
+              bq[pos] = q;
+            }
+          }
+      // every point within R cells' reach (distance <= R cs) has been seen
+      const double reach = (double)R * (double)cs;
+      exact = nb == kk && bd[kk - 1] <= reach * reach;
+    }
+    // R32: distances truncated at the 6 r neighbourhood (every point within 6 r <= 6 cs was
+    // seen); a neighbour beyond it, or a missing one, counts as 6 r
+    const double cap = (double)kMaxRing * (double)r_param;
+    int short_k = 0;
+    double sum = 0.0;
+    for (int t = 0; t < kk; ++t) {
+      double d = cap;
+      if (t < nb && bd[t] <= cap * cap) d = sqrt(bd[t]);
+      else ++short_k;
+      sum += d;
+      s_d += d;
+      s_d2 += d * d;
+    }
+    if (short_k) atomicAdd(&flags[0], 1u);
+    dbar[i] = kk ? sum / (double)kk : 0.0;
+  }
+  __shared__ double s_p[4][kStepThreads / 32];
+  double v[4] = {s_r, s_r2, s_d, s_d2};
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[a] += __shfl_xor_sync(0xffffffffu, v[a], o);
+    if ((threadIdx.x & 31) == 0) s_p[a][threadIdx.x >> 5] = v[a];
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double t = 0;
+    for (int w = 0; w < kStepThreads / 32; ++w) t += s_p[threadIdx.x][w];
+    part[4 * blockIdx.x + threadIdx.x] = t;
+  }
+}
+
+// The statistics (R31-R32) into the device report: population sigma of rho and of the
+// pooled k-distances, the thresholds and d_merge.
+__global__ void k_step_stats(int64_t n, int k, int blocks, const double* part, bgs_density_params prm,
+                             bgs_density_report* rep) {
+  if (threadIdx.x != 0) return;
+  double S[4] = {0, 0, 0, 0};
+  for (int b = 0; b < blocks; ++b)
+    for (int a = 0; a < 4; ++a) S[a] += part[4 * b + a];
+  const double N = (double)n, M = (double)n * (double)(k < n - 1 ? k : n - 1);
+  rep->n_in = n;
+  rep->mu_rho = S[0] / N;
+  rep->sigma_rho = sqrt(fmax(0.0, S[1] / N - rep->mu_rho * rep->mu_rho));
+  rep->rho_low = rep->mu_rho - (double)prm.alpha * rep->sigma_rho;
+  rep->rho_high = rep->mu_rho + (double)prm.beta * rep->sigma_rho;
+  rep->mu_d = M > 0 ? S[2] / M : 0.0;
+  rep->sigma_d = M > 0 ? sqrt(fmax(0.0, S[3] / M - rep->mu_d * rep->mu_d)) : 0.0;
+  rep->d_merge = rep->mu_d + (double)prm.gamma * rep->sigma_d;
+}
+
+// R33: each dense point's nearest other dense point within d_merge (ties: lower index).
+__global__ void __launch_bounds__(kStepThreads) k_merge_nn(int64_t n, const float* __restrict__ means, float inv_cs,
+                                                           float cs, uint32_t mask, const uint32_t* __restrict__ sval,
+                                                           const uint32_t* __restrict__ start,
+                                                           const uint32_t* __restrict__ end,
+                                                           const uint32_t* __restrict__ rho,
+                                                           const bgs_density_report* rep, int32_t* nn) {
+  const double hi = rep->rho_high, dm = rep->d_merge, lim = dm * dm;
+  const int R = (int)ceil(dm / (double)cs);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int best = -1;
+    if ((double)rho[i] > hi) {
+      int cx, cy, cz;
+      cell_of(means, i, inv_cs, cx, cy, cz);
+      double bd = 0.0;
+      for (int dz = -R; dz <= R; ++dz)
+        for (int dy = -R; dy <= R; ++dy)
+          for (int dx = -R; dx <= R; ++dx) {
+            const uint32_t h = cell_hash(cx + dx, cy + dy, cz + dz, mask);
+            const uint32_t e = end[h];
+            for (uint32_t j = start[h]; j < e; ++j) {
+              const uint32_t q = sval[j];
+              if (q == (uint32_t)i || !((double)rho[q] > hi)) continue;
+              const double d2 = sqd(means, i, q);
+              if (d2 > lim) continue;
+              if (best < 0 || d2 < bd || (d2 == bd && (int)q < best)) {
+                bd = d2;
+                best = (int)q;
+              }
+            }
+          }
+    }
+    nn[i] = best;
+  }
+}
+
+// R33/R35: keep flag (not the higher member of a mutual pair) and children per point,
+// packed as keep << 32 | children for one scan.
+__global__ void __launch_bounds__(kStepThreads) k_step_flags(int64_t n, const int32_t* __restrict__ nn,
+                                                             const uint32_t* __restrict__ rho,
+                                                             const bgs_density_report* rep, int max_new,
+                                                             unsigned long long* packed) {
+  const double lo = rep->rho_low;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t q = nn[i];
+    const bool removed = q >= 0 && q < i && nn[q] == (int32_t)i;
+    uint32_t c = 0;
+    if (lo > 0.0 && (double)rho[i] < lo) c = (uint32_t)min((double)max_new, ceil(lo - (double)rho[i]));
+    packed[i] = ((unsigned long long)(removed ? 0u : 1u) << 32) | c;
+  }
+}
+
+// exclusive scan of packed (two 32-bit lanes, no carry between them): per-block scan,
+// one block scans the block totals, then the block offsets are added.
+__global__ void __launch_bounds__(1024) k_scan64_blocks(int64_t n, unsigned long long* v, unsigned long long* blk) {
+  __shared__ unsigned long long s_w[32];
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const unsigned long long x = i < n ? v[i] : 0ull;
+  unsigned long long inc = x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    unsigned long long t = s_w[lane], ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    s_w[lane] = ti - t;
+    if (lane == 31) blk[blockIdx.x] = ti;
+  }
+  __syncthreads();
+  if (i < n) v[i] = inc - x + s_w[w];
+}
+
+__global__ void k_scan64_top(int64_t nb, unsigned long long* blk, int64_t n, bgs_density_report* rep) {
+  if (threadIdx.x != 0) return;
+  unsigned long long run = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    const unsigned long long t = blk[b];
+    blk[b] = run;
+    run += t;
+  }
+  const int64_t keep = (int64_t)(run >> 32), kids = (int64_t)(run & 0xffffffffull);
+  rep->n_pairs = n - keep;
+  rep->n_children = kids;
+  rep->n_out = keep + kids;
+}
+
+__global__ void __launch_bounds__(1024) k_scan64_add(int64_t n, unsigned long long* v, const unsigned long long* blk) {
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  if (i < n) v[i] += blk[blockIdx.x];
+}
+
+struct ThetaView {  // theta's segments for a given count
+  const float *means, *ls, *q, *op, *sh;
+};
+__device__ __forceinline__ ThetaView tview(const float* t, int64_t n) {
+  return {t, t + 3 * n, t + 6 * n, t + 10 * n, t + 11 * n};
+}
+
+// R34-R36: the new theta / m / v (n_out Gaussians) in theta's segment layout.
+__global__ void __launch_bounds__(kStepThreads) k_step_emit(int64_t n, int64_t n_out, const float* __restrict__ th,
+                                                            const float* __restrict__ m, const float* __restrict__ v,
+                                                            const int32_t* __restrict__ nn,
+                                                            const unsigned long long* __restrict__ off,
+                                                            const double* __restrict__ dbar,
+                                                            const bgs_density_report* rep, const float* normals,
+                                                            const float* uniforms, bgs_density_params prm,
+                                                            float* th_o, float* m_o, float* v_o) {
+  const int64_t n_keep = n_out - rep->n_children;
+  const ThetaView I = tview(th, n), Mi = tview(m, n), Vi = tview(v, n);
+  float* const seg_o[3] = {th_o, m_o, v_o};
+  auto put = [&](int which, int64_t o, const float* mean, const float* ls, const float* q, float op, const float* sh) {
+    float* b = seg_o[which];
+    for (int a = 0; a < 3; ++a) b[3 * o + a] = mean[a];
+    for (int a = 0; a < 3; ++a) b[3 * n_out + 3 * o + a] = ls[a];
+    for (int a = 0; a < 4; ++a) b[6 * n_out + 4 * o + a] = q[a];
+    b[10 * n_out + o] = op;
+    for (int a = 0; a < 48; ++a) b[11 * n_out + 48 * o + a] = sh[a];
+  };
+  const float zero[48] = {};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long pk = off[i];
+    const int64_t o = (int64_t)(pk >> 32);
+    const uint32_t c0 = (uint32_t)(pk & 0xffffffffull);
+    const unsigned long long nx = i + 1 < n ? off[i + 1] : ((unsigned long long)n_keep << 32) | (unsigned long long)rep->n_children;
+    const bool keep = (nx >> 32) != (pk >> 32);
+    const uint32_t nc = (uint32_t)(nx & 0xffffffffull) - c0;
+    const int32_t q = nn[i];
+    if (keep) {
+      if (q > i && nn[q] == (int32_t)i) {  // the merged pair (i, q), kept at i (R34)
+        const double op = 1.0 / (1.0 + exp(-(double)I.op[i])), oq = 1.0 / (1.0 + exp(-(double)I.op[q]));
+        const double w = op + oq;
+        float mean[3], ls[3], sh[48];
+        for (int a = 0; a < 3; ++a) {
+          mean[a] = (float)((op * (double)I.means[3 * i + a] + oq * (double)I.means[3 * (int64_t)q + a]) / w);
+          ls[a] = (float)log(0.5 * (exp((double)I.ls[3 * i + a]) + exp((double)I.ls[3 * (int64_t)q + a])));
+        }
+        const float* quat = op >= oq ? I.q + 4 * i : I.q + 4 * (int64_t)q;
+        const double oo = fmin(0.999, w);
+        for (int a = 0; a < 48; ++a)
+          sh[a] = (float)((op * (double)I.sh[48 * i + a] + oq * (double)I.sh[48 * (int64_t)q + a]) / w);
+        put(0, o, mean, ls, quat, (float)log(oo / (1.0 - oo)), sh);
+        put(1, o, zero, zero, zero, 0.f, zero);
+        put(2, o, zero, zero, zero, 0.f, zero);
+      } else {
+        put(0, o, I.means + 3 * i, I.ls + 3 * i, I.q + 4 * i, I.op[i], I.sh + 48 * i);
+        put(1, o, Mi.means + 3 * i, Mi.ls + 3 * i, Mi.q + 4 * i, Mi.op[i], Mi.sh + 48 * i);
+        put(2, o, Vi.means + 3 * i, Vi.ls + 3 * i, Vi.q + 4 * i, Vi.op[i], Vi.sh + 48 * i);
+      }
+    }
+    // R35: children of a sparse point, numbered in (parent, j) order
+    const double sig = (double)prm.alpha_sigma * dbar[i];
+    for (uint32_t j = 0; j < nc; ++j) {
+      const int64_t ci = (int64_t)c0 + j;
+      float mean[3];
+      for (int a = 0; a < 3; ++a)
+        mean[a] = (float)((double)I.means[3 * i + a] + sig * (double)normals[3 * ci + a] +
+                          (double)prm.delta * (double)uniforms[3 * ci + a]);
+      const int64_t oc = n_keep + ci;
+      put(0, oc, mean, I.ls + 3 * i, I.q + 4 * i, I.op[i], I.sh + 48 * i);
+      put(1, oc, zero, zero, zero, 0.f, zero);
+      put(2, oc, zero, zero, zero, 0.f, zero);
+    }
+  }
+}
+
 }  // namespace bgs
 
 using namespace bgs;
@@ -209,6 +570,104 @@ bgs_status bgs_local_density(const float* means, int64_t n, float r, float alpha
   k_density_finish<<<1, 1, 0, s>>>(n, w.sums, alpha, beta, stats);
   note_launch();
   return check_launch("k_density_finish");
+}
+
+
+size_t bgs_density_step_workspace_bytes(int64_t n) {
+  size_t total = 0;
+  return step_layout(n, nullptr, nullptr, &total) ? total : 0;
+}
+
+static bool params_ok(const bgs_density_params* p) {
+  return p && p->r > 0.0f && p->alpha >= 0.0f && p->beta >= 0.0f && p->gamma >= 0.0f && p->alpha_sigma > 0.0f &&
+         p->delta >= 0.0f && p->k >= 1 && p->k <= kKnnMax && p->max_new >= 0 && p->max_new <= 64;
+}
+
+bgs_status bgs_density_plan(const float* theta, int64_t n, const bgs_density_params* p, void* workspace, size_t bytes,
+                            void* stream) {
+  StepWs w;
+  size_t total = 0;
+  if (!theta || !workspace || !params_ok(p) || ((uintptr_t)workspace & 255u) ||
+      !step_layout(n, (char*)workspace, &w, &total) || bytes < total)
+    return BGS_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  const float* means = theta;  // theta's first segment
+  const float cs = p->r * 1.0001f, inv_cs = 1.0f / cs;
+  const uint32_t mask = w.g.M - 1;
+  if (cudaMemsetAsync(w.g.hist, 0, 4 * 4 * kDensBins, s) != cudaSuccess ||
+      cudaMemsetAsync(w.g.counters, 0, 4 * 32, s) != cudaSuccess ||
+      cudaMemsetAsync(w.g.start, 0, 4 * (size_t)w.g.M, s) != cudaSuccess ||
+      cudaMemsetAsync(w.g.end, 0, 4 * (size_t)w.g.M, s) != cudaSuccess ||
+      cudaMemsetAsync(w.flags, 0, 16, s) != cudaSuccess ||
+      cudaMemsetAsync(w.rep, 0, sizeof(bgs_density_report), s) != cudaSuccess)
+    return check_launch("density step memset");
+  const int grid = 4 * num_sms();
+  k_cell_keys<<<grid, 256, 0, s>>>(n, means, inv_cs, mask, w.g.key[0], w.g.val[0], w.g.hist);
+  note_launch();
+  bgs_status st = check_launch("k_cell_keys");
+  if (st != BGS_OK) return st;
+  const int passes = (int)((w.g.bits + 7) / 8);
+  for (int q = 0; q < passes; ++q) {
+    if (cudaMemsetAsync(w.g.status, 0, 4 * 256 * (size_t)w.g.status_tiles, s) != cudaSuccess)
+      return check_launch("density status memset");
+    const int a = q & 1, b = (q + 1) & 1;
+    st = launch_sort_pass32(w.g.key[a], w.g.val[a], w.g.key[b], w.g.val[b], w.g.hist + q * kDensBins, w.g.status,
+                            w.g.counters + 1 + q, w.g.counters + 8, 8 * q, n, s);
+    if (st != BGS_OK) return st;
+  }
+  const int fb = passes & 1;
+  k_bucket_ranges<<<grid, 256, 0, s>>>(n, w.g.key[fb], w.g.start, w.g.end);
+  note_launch();
+  if ((st = check_launch("k_bucket_ranges")) != BGS_OK) return st;
+  k_rho_knn<<<(int)w.stat_blocks, kStepThreads, 0, s>>>(n, means, inv_cs, cs, p->r * p->r, p->r, mask, p->k,
+                                                        w.g.val[fb],
+                                                        w.g.start, w.g.end, w.rho, w.dbar, w.part, w.flags);
+  note_launch();
+  if ((st = check_launch("k_rho_knn")) != BGS_OK) return st;
+  k_step_stats<<<1, 32, 0, s>>>(n, p->k, (int)w.stat_blocks, w.part, *p, w.rep);
+  note_launch();
+  if ((st = check_launch("k_step_stats")) != BGS_OK) return st;
+  k_merge_nn<<<grid, kStepThreads, 0, s>>>(n, means, inv_cs, cs, mask, w.g.val[fb], w.g.start, w.g.end, w.rho, w.rep,
+                                          w.nn);
+  note_launch();
+  if ((st = check_launch("k_merge_nn")) != BGS_OK) return st;
+  k_step_flags<<<grid, kStepThreads, 0, s>>>(n, w.nn, w.rho, w.rep, p->max_new, w.packed);
+  note_launch();
+  if ((st = check_launch("k_step_flags")) != BGS_OK) return st;
+  k_scan64_blocks<<<(int)w.scan_blocks, 1024, 0, s>>>(n, w.packed, w.blk);
+  note_launch();
+  k_scan64_top<<<1, 32, 0, s>>>(w.scan_blocks, w.blk, n, w.rep);
+  note_launch();
+  k_scan64_add<<<(int)w.scan_blocks, 1024, 0, s>>>(n, w.packed, w.blk);
+  note_launch();
+  return check_launch("density step scan");
+}
+
+bgs_status bgs_density_result(const void* workspace, int64_t n, bgs_density_report* out, uint32_t* short_knn) {
+  StepWs w;
+  if (!workspace || !out || !step_layout(n, (char*)workspace, &w, nullptr)) return BGS_ERR_INVALID;
+  if (cudaMemcpy(out, w.rep, sizeof(bgs_density_report), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return check_launch("bgs_density_result");
+  if (short_knn && cudaMemcpy(short_knn, w.flags, 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return check_launch("bgs_density_result");
+  return BGS_OK;
+}
+
+bgs_status bgs_density_apply(const float* theta, const float* exp_avg, const float* exp_avg_sq, int64_t n,
+                             const void* workspace, const bgs_density_params* p, const float* normals,
+                             const float* uniforms, int64_t n_children, float* theta_out, float* exp_avg_out,
+                             float* exp_avg_sq_out, int64_t n_out, void* stream) {
+  StepWs w;
+  if (!theta || !exp_avg || !exp_avg_sq || !workspace || !params_ok(p) || !theta_out || !exp_avg_out ||
+      !exp_avg_sq_out || n_out < 1 || n_children < 0 || (n_children > 0 && (!normals || !uniforms)) ||
+      !step_layout(n, (char*)workspace, &w, nullptr))
+    return BGS_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_step_emit<<<4 * num_sms(), kStepThreads, 0, s>>>(n, n_out, theta, exp_avg, exp_avg_sq, w.nn, w.packed, w.dbar,
+                                                     w.rep, normals, uniforms, *p, theta_out, exp_avg_out,
+                                                     exp_avg_sq_out);
+  note_launch();
+  return check_launch("k_step_emit");
 }
 
 }  // extern "C"

@@ -53,3 +53,53 @@ def test_density_on_theta_means_segment(bgs):
     counts, _ = bgs.bgs_local_density(theta[: 3 * s.n], 0.05)
     ref = oracle.local_density(gen.segments(s.theta, s.n)["means"], 0.05)
     assert np.array_equal(counts.cpu().numpy().view(np.uint32), ref)
+
+
+# ------------------------------------------------------------------ the density-control step
+def _step_fixtures():
+    r = np.random.default_rng(11)
+    clustered = np.concatenate([r.normal(0, 0.05, (600, 3)), r.uniform(-1.5, 1.5, (60, 3))])
+    contrast = np.concatenate([r.uniform(0, 1, (2500, 3)), r.uniform(0, 1, (25, 3)) + [1.5, 0, 0]])
+    s = gen.garden(seed=3, n=3000, n_cams=1)
+    garden = gen.segments(s.theta, s.n)["means"]
+    return {"clustered": (clustered, 0.05), "contrast": (contrast, None), "garden3k": (garden, None)}
+
+
+@pytest.mark.parametrize("name", list(_step_fixtures()))
+def test_density_step_parity(bgs, name):
+    from oracle import density as D
+
+    pts, rad = _step_fixtures()[name]
+    pts = np.ascontiguousarray(pts, np.float32)
+    r = np.random.default_rng(12)
+    n = pts.shape[0]
+    theta = np.concatenate([pts.ravel(), r.normal(np.log(0.01), 0.1, 3 * n), r.normal(0, 1, 4 * n),
+                            r.normal(0, 2, n), r.normal(0, 0.2, 48 * n)]).astype(np.float32)
+    m = r.normal(0, 1, 59 * n).astype(np.float32)
+    v = r.random(59 * n).astype(np.float32)
+    if rad is None:
+        rad = float(np.median(D.knn(pts, 8)[0][:, -1]))  # r = median 8-NN distance
+    prm = bgs.DensityParams(rad)
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(5)
+    th2, m2, v2, n2, rep, short, (z, u) = bgs.density_control(
+        torch.from_numpy(theta).to(dev), torch.from_numpy(m).to(dev), torch.from_numpy(v).to(dev), n, prm, g)
+    torch.cuda.synchronize()
+    print(name, "points with < 8 neighbours within 6 r:", short)
+    st = D.stats(theta, n, r=float(np.float32(rad)), k=8)
+    for key, got in (("mu_rho", rep.mu_rho), ("sigma_rho", rep.sigma_rho), ("rho_low", rep.rho_low),
+                     ("rho_high", rep.rho_high), ("mu_d", rep.mu_d), ("sigma_d", rep.sigma_d),
+                     ("d_merge", rep.d_merge)):
+        assert abs(got - st[key]) <= 1e-12 * max(1.0, abs(st[key])), (key, got, st[key])
+    pairs = D.merge_pairs(theta, n, st)
+    c = D.child_counts(st, n, max_new=4)
+    assert rep.n_pairs == len(pairs) and rep.n_children == int(c.sum()) and n2 == rep.n_out
+    th_ref, m_ref, v_ref, n_ref = D.apply(theta, m, v, n, st, pairs, c, z.cpu().numpy().astype(np.float64),
+                                          u.cpu().numpy().astype(np.float64), alpha_sigma=1.5,
+                                          delta=float(np.float32(0.1 * np.float32(rad))))
+    assert n2 == n_ref
+    print(name, "n", n, "->", n2, "pairs", len(pairs), "children", int(c.sum()))
+    np.testing.assert_allclose(th2.cpu().numpy(), th_ref, rtol=2e-6, atol=1e-6)
+    np.testing.assert_array_equal(m2.cpu().numpy(), m_ref)
+    np.testing.assert_array_equal(v2.cpu().numpy(), v_ref)
