@@ -47,6 +47,8 @@ def parse():
     p.add_argument("--views", type=int, default=16)
     p.add_argument("--num-gaussians", dest="n", type=int, default=None,
                    help="override the Gaussian count (debug only)")
+    p.add_argument("--density-every", type=int, default=0,
+                   help="run the NEXT-1 density-control step every D training steps (configs[4]; 0 = off)")
     p.add_argument("--update", default="sharded", choices=["sharded", "allreduce"],
                    help="G > 1: reduce-scatter + Adam on a 1/G shard + all-gather (default), or all-reduce + "
                         "full Adam on every rank")
@@ -78,7 +80,8 @@ def arm_config(scene, args, world):
                         f"{'reduce-scatter + sharded Adam + all-gather' if world > 1 and args.update == 'sharded' else 'all-reduce + Adam'})",
             "views_per_step": args.views, "n_gaussians": scene.n, "width": cam.width, "height": cam.height,
             "parallelism": f"view-dp{world}", "l2": "inputs larger than L2 (theta 1.37 GB, keys > 126 MB)",
-            "loss": "0.8 L1 + 0.2 D-SSIM (11x11 Gaussian window)" if args.loss == "l1dssim" else "L1"}
+            "loss": "0.8 L1 + 0.2 D-SSIM (11x11 Gaussian window)" if args.loss == "l1dssim" else "L1",
+            "density_every": args.density_every}
 
 
 def _device_index(local_rank):
@@ -220,16 +223,91 @@ def run_ours(args, rank, world, local_rank):
     scale = 1.0 / (3.0 * W * H * args.views)
     loss_ws = (torch.empty(bgs.bgs_loss_workspace_bytes(W, H), dtype=torch.uint8, device=dev)
                if args.loss == "l1dssim" else None)
-    gs = bgs.gaussians(theta, n, deg)
-    frames = [rj.frame for rj in rends]
     cam_structs = [bgs.camera(c) for c in cams]
     stream = torch.cuda.current_stream()
     stage_names = ["preprocess", "sort", "render_fwd", "loss", "blend_bwd", "preprocess_bwd", "allreduce", "adam"]
+    if args.density_every:
+        stage_names.append("density")
     # all timing events of the timed region are created up front (creating them inside the
     # loop adds host work between launches)
-    n_marks = args.steps * (7 * len(cam_structs) + 5)
+    n_marks = args.steps * (7 * len(cam_structs) + 7)
     pool = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
     step_no = [0]
+
+    # the training state; the periodic density-control step (NEXT-1, --density-every)
+    # replaces it with one of another size
+    S = {"theta": theta, "grad": grad, "m": m, "v": v, "n": n, "rends": rends,
+         "lo": sh_lo if sharded else 0, "hi": sh_hi if sharded else 59 * n}
+
+    def derive():
+        S["gs"] = bgs.gaussians(S["theta"][:59 * S["n"]], S["n"], deg)  # (sharded: theta is padded)
+        S["frames"] = [rj.frame for rj in S["rends"]]
+
+    derive()
+    del theta, grad, m, v, rends
+    dens_prm = None
+    dens_log = []
+    if args.density_every:
+        # r = the median 8-NN distance of the initial scene, estimated from a
+        # 100k-point sample (8-NN distances scale as (sample / n)^(1/3) under thinning)
+        from scipy.spatial import cKDTree
+
+        mu = gen.segments(scene.theta, n)["means"]
+        sub = mu[gen.rng(77).choice(n, min(n, 100_000), replace=False)].astype(np.float64)
+        d8 = cKDTree(sub).query(sub, k=9)[0][:, 8]
+        dens_prm = bgs.DensityParams(float(np.median(d8) * (len(sub) / n) ** (1.0 / 3.0)))
+
+    def rebuild(theta_full, m_full, v_full, n_new, max_keys):
+        # theta / Adam moments of n_new Gaussians (unpadded 59 n_new) into the layout of this
+        # run (sharded: padded theta and grad, moments of this rank's shard), new frames
+        tot = 59 * n_new
+        old = S.pop("rends")
+        S.pop("frames", None)
+        del old
+        if sharded:
+            shard, padded = dp.shard_layout(tot, world)
+            lo, hi = dp.shard_range(rank, world, tot)
+            th = torch.zeros(padded, dtype=torch.float32, device=dev)
+            th[:tot].copy_(theta_full)
+            mm = torch.zeros(padded, dtype=torch.float32, device=dev)
+            vv = torch.zeros(padded, dtype=torch.float32, device=dev)
+            mm[:tot].copy_(m_full)
+            vv[:tot].copy_(v_full)
+            S["m"], S["v"] = mm[lo:hi].clone(), vv[lo:hi].clone()
+            S["lo"], S["hi"] = lo, hi
+        else:
+            th = theta_full.clone()
+            S["m"], S["v"] = m_full.clone(), v_full.clone()
+            S["lo"], S["hi"] = 0, tot
+        S["theta"], S["grad"], S["n"] = th, torch.zeros_like(th), n_new
+        r0 = bgs.Renderer(n_new, W, H, max_keys=max_keys, device=dev)
+        S["rends"] = [r0] + [r0 if args.one_frame else bgs.Renderer(n_new, W, H, max_keys=max_keys, device=dev)
+                             for _ in cams[1:]]
+        derive()
+
+    def full_moments():
+        tot = 59 * S["n"]
+        if not sharded:
+            return S["m"][:tot], S["v"][:tot]
+        shard, padded = dp.shard_layout(tot, world)
+        mf = torch.empty(padded, dtype=torch.float32, device=dev)
+        vf = torch.empty(padded, dtype=torch.float32, device=dev)
+        dist.all_gather_into_tensor(mf, S["m"])
+        dist.all_gather_into_tensor(vf, S["v"])
+        return mf[:tot], vf[:tot]
+
+    def density_step():
+        # NEXT-1 (§III-C): the same deterministic step on every rank (identical
+        # theta and moments, the variates from a generator seeded by the step number)
+        n0 = S["n"]
+        mf, vf = full_moments()
+        g = torch.Generator(device=dev)
+        g.manual_seed(1000 + step_no[0])
+        th2, m2, v2, n2, rep, _, _ = bgs.density_control(S["theta"][:59 * n0], mf, vf, n0, dens_prm, g)
+        mk = int(S["rends"][0].max_keys * max(1.0, n2 / n0)) + 4096
+        rebuild(th2, m2, v2, n2, mk)
+        dens_log.append({"step": step_no[0], "n_before": n0, "n_after": n2, "pairs": int(rep.n_pairs),
+                         "children": int(rep.n_children)})
 
     def one_step(tgts, record=None):
         step_no[0] += 1
@@ -241,8 +319,9 @@ def run_ours(args, rank, world, local_rank):
                 e.record(stream)
                 marks.append(e)
 
+        gs, grad, frames = S["gs"], S["grad"], S["frames"]
         for j, cs in enumerate(cam_structs):
-            rj = rends[j]
+            rj = S["rends"][j]
             marks = []
             mark(marks)
             bgs.bgs_preprocess(gs, cs, rj.frame)
@@ -268,10 +347,11 @@ def run_ours(args, rank, world, local_rank):
         if not args.one_frame:  # a10 once over the batch's views: theta/grad cross HBM once
             bgs.bgs_preprocess_bwd_batch(gs, frames, grad)
         mark(marks)
+        theta, m, v, n, lo, hi = S["theta"], S["m"], S["v"], S["n"], S["lo"], S["hi"]
         if sharded:  # NCCL over NVLink: reduce-scatter, Adam on the shard, all-gather
             g_shard = dp.reduce_scatter_grads(grad, rank, world)
             mark(marks)
-            bgs.bgs_adam_step_range(theta[sh_lo:sh_hi], g_shard, m, v, n, sh_lo, sh_hi - sh_lo, hp, step_no[0])
+            bgs.bgs_adam_step_range(theta[lo:hi], g_shard, m, v, n, lo, hi - lo, hp, step_no[0])
             bgs.bgs_zero(grad)  # the rest of grad still holds this rank's partial sums
             mark(marks)
             dp.all_gather_params(theta, rank, world)
@@ -280,6 +360,9 @@ def run_ours(args, rank, world, local_rank):
             mark(marks)
             bgs.bgs_adam_step(theta, grad, m, v, n, hp, step_no[0])
             mark(marks)
+        mark(marks)
+        if args.density_every and step_no[0] % args.density_every == 0:
+            density_step()  # periodic (configs[4]); changes n
         mark(marks)
         if record is not None:
             record["marks"].append(("batch", marks))
@@ -295,7 +378,11 @@ def run_ours(args, rank, world, local_rank):
 
     # the step trains theta (Adam), which changes the workload; the e2e loop restarts from
     # this snapshot so both loops time the same sequence of training states
-    snap = (theta.clone(), m.clone(), v.clone(), step_no[0]) if not args.no_e2e else None
+    snap = None
+    if not args.no_e2e:
+        mf, vf = full_moments()
+        snap = (S["theta"][:59 * S["n"]].clone(), mf.clone(), vf.clone(), S["n"], step_no[0],
+                S["rends"][0].max_keys)
 
     # ---- device-resident timed region (inputs larger than L2: theta 1.37 GB, keys GBs)
     record = {"next": 0, "marks": []}
@@ -315,7 +402,7 @@ def run_ours(args, rank, world, local_rank):
     barrier()
     launches = bgs.launch_count() - launches0
     ms_local = t0.elapsed_time(t1)
-    for rj in rends:
+    for rj in S["rends"]:
         st, k_last = bgs.bgs_frame_status(rj.frame)
         assert st == bgs.BGS_OK, "key capacity overflow in the timed region"
     # per-stage means
@@ -328,6 +415,8 @@ def run_ours(args, rank, world, local_rank):
             sums["preprocess_bwd"] += mk[0].elapsed_time(mk[1])
             sums["allreduce"] += mk[1].elapsed_time(mk[2]) + mk[3].elapsed_time(mk[4])
             sums["adam"] += mk[2].elapsed_time(mk[3])
+            if args.density_every:
+                sums["density"] += mk[4].elapsed_time(mk[5])
     per_step = {s: sums[s] / args.steps for s in stage_names}
 
 
@@ -341,11 +430,8 @@ def run_ours(args, rank, world, local_rank):
             loss_host.copy_(loss, non_blocking=True)
 
         e2e_step()  # warm-up of the copy path
-        theta.copy_(snap[0])
-        m.copy_(snap[1])
-        v.copy_(snap[2])
-        step_no[0] = snap[3]
-        grad.zero_()
+        rebuild(snap[0], snap[1], snap[2], snap[3], snap[5])  # the pre-timing training state
+        step_no[0] = snap[4]
         del snap
         torch.cuda.synchronize()
         barrier()
@@ -369,7 +455,8 @@ def run_ours(args, rank, world, local_rank):
     # ---- workload counters (not timed) for the roofline numerators
     stats = {"visible": 0, "num_keys": 0, "evals_fwd": 0, "evals_bwd": 0, "evals_slot": 0, "max_list": 0,
              "blended": 0, "evals_fwd_culled": 0, "evals_bwd_culled": 0}
-    for rj, cs in zip(rends, cam_structs):
+    gs, n = S["gs"], S["n"]
+    for rj, cs in zip(S["rends"], cam_structs):
         bgs.bgs_preprocess(gs, cs, rj.frame)
         bgs.bgs_sort(rj.frame)
         bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
@@ -410,7 +497,7 @@ def run_ours(args, rank, world, local_rank):
     # what the blend kernels must evaluate: list entries whose alpha >= 1/255 box reaches the
     # pixel's warp block (exact skip of the rest)
     Efc, Ebc = stats["evals_fwd_culled"] / steps_views, stats["evals_bwd_culled"] / steps_views
-    frame_v = rend.views()
+    frame_v = S["rends"][0].views()
     passes = frame_v.sort_passes
 
     def frac(stage, achieved, peak, unit, bound):
@@ -473,6 +560,9 @@ def run_ours(args, rank, world, local_rank):
                      "E_slot_over_E_f_culled": stats["evals_slot"] / max(1, stats["evals_fwd_culled"]),
                      "max_tile_list": stats["max_list"]},
         "e2e": e2e, "cpu_baseline": cpu,
+        "density": None if not args.density_every else {
+            "every": args.density_every, "r": round(float(dens_prm.r), 6), "events_timed_and_e2e": dens_log,
+            "n_final": S["n"]},
     }
     print(json.dumps(line), flush=True)
 

@@ -260,14 +260,14 @@ typedef struct {      /* filled on the device by bgs_density_plan */
 size_t bgs_density_step_workspace_bytes(int64_t n);
 /* Plan (asynchronous): on theta[59n] (device; the means segment is read): rho and the k
  * nearest neighbours per point (exact; rings of grid cells), the statistics and d_merge
- * (R31-R32; neighbour distances truncated at 6 r), mutual-nearest dense pairs within d_merge (R33), the children of sparse points
+ * (R31-R32; neighbour distances truncated at 3 r), mutual-nearest dense pairs within d_merge (R33), the children of sparse points
  * (R35), the output offsets and n_out -- all kept in the workspace (device, 256-byte
  * aligned, >= bgs_density_step_workspace_bytes(n)). */
 bgs_status bgs_density_plan(const float* theta, int64_t n, const bgs_density_params* p /*host*/, void* workspace,
                             size_t bytes, void* stream);
 /* After the caller synchronised the plan's stream: the report (host out; n_out and
  * n_children size the apply call's buffers) and the number of points with fewer than k
- * neighbours within 6 r (their missing distances count as 6 r, R32). */
+ * neighbours within 3 r (their missing distances count as 3 r, R32). */
 bgs_status bgs_density_result(const void* workspace, int64_t n, bgs_density_report* out /*host*/,
                               uint32_t* short_knn /*host, may be NULL*/);
 /* Apply (asynchronous): theta_out / exp_avg_out / exp_avg_sq_out [59 n_out] (device) =

@@ -10,7 +10,7 @@ Readings (R31-R36):
   R31  rho(p) = #{q != p : |q - p| <= r} (the C++ oracle's float decision, orc_local_density);
        rho_low / rho_high = mu -/+ alpha / beta sigma over all rho (population sigma).
   R32  neighbour distances: each point's k = 8 nearest other points (double, ties by index),
-       each truncated at 6 r (a neighbour farther than 6 r, or a missing one, counts as 6 r:
+       each truncated at 3 r (a neighbour farther than 3 r, or a missing one, counts as 3 r:
        the search stays inside a fixed neighbourhood of the density grid, and an isolated
        point's densification spread stays bounded); d_bar_p = their mean; mu_d,
        sigma_d over all n k truncated distances pooled; d_merge = mu_d + gamma
@@ -76,9 +76,9 @@ def stats(theta, n, r, alpha=1.0, beta=1.0, gamma=1.0, k=8):
     rho = oracle.local_density(s["means"], r).astype(np.int64)
     th = oracle.density_thresholds(rho, alpha, beta)
     dist, _ = knn(s["means"], k)
-    cap = 6.0 * float(np.float32(r))
+    cap = 3.0 * float(np.float32(r))
     dist = np.minimum(dist, cap)
-    if dist.shape[1] < k:  # fewer than k other points: the missing ones count as 6 r
+    if dist.shape[1] < k:  # fewer than k other points: the missing ones count as 3 r
         dist = np.concatenate([dist, np.full((dist.shape[0], k - dist.shape[1]), cap)], 1)
     mu_d = float(dist.mean())
     sd_d = float(np.sqrt(((dist - mu_d) ** 2).mean()))

@@ -296,7 +296,7 @@ def density_control(theta, exp_avg, exp_avg_sq, n, params: DensityParams, genera
     read of the report (n_out sizes the new buffers), the method's random draws
     (N(0,1) / U(-1,1) variates, torch generator on the device), apply.  Returns
     (theta', exp_avg', exp_avg_sq', n', report, short_knn, (normals, uniforms)), short_knn =
-    points with fewer than k neighbours within 6 r (R32)."""
+    points with fewer than k neighbours within 3 r (R32)."""
     dev = theta.device
     nbytes = int(_lib.bgs_density_step_workspace_bytes(n))
     if nbytes == 0:

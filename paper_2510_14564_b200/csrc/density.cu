@@ -161,15 +161,15 @@ __global__ void k_density_finish(int64_t n, const unsigned long long* sums, floa
 
 // ============================================================================ density step
 // NEXT-1, the rest of T1 (§III-C2-C4 l.188-228; readings R31-R36 in DESIGN.md §3):
-// per point rho (as above) and its k nearest neighbours within 6 r (rings of grid cells are
-// added until the k-th candidate lies within the searched radius, at most 6 rings; distances
-// beyond 6 r count as 6 r, R32),
+// per point rho (as above) and its k nearest neighbours within 3 r (rings of grid cells are
+// added until the k-th candidate lies within the searched radius, at most 3 rings; distances
+// beyond 3 r count as 3 r, R32),
 // the pooled neighbour-distance statistics and d_merge, mutual-nearest dense pairs within
 // d_merge, the densification deficit of sparse points, and the compaction of the new
 // theta / Adam moments.  Distances for kNN and merging are squared in double from the float
 // coordinates ((dx^2 + dy^2) + dz^2, dx exact), with ties by the lower index -- the oracle's
 // (oracle/density.py) decisions.
-constexpr int kKnnMax = 16, kMaxRing = 6, kStepThreads = 256;
+constexpr int kKnnMax = 16, kMaxRing = 3, kStepThreads = 256;
 
 struct StepWs {
   DensityWs g;                  // the hashed grid (cell size r * 1.0001)
@@ -179,7 +179,7 @@ struct StepWs {
   unsigned long long* packed;   // [n] (keep << 32 | children), then its exclusive scan
   unsigned long long* blk;      // [scan blocks] block totals
   double* part;                 // [stat blocks][4] {sum rho, sum rho^2, sum d, sum d^2}
-  uint32_t* flags;              // [4] {points with < k neighbours within 6 r, ...}
+  uint32_t* flags;              // [4] {points with < k neighbours within 3 r, ...}
   bgs_density_report* rep;      // device copy of the report
   int64_t stat_blocks, scan_blocks;
 };
@@ -259,7 +259,9 @@ __global__ void __launch_bounds__(kStepThreads) k_rho_knn(int64_t n, const float
     rho_out[i] = c;
     s_r += (double)c;
     s_r2 += (double)c * (double)c;
-    // kNN: sorted (d2, q) lists; a point reached through two colliding cells is inserted once
+    // kNN: sorted (d2, q) lists; a point reached through two colliding cells is inserted once.
+    // Ring R = the shell of cells at Chebyshev distance R; after rings 0..R every point within
+    // R cs of p has been seen.
     double bd[kKnnMax];
     uint32_t bq[kKnnMax];
     int nb = 0;
@@ -294,8 +296,8 @@ __global__ void __launch_bounds__(kStepThreads) k_rho_knn(int64_t n, const float
       const double reach = (double)R * (double)cs;
       exact = nb == kk && bd[kk - 1] <= reach * reach;
     }
-    // R32: distances truncated at the 6 r neighbourhood (every point within 6 r <= 6 cs was
-    // seen); a neighbour beyond it, or a missing one, counts as 6 r
+    // R32: distances truncated at the 3 r neighbourhood (every point within 3 r <= 3 cs was
+    // seen); a neighbour beyond it, or a missing one, counts as 3 r
     const double cap = (double)kMaxRing * (double)r_param;
     int short_k = 0;
     double sum = 0.0;
@@ -360,22 +362,29 @@ __global__ void __launch_bounds__(kStepThreads) k_merge_nn(int64_t n, const floa
       int cx, cy, cz;
       cell_of(means, i, inv_cs, cx, cy, cz);
       double bd = 0.0;
-      for (int dz = -R; dz <= R; ++dz)
-        for (int dy = -R; dy <= R; ++dy)
-          for (int dx = -R; dx <= R; ++dx) {
-            const uint32_t h = cell_hash(cx + dx, cy + dy, cz + dz, mask);
-            const uint32_t e = end[h];
-            for (uint32_t j = start[h]; j < e; ++j) {
-              const uint32_t q = sval[j];
-              if (q == (uint32_t)i || !((double)rho[q] > hi)) continue;
-              const double d2 = sqd(means, i, q);
-              if (d2 > lim) continue;
-              if (best < 0 || d2 < bd || (d2 == bd && (int)q < best)) {
-                bd = d2;
-                best = (int)q;
+      // rings of cells outwards; after ring R every point within R cs has been seen, so the
+      // search stops once the best candidate lies within that reach (or at d_merge's ring)
+      for (int Rg = 0; Rg <= R; ++Rg) {
+        for (int dz = -Rg; dz <= Rg; ++dz)
+          for (int dy = -Rg; dy <= Rg; ++dy)
+            for (int dx = -Rg; dx <= Rg; ++dx) {
+              if (max(abs(dx), max(abs(dy), abs(dz))) != Rg) continue;
+              const uint32_t h = cell_hash(cx + dx, cy + dy, cz + dz, mask);
+              const uint32_t e = end[h];
+              for (uint32_t j = start[h]; j < e; ++j) {
+                const uint32_t q = sval[j];
+                if (q == (uint32_t)i || !((double)rho[q] > hi)) continue;
+                const double d2 = sqd(means, i, q);
+                if (d2 > lim) continue;
+                if (best < 0 || d2 < bd || (d2 == bd && (int)q < best)) {
+                  bd = d2;
+                  best = (int)q;
+                }
               }
             }
-          }
+        const double reach = (double)Rg * (double)cs;
+        if (best >= 0 && bd <= reach * reach) break;
+      }
     }
     nn[i] = best;
   }

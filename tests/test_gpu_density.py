@@ -86,7 +86,7 @@ def test_density_step_parity(bgs, name):
     th2, m2, v2, n2, rep, short, (z, u) = bgs.density_control(
         torch.from_numpy(theta).to(dev), torch.from_numpy(m).to(dev), torch.from_numpy(v).to(dev), n, prm, g)
     torch.cuda.synchronize()
-    print(name, "points with < 8 neighbours within 6 r:", short)
+    print(name, "points with < 8 neighbours within 3 r:", short)
     st = D.stats(theta, n, r=float(np.float32(rad)), k=8)
     for key, got in (("mu_rho", rep.mu_rho), ("sigma_rho", rep.sigma_rho), ("rho_low", rep.rho_low),
                      ("rho_high", rep.rho_high), ("mu_d", rep.mu_d), ("sigma_d", rep.sigma_d),

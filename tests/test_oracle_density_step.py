@@ -39,14 +39,14 @@ def test_knn_matches_kdtree():
     np.testing.assert_allclose(dist, d[:, 1:], rtol=1e-12)
     assert (idx == i[:, 1:]).mean() > 0.999  # identical up to exact distance ties
     th, n = _theta(pts)
-    st = D.stats(th, n, r=0.6)  # 6 r = 3.6 exceeds every 8-NN distance of this cloud
+    st = D.stats(th, n, r=1.2)  # 3 r = 3.6 exceeds every 8-NN distance of this cloud
     assert d[:, 1:].max() < 3.6
     assert abs(st["mu_d"] - d[:, 1:].mean()) < 1e-12
     assert abs(st["d_merge"] - (st["mu_d"] + st["sigma_d"])) < 1e-15  # gamma = 1
     np.testing.assert_allclose(st["d_bar"], oracle.knn_mean_distance(pts, 8), rtol=1e-12)
-    # R32's truncation at 6 r (r = 0.1: many 8-NN distances exceed 0.6)
-    st2 = D.stats(th, n, r=0.1)
-    cap = 6 * float(np.float32(0.1))
+    # R32's truncation at 3 r (r = 0.2: many 8-NN distances exceed 0.6)
+    st2 = D.stats(th, n, r=0.2)
+    cap = 3 * float(np.float32(0.2))
     dt = np.minimum(d[:, 1:], cap)
     assert (d[:, 1:] > cap).any()
     np.testing.assert_allclose(st2["d_bar"], dt.mean(1), rtol=1e-12)
