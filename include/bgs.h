@@ -280,6 +280,32 @@ bgs_status bgs_density_apply(const float* theta, const float* exp_avg, const flo
                              const float* uniforms, int64_t n_children, float* theta_out, float* exp_avg_out,
                              float* exp_avg_sq_out, int64_t n_out, void* stream);
 
+/* ---------------------------------------------------------------- NEXT-3 / NEXT-4: T2 sampling */
+/* PAPER.md §IV-C1 (l.253-268): per 16x16 tile, each pixel's rendered colour (clamped to
+ * [0,1]) quantised to 16 levels per channel (c8 = min(255, floor(256 c)), level = c8 / 16),
+ * key = R 256 + G 16 + B, aggregated in a 4096-slot shared-memory table (R37-R38).  Outputs
+ * (device): nb[tiles] = occupied buckets; for bucket j < nb[t] of tile t, at [t * 256 + j]
+ * in ascending key order: keys (u16), counts (pixels), color_sum[3], opacity_sum
+ * (sum of 1 - final_T).  image [3][h][w], final_T [h][w] (device). */
+bgs_status bgs_tile_buckets(const float* image, const float* final_T, int32_t w, int32_t h, uint32_t* nb,
+                            uint16_t* keys, uint32_t* counts, float* color_sum, float* opacity_sum, void* stream);
+/* Workspace bytes for bgs_importance / bgs_importance_keep over n Gaussians (0 if n < 1). */
+size_t bgs_importance_workspace_bytes(int64_t n);
+/* PAPER.md §IV-C3 (l.279-284): I_g = (1/N_g) sum_i sim(c_g, c_i) alpha_g(i) over the pixels
+ * of g's tiles where alpha_g(i) >= 1/255, sim = 1 - |c_g - c_i| / sqrt(3) (R39), for the
+ * frame's last bgs_sort and the image it rendered (device [3][h][w]).  importance[n] and
+ * count[n] (N_g; may be NULL) out (device).  Not on the training hot path. */
+bgs_status bgs_importance(const bgs_frame* f /*host*/, const float* image, float* importance, uint32_t* count,
+                          void* workspace, size_t bytes, void* stream);
+/* R40: keep[i] = 1 for the first ceil(fraction n) Gaussians by ascending
+ * importance (descending if invert), ties by index; 0 for the rest (device u8 [n] out). */
+bgs_status bgs_importance_keep(const float* importance, int64_t n, float fraction, int32_t invert, uint8_t* keep,
+                               void* workspace, size_t bytes, void* stream);
+/* NEXT-4 render-only serving: later bgs_preprocess calls on this frame cull every Gaussian
+ * with keep[i] == 0 ("the precomputed importance information is retained for use during
+ * rendering", l.284).  keep: device u8 [n], caller-owned, or NULL to render all. */
+bgs_status bgs_frame_set_keep(bgs_frame* f /*host*/, const uint8_t* keep);
+
 /* ---------------------------------------------------------------- status / debug */
 /* After the caller synchronised the frame's stream: K (host out) and BGS_OK, or
  * BGS_ERR_CAPACITY when K > max_keys (re-run with a larger workspace). */

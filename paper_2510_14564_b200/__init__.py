@@ -122,6 +122,11 @@ _SIGS = {
     "bgs_density_result": (C.c_int, [_P, C.c_int64, C.POINTER(DensityReport), C.POINTER(C.c_uint32)]),
     "bgs_density_apply": (C.c_int, [_P, _P, _P, C.c_int64, _P, C.POINTER(DensityParams), _P, _P, C.c_int64, _P, _P,
                                     _P, C.c_int64, _P]),
+    "bgs_tile_buckets": (C.c_int, [_P, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
+    "bgs_importance_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "bgs_importance": (C.c_int, [C.POINTER(Frame), _P, _P, _P, _P, C.c_size_t, _P]),
+    "bgs_importance_keep": (C.c_int, [_P, C.c_int64, C.c_float, C.c_int32, _P, _P, C.c_size_t, _P]),
+    "bgs_frame_set_keep": (C.c_int, [C.POINTER(Frame), _P]),
     "bgs_status_string": (C.c_char_p, [C.c_int]),
     "bgs_last_error": (C.c_char_p, []),
     "bgs_launch_count": (C.c_uint64, []),
@@ -317,6 +322,50 @@ def density_control(theta, exp_avg, exp_avg_sq, n, params: DensityParams, genera
                                   _ptr(normals), _ptr(uniforms), nc, _ptr(th2), _ptr(m2), _ptr(v2), n_out,
                                   _stream(stream)), "bgs_density_apply")
     return th2, m2, v2, n_out, rep, int(short.value), (normals[:nc], uniforms[:nc])
+
+
+def bgs_tile_buckets(image, final_T, w, h, stream=None):
+    """NEXT-3 (§IV-C1): per-tile colour buckets -> (nb, keys, counts, color_sum, opacity_sum)."""
+    dev = image.device
+    nt = ((w + 15) // 16) * ((h + 15) // 16)
+    nb = torch.empty(nt, dtype=torch.int32, device=dev)
+    keys = torch.empty(nt * 256, dtype=torch.int16, device=dev)
+    counts = torch.empty(nt * 256, dtype=torch.int32, device=dev)
+    csum = torch.empty(nt * 256 * 3, dtype=torch.float32, device=dev)
+    osum = torch.empty(nt * 256, dtype=torch.float32, device=dev)
+    _check(_lib.bgs_tile_buckets(_ptr(image), _ptr(final_T), w, h, _ptr(nb), _ptr(keys), _ptr(counts), _ptr(csum),
+                                 _ptr(osum), _stream(stream)), "bgs_tile_buckets")
+    return nb, keys, counts, csum, osum
+
+
+def bgs_importance(frame: Frame, image, n, workspace=None, stream=None):
+    """NEXT-3 (§IV-C3): (importance [n], N_g [n]) for the frame's last render."""
+    dev = image.device
+    nbytes = int(_lib.bgs_importance_workspace_bytes(n))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    imp = torch.empty(n, dtype=torch.float32, device=dev)
+    cnt = torch.empty(n, dtype=torch.int32, device=dev)
+    _check(_lib.bgs_importance(C.byref(frame), _ptr(image), _ptr(imp), _ptr(cnt), _ptr(workspace),
+                               workspace.numel(), _stream(stream)), "bgs_importance")
+    return imp, cnt
+
+
+def bgs_importance_keep(importance, fraction, invert=False, workspace=None, stream=None):
+    """R40: the keep mask (uint8 [n]) of the first ceil(fraction n) Gaussians by importance."""
+    n = importance.numel()
+    dev = importance.device
+    nbytes = int(_lib.bgs_importance_workspace_bytes(n))
+    if workspace is None or workspace.numel() < nbytes:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    keep = torch.empty(n, dtype=torch.uint8, device=dev)
+    _check(_lib.bgs_importance_keep(_ptr(importance), n, float(fraction), int(bool(invert)), _ptr(keep),
+                                    _ptr(workspace), workspace.numel(), _stream(stream)), "bgs_importance_keep")
+    return keep
+
+
+def bgs_frame_set_keep(frame: Frame, keep):
+    _check(_lib.bgs_frame_set_keep(C.byref(frame), None if keep is None else _ptr(keep)), "bgs_frame_set_keep")
 
 
 def launch_count() -> int:

@@ -96,6 +96,7 @@ struct Frame {
   uint32_t* item_off;      // [n] exclusive scan of rank_cnt
   uint2* rank_rect;        // [n] packed tile rect per depth rank
   uint8_t* cbits;          // [n] frozen clamp decisions (rgb / J) for the backward (R18)
+  const uint8_t* keep;     // [n] NEXT-4 keep mask (device, caller-owned) or null: keep[i] == 0 culls i
 };
 static_assert(sizeof(Frame) <= sizeof(bgs_frame), "Frame must fit in bgs_frame::opaque");
 constexpr uint64_t kFrameMagic = 0xB6500F7A3E5ull;

@@ -41,6 +41,7 @@ struct PreParams {
   uint2* rect;              // {x0 | y0 << 16, w | h << 16} of visible Gaussians (depth-first sort)
   float4* grad2d;
   uint8_t* cbits;
+  const uint8_t* keep;      // NEXT-4 keep mask or null
 };
 
 __global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
@@ -55,6 +56,7 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
   p.radius[i] = 0;
   p.tiles_touched[i] = 0;
   if (t2 <= c.near_plane) return;
+  if (p.keep && !p.keep[i]) return;  // NEXT-4: dropped by the importance keep rule (R40)
   // clip, perspective divide (R4), pixel coordinates (R1)
   const float c0 = fmaf(c.P[8], mz, fmaf(c.P[4], my, fmaf(c.P[0], mx, c.P[12])));
   const float c1 = fmaf(c.P[9], mz, fmaf(c.P[5], my, fmaf(c.P[1], mx, c.P[13])));
@@ -339,6 +341,7 @@ bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
   p.rect = F->rect;
   p.grad2d = F->grad2d;
   p.cbits = F->cbits;
+  p.keep = F->keep;
   const int64_t blocks = (F->n + 255) / 256;
   k_preprocess<<<(unsigned)blocks, 256, 0, s>>>(p);
   note_launch();
