@@ -20,6 +20,10 @@ constexpr int kCkPoolSeg = 2048;
 constexpr int kChunkItemsF = 16384;
 constexpr int kDirectMaxCells = 12800;  // (tiles_x + 1)(tiles_y + 1) bound  // the checkpoint / state pools are sized for seg_len >= this
 
+// blend work-unit planning (k_*_plan_*): 128 cost buckets (4 per octave, costliest first),
+// plan[0..127] counts, plan[128..255] offsets, plan[256] the split-state bump
+constexpr int kPlanBuckets = 128, kPlanWords = 2 * kPlanBuckets + 32;
+
 // counters[] slots (u32 words in the workspace)
 enum : int {
   C_K_LO = 0, C_K_HI = 1,     // K as u64
@@ -73,6 +77,7 @@ struct Frame {
   uint32_t* sort_hist;     // [8][256]
   uint32_t* sort_status;   // [sort_tiles_max][256]
   uint32_t* counters;      // [C_NUM]
+  uint32_t* plan;          // [kPlanWords] work-unit planning: bucket counts, offsets, bump
   float4* grad2d;          // [n][3]
   uint32_t* tile_count;    // [num_tiles] keys per tile (from the duplication)
   uint32_t* order_fwd;     // [8 tiles] forward work items (tile << 3 | 8x4 block), longest first

@@ -42,7 +42,7 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
   size_t radius, depth, record, tiles_touched, rect, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
-      sort_status, counters, grad2d, tile_count, order_fwd, order_bwd, block_cost, ck_table, ck_pool, spec_base, spec_n,
+      sort_status, counters, plan, grad2d, tile_count, order_fwd, order_bwd, block_cost, ck_table, ck_pool, spec_base, spec_n,
       arrive, spec_state, spec_last, chunk_cnt, dkey0, dkey1,
       dval0, dval1, rank_cnt, item_off, rank_rect, cbits, total;
   int64_t ck_cap;
@@ -91,6 +91,7 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.sort_hist = take(4 * 8 * 256);
   L.sort_status = take(4 * 256 * (size_t)L.sort_tiles_max);
   L.counters = take(4 * C_NUM);
+  L.plan = take(4 * kPlanWords);
   L.grad2d = take(48 * N);
   const size_t NT = (size_t)L.num_tiles;
   L.tile_count = take(4 * NT);
@@ -235,6 +236,7 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->sort_hist = (uint32_t*)(base + L.sort_hist);
   F->sort_status = (uint32_t*)(base + L.sort_status);
   F->counters = (uint32_t*)(base + L.counters);
+  F->plan = (uint32_t*)(base + L.plan);
   F->grad2d = (float4*)(base + L.grad2d);
   F->tile_count = (uint32_t*)(base + L.tile_count);
   F->order_fwd = (uint32_t*)(base + L.order_fwd);

@@ -261,52 +261,53 @@ static int bwd_grid() {
 // Backward work units, longest first: every (tile, 8x4 block) item with a non-empty walk
 // (block_cost = its largest n_contrib, from the forward) contributes one unit per segment:
 // segments [k seg_len, (k + 1) seg_len) for each consecutive recorded boundary, and a last
-// segment up to the walk's end.  One CTA buckets units by length (4 buckets per octave).
-constexpr int kPlanThreads = 1024, kPlanBuckets = 128;
+// segment up to the walk's end.  Bucketed by length (4 buckets per octave) in three grid
+// steps like the forward's plan (k_plan_scan is in render_fwd.cu).
+__global__ void __launch_bounds__(kPlanBuckets) k_plan_scan(uint32_t* plan, uint32_t* counters, int units_slot,
+                                                           int reset0, int reset1);
 
+// segments of item t: boundaries b = 1.. with b seg_len < wl and a valid checkpoint slot
+__device__ __forceinline__ int bwd_nseg(int t, uint32_t wl, const uint32_t* ck_table, uint32_t ck_cap, int seg_len) {
+  int nb = 0;
+  while (nb < kCkMax && (uint32_t)(nb + 1) * (uint32_t)seg_len < wl && ck_table[(size_t)t * kCkMax + nb] < ck_cap)
+    ++nb;
+  return nb + 1;
+}
 
-__global__ void __launch_bounds__(kPlanThreads) k_bwd_plan(const uint32_t* __restrict__ block_cost, int32_t n_items,
-                                                           const uint32_t* __restrict__ ck_table, uint32_t ck_cap,
-                                                           int32_t seg_len, uint32_t* counters, uint32_t* units) {
+__global__ void __launch_bounds__(256) k_bwd_plan_count(const uint32_t* __restrict__ block_cost, int32_t n_items,
+                                                       const uint32_t* __restrict__ ck_table, uint32_t ck_cap,
+                                                       int32_t seg_len, const uint32_t* counters, uint32_t* plan) {
   __shared__ uint32_t s_b[kPlanBuckets];
   for (int k = threadIdx.x; k < kPlanBuckets; k += blockDim.x) s_b[k] = 0;
-  if (threadIdx.x == 0) counters[C_BWD_TICKET] = 0;
   __syncthreads();
   const bool overflow = counters[C_OVERFLOW] != 0;
-  // segments of item t: boundaries b = 1.. with b seg_len < wl and a valid checkpoint slot
-  auto nseg_of = [&](int t, uint32_t wl) {
-    int nb = 0;
-    while (nb < kCkMax && (uint32_t)(nb + 1) * (uint32_t)seg_len < wl && ck_table[(size_t)t * kCkMax + nb] < ck_cap)
-      ++nb;
-    return nb + 1;
-  };
-  for (int t = threadIdx.x; t < n_items; t += blockDim.x) {
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_items; t += gridDim.x * blockDim.x) {
     const uint32_t wl = overflow ? 0u : block_cost[t];
     if (!wl) continue;
-    const int ns = nseg_of(t, wl);
+    const int ns = bwd_nseg(t, wl, ck_table, ck_cap, seg_len);
     if (ns > 1) atomicAdd(&s_b[cost_bucket((uint32_t)seg_len)], (uint32_t)(ns - 1));
     atomicAdd(&s_b[cost_bucket(wl - (uint32_t)(ns - 1) * (uint32_t)seg_len)], 1u);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t run = 0;
-    for (int b = 0; b < kPlanBuckets; ++b) {
-      const uint32_t c = s_b[b];
-      s_b[b] = run;
-      run += c;
-    }
-    counters[C_BWD_UNITS] = run;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < n_items; t += blockDim.x) {
+  for (int k = threadIdx.x; k < kPlanBuckets; k += blockDim.x)
+    if (s_b[k]) atomicAdd(&plan[k], s_b[k]);
+}
+
+__global__ void __launch_bounds__(256) k_bwd_plan_place(const uint32_t* __restrict__ block_cost, int32_t n_items,
+                                                       const uint32_t* __restrict__ ck_table, uint32_t ck_cap,
+                                                       int32_t seg_len, const uint32_t* counters, uint32_t* plan,
+                                                       uint32_t* units) {
+  const bool overflow = counters[C_OVERFLOW] != 0;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_items; t += gridDim.x * blockDim.x) {
     const uint32_t wl = overflow ? 0u : block_cost[t];
     if (!wl) continue;
-    const int ns = nseg_of(t, wl);
+    const int ns = bwd_nseg(t, wl, ck_table, ck_cap, seg_len);
     if (ns > 1) {
-      const uint32_t base = atomicAdd(&s_b[cost_bucket((uint32_t)seg_len)], (uint32_t)(ns - 1));
+      const uint32_t base = atomicAdd(&plan[kPlanBuckets + cost_bucket((uint32_t)seg_len)], (uint32_t)(ns - 1));
       for (int k = 0; k < ns - 1; ++k) units[base + k] = (uint32_t)t | ((uint32_t)k << 25);
     }
-    const uint32_t pos = atomicAdd(&s_b[cost_bucket(wl - (uint32_t)(ns - 1) * (uint32_t)seg_len)], 1u);
+    const uint32_t pos =
+        atomicAdd(&plan[kPlanBuckets + cost_bucket(wl - (uint32_t)(ns - 1) * (uint32_t)seg_len)], 1u);
     units[pos] = (uint32_t)t | ((uint32_t)(ns - 1) << 25) | (1u << 31);
   }
 }
@@ -314,9 +315,14 @@ __global__ void __launch_bounds__(kPlanThreads) k_bwd_plan(const uint32_t* __res
 bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
                             cudaStream_t s) {
   const uint32_t cap = (uint32_t)(F->ck_cap < 0xffffffffll ? F->ck_cap : 0xffffffffll);
-  k_bwd_plan<<<1, kPlanThreads, 0, s>>>(F->block_cost, 8 * F->num_tiles, F->ck_table, cap, F->seg_len, F->counters,
-                                        F->order_bwd);
-  note_launch();
+  const int n_items = 8 * F->num_tiles;
+  const int pgrid = (n_items + 255) / 256 < 2 * num_sms() ? (n_items + 255) / 256 : 2 * num_sms();
+  if (cudaMemsetAsync(F->plan, 0, 4 * kPlanWords, s) != cudaSuccess) return check_launch("bwd plan memset");
+  k_bwd_plan_count<<<pgrid, 256, 0, s>>>(F->block_cost, n_items, F->ck_table, cap, F->seg_len, F->counters, F->plan);
+  k_plan_scan<<<1, kPlanBuckets, 0, s>>>(F->plan, F->counters, C_BWD_UNITS, C_BWD_TICKET, -1);
+  k_bwd_plan_place<<<pgrid, 256, 0, s>>>(F->block_cost, n_items, F->ck_table, cap, F->seg_len, F->counters, F->plan,
+                                         F->order_bwd);
+  note_launch(3);
   bgs_status st = check_launch("k_bwd_plan");
   if (st != BGS_OK) return st;
   k_render_bwd<<<bwd_grid(), kBwdWarpsPerCta * 32, 0, s>>>(
