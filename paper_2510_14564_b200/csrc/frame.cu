@@ -51,7 +51,7 @@ struct Layout {
   bool direct;
 };
 
-constexpr int kScanTile = 2048;
+constexpr int kScanTile = 4096;  // = kScanThreads * kScanItems of k_scan (preprocess.cu)
 constexpr int kSortTile = 4096;
 
 static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layout& L) {

@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
 // K8: single-pass exclusive scan with decoupled look-back (dynamic tile ids).
 // status word: bits 62-63 = flag (1 aggregate, 2 inclusive prefix), bits 0-61 = value.
 // ---------------------------------------------------------------------------
-constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+constexpr int kScanThreads = 256, kScanItems = 16, kScanTile = kScanThreads * kScanItems;
 constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
@@ -240,11 +240,22 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
   const int64_t base = tile * kScanTile + (int64_t)tid * kScanItems;
   uint32_t v[kScanItems];
   unsigned long long local = 0;
+  const bool full = base + kScanItems <= n;  // 16-byte vector loads (in is 256-byte aligned)
+  if (full) {
 #pragma unroll
-  for (int k = 0; k < kScanItems; ++k) {
-    v[k] = (base + k < n) ? in[base + k] : 0u;
-    local += v[k];
+    for (int k = 0; k < kScanItems / 4; ++k) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(in + base) + k);
+      v[4 * k] = q.x;
+      v[4 * k + 1] = q.y;
+      v[4 * k + 2] = q.z;
+      v[4 * k + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) v[k] = (base + k < n) ? in[base + k] : 0u;
   }
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) local += v[k];
   // block exclusive scan of per-thread totals
   unsigned long long incl = local;
 #pragma unroll
@@ -292,10 +303,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
   }
   __syncthreads();
   unsigned long long run = s_prefix + warp_off + (incl - local);
+  uint32_t o[kScanItems];
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
-    if (base + k < n) out[base + k] = (uint32_t)(run > 0xffffffffull ? 0xffffffffull : run);
+    o[k] = (uint32_t)(run > 0xffffffffull ? 0xffffffffull : run);
     run += v[k];
+  }
+  if (full) {
+#pragma unroll
+    for (int k = 0; k < kScanItems / 4; ++k)
+      reinterpret_cast<uint4*>(out + base)[k] = make_uint4(o[4 * k], o[4 * k + 1], o[4 * k + 2], o[4 * k + 3]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+      if (base + k < n) out[base + k] = o[k];
   }
   if (tile == num_tiles - 1 && tid == 0) {
     const unsigned long long K = s_prefix + total;
