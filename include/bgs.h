@@ -325,6 +325,9 @@ bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contri
 /* Depth-first path with the radix tile split (two 8-bit onesweep passes over the K items)
  * instead of the direct chunked split; same values and ranges. */
 #define BGS_DEBUG_SORT_RADIX_SPLIT 4
+/* Kept selectable: the blend backward on 8x4-pixel units (one pixel per lane) instead of
+ * the default 8x8 units (two pixels per lane). */
+#define BGS_DEBUG_BWD_8X4 8
 bgs_status bgs_frame_set_debug(bgs_frame* f /*host*/, int32_t flags);
 
 /* Scheduling parameter of the blend kernels (default 4096): a (tile, 8x4 pixel block) work

@@ -25,6 +25,7 @@ BGS_OK, BGS_ERR_INVALID, BGS_ERR_CAPACITY, BGS_ERR_CUDA, BGS_ERR_UNSUPPORTED = 0
 BGS_DEBUG_SKIP_SORT = 1
 BGS_DEBUG_SORT_ONESWEEP64 = 2
 BGS_DEBUG_SORT_RADIX_SPLIT = 4
+BGS_DEBUG_BWD_8X4 = 8
 
 
 class BgsError(RuntimeError):

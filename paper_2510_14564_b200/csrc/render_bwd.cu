@@ -62,6 +62,11 @@ __device__ __forceinline__ bool box_hits(const float4 a, float bx0, float by0, f
   return a.x + a.z >= bx0 && a.x - a.z <= bx1 && a.y + a.w >= by0 && a.y - a.w <= by1;
 }
 
+// PPL = pixels per lane: 1 -> the unit is an 8x4 block (one forward item), 2 -> an 8x8
+// block (two vertically adjacent forward items, lane l on pixels (x, y) and (x, y + 4)):
+// each entry's staging, shared-memory record reads and 9-value warp reduction then serve
+// 64 pixels instead of 32.
+template <int PPL>
 __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ values, const float4* __restrict__ record,
     const uint32_t* __restrict__ counters, Cam cam, const uint32_t* __restrict__ units, uint32_t* ticket,
@@ -96,42 +101,60 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     if (lane == 0) item = atomicAdd(ticket, 1u);
     item = __shfl_sync(0xffffffffu, item, 0);
     if (item >= n_units) break;
-    // unit = (tile << 3 | block) | segment k << 25 | last segment << 31
+    // unit = (tile << log2(8 / PPL) | block) | segment k << 25 | last segment << 31
     const uint32_t code = units[item];
     const uint32_t it = code & ((1u << 25) - 1u);
     const int seg = (int)((code >> 25) & 63u);
     const bool last_seg = (code >> 31) != 0;
-    const int tile = (int)(it >> 3), blk = (int)(it & 7);
+    const int per_tile = 8 / PPL;
+    const int tile = (int)(it / per_tile), blk = (int)(it % per_tile);
     const int tx = tile % cam.tiles_x, ty = tile / cam.tiles_x;
-    const int bx = tx * kTile + (blk & 1) * 8, by = ty * kTile + (blk >> 1) * 4;
-    const int px = bx + (lane & 7), py = by + (lane >> 3);
-    const float bx0 = (float)bx, by0 = (float)by, bx1 = bx0 + 7.0f, by1 = by0 + 3.0f;
-    const bool inside = px < cam.W && py < cam.H;
-    const float pxf = (float)px, pyf = (float)py;
+    const int bx = tx * kTile + (blk & 1) * 8, by = ty * kTile + (blk >> 1) * 4 * PPL;
+    const int px = bx + (lane & 7);
+    const float bx0 = (float)bx, by0 = (float)by, bx1 = bx0 + 7.0f, by1 = by0 + (float)(4 * PPL - 1);
+    const float pxf = (float)px;
     uint2 rg = ranges[tile];
     if (overflow) rg = make_uint2(0, 0);
-    const int64_t pix = (int64_t)py * cam.W + px;
-    const uint32_t my_last = inside ? n_contrib[pix] : 0u;
-    const int wmax = (int)min(__reduce_max_sync(0xffffffffu, my_last), rg.y - rg.x);
+    // per pixel h of the lane: forward item (8x4 block) fit[h], pixel (px, py[h])
+    bool inside[PPL];
+    int64_t pix[PPL];
+    uint32_t my_last[PPL], fit[PPL];
+    float pyf[PPL];
+    uint32_t lmax = 0;
+#pragma unroll
+    for (int h = 0; h < PPL; ++h) {
+      const int py = by + 4 * h + (lane >> 3);
+      fit[h] = PPL == 1 ? it : (uint32_t)tile * 8u + (uint32_t)((blk & 1) + 4 * (blk >> 1) + 2 * h);
+      inside[h] = px < cam.W && py < cam.H;
+      pix[h] = (int64_t)py * cam.W + px;
+      pyf[h] = (float)py;
+      my_last[h] = inside[h] ? n_contrib[pix[h]] : 0u;
+      lmax = max(lmax, my_last[h]);
+    }
+    const int wmax = (int)min(__reduce_max_sync(0xffffffffu, lmax), rg.y - rg.x);
     // this unit walks list positions [lo, top): segment seg of the block's walk
     const int lo = seg * seg_len;
     const int top = last_seg ? wmax : min(wmax, lo + seg_len);
     if (top <= lo) continue;
-    float T = inside ? final_T[pix] : 1.0f;
-    float dLr = 0.f, dLg = 0.f, dLb = 0.f;
-    if (inside) {
-      dLr = dl_dimage[pix];
-      dLg = dl_dimage[plane + pix];
-      dLb = dl_dimage[2 * plane + pix];
-    }
-    // the colour behind the current entry enters the gradient only as DS = dL/dC . S
-    float DS = T * (dLr * cam.bg[0] + dLg * cam.bg[1] + dLb * cam.bg[2]);
-    if (!last_seg && (int)my_last > top) {
-      // the pixel's walk continues past this segment: start from the forward's checkpoint
-      // {T, colour behind} at boundary seg + 1
-      const float4 c = ck_pool[(size_t)ck_table[(size_t)it * kCkMax + seg] * 32 + lane];
-      T = c.x;
-      DS = dLr * c.y + dLg * c.z + dLb * c.w;
+    float T[PPL], dLr[PPL], dLg[PPL], dLb[PPL], DS[PPL];
+#pragma unroll
+    for (int h = 0; h < PPL; ++h) {
+      T[h] = inside[h] ? final_T[pix[h]] : 1.0f;
+      dLr[h] = dLg[h] = dLb[h] = 0.f;
+      if (inside[h]) {
+        dLr[h] = dl_dimage[pix[h]];
+        dLg[h] = dl_dimage[plane + pix[h]];
+        dLb[h] = dl_dimage[2 * plane + pix[h]];
+      }
+      // the colour behind the current entry enters the gradient only as DS = dL/dC . S
+      DS[h] = T[h] * (dLr[h] * cam.bg[0] + dLg[h] * cam.bg[1] + dLb[h] * cam.bg[2]);
+      if (!last_seg && (int)my_last[h] > top) {
+        // the pixel's walk continues past this segment: start from the forward's checkpoint
+        // {T, colour behind} at boundary seg + 1 of its own forward item
+        const float4 c = ck_pool[(size_t)ck_table[(size_t)fit[h] * kCkMax + seg] * 32 + lane];
+        T[h] = c.x;
+        DS[h] = dLr[h] * c.y + dLg[h] * c.z + dLb[h] * c.w;
+      }
     }
     const int nst = (top - lo + 31) / 32;
     // lane's list position in step s (back to front; below lo = no entry)
@@ -178,54 +201,62 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
       const uint32_t id_nnn = load_id(s + 3);
       // (4) walk step s, back to front.  Per entry and pixel the partials are
       //   dL/dxy = dp (2A dx + B dy, 2C dy + B dx), dp {dx^2, dx dy, dy^2}, dL/do-part, w dL/dC
-      // (dp = dL/dpower); the conic's factors (-1/2, -1, -1/2) are applied to the warp totals
+      // (dp = dL/dpower), summed over the lane's pixels; the conic's factors (-1/2, -1, -1/2)
+      // are applied to the warp totals
       const int m = __popc(bal);
       for (int k = m - 1; k >= 0; --k) {
         const uint32_t pos = spos[k];
-        bool act = pos < my_last;
+        bool any_act = false;
         float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
-        if (act) {
+        bool act[PPL];
+#pragma unroll
+        for (int h = 0; h < PPL; ++h) act[h] = pos < my_last[h];
+        bool act_any = act[0];
+#pragma unroll
+        for (int h = 1; h < PPL; ++h) act_any |= act[h];
+        if (act_any) {
           const float4 r0 = sr0[k];
           const float4 r1 = sr1[k];
           const float4 r2 = sr2[k];
-          const float dx = r0.x - pxf, dy = r0.y - pyf;
-          const float dxx = dx * dx, dyy = dy * dy, dxy = dx * dy;
-          const float power = fmaf(r1.x, dxx, fmaf(r1.z, dyy, r1.y * dxy));
-          float G = 0.0f, og = 0.0f, alpha = 0.0f;
-          // power below the exact alpha < 1/255 bound (pthr): skipped without the MUFU path
-          if (power > 0.0f || power < r2.w) {
-            act = false;
-          } else {
-            G = fast_exp(power);
-            og = r1.w * G;
-            alpha = fminf(0.99f, og);
-            if (alpha < (1.0f / 255.0f)) act = false;
-          }
-          if (act) {
+          const float dx = r0.x - pxf;
+          const float dxx = dx * dx;
+#pragma unroll
+          for (int h = 0; h < PPL; ++h) {
+            if (!act[h]) continue;
+            const float dy = r0.y - pyf[h];
+            const float dyy = dy * dy, dxy = dx * dy;
+            const float power = fmaf(r1.x, dxx, fmaf(r1.z, dyy, r1.y * dxy));
+            // power below the exact alpha < 1/255 bound (pthr): skipped without the MUFU path
+            if (power > 0.0f || power < r2.w) continue;
+            const float G = fast_exp(power);
+            const float og = r1.w * G;
+            const float alpha = fminf(0.99f, og);
+            if (alpha < (1.0f / 255.0f)) continue;
+            any_act = true;
             // MUFU reciprocal (1 - alpha >= 0.01): ~2^-22 relative per step, far inside the
             // 1e-3 gradient tolerance, instead of the multi-instruction IEEE division
             const float ioma = __fdividef(1.0f, 1.0f - alpha);
-            T = T * ioma;  // transmittance in front of this Gaussian
-            const float w = alpha * T;
-            g6 = w * dLr;
-            g7 = w * dLg;
-            g8 = w * dLb;
+            T[h] = T[h] * ioma;  // transmittance in front of this Gaussian
+            const float w = alpha * T[h];
+            g6 = fmaf(w, dLr[h], g6);
+            g7 = fmaf(w, dLg[h], g7);
+            g8 = fmaf(w, dLb[h], g8);
             // dL/dalpha = sum_c dL_c (c_c T - S_c / (1 - alpha)) = T (dL . c) - DS / (1 - alpha)
-            const float dLc = fmaf(dLb, r2.z, fmaf(dLg, r2.y, dLr * r2.x));
-            const float dLda = fmaf(T, dLc, -(DS * ioma));
-            DS = fmaf(dLc, w, DS);  // S += c w
+            const float dLc = fmaf(dLb[h], r2.z, fmaf(dLg[h], r2.y, dLr[h] * r2.x));
+            const float dLda = fmaf(T[h], dLc, -(DS[h] * ioma));
+            DS[h] = fmaf(dLc, w, DS[h]);  // S += c w
             if (og <= 0.99f) {  // unclamped alpha: gradient to opacity and G (R18)
-              g5 = dLda * G;
+              g5 = fmaf(dLda, G, g5);
               const float dp = dLda * og;  // dL/dpower
-              g0 = dp * fmaf(2.0f * r1.x, dx, r1.y * dy);
-              g1 = dp * fmaf(2.0f * r1.z, dy, r1.y * dx);
-              g2 = dp * dxx;
-              g3 = dp * dxy;
-              g4 = dp * dyy;
+              g0 = fmaf(dp, fmaf(2.0f * r1.x, dx, r1.y * dy), g0);
+              g1 = fmaf(dp, fmaf(2.0f * r1.z, dy, r1.y * dx), g1);
+              g2 = fmaf(dp, dxx, g2);
+              g3 = fmaf(dp, dxy, g3);
+              g4 = fmaf(dp, dyy, g4);
             }
           }
         }
-        if (__any_sync(0xffffffffu, act)) {
+        if (__any_sync(0xffffffffu, any_act)) {
           const float gv[9] = {g0, g1, g2, g3, g4, g5, g6, g7, g8};
           int idx;
           const float tot = warp_reduce_scatter9(gv, lane, idx);
@@ -248,11 +279,12 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
   }
 }
 
+template <int PPL>
 static int bwd_grid() {
   static int grid = 0;
   if (!grid) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_bwd, kBwdWarpsPerCta * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_bwd<PPL>, kBwdWarpsPerCta * 32, 0);
     grid = (per_sm < 1 ? 1 : per_sm) * num_sms();
   }
   return grid;
@@ -266,25 +298,45 @@ static int bwd_grid() {
 __global__ void __launch_bounds__(kPlanBuckets) k_plan_scan(uint32_t* plan, uint32_t* counters, int units_slot,
                                                            int reset0, int reset1);
 
-// segments of item t: boundaries b = 1.. with b seg_len < wl and a valid checkpoint slot
-__device__ __forceinline__ int bwd_nseg(int t, uint32_t wl, const uint32_t* ck_table, uint32_t ck_cap, int seg_len) {
+// segments of unit t (its PPL forward items fit = first + 2 h): boundaries b = 1.. with
+// b seg_len < the unit's walk, where every item whose own walk crosses b has a checkpoint
+__device__ __forceinline__ void bwd_unit(int t, int ppl, const uint32_t* block_cost, bool overflow, uint32_t& wl,
+                                         uint32_t* fit) {
+  wl = 0;
+  const int per_tile = 8 / ppl, tile = t / per_tile, blk = t % per_tile;
+  for (int h = 0; h < ppl; ++h) {
+    fit[h] = ppl == 1 ? (uint32_t)t : (uint32_t)tile * 8u + (uint32_t)((blk & 1) + 4 * (blk >> 1) + 2 * h);
+    wl = max(wl, overflow ? 0u : block_cost[fit[h]]);
+  }
+}
+
+__device__ __forceinline__ int bwd_nseg(const uint32_t* fit, int ppl, uint32_t wl, const uint32_t* block_cost,
+                                        const uint32_t* ck_table, uint32_t ck_cap, int seg_len) {
   int nb = 0;
-  while (nb < kCkMax && (uint32_t)(nb + 1) * (uint32_t)seg_len < wl && ck_table[(size_t)t * kCkMax + nb] < ck_cap)
+  while (nb < kCkMax && (uint32_t)(nb + 1) * (uint32_t)seg_len < wl) {
+    bool ok = true;
+    for (int h = 0; h < ppl; ++h)
+      if (block_cost[fit[h]] > (uint32_t)(nb + 1) * (uint32_t)seg_len)
+        ok &= ck_table[(size_t)fit[h] * kCkMax + nb] < ck_cap;
+    if (!ok) break;
     ++nb;
+  }
   return nb + 1;
 }
 
-__global__ void __launch_bounds__(256) k_bwd_plan_count(const uint32_t* __restrict__ block_cost, int32_t n_items,
-                                                       const uint32_t* __restrict__ ck_table, uint32_t ck_cap,
-                                                       int32_t seg_len, const uint32_t* counters, uint32_t* plan) {
+__global__ void __launch_bounds__(256) k_bwd_plan_count(const uint32_t* __restrict__ block_cost, int32_t n_units,
+                                                       int32_t ppl, const uint32_t* __restrict__ ck_table,
+                                                       uint32_t ck_cap, int32_t seg_len, const uint32_t* counters,
+                                                       uint32_t* plan) {
   __shared__ uint32_t s_b[kPlanBuckets];
   for (int k = threadIdx.x; k < kPlanBuckets; k += blockDim.x) s_b[k] = 0;
   __syncthreads();
   const bool overflow = counters[C_OVERFLOW] != 0;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_items; t += gridDim.x * blockDim.x) {
-    const uint32_t wl = overflow ? 0u : block_cost[t];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_units; t += gridDim.x * blockDim.x) {
+    uint32_t wl, fit[2];
+    bwd_unit(t, ppl, block_cost, overflow, wl, fit);
     if (!wl) continue;
-    const int ns = bwd_nseg(t, wl, ck_table, ck_cap, seg_len);
+    const int ns = bwd_nseg(fit, ppl, wl, block_cost, ck_table, ck_cap, seg_len);
     if (ns > 1) atomicAdd(&s_b[cost_bucket((uint32_t)seg_len)], (uint32_t)(ns - 1));
     atomicAdd(&s_b[cost_bucket(wl - (uint32_t)(ns - 1) * (uint32_t)seg_len)], 1u);
   }
@@ -293,15 +345,16 @@ __global__ void __launch_bounds__(256) k_bwd_plan_count(const uint32_t* __restri
     if (s_b[k]) atomicAdd(&plan[k], s_b[k]);
 }
 
-__global__ void __launch_bounds__(256) k_bwd_plan_place(const uint32_t* __restrict__ block_cost, int32_t n_items,
-                                                       const uint32_t* __restrict__ ck_table, uint32_t ck_cap,
-                                                       int32_t seg_len, const uint32_t* counters, uint32_t* plan,
-                                                       uint32_t* units) {
+__global__ void __launch_bounds__(256) k_bwd_plan_place(const uint32_t* __restrict__ block_cost, int32_t n_units,
+                                                       int32_t ppl, const uint32_t* __restrict__ ck_table,
+                                                       uint32_t ck_cap, int32_t seg_len, const uint32_t* counters,
+                                                       uint32_t* plan, uint32_t* units) {
   const bool overflow = counters[C_OVERFLOW] != 0;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_items; t += gridDim.x * blockDim.x) {
-    const uint32_t wl = overflow ? 0u : block_cost[t];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_units; t += gridDim.x * blockDim.x) {
+    uint32_t wl, fit[2];
+    bwd_unit(t, ppl, block_cost, overflow, wl, fit);
     if (!wl) continue;
-    const int ns = bwd_nseg(t, wl, ck_table, ck_cap, seg_len);
+    const int ns = bwd_nseg(fit, ppl, wl, block_cost, ck_table, ck_cap, seg_len);
     if (ns > 1) {
       const uint32_t base = atomicAdd(&plan[kPlanBuckets + cost_bucket((uint32_t)seg_len)], (uint32_t)(ns - 1));
       for (int k = 0; k < ns - 1; ++k) units[base + k] = (uint32_t)t | ((uint32_t)k << 25);
@@ -315,19 +368,27 @@ __global__ void __launch_bounds__(256) k_bwd_plan_place(const uint32_t* __restri
 bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
                             cudaStream_t s) {
   const uint32_t cap = (uint32_t)(F->ck_cap < 0xffffffffll ? F->ck_cap : 0xffffffffll);
-  const int n_items = 8 * F->num_tiles;
-  const int pgrid = (n_items + 255) / 256 < 2 * num_sms() ? (n_items + 255) / 256 : 2 * num_sms();
+  // 8x8 units (two pixels per lane) unless BGS_DEBUG_BWD_8X4 asks for the 8x4 ones
+  const int ppl = (F->debug_flags & BGS_DEBUG_BWD_8X4) ? 1 : 2;
+  const int n_units = 8 / ppl * F->num_tiles;
+  const int pgrid = (n_units + 255) / 256 < 2 * num_sms() ? (n_units + 255) / 256 : 2 * num_sms();
   if (cudaMemsetAsync(F->plan, 0, 4 * kPlanWords, s) != cudaSuccess) return check_launch("bwd plan memset");
-  k_bwd_plan_count<<<pgrid, 256, 0, s>>>(F->block_cost, n_items, F->ck_table, cap, F->seg_len, F->counters, F->plan);
+  k_bwd_plan_count<<<pgrid, 256, 0, s>>>(F->block_cost, n_units, ppl, F->ck_table, cap, F->seg_len, F->counters,
+                                         F->plan);
   k_plan_scan<<<1, kPlanBuckets, 0, s>>>(F->plan, F->counters, C_BWD_UNITS, C_BWD_TICKET, -1);
-  k_bwd_plan_place<<<pgrid, 256, 0, s>>>(F->block_cost, n_items, F->ck_table, cap, F->seg_len, F->counters, F->plan,
-                                         F->order_bwd);
+  k_bwd_plan_place<<<pgrid, 256, 0, s>>>(F->block_cost, n_units, ppl, F->ck_table, cap, F->seg_len, F->counters,
+                                         F->plan, F->order_bwd);
   note_launch(3);
   bgs_status st = check_launch("k_bwd_plan");
   if (st != BGS_OK) return st;
-  k_render_bwd<<<bwd_grid(), kBwdWarpsPerCta * 32, 0, s>>>(
-      F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,
-      dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool);
+  if (ppl == 2)
+    k_render_bwd<2><<<bwd_grid<2>(), kBwdWarpsPerCta * 32, 0, s>>>(
+        F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,
+        dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool);
+  else
+    k_render_bwd<1><<<bwd_grid<1>(), kBwdWarpsPerCta * 32, 0, s>>>(
+        F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,
+        dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool);
   note_launch();
   return check_launch("k_render_bwd");
 }

@@ -235,9 +235,12 @@ def test_render_bwd_parity(bgs, name):
         assert err <= GRAD_TOL, (name, gname, err)
 
 
-@pytest.mark.parametrize("name,seg_len", [("tiny", None), ("dense", None), ("garden20k", None), ("dense", 32),
-                                          ("dense", 96), ("garden20k", 64), ("ragged", 32)])
-def test_blend_bwd_intermediate_parity(bgs, name, seg_len):
+@pytest.mark.parametrize("name,seg_len,units", [("tiny", None, "8x8"), ("dense", None, "8x8"),
+                                                ("garden20k", None, "8x8"), ("dense", 32, "8x8"),
+                                                ("dense", 96, "8x8"), ("garden20k", 64, "8x8"),
+                                                ("ragged", 32, "8x8"), ("ragged", None, "8x4"),
+                                                ("dense", 32, "8x4"), ("garden20k", 64, "8x4")])
+def test_blend_bwd_intermediate_parity(bgs, name, seg_len, units):
     """a9 alone: the per-view blend gradients {dxy, dconic, dopacity, drgb} in grad2d vs
     the oracle's O15 sums (double).  seg_len: long walks split into list segments that
     start from the forward's checkpoints (bgs_frame_set_seg_len)."""
@@ -246,7 +249,8 @@ def test_blend_bwd_intermediate_parity(bgs, name, seg_len):
     else:
         s = scenes()[name]()
     cam = s.cameras[0]
-    r, theta, out = run_gpu(bgs, s, cam, max_keys=1 << 22, seg_len=seg_len)
+    flags = bgs.BGS_DEBUG_BWD_8X4 if units == "8x4" else 0  # 8x4 units: one pixel per lane
+    r, theta, out = run_gpu(bgs, s, cam, max_keys=1 << 22, seg_len=seg_len, flags=flags)
     if seg_len is not None:  # the split path is exercised: walks span several segments
         assert int(out["n_contrib"].max()) > 3 * seg_len
     ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
@@ -482,6 +486,31 @@ def test_split_backward_matches_unsplit(bgs, seg_len):
         r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=1 << 22, device=dev)
         bgs.bgs_frame_set_seg_len(r.frame, sl)
         out = r.forward(theta, cam, s.sh_degree)
+        g = torch.zeros_like(theta)
+        r.backward(theta, s.sh_degree, dl, out, g)
+        torch.cuda.synchronize()
+        grads.append(g.double())
+    a, b = grads
+    for gname, idx in oracle.group_slices(s.n).items():
+        idx_t = torch.as_tensor(np.arange(59 * s.n)[idx], device=dev)
+        err = float((a[idx_t] - b[idx_t]).norm() / max(float(a[idx_t].norm()), 1e-300))
+        assert err <= 1e-4, (gname, err)
+
+
+def test_bwd_unit_shapes_agree(bgs):
+    """8x8 (two pixels per lane) and 8x4 backward units are two schedules of the same sums:
+    theta gradients agree to float-atomic rounding (garden-shaped scene, split walks)."""
+    s = gen.garden(seed=3, n=30000, n_cams=2)
+    cam = s.cameras[0]
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    dl = torch.from_numpy(gen.random_dl_dimage(9, cam.width, cam.height)).to(dev)
+    grads = []
+    for flags in (0, bgs.BGS_DEBUG_BWD_8X4):
+        r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=1 << 22, device=dev, debug_flags=flags)
+        bgs.bgs_frame_set_seg_len(r.frame, 64)
+        out = r.forward(theta, cam, s.sh_degree)
+        out = r.forward(theta, cam, s.sh_degree)  # hinted: split forward, recorded checkpoints
         g = torch.zeros_like(theta)
         r.backward(theta, s.sh_degree, dl, out, g)
         torch.cuda.synchronize()
