@@ -675,7 +675,7 @@ def run_reference(args, rank, world):
     sec = (time.perf_counter() - t) / args.steps
     value = 1.0 / (sec * args.thin)
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3 * args.thin, 3),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3 * args.thin * args.views, 3),  # a step = args.views views
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32",
             "data": "synthetic", "config": arm_config(scene, args, world),
             "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "oracle",
