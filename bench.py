@@ -47,6 +47,9 @@ def parse():
     p.add_argument("--views", type=int, default=16)
     p.add_argument("--num-gaussians", dest="n", type=int, default=None,
                    help="override the Gaussian count (debug only)")
+    p.add_argument("--fuse-adam", action="store_true",
+                   help="G = 1: the chain rule and Adam in one pass (bgs_preprocess_bwd_batch_adam; measured "
+                        "slower at garden, 5.7 -> 8.3 ms per step, so off by default)")
     p.add_argument("--streams", type=int, default=1,
                    help="CUDA streams the step's views are spread over (round-robin; measured at garden: 1 -> 239.3, 2 -> 242.0, 3 -> 220.3 views/s, so 1 by default)")
     p.add_argument("--density-every", type=int, default=0,
@@ -74,12 +77,20 @@ def load_peaks():
         return PEAKS_FALLBACK, "fallback"
 
 
+def _update_desc(args, world):
+    if world > 1:
+        return "reduce-scatter + sharded Adam + all-gather" if args.update == "sharded" else "all-reduce + Adam"
+    if args.fuse_adam and not args.one_frame and args.views <= 16:
+        return "chain rule fused with Adam"
+    return "all-reduce (none at G = 1) + Adam"
+
+
 def arm_config(scene, args, world):
     """The workload description shared by both arms (ours and --impl reference)."""
     cam = scene.cameras[0]
     return {"workload": f"{scene.name}-shaped {scene.n} Gaussians, {cam.width}x{cam.height}, SH degree "
                         f"{scene.sh_degree}, batch of {args.views} views per step (fwd+bwd each, then "
-                        f"{'reduce-scatter + sharded Adam + all-gather' if world > 1 and args.update == 'sharded' else 'all-reduce + Adam'})",
+                        f"{_update_desc(args, world)})",
             "views_per_step": args.views, "n_gaussians": scene.n, "width": cam.width, "height": cam.height,
             "parallelism": f"view-dp{world}", "l2": "inputs larger than L2 (theta 1.37 GB, keys > 126 MB)",
             "loss": "0.8 L1 + 0.2 D-SSIM (11x11 Gaussian window)" if args.loss == "l1dssim" else "L1",
@@ -174,6 +185,8 @@ def run_ours(args, rank, world, local_rank):
     cams = [cams_all[v] for v in mine]
     W, H = cams[0].width, cams[0].height
     sharded = world > 1 and args.update == "sharded"
+    # one GPU, one chain-rule launch: a10 and a11 fused (no collective between them)
+    fused = world == 1 and not args.one_frame and args.fuse_adam and args.views <= 16
     total = 59 * n
     if sharded:
         # reduce-scatter -> Adam on this rank's 1/G shard -> all-gather: theta
@@ -366,11 +379,16 @@ def run_ours(args, rank, world, local_rank):
             stream.wait_event(ev)
         marks = []
         mark(marks)
-        if not args.one_frame:  # a10 once over the batch's views: theta/grad cross HBM once
+        theta, m, v, n, lo, hi = S["theta"], S["m"], S["v"], S["n"], S["lo"], S["hi"]
+        if fused:  # a10 + a11 in one pass per Gaussian: the gradient never reaches memory
+            bgs.bgs_preprocess_bwd_batch_adam(gs, frames, theta, None, m, v, hp, step_no[0])
+        elif not args.one_frame:  # a10 once over the batch's views: theta/grad cross HBM once
             bgs.bgs_preprocess_bwd_batch(gs, frames, grad)
         mark(marks)
-        theta, m, v, n, lo, hi = S["theta"], S["m"], S["v"], S["n"], S["lo"], S["hi"]
-        if sharded:  # NCCL over NVLink: reduce-scatter, Adam on the shard, all-gather
+        if fused:
+            mark(marks)
+            mark(marks)
+        elif sharded:  # NCCL over NVLink: reduce-scatter, Adam on the shard, all-gather
             g_shard = dp.reduce_scatter_grads(grad, rank, world)
             mark(marks)
             bgs.bgs_adam_step_range(theta[lo:hi], g_shard, m, v, n, lo, hi - lo, hp, step_no[0])
@@ -538,17 +556,24 @@ def run_ours(args, rank, world, local_rank):
     frac("render_fwd", (OPS_FWD_VISIT * Efc + OPS_FWD_BLEND * Ebl) / per_launch("render_fwd") / 1e12, fp32_peak,
          "T lane-ops/s", "alu")
     frac("blend_bwd", OPS_BWD_EVAL * Ebc / per_launch("blend_bwd") / 1e12, fp32_peak, "T lane-ops/s", "alu")
-    if args.one_frame:  # per view: theta 236 + blend grads 36 + grad RMW 472 per visible Gaussian
+    if fused:  # a10 + a11: theta 236 read + 708 written (theta, m, v) + m, v 472 read per Gaussian, + per
+        # (view, visible Gaussian) blend gradients 36 + radius 4 + clamp bits 1; radius 4 per (view, culled)
+        pb_bytes = 1416 * n + (37 * V + 4 * n) * steps_views
+        frac("preprocess_bwd", pb_bytes / max(per_step["preprocess_bwd"] / 1e3, 1e-12) / 1e9, hbm, "GB/s", "hbm")
+        roof["preprocess_bwd"]["ms_per_launch"] = per_step["preprocess_bwd"]
+        roof["preprocess_bwd"]["fused_with_adam"] = True
+    elif args.one_frame:  # per view: theta 236 + blend grads 36 + grad RMW 472 per visible Gaussian
         frac("preprocess_bwd", 744 * V / per_launch("preprocess_bwd") / 1e9, hbm, "GB/s", "hbm")
     else:  # batched over the rank's views: theta 236 + grad RMW 472 per Gaussian once, + per
         # (view, visible Gaussian) the blend gradients 36 + radius 4 + clamp bits 1; radius 4 per (view, culled)
         pb_bytes = 708 * n + (37 * V + 4 * n) * steps_views
         frac("preprocess_bwd", pb_bytes / max(per_step["preprocess_bwd"] / 1e3, 1e-12) / 1e9, hbm, "GB/s", "hbm")
         roof["preprocess_bwd"]["ms_per_launch"] = per_step["preprocess_bwd"] / -(-steps_views // 16)
-    adam_bytes = 1888 * n / (world if sharded else 1) + (236 * n if sharded else 0)  # + zeroing grad
-    roof["adam"] = {"bound": "hbm", "achieved": adam_bytes / max(per_step["adam"] / 1e3, 1e-12) / 1e9, "peak": hbm,
-                    "unit": "GB/s", "ms_per_launch": per_step["adam"]}
-    roof["adam"]["frac"] = roof["adam"]["achieved"] / hbm
+    if not fused:
+        adam_bytes = 1888 * n / (world if sharded else 1) + (236 * n if sharded else 0)  # + zeroing grad
+        roof["adam"] = {"bound": "hbm", "achieved": adam_bytes / max(per_step["adam"] / 1e3, 1e-12) / 1e9,
+                        "peak": hbm, "unit": "GB/s", "ms_per_launch": per_step["adam"]}
+        roof["adam"]["frac"] = roof["adam"]["achieved"] / hbm
     # the dominant KERNEL: stages that are one kernel launch (the sort stage is 13 kernels;
     # it is reported in stages_roofline)
     dom = max((s for s in roof if s != "sort"), key=lambda s: per_step[s])

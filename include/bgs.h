@@ -180,6 +180,18 @@ bgs_status bgs_preprocess_bwd(const bgs_gaussians* g /*host*/, bgs_frame* f /*ho
 bgs_status bgs_preprocess_bwd_batch(const bgs_gaussians* g /*host*/, bgs_frame* const* frames /*host*/,
                                     int32_t nframes, float* grad, void* stream);
 
+/* a10 + a11 fused for one GPU (no collective between them): the batched chain rule of
+ * bgs_preprocess_bwd_batch, then -- in the same kernel, per Gaussian -- the Adam update of
+ * bgs_adam_step with the batch's gradient, which is never written to memory (dense: a
+ * Gaussian no view sees takes g = 0, R26).  theta (device) must be the buffer g views
+ * (g->means == theta); exp_avg / exp_avg_sq [59n] (device).  With nframes > 16 the earlier
+ * launches accumulate into grad [59n] (device, zero on entry, zeroed on exit), else grad may
+ * be NULL.  Bit-identical to bgs_preprocess_bwd_batch into a zero grad + bgs_adam_step. */
+bgs_status bgs_preprocess_bwd_batch_adam(const bgs_gaussians* g /*host*/, bgs_frame* const* frames /*host*/,
+                                         int32_t nframes, float* theta, float* grad, float* exp_avg,
+                                         float* exp_avg_sq, const bgs_adam_hparams* hp /*host*/, int64_t step,
+                                         void* stream);
+
 /* a11: fused Adam over theta[59n] (R21, PyTorch semantics: bias-corrected, eps after
  * sqrt), per-group learning rate, grad zeroed on exit.  step is 1-based. */
 bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,

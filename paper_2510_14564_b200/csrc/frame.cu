@@ -326,6 +326,28 @@ bgs_status bgs_preprocess_bwd_batch(const bgs_gaussians* g, bgs_frame* const* fr
   return launch_preprocess_bwd_batch(g, F, nframes, grad, (cudaStream_t)stream);
 }
 
+bgs_status bgs_preprocess_bwd_batch_adam(const bgs_gaussians* g, bgs_frame* const* frames, int32_t nframes,
+                                         float* theta, float* grad, float* exp_avg, float* exp_avg_sq,
+                                         const bgs_adam_hparams* hp, int64_t step, void* stream) {
+  if (!frames || nframes < 1 || nframes > 4096 || !hp || step < 1) return BGS_ERR_INVALID;
+  static thread_local Frame* F[4096];
+  for (int v = 0; v < nframes; ++v) {
+    if (!frame_ok(frames[v]) || !frame_of(frames[v])->cam_valid) return BGS_ERR_INVALID;
+    F[v] = frame_of(frames[v]);
+    if (F[v]->n != F[0]->n) return BGS_ERR_INVALID;
+  }
+  bgs_status st = validate_gaussians(g, F[0]);
+  if (st != BGS_OK) return st;
+  const int64_t n = F[0]->n;
+  if (n == 0) return BGS_OK;
+  if (!theta || !exp_avg || !exp_avg_sq || (const float*)g->means != theta) return BGS_ERR_INVALID;
+  if (nframes > kPreBwdMaxViews && (!grad || ((uintptr_t)grad & 3u))) return BGS_ERR_INVALID;
+  if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f && hp->beta2 >= 0.0f && hp->beta2 < 1.0f && hp->eps >= 0.0f))
+    return BGS_ERR_INVALID;
+  return launch_preprocess_bwd_batch_impl(g, F, nframes, nframes > kPreBwdMaxViews ? grad : nullptr, theta,
+                                          exp_avg, exp_avg_sq, hp, step, (cudaStream_t)stream);
+}
+
 bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
                          const bgs_adam_hparams* hp, int64_t step, void* stream) {
   if (n < 0 || !hp || step < 1) return BGS_ERR_INVALID;

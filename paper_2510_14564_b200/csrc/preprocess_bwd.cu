@@ -42,9 +42,35 @@ struct PreBwdParams {
   int64_t n;
   int32_t deg, nviews;
   bool quat_vec4, sh_vec4, gq_vec4, gsh_vec4;  // 16-byte aligned -> vector paths
-  float* grad;  // theta layout
+  float* grad;  // theta layout (fused Adam: the partial sums of earlier launches, or null)
+  // fused Adam (R21; bgs_preprocess_bwd_batch_adam): theta += Adam(sum of the gradient)
+  bool adam;
+  float* theta;  // writable theta (the buffer the pointers above view)
+  float* m;
+  float* v;
+  float step_size[6], b1, b2, eps, inv_sqrt_bc2;
   PreBwdView view[kPreBwdMaxViews];
 };
+
+// One gradient element e of theta's layout: grad[e] += g, or (fused) the Adam update of
+// theta[e] with g plus the partial sum of earlier launches (R21, adam.cu's arithmetic).
+__device__ __forceinline__ void put_grad(const PreBwdParams& p, int64_t e, float g, int grp) {
+  if (!p.adam) {
+    p.grad[e] += g;
+    return;
+  }
+  if (p.grad) {
+    g += p.grad[e];
+    p.grad[e] = 0.0f;
+  }
+  float m = p.m[e], v = p.v[e];
+  m = fmaf(p.b1, m, (1.0f - p.b1) * g);
+  v = fmaf(p.b2, v, (1.0f - p.b2) * g * g);
+  const float denom = sqrtf(v) * p.inv_sqrt_bc2 + p.eps;
+  p.theta[e] = p.theta[e] - p.step_size[grp] * (m / denom);
+  p.m[e] = m;
+  p.v[e] = v;
+}
 
 constexpr int kBwdThreads = 64;
 constexpr int kRow = 49;  // padded row stride (floats) of the staged SH block: conflict-free
@@ -271,16 +297,14 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
     // ---- opacity
     {
       const float o = 1.0f / (1.0f + expf(-p.ologits[i]));
-      p.grad[10 * n + i] += gop * o * (1.0f - o);
+      put_grad(p, 10 * n + i, gop * o * (1.0f - o), 3);
     }
-    float* gm = p.grad + 3 * i;
-    gm[0] += dmx;
-    gm[1] += dmy;
-    gm[2] += dmz;
+    put_grad(p, 3 * i, dmx, 0);
+    put_grad(p, 3 * i + 1, dmy, 0);
+    put_grad(p, 3 * i + 2, dmz, 0);
     // ---- Sigma = M M^T, M = R diag(s): the summed dL/dSigma to (s, q) once
     const float GS[3][3] = {{GS00, GS01, GS02}, {GS01, GS11, GS12}, {GS02, GS12, GS22}};
     float gR[3][3];
-    float* gls = p.grad + 3 * n + 3 * i;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       float gsk = 0.f;
@@ -290,7 +314,7 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
         gsk += gM * R[r][k];
         gR[r][k] = gM * s[k];
       }
-      gls[k] += gsk * s[k];
+      put_grad(p, 3 * n + 3 * i + k, gsk * s[k], 1);
     }
     const float gw = 2.f * (-z * gR[0][1] + y * gR[0][2] + z * gR[1][0] - x * gR[1][2] - y * gR[2][0] + x * gR[2][1]);
     const float gx_ = 2.f * (y * gR[0][1] + z * gR[0][2] + y * gR[1][0] - 2.f * x * gR[1][1] - w * gR[1][2] +
@@ -301,7 +325,12 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
                              y * gR[1][2] + x * gR[2][0] + y * gR[2][1]);
     const float qd = gw * w + gx_ * x + gy_ * y + gz_ * z;
     const float d0 = (gw - w * qd) * iq, d1 = (gx_ - x * qd) * iq, d2 = (gy_ - y * qd) * iq, d3 = (gz_ - z * qd) * iq;
-    if (p.gq_vec4) {
+    if (p.adam) {
+      put_grad(p, 6 * n + 4 * i, d0, 2);
+      put_grad(p, 6 * n + 4 * i + 1, d1, 2);
+      put_grad(p, 6 * n + 4 * i + 2, d2, 2);
+      put_grad(p, 6 * n + 4 * i + 3, d3, 2);
+    } else if (p.gq_vec4) {
       float4* gq = reinterpret_cast<float4*>(p.grad + 6 * n) + i;
       float4 q4 = *gq;
       q4.x += d0;
@@ -317,10 +346,22 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
       gq[3] += d3;
     }
   }
+  else if (p.adam && i < n) {
+    // fused Adam is dense (R26): a Gaussian no view sees still takes g = 0
+    for (int e = 0; e < 3; ++e) put_grad(p, 3 * i + e, 0.0f, 0);
+    for (int e = 0; e < 3; ++e) put_grad(p, 3 * n + 3 * i + e, 0.0f, 1);
+    for (int e = 0; e < 4; ++e) put_grad(p, 6 * n + 4 * i + e, 0.0f, 2);
+    put_grad(p, 10 * n + i, 0.0f, 3);
+  }
   __syncwarp();
   // ---- coalesced read-modify-write of the warp's contiguous SH-gradient block
   //      (coefficients above the active degree stay zero in the row: no gradient, R12)
-  if (p.gsh_vec4) {
+  if (p.adam) {  // every coefficient of every Gaussian (dense Adam); group sh_dc = first 3
+    for (int c = lane; c < 48 * nvalid; c += 32) {
+      const int g = c / 48, e = c % 48;
+      put_grad(p, 11 * n + 48 * wbase + c, s_dsh[warp][g * kRow + e], e < 3 ? 4 : 5);
+    }
+  } else if (p.gsh_vec4) {
     float4* dst = reinterpret_cast<float4*>(p.grad + 11 * n) + 12 * wbase;
     for (int c = lane; c < 12 * nvalid; c += 32) {
       const int g = c / 12, e = 4 * (c % 12);
@@ -343,12 +384,30 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
   }
 }
 
-// a10 over a batch of views: grad += sum over the frames of each view's chain rule.
-bgs_status launch_preprocess_bwd_batch(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
-                                       cudaStream_t s) {
+// a10 over a batch of views: grad += sum over the frames of each view's chain rule; with
+// `adam` (hp != null) the last launch applies Adam instead of writing grad (grad may then be
+// null when one launch covers all views).
+bgs_status launch_preprocess_bwd_batch_impl(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
+                                            float* theta, float* m, float* v, const bgs_adam_hparams* hp,
+                                            int64_t step, cudaStream_t s) {
   const int64_t n = frames[0]->n;
   if (n == 0) return BGS_OK;
   PreBwdParams p;
+  p.adam = false;
+  p.theta = theta;
+  p.m = m;
+  p.v = v;
+  if (hp) {
+    const float lr[6] = {hp->lr_means, hp->lr_log_scales, hp->lr_quats, hp->lr_opacity, hp->lr_sh_dc,
+                         hp->lr_sh_rest};
+    const double bc1 = 1.0 - pow((double)hp->beta1, (double)step);
+    const double bc2 = 1.0 - pow((double)hp->beta2, (double)step);
+    for (int k = 0; k < 6; ++k) p.step_size[k] = (float)((double)lr[k] / bc1);
+    p.b1 = hp->beta1;
+    p.b2 = hp->beta2;
+    p.eps = hp->eps;
+    p.inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+  }
   p.means = g->means;
   p.log_scales = g->log_scales;
   p.quats = g->quats;
@@ -359,11 +418,12 @@ bgs_status launch_preprocess_bwd_batch(const bgs_gaussians* g, Frame* const* fra
   auto al16 = [](const void* q) { return ((uintptr_t)q & 15u) == 0; };
   p.quat_vec4 = al16(g->quats);
   p.sh_vec4 = al16(g->sh);
-  p.gq_vec4 = al16(grad + 6 * n);
-  p.gsh_vec4 = al16(grad + 11 * n);
+  p.gq_vec4 = grad && al16(grad + 6 * n);
+  p.gsh_vec4 = grad && al16(grad + 11 * n);
   p.grad = grad;
   for (int v0 = 0; v0 < nviews; v0 += kPreBwdMaxViews) {
     p.nviews = nviews - v0 < kPreBwdMaxViews ? nviews - v0 : kPreBwdMaxViews;
+    p.adam = hp != nullptr && v0 + p.nviews >= nviews;  // the last launch applies Adam
     for (int v = 0; v < p.nviews; ++v) {
       const Frame* F = frames[v0 + v];
       p.view[v].cam = F->cam;
@@ -377,6 +437,11 @@ bgs_status launch_preprocess_bwd_batch(const bgs_gaussians* g, Frame* const* fra
     if (st != BGS_OK) return st;
   }
   return BGS_OK;
+}
+
+bgs_status launch_preprocess_bwd_batch(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
+                                       cudaStream_t s) {
+  return launch_preprocess_bwd_batch_impl(g, frames, nviews, grad, nullptr, nullptr, nullptr, nullptr, 0, s);
 }
 
 bgs_status launch_preprocess_bwd(const bgs_gaussians* g, Frame* F, float* grad, cudaStream_t s) {
