@@ -595,8 +595,8 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "ms_per_view": round(ms_step / args.views, 4),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded garden-shaped scene, gen/; random-init parameters; targets = render of a "
-                "perturbed copy)",
+        "data": f"synthetic (seeded {scene.name}-shaped scene, gen/; random-init parameters; targets = render of "
+                "a perturbed copy)",
         "config": arm_config(scene, args, world),
         "clocks": clocks, "gpu_launches": int(launches), "roofline": roofline,
         "stages_ms_per_step": {k2: round(v2, 4) for k2, v2 in per_step.items()},
