@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--view", type=int, default=0)
     ap.add_argument("--only", default=None, help="comma-separated stage names")
     ap.add_argument("--step", type=int, default=0, help="run N full one-view training steps (for ncu)")
-    ap.add_argument("--debug-flags", type=int, default=0, help="--seg-lens: frame debug flags (timing experiments)")
+    ap.add_argument("--debug-flags", type=int, default=0, help="frame debug flags (timing experiments)")
     ap.add_argument("--views", type=int, default=1, help="--step: views per step (batched chain rule)")
     ap.add_argument("--seg-lens", default=None, help="comma-separated seg_len values: time fwd/bwd for each")
     a = ap.parse_args()
@@ -33,7 +33,7 @@ def main():
     dev = torch.device("cuda")
     theta = torch.from_numpy(s.theta).to(dev)
     grad = torch.zeros_like(theta)
-    r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=1 << 26, device=dev)
+    r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=1 << 26, device=dev, debug_flags=a.debug_flags)
     out = r.forward(theta, cam, s.sh_degree)
     dl = torch.full((3, cam.height, cam.width), 1e-6, device=dev)
     g = bgs.gaussians(theta, s.n, s.sh_degree)
