@@ -16,8 +16,15 @@ constexpr int kTilePixels = kTile * kTile;
 constexpr int kCkMax = 63;
 constexpr int kSegLenDefault = 4096;
 constexpr int kCkPoolSeg = 2048;
-// direct tile split (sort.cu): 16384-item chunks; per-warp shared-memory tile counters
-constexpr int kChunkItemsF = 16384;
+// direct tile split (sort.cu): chunks of 2048..16384 items (a power of two chosen on the
+// device from K so that there are >= kChunkTarget chunks: one warp each); per-warp
+// shared-memory tile counters
+constexpr int kChunkItemsMin = 2048, kChunkItemsMax = 16384, kChunkTarget = 2048;
+__host__ __device__ __forceinline__ uint32_t chunk_items_of(uint32_t K) {
+  uint32_t c = kChunkItemsMax;
+  while (c > (uint32_t)kChunkItemsMin && K / c < (uint32_t)kChunkTarget) c >>= 1;
+  return c;
+}
 constexpr int kDirectMaxCells = 12800;  // (tiles_x + 1)(tiles_y + 1) bound  // the checkpoint / state pools are sized for seg_len >= this
 
 // blend work-unit planning (k_*_plan_*): 128 cost buckets (4 per octave, costliest first),

@@ -109,7 +109,7 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.spec_state = take(512 * (size_t)L.ck_cap);
   L.spec_last = take(128 * (size_t)L.ck_cap);
   L.direct = (int64_t)(L.tiles_x + 1) * (L.tiles_y + 1) <= kDirectMaxCells;
-  L.chunk_cnt = L.direct ? take(4 * NT * (size_t)((max_keys + kChunkItemsF - 1) / kChunkItemsF)) : 0;
+  L.chunk_cnt = L.direct ? take(4 * NT * (size_t)((max_keys + kChunkItemsMin - 1) / kChunkItemsMin)) : 0;
   L.dkey0 = take(4 * N);
   L.dkey1 = take(4 * N);
   L.dval0 = take(4 * N);

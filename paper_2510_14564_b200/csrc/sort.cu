@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kDupThreads) k_emit_ranked(int64_t n, const ui
 // ---------------------------------------------------------------- direct tile split
 // Replaces (3)-(4) of the depth-first path when the tile grid is small enough for
 // per-warp shared-memory tile counters: the depth-ordered item sequence is cut into
-// chunks of kChunkItems items; (a) each chunk counts its items per tile (its ranks'
+// chunks of chunk_items_of(K) items (common.cuh); (a) each chunk counts its items per tile (its ranks'
 // rects, clipped to the chunk, added as 2D difference rectangles and prefix-summed);
 // (b) a column scan over chunks gives each (chunk, tile) its offset inside the tile's
 // list; (c) each chunk emits its items in depth order straight to their final positions,
@@ -283,7 +283,6 @@ __global__ void __launch_bounds__(kDupThreads) k_emit_ranked(int64_t n, const ui
 // a 32-item batch, equal tiles are ranked by match_any).  The order is the stable split
 // of the depth-ordered sequence by tile -- the same (tile, depth, index) order -- with no
 // keys materialised and no radix passes over K.
-constexpr int kChunkItems = kChunkItemsF;
 constexpr int kChunkWarps = 4;
 
 // largest rank r with item_off[r] <= a (a rank with zero items shares its offset with the
@@ -314,12 +313,12 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_chunk_hist(int64_t n, cons
   const int gw = tiles_x + 1, cells = gw * (tiles_y + 1), nt = tiles_x * tiles_y;
   int32_t* G = s_grid + warp * cells;
   const uint32_t K = counters[C_SCAN_TOTAL];
-  const uint32_t n_chunks = (K + kChunkItems - 1) / kChunkItems;
+  const uint32_t CI = chunk_items_of(K), n_chunks = (K + CI - 1) / CI;
   const uint32_t c = blockIdx.x * kChunkWarps + warp;
   if (c >= n_chunks) return;
   for (int k = lane; k < cells; k += 32) G[k] = 0;
   __syncwarp();
-  const uint32_t a = c * kChunkItems, b = min(K, a + kChunkItems);
+  const uint32_t a = c * CI, b = min(K, a + CI);
   auto add_rect = [&](int x0, int y0, int x1, int y1) {  // [x0, x1) x [y0, y1), non-empty
     atomicAdd(&G[y0 * gw + x0], 1);
     atomicAdd(&G[y0 * gw + x1], -1);
@@ -385,7 +384,8 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(uint32_t* chunk_cnt, int32_
   __shared__ uint32_t s[32][33];
   if (counters[C_OVERFLOW]) return;
   const uint32_t K = counters[C_SCAN_TOTAL];
-  const int n_chunks = (int)((K + kChunkItems - 1) / kChunkItems);
+  const uint32_t CI = chunk_items_of(K);
+  const int n_chunks = (int)((K + CI - 1) / CI);
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int t = blockIdx.x * 32 + tx;
   const int per = (n_chunks + 31) / 32;
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
   if (counters[C_OVERFLOW]) return;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t K = counters[C_SCAN_TOTAL];
-  const uint32_t n_chunks = (K + kChunkItems - 1) / kChunkItems;
+  const uint32_t CI = chunk_items_of(K), n_chunks = (K + CI - 1) / CI;
   const uint32_t c = blockIdx.x * kEmitWarps + warp;
   if (c >= n_chunks) return;
   const int nt_pad = (nt + 3) & ~3;
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
   const uint32_t* row = chunk_cnt + (size_t)c * nt;
   for (int t = lane; t < nt; t += 32) nxt[t] = ranges[t].x + row[t];
   __syncwarp();
-  const uint32_t a = c * kChunkItems, b = min(K, a + kChunkItems);
+  const uint32_t a = c * CI, b = min(K, a + CI);
   int64_t rb = rank_of_item(item_off, n, a, lane);
   auto load_win = [&](int64_t base, uint32_t& t, uint32_t& off, uint32_t& gid, uint2& rc) {
     const int64_t r = base + lane;
@@ -639,7 +639,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
     // (3') direct tile split: per-(chunk, tile) counts, column scan, ranges, emission
     F->final_buf = 0;
     const int gw = F->tiles_x + 1, cells = gw * (F->tiles_y + 1), nt = F->num_tiles;
-    const int64_t max_chunks = (F->max_keys + kChunkItems - 1) / kChunkItems;
+    const int64_t max_chunks = (F->max_keys + kChunkItemsMin - 1) / kChunkItemsMin;  // device picks the size
     const int blocks = (int)((max_chunks + kChunkWarps - 1) / kChunkWarps);
     static bool attr = false;
     if (!attr) {

@@ -23,6 +23,11 @@ METRICS = [
     ("launch__registers_per_thread", "regs"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
     ("smsp__inst_executed.sum", "warp inst"),
+    ("smsp__inst_executed_pipe_xu.sum", "xu (MUFU) inst"),
+    ("lts__t_sectors_op_red.sum", "L2 RED sectors"),
+    ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "L1 global ld sectors"),
+    ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "L1 global ld requests"),
+    ("sm__cycles_elapsed.avg.per_second", "SM clock"),
 ]
 
 
