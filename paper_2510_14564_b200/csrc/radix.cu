@@ -19,6 +19,7 @@ namespace bgs {
 constexpr int kSortThreads = 256, kSortItems = 16, kSortTile = kSortThreads * kSortItems, kRadix = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr uint32_t kStA = 1u << 30, kStP = 2u << 30, kStMask = (1u << 30) - 1;
+constexpr int kLookBatch = 8;
 
 __device__ __forceinline__ uint64_t load_k(const uint32_t* counters) {
   return ((uint64_t)counters[C_K_HI] << 32) | counters[C_K_LO];
@@ -141,16 +142,28 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
       for (int w = 0; w < warp; ++w) off += S.scan_tmp[w];
       S.tile_start[tid] = off + incl - cnt;
     }
-    // look-back for digit tid
+    // look-back for digit tid: the statuses of kLookBatch predecessors are loaded together
+    // (independent loads in flight), then consumed in order until an inclusive prefix; an
+    // entry not yet published is re-polled alone.  A serial one-at-a-time walk through
+    // aggregate-only predecessors cost one L2 round trip per tile in the first wave.
     uint32_t prefix = 0;
     if (tile > 0) {
-      for (int64_t j = tile - 1; j >= 0; --j) {
-        uint32_t sv;
-        do {
-          sv = ld_relaxed_u32(&status[j * kRadix + tid]);
-        } while ((sv >> 30) == 0);
-        prefix += sv & kStMask;
-        if ((sv >> 30) == 2) break;
+      int64_t j = tile - 1;
+      bool done = false;
+      while (!done) {
+        uint32_t sv[kLookBatch];
+#pragma unroll
+        for (int q = 0; q < kLookBatch; ++q)
+          sv[q] = (j - q >= 0) ? ld_relaxed_u32(&status[(j - q) * kRadix + tid]) : kStP;
+#pragma unroll
+        for (int q = 0; q < kLookBatch; ++q) {
+          if (done) break;
+          uint32_t v = sv[q];
+          while ((v >> 30) == 0) v = ld_relaxed_u32(&status[(j - q) * kRadix + tid]);
+          prefix += v & kStMask;
+          done = (v >> 30) == 2;
+        }
+        j -= kLookBatch;
       }
       st_relaxed_u32(&st[tid], kStP | (prefix + cnt));
     }
