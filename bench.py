@@ -334,7 +334,7 @@ def run_ours(args, rank, world, local_rank):
         dens_log.append({"step": step_no[0], "n_before": n0, "n_after": n2, "pairs": int(rep.n_pairs),
                          "children": int(rep.n_children)})
 
-    def one_step(tgts, record=None):
+    def one_step(tgts, record=None, tgt_events=None):
         step_no[0] += 1
 
         def mark(marks):
@@ -362,6 +362,8 @@ def run_ours(args, rank, world, local_rank):
                 mark(marks)
                 bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
                 mark(marks)
+                if tgt_events is not None:  # this view's target has arrived (H2D on the copy stream)
+                    sj.wait_event(tgt_events[j])
                 if loss_ws is not None:  # the 3DGS loss 0.8 L1 + 0.2 D-SSIM (NEXT-2), batch mean
                     bgs.bgs_l1_dssim_loss_grad(rj.image, tgts[j], W, H, 0.2, 1.0 / args.views, dl, loss, loss_ws)
                 else:  # L1 (R19)
@@ -463,10 +465,19 @@ def run_ours(args, rank, world, local_rank):
     # ---- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        copy_stream = torch.cuda.Stream(device=dev)
+        tgt_events = [torch.cuda.Event() for _ in cams]
+
         def e2e_step():
-            for j in range(len(cams)):
-                targets_e2e[j].copy_(targets_host[j], non_blocking=True)
-            one_step(targets_e2e)
+            # the step's 16 targets go H2D on a copy stream (after the previous step released
+            # the buffers); view j's loss waits for target j only, so the copies overlap the
+            # earlier views' work
+            copy_stream.wait_stream(stream)
+            with torch.cuda.stream(copy_stream):
+                for j in range(len(cams)):
+                    targets_e2e[j].copy_(targets_host[j], non_blocking=True)
+                    tgt_events[j].record(copy_stream)
+            one_step(targets_e2e, tgt_events=tgt_events)
             loss_host.copy_(loss, non_blocking=True)
 
         e2e_step()  # warm-up of the copy path
