@@ -181,6 +181,9 @@ struct StepWs {
   double* part;                 // [stat blocks][4] {sum rho, sum rho^2, sum d, sum d^2}
   uint32_t* flags;              // [4] {points with < k neighbours within 3 r, ...}
   bgs_density_report* rep;      // device copy of the report
+  float4* spts;                 // [n] {x, y, z, index bits} in grid (bucket) order
+  uint32_t* srho;               // [n] rho in grid order
+  uint32_t* occ;                // [M / 32] bucket occupancy bits (L2-resident: empty cells skip start/end)
   int64_t stat_blocks, scan_blocks;
 };
 
@@ -196,7 +199,11 @@ static bool step_layout(int64_t n, char* base, StepWs* w, size_t* total) {
   };
   const size_t a_rho = take(4 * (size_t)n), a_dbar = take(8 * (size_t)n), a_nn = take(4 * (size_t)n),
                a_pk = take(8 * (size_t)n), a_blk = take(8 * (size_t)(scan_blocks + 1)),
-               a_part = take(32 * (size_t)stat_blocks), a_fl = take(16), a_rep = take(sizeof(bgs_density_report));
+               a_part = take(32 * (size_t)stat_blocks), a_fl = take(16), a_rep = take(sizeof(bgs_density_report)),
+               a_sp = take(16 * (size_t)n), a_sr = take(4 * (size_t)n);
+  uint32_t Mb = 1024;  // the grid's bucket count, as dens_layout picks it
+  while ((int64_t)Mb < 2 * n) Mb <<= 1;
+  const size_t a_occ = take(4 * (size_t)(Mb / 32));
   if (total) *total = o;
   if (w && base) {
     dens_layout(n, base, &w->g, nullptr);
@@ -208,6 +215,9 @@ static bool step_layout(int64_t n, char* base, StepWs* w, size_t* total) {
     w->part = (double*)(base + a_part);
     w->flags = (uint32_t*)(base + a_fl);
     w->rep = (bgs_density_report*)(base + a_rep);
+    w->spts = (float4*)(base + a_sp);
+    w->srho = (uint32_t*)(base + a_sr);
+    w->occ = (uint32_t*)(base + a_occ);
     w->stat_blocks = stat_blocks;
     w->scan_blocks = scan_blocks;
   }
@@ -221,20 +231,66 @@ __device__ __forceinline__ double sqd(const float* means, int64_t p, int64_t q) 
   return (dx * dx + dy * dy) + dz * dz;
 }
 
-// rho (27 cells, float decision) + the k nearest (double, rings until exact) per point;
-// per-block partial sums of rho, rho^2, the k distances and their squares.
-__global__ void __launch_bounds__(kStepThreads) k_rho_knn(int64_t n, const float* __restrict__ means, float inv_cs,
+// the points in grid order: neighbour scans read a bucket's points as consecutive float4s
+// (no index -> coordinate gather per candidate)
+__global__ void __launch_bounds__(256) k_sorted_pts(int64_t n, const float* __restrict__ means,
+                                                   const uint32_t* __restrict__ sval, float4* spts) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = sval[j];
+    spts[j] = make_float4(means[3 * (int64_t)q], means[3 * (int64_t)q + 1], means[3 * (int64_t)q + 2],
+                          __uint_as_float(q));
+  }
+}
+
+__device__ __forceinline__ bool occupied(const uint32_t* occ, uint32_t h) { return (occ[h >> 5] >> (h & 31)) & 1u; }
+
+__device__ __forceinline__ double sqd_f(float px, float py, float pz, const float4 q) {
+  const double dx = (double)q.x - (double)px, dy = (double)q.y - (double)py, dz = (double)q.z - (double)pz;
+  return (dx * dx + dy * dy) + dz * dz;
+}
+
+// rho (27 cells, float decision) + the k nearest (double) per point, one thread per point in
+// grid order (a warp's points share their neighbour buckets); rings 0-1 serve both, rings
+// 2..3 only the kNN of points whose k-th neighbour is farther than one cell.  Per-block
+// partial sums of rho, rho^2, the k distances and their squares.
+__global__ void __launch_bounds__(kStepThreads) k_rho_knn(int64_t n, const float4* __restrict__ spts, float inv_cs,
                                                           float cs, float r2, float r_param, uint32_t mask, int k,
-                                                          const uint32_t* __restrict__ sval,
                                                           const uint32_t* __restrict__ start,
-                                                          const uint32_t* __restrict__ end, uint32_t* rho_out,
+                                                          const uint32_t* __restrict__ end,
+                                                          const uint32_t* __restrict__ occ, uint32_t* rho_out,
                                                           double* dbar, double* part, uint32_t* flags) {
   double s_r = 0, s_r2 = 0, s_d = 0, s_d2 = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    int cx, cy, cz;
-    cell_of(means, i, inv_cs, cx, cy, cz);
-    const float px = means[3 * i], py = means[3 * i + 1], pz = means[3 * i + 2];
-    // rho: the 27 neighbour buckets, each distinct bucket once
+  const int kk = (int)((int64_t)k < n - 1 ? (int64_t)k : n - 1);
+  for (int64_t jp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jp < n; jp += (int64_t)gridDim.x * blockDim.x) {
+    const float4 me = spts[jp];
+    const uint32_t i = __float_as_uint(me.w);
+    const float px = me.x, py = me.y, pz = me.z;
+    const int cx = (int)floorf(px * inv_cs), cy = (int)floorf(py * inv_cs), cz = (int)floorf(pz * inv_cs);
+    double bd[kKnnMax];
+    uint32_t bq[kKnnMax];
+    int nb = 0;
+    // the current k-th best (d2, q) in registers: the common case -- a candidate farther
+    // than it -- is rejected without touching the (local-memory) sorted list
+    double wd = 1.0e300;
+    uint32_t wq = 0xffffffffu;
+    auto insert = [&](double d2, uint32_t q) {
+      if (d2 > wd || (d2 == wd && q >= wq)) return;
+      for (int t = 0; t < nb; ++t)
+        if (bq[t] == q) return;  // reached again through a colliding cell
+      int pos = nb < kk ? nb++ : kk - 1;
+      while (pos > 0 && (bd[pos - 1] > d2 || (bd[pos - 1] == d2 && bq[pos - 1] > q))) {
+        bd[pos] = bd[pos - 1];
+        bq[pos] = bq[pos - 1];
+        --pos;
+      }
+      bd[pos] = d2;
+      bq[pos] = q;
+      if (nb == kk) {
+        wd = bd[kk - 1];
+        wq = bq[kk - 1];
+      }
+    };
+    // rings 0-1: the 27 buckets (each distinct one once) for rho and the kNN
     uint32_t seen[27];
     int nseen = 0;
     uint32_t c = 0;
@@ -246,53 +302,36 @@ __global__ void __launch_bounds__(kStepThreads) k_rho_knn(int64_t n, const float
           for (int t = 0; t < nseen; ++t) dup |= seen[t] == h;
           if (dup) continue;
           seen[nseen++] = h;
+          if (!occupied(occ, h)) continue;
           const uint32_t e = end[h];
           for (uint32_t j = start[h]; j < e; ++j) {
-            const uint32_t q = sval[j];
-            if (q == (uint32_t)i) continue;
-            const float ddx = means[3 * (int64_t)q] - px;
-            const float ddy = means[3 * (int64_t)q + 1] - py;
-            const float ddz = means[3 * (int64_t)q + 2] - pz;
+            const float4 qp = spts[j];
+            const uint32_t q = __float_as_uint(qp.w);
+            if (q == i) continue;
+            const float ddx = qp.x - px, ddy = qp.y - py, ddz = qp.z - pz;
             if ((ddx * ddx + ddy * ddy) + ddz * ddz <= r2) ++c;
+            if (kk > 0) insert(sqd_f(px, py, pz, qp), q);
           }
         }
     rho_out[i] = c;
     s_r += (double)c;
     s_r2 += (double)c * (double)c;
-    // kNN: sorted (d2, q) lists; a point reached through two colliding cells is inserted once.
-    // Ring R = the shell of cells at Chebyshev distance R; after rings 0..R every point within
-    // R cs of p has been seen.
-    double bd[kKnnMax];
-    uint32_t bq[kKnnMax];
-    int nb = 0;
-    const int kk = (int)((int64_t)k < n - 1 ? (int64_t)k : n - 1);
-    bool exact = kk == 0;
-    for (int R = 0; R <= kMaxRing && !exact; ++R) {
+    // every point within R cs has been seen after ring R; rings 2..kMaxRing when needed
+    bool exact = kk == 0 || (nb == kk && bd[kk - 1] <= (double)cs * (double)cs);
+    for (int R = 2; R <= kMaxRing && !exact; ++R) {
       for (int dz = -R; dz <= R; ++dz)
         for (int dy = -R; dy <= R; ++dy)
           for (int dx = -R; dx <= R; ++dx) {
             if (max(abs(dx), max(abs(dy), abs(dz))) != R) continue;  // the shell of ring R
             const uint32_t h = cell_hash(cx + dx, cy + dy, cz + dz, mask);
+            if (!occupied(occ, h)) continue;
             const uint32_t e = end[h];
             for (uint32_t j = start[h]; j < e; ++j) {
-              const uint32_t q = sval[j];
-              if (q == (uint32_t)i) continue;
-              const double d2 = sqd(means, i, q);
-              if (nb == kk && (d2 > bd[kk - 1] || (d2 == bd[kk - 1] && q >= bq[kk - 1]))) continue;
-              bool dup = false;
-              for (int t = 0; t < nb; ++t) dup |= bq[t] == q;
-              if (dup) continue;
-              int pos = nb < kk ? nb++ : kk - 1;
-              while (pos > 0 && (bd[pos - 1] > d2 || (bd[pos - 1] == d2 && bq[pos - 1] > q))) {
-                bd[pos] = bd[pos - 1];
-                bq[pos] = bq[pos - 1];
-                --pos;
-              }
-              bd[pos] = d2;
-              bq[pos] = q;
+              const float4 qp = spts[j];
+              const uint32_t q = __float_as_uint(qp.w);
+              if (q != i) insert(sqd_f(px, py, pz, qp), q);
             }
           }
-      // every point within R cells' reach (distance <= R cs) has been seen
       const double reach = (double)R * (double)cs;
       exact = nb == kk && bd[kk - 1] <= reach * reach;
     }
@@ -328,6 +367,19 @@ __global__ void __launch_bounds__(kStepThreads) k_rho_knn(int64_t n, const float
   }
 }
 
+__global__ void __launch_bounds__(256) k_bucket_occ(int64_t n, const uint32_t* __restrict__ key, uint32_t* occ) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = key[i];
+    if (i == 0 || key[i - 1] != h) atomicOr(&occ[h >> 5], 1u << (h & 31));
+  }
+}
+
+__global__ void __launch_bounds__(256) k_sorted_rho(int64_t n, const float4* __restrict__ spts,
+                                                   const uint32_t* __restrict__ rho, uint32_t* srho) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    srho[j] = rho[__float_as_uint(spts[j].w)];
+}
+
 // The statistics (R31-R32) into the device report: population sigma of rho and of the
 // pooled k-distances, the thresholds and d_merge.
 __global__ void k_step_stats(int64_t n, int k, int blocks, const double* part, bgs_density_params prm,
@@ -347,20 +399,23 @@ __global__ void k_step_stats(int64_t n, int k, int blocks, const double* part, b
   rep->d_merge = rep->mu_d + (double)prm.gamma * rep->sigma_d;
 }
 
-// R33: each dense point's nearest other dense point within d_merge (ties: lower index).
-__global__ void __launch_bounds__(kStepThreads) k_merge_nn(int64_t n, const float* __restrict__ means, float inv_cs,
-                                                           float cs, uint32_t mask, const uint32_t* __restrict__ sval,
+// R33: each dense point's nearest other dense point within d_merge (ties: lower index); one
+// thread per point in grid order, candidates read as consecutive float4s with their rho.
+__global__ void __launch_bounds__(kStepThreads) k_merge_nn(int64_t n, const float4* __restrict__ spts,
+                                                           const uint32_t* __restrict__ srho, float inv_cs,
+                                                           float cs, uint32_t mask,
                                                            const uint32_t* __restrict__ start,
                                                            const uint32_t* __restrict__ end,
-                                                           const uint32_t* __restrict__ rho,
+                                                           const uint32_t* __restrict__ occ,
                                                            const bgs_density_report* rep, int32_t* nn) {
   const double hi = rep->rho_high, dm = rep->d_merge, lim = dm * dm;
   const int R = (int)ceil(dm / (double)cs);
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t jp = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; jp < n; jp += (int64_t)gridDim.x * blockDim.x) {
+    const float4 me = spts[jp];
+    const uint32_t i = __float_as_uint(me.w);
     int best = -1;
-    if ((double)rho[i] > hi) {
-      int cx, cy, cz;
-      cell_of(means, i, inv_cs, cx, cy, cz);
+    if ((double)srho[jp] > hi) {
+      const int cx = (int)floorf(me.x * inv_cs), cy = (int)floorf(me.y * inv_cs), cz = (int)floorf(me.z * inv_cs);
       double bd = 0.0;
       // rings of cells outwards; after ring R every point within R cs has been seen, so the
       // search stops once the best candidate lies within that reach (or at d_merge's ring)
@@ -370,11 +425,13 @@ __global__ void __launch_bounds__(kStepThreads) k_merge_nn(int64_t n, const floa
             for (int dx = -Rg; dx <= Rg; ++dx) {
               if (max(abs(dx), max(abs(dy), abs(dz))) != Rg) continue;
               const uint32_t h = cell_hash(cx + dx, cy + dy, cz + dz, mask);
+              if (!occupied(occ, h)) continue;
               const uint32_t e = end[h];
               for (uint32_t j = start[h]; j < e; ++j) {
-                const uint32_t q = sval[j];
-                if (q == (uint32_t)i || !((double)rho[q] > hi)) continue;
-                const double d2 = sqd(means, i, q);
+                const float4 qp = spts[j];
+                const uint32_t q = __float_as_uint(qp.w);
+                if (q == i || !((double)srho[j] > hi)) continue;
+                const double d2 = sqd_f(me.x, me.y, me.z, qp);
                 if (d2 > lim) continue;
                 if (best < 0 || d2 < bd || (d2 == bd && (int)q < best)) {
                   bd = d2;
@@ -628,15 +685,21 @@ bgs_status bgs_density_plan(const float* theta, int64_t n, const bgs_density_par
   k_bucket_ranges<<<grid, 256, 0, s>>>(n, w.g.key[fb], w.g.start, w.g.end);
   note_launch();
   if ((st = check_launch("k_bucket_ranges")) != BGS_OK) return st;
-  k_rho_knn<<<(int)w.stat_blocks, kStepThreads, 0, s>>>(n, means, inv_cs, cs, p->r * p->r, p->r, mask, p->k,
-                                                        w.g.val[fb],
-                                                        w.g.start, w.g.end, w.rho, w.dbar, w.part, w.flags);
+  k_sorted_pts<<<grid, 256, 0, s>>>(n, means, w.g.val[fb], w.spts);
+  note_launch();
+  if (cudaMemsetAsync(w.occ, 0, 4 * (size_t)(w.g.M / 32), s) != cudaSuccess) return check_launch("occ memset");
+  k_bucket_occ<<<grid, 256, 0, s>>>(n, w.g.key[fb], w.occ);
+  note_launch();
+  k_rho_knn<<<(int)w.stat_blocks, kStepThreads, 0, s>>>(n, w.spts, inv_cs, cs, p->r * p->r, p->r, mask, p->k,
+                                                        w.g.start, w.g.end, w.occ, w.rho, w.dbar, w.part, w.flags);
   note_launch();
   if ((st = check_launch("k_rho_knn")) != BGS_OK) return st;
+  k_sorted_rho<<<grid, 256, 0, s>>>(n, w.spts, w.rho, w.srho);
+  note_launch();
   k_step_stats<<<1, 32, 0, s>>>(n, p->k, (int)w.stat_blocks, w.part, *p, w.rep);
   note_launch();
   if ((st = check_launch("k_step_stats")) != BGS_OK) return st;
-  k_merge_nn<<<grid, kStepThreads, 0, s>>>(n, means, inv_cs, cs, mask, w.g.val[fb], w.g.start, w.g.end, w.rho, w.rep,
+  k_merge_nn<<<grid, kStepThreads, 0, s>>>(n, w.spts, w.srho, inv_cs, cs, mask, w.g.start, w.g.end, w.occ, w.rep,
                                           w.nn);
   note_launch();
   if ((st = check_launch("k_merge_nn")) != BGS_OK) return st;
