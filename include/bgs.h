@@ -340,6 +340,10 @@ bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contri
 /* Kept selectable: the blend backward on 8x4-pixel units (one pixel per lane) instead of
  * the default 8x8 units (two pixels per lane). */
 #define BGS_DEBUG_BWD_8X4 8
+/* Parity mode (R23): the blend kernels evaluate exp with the canonical expression tree the
+ * oracle also uses (instead of MUFU.EX2) and the forward does not split walks, so every
+ * blend decision, n_contrib and the image are bit-identical to the oracle's. */
+#define BGS_DEBUG_PARITY_EXP 64
 bgs_status bgs_frame_set_debug(bgs_frame* f /*host*/, int32_t flags);
 
 /* Scheduling parameter of the blend kernels (default 4096): a (tile, 8x4 pixel block) work

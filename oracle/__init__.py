@@ -24,6 +24,7 @@ LIB = os.path.join(HERE, "liborc.so")
 NO_LOWPASS, NO_JCLAMP, FULL_RECT = 1, 2, 4
 NO_ALPHA_CLAMP, NO_ALPHA_CUTOFF, NO_EARLY_STOP, NO_POWER_GUARD = 8, 16, 32, 64
 PLAIN = 127
+CANON_EXP = 128  # R23 parity mode: the canonical exponential the GPU's parity mode also uses
 # clamp bits
 CB_R, CB_G, CB_B, CB_JX, CB_JX_NEG, CB_JY, CB_JY_NEG = 1, 2, 4, 8, 16, 32, 64
 
@@ -91,6 +92,7 @@ def lib():
                 "orc_adam": [C.c_int64, P, P, P, P, P, C.c_double, C.c_double, C.c_double, C.c_int64],
                 "orc_local_density": [C.c_int64, P, C.c_float, P],
                 "orc_knn_mean": [C.c_int64, P, C.c_int32, P],
+                "orc_canon_exp": [C.c_int64, P, P],
             }
             for name, args in sig.items():
                 fn = getattr(l, name)
@@ -224,6 +226,14 @@ def adam(theta, grad, m, v, n, lr6, b1=0.9, b2=0.999, eps=1e-15, step=1):
     lr = np.asarray(lr6, np.float64)
     lib().orc_adam(n, _p(th), _p(gr), _p(mm), _p(vv), _p(lr), b1, b2, eps, step)
     return th, mm, vv
+
+
+def canon_exp(x) -> np.ndarray:
+    """R23 parity mode: the canonical float exponential (bgs_oracle.cpp canon_exp)."""
+    a = np.ascontiguousarray(x, np.float32)
+    out = np.zeros_like(a)
+    lib().orc_canon_exp(a.size, _p(a), _p(out))
+    return out
 
 
 def local_density(means, r) -> np.ndarray:

@@ -51,7 +51,24 @@ enum : uint32_t {
   ORC_NO_ALPHA_CUTOFF = 16u, // R14 skip alpha < 1/255
   ORC_NO_EARLY_STOP = 32u,   // R15
   ORC_NO_POWER_GUARD = 64u,  // R14 skip power > 0
+  ORC_CANON_EXP = 128u,      // R23 parity mode: G from canon_exp instead of std::exp
 };
+
+// R23's optional parity mode: a canonical exponential both sides evaluate
+// with the same IEEE binary32 operations -- x = power * log2(e); n = floor(x); f = x - n
+// (exact); 2^f from the degree-8 Taylor polynomial of e^(f ln 2) in Horner form with fused
+// multiply-adds; times 2^n (exact) -- so alpha, and every blend decision, is reproducible
+// bit for bit.
+float canon_exp(float power) {
+  const float x = power * 1.4426950408889634f;
+  const float n = std::floor(x);
+  const float f = x - n;
+  const float c[9] = {1.0f, 6.9314718e-1f, 2.4022651e-1f, 5.5504109e-2f, 9.6181291e-3f, 1.3333558e-3f,
+                      1.5403530e-4f, 1.5252734e-5f, 1.3215487e-6f};  // (ln 2)^k / k!
+  float p = c[8];
+  for (int k = 7; k >= 0; --k) p = std::fma(p, f, c[k]);
+  return std::ldexp(p, (int)n);
+}
 
 // clamp bits per Gaussian (decisions frozen for the backward, R18)
 enum : uint8_t {
@@ -322,7 +339,7 @@ WalkOut walk_pixel(const Gauss2D& g, const uint32_t* values, uint32_t start, uin
     const float dy = g.xy[2 * id + 1] - pyf;
     const float power = std::fma(A, dx * dx, std::fma(Cc, dy * dy, B * (dx * dy)));
     if (!(mode & ORC_NO_POWER_GUARD) && power > 0.0f) continue;
-    const float G = std::exp(power);
+    const float G = (mode & ORC_CANON_EXP) ? canon_exp(power) : std::exp(power);
     const float og = g.opacity[id] * G;
     bool aclamp = false;
     float alpha = og;
@@ -829,6 +846,11 @@ void orc_knn_mean(int64_t n, const float* means, int32_t k, double* out) {
     for (size_t t = 0; t < kk; ++t) acc += d[t];
     out[i] = kk ? acc / (double)kk : 0.0;
   }
+}
+
+// R23 parity mode's exponential, exposed for its pin (tests/test_oracle_blend.py)
+void orc_canon_exp(int64_t n, const float* x, float* out) {
+  for (int64_t i = 0; i < n; ++i) out[i] = canon_exp(x[i]);
 }
 
 // O17: Adam (R21), PyTorch semantics, in double.  lr[6] = means, log_scales,

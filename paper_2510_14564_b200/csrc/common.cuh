@@ -164,6 +164,28 @@ __device__ __forceinline__ float fast_exp(float x) {
   return y;
 }
 
+// The parity mode's exponential (BGS_DEBUG_PARITY_EXP; R23): a fixed expression tree that
+// the oracle evaluates identically (oracle/bgs_oracle.cpp, canon_exp), so alpha -- and every
+// blend decision -- is bit-identical on both sides: 2^x with x = power * log2(e) (one float
+// multiply), x = n + f (n = floor x, f exact), 2^f by the degree-8 Taylor polynomial of
+// e^(f ln 2) in Horner form with fmaf, scaled by 2^n exactly (ldexpf).  Relative error vs
+// exp <= 1.5e-6 (mostly the rounding of x), inside the pre-skip and culling margins.
+__device__ __forceinline__ float canon_exp(float power) {
+  const float x = power * 1.4426950408889634f;
+  const float n = floorf(x);
+  const float f = x - n;
+  float p = 1.3215487e-6f;
+  p = fmaf(p, f, 1.5252734e-5f);
+  p = fmaf(p, f, 1.5403530e-4f);
+  p = fmaf(p, f, 1.3333558e-3f);
+  p = fmaf(p, f, 9.6181291e-3f);
+  p = fmaf(p, f, 5.5504109e-2f);
+  p = fmaf(p, f, 2.4022651e-1f);
+  p = fmaf(p, f, 6.9314718e-1f);
+  p = fmaf(p, f, 1.0f);
+  return ldexpf(p, (int)n);
+}
+
 // look-back status words: relaxed, GPU-scope (L2-coherent; no .sys-scope round trip).  A
 // status word carries its own flag bits, so no ordering with other data is needed.
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {

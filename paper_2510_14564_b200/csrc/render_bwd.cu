@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     const uint32_t* __restrict__ counters, Cam cam, const uint32_t* __restrict__ units, uint32_t* ticket,
     const float* __restrict__ dl_dimage, const float* __restrict__ final_T, const uint32_t* __restrict__ n_contrib,
     float4* __restrict__ grad2d, int32_t seg_len, const uint32_t* __restrict__ ck_table,
-    const float4* __restrict__ ck_pool) {
+    const float4* __restrict__ ck_pool, int32_t canon) {
   __shared__ float4 s_rec[kBwdWarpsPerCta][3][32];
   __shared__ uint32_t s_pos[kBwdWarpsPerCta][32];
   __shared__ uint32_t s_id[kBwdWarpsPerCta][32];
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
             const float power = fmaf(r1.x, dxx, fmaf(r1.z, dyy, r1.y * dxy));
             // power below the exact alpha < 1/255 bound (pthr): skipped without the MUFU path
             if (power > 0.0f || power < r2.w) continue;
-            const float G = fast_exp(power);
+            const float G = canon ? canon_exp(power) : fast_exp(power);
             const float og = r1.w * G;
             const float alpha = fminf(0.99f, og);
             if (alpha < (1.0f / 255.0f)) continue;
@@ -384,11 +384,13 @@ bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final
   if (ppl == 2)
     k_render_bwd<2><<<bwd_grid<2>(), kBwdWarpsPerCta * 32, 0, s>>>(
         F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,
-        dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool);
+        dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool,
+        (F->debug_flags & BGS_DEBUG_PARITY_EXP) ? 1 : 0);
   else
     k_render_bwd<1><<<bwd_grid<1>(), kBwdWarpsPerCta * 32, 0, s>>>(
         F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,
-        dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool);
+        dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool,
+        (F->debug_flags & BGS_DEBUG_PARITY_EXP) ? 1 : 0);
   note_launch();
   return check_launch("k_render_bwd");
 }

@@ -69,6 +69,7 @@ struct FwdArgs {
   uint32_t* arrive;           // segments of a split item finished so far
   float4* spec_state;         // [slot][32] {T or prod(1 - alpha), C rgb}
   uint32_t* spec_last;        // [slot][32] last | stopped << 31
+  int32_t canon;              // BGS_DEBUG_PARITY_EXP: canon_exp instead of MUFU.EX2
 };
 
 __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const FwdArgs a, const Cam cam) {
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const FwdArgs a, 
             // one predicate: pixel done, R14's power > 0 guard, or power below the exact
             // alpha < 1/255 bound (pthr, preprocess) -- the last skips the MUFU path
             if (done | (power > 0.0f) | (power < r2.w)) continue;
-            const float alpha = fminf(0.99f, r1.w * fast_exp(power));
+            const float alpha = fminf(0.99f, r1.w * (a.canon ? canon_exp(power) : fast_exp(power)));
             if (alpha < (1.0f / 255.0f)) continue;
             const float tT = T * (1.0f - alpha);
             if (tT < 1e-4f) {
@@ -424,7 +425,9 @@ static int fwd_grid() {
 bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n_contrib, cudaStream_t s) {
   const int n_items = 8 * F->num_tiles;
   const uint32_t cap = (uint32_t)(F->ck_cap < 0xffffffffll ? F->ck_cap : 0xffffffffll);
-  const bool hinted = F->have_cost != 0;
+  // parity mode: no speculative segments (their merges re-associate T, R23)
+  const bool parity = (F->debug_flags & BGS_DEBUG_PARITY_EXP) != 0;
+  const bool hinted = F->have_cost != 0 && !parity;
   k_fwd_plan<<<1, kFwdPlanThreads, 0, s>>>(hinted ? F->block_cost : F->tile_count, hinted ? 0 : 3, hinted ? 1 : 0,
                                            n_items, F->seg_len, cap, F->counters, F->order_fwd, F->spec_base,
                                            F->spec_n, F->arrive);
@@ -452,6 +455,7 @@ bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n
   a.arrive = F->arrive;
   a.spec_state = F->spec_state;
   a.spec_last = F->spec_last;
+  a.canon = parity ? 1 : 0;
   k_render_fwd<<<fwd_grid(), kFwdWarps * 32, 0, s>>>(a, F->cam);
   note_launch();
   F->have_cost = 1;

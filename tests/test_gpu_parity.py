@@ -635,3 +635,32 @@ def test_fused_chain_rule_adam_equals_unfused(bgs, repeat):
     assert not (th1 == theta).all()
     if grad2 is not None:
         assert not grad2.any()
+
+
+@pytest.mark.parametrize("name", ["tiny", "dense", "ragged", "garden20k"])
+def test_parity_mode_is_bit_exact(bgs, name):
+    """R23's parity mode (BGS_DEBUG_PARITY_EXP): the GPU's canonical exponential is the
+    oracle's (mode CANON_EXP), the forward walks serially, so n_contrib, final_T and the
+    image equal the oracle's on EVERY pixel (no near-tie exclusions), and the backward
+    meets the usual gradient tolerance."""
+    s = gen.garden(seed=1, n=20000, n_cams=4) if name == "garden20k" else scenes()[name]()
+    cam = s.cameras[0]
+    r, theta, out = run_gpu(bgs, s, cam, max_keys=1 << 22, flags=bgs.BGS_DEBUG_PARITY_EXP)
+    out = r.forward(theta, cam, s.sh_degree)  # a hinted re-render stays unsplit in parity mode
+    torch.cuda.synchronize()
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam, mode=oracle.CANON_EXP)
+    assert np.array_equal(out["n_contrib"].cpu().numpy(), ref["n_contrib"])
+    assert np.array_equal(out["final_T"].cpu().numpy(), ref["final_T"])
+    # colours: rgb (free-order SH sums, <= 1e-6) is the only input not bit-identical
+    assert np.abs(out["image"].cpu().numpy() - ref["image"]).max() <= 2e-6
+    dl_np = gen.random_dl_dimage(13, cam.width, cam.height, scale=1e-3)
+    grad = torch.zeros_like(theta)
+    r.backward(theta, s.sh_degree, torch.from_numpy(dl_np).cuda(), out, grad)
+    torch.cuda.synchronize()
+    g_ref = oracle.backward(s.theta, s.n, s.sh_degree, cam, ref, dl_np, mode=oracle.CANON_EXP)["grad"]
+    g = grad.cpu().numpy().astype(np.float64)
+    for gname, idx in oracle.group_slices(s.n).items():
+        den = np.linalg.norm(g_ref[idx])
+        if den == 0:
+            continue
+        assert np.linalg.norm(g[idx] - g_ref[idx]) / den <= GRAD_TOL, gname

@@ -249,3 +249,27 @@ def test_plain_mode_equals_paper_formula(seed):
     assert (f["pre"]["radius"] > 0).sum() == s.n
     ref = _p146_literal(s.theta, s.n, cam, f["pre"]["rgb"].astype(np.float64))
     assert np.abs(f["image"] - ref).max() < 2e-5
+
+
+def test_canon_exp_is_exp_to_float_accuracy():
+    # R23 parity mode: the canonical exponential is exp within a few float ulps on the blend's
+    # range (power <= 0 down to the alpha cutoff: power >= ln(1/255) - margin > -12)
+    x = np.linspace(-12.0, 0.0, 200001).astype(np.float32)
+    got = oracle.canon_exp(x).astype(np.float64)
+    ref = np.exp(x.astype(np.float64))
+    # the float rounding of x = power * log2(e) (|x| <= 17.3: <= 2^-20 absolute) dominates;
+    # the polynomial adds < 2^-22 (the same budget as MUFU.EX2 on that x)
+    assert (np.abs(got - ref) <= 1.5e-6 * ref).all()
+    mid = x > -4.0
+    assert (np.abs(got - ref)[mid] <= 4e-7 * ref[mid]).all()
+    assert oracle.canon_exp(np.float32([0.0]))[0] == 1.0  # 2^0 * p(0) = 1 exactly
+
+
+def test_parity_mode_forward_close_to_default():
+    s = gen.small_scene(5, 700, 48, 40)
+    cam = s.cameras[0]
+    a = oracle.forward(s.theta, s.n, s.sh_degree, cam)
+    b = oracle.forward(s.theta, s.n, s.sh_degree, cam, mode=oracle.CANON_EXP)
+    ok = (a["flags"] == 0) & (b["flags"] == 0)
+    assert np.array_equal(a["n_contrib"][ok], b["n_contrib"][ok])
+    assert np.abs(a["image"] - b["image"])[:, ok].max() <= 1e-5
