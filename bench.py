@@ -518,6 +518,27 @@ def run_ours(args, rank, world, local_rank):
             else:
                 stats[k2] += s.get(k2, 0)
 
+    # ---- shape statistics of the workload (reporting only, not timed): the
+    # per-pixel walk lengths of view 0 and the local-density contrast the paper measures
+    # (>= 100x between dense and sparse regions), rho at r = the scene's median
+    # 8-NN distance (estimated from a 100k-point sample)
+    shape = None
+    if rank == 0:
+        nc = S["rends"][0].n_contrib.to(torch.float64).flatten()
+        qs = torch.quantile(nc[torch.randperm(nc.numel(), device=dev)[:1 << 20]],
+                            torch.tensor([0.5, 0.99], dtype=torch.float64, device=dev)).tolist()
+        from scipy.spatial import cKDTree
+
+        mu = gen.segments(scene.theta, scene.n)["means"]
+        sub = mu[gen.rng(77).choice(scene.n, min(scene.n, 100_000), replace=False)].astype(np.float64)
+        r8 = float(np.median(cKDTree(sub).query(sub, k=9)[0][:, 8]) * (len(sub) / scene.n) ** (1.0 / 3.0))
+        rho, _ = bgs.bgs_local_density(torch.from_numpy(mu.copy()).to(dev), r8)
+        rq = torch.quantile(rho.to(torch.float64)[torch.randperm(rho.numel(), device=dev)[:1 << 20]],
+                            torch.tensor([0.05, 0.5, 0.95, 0.99], dtype=torch.float64, device=dev)).tolist()
+        shape = {"n_contrib_view0": {"median": qs[0], "p99": qs[1], "max": float(nc.max())},
+                 "local_density_r": r8, "local_density_quantiles_p5_p50_p95_p99": rq,
+                 "density_contrast_p99_over_p5": rq[3] / max(rq[0], 1.0)}
+
     # ---- max over ranks
     t = torch.tensor([ms_local], device=dev)
     if world > 1:
@@ -616,7 +637,7 @@ def run_ours(args, rank, world, local_rank):
         "workload": {"V_per_view": V, "K_per_view": K, "E_f_per_view": Ef, "E_b_per_view": Eb,
                      "E_f_culled_per_view": Efc, "E_b_culled_per_view": Ebc, "blended_per_view": Ebl,
                      "E_slot_over_E_f_culled": stats["evals_slot"] / max(1, stats["evals_fwd_culled"]),
-                     "max_tile_list": stats["max_list"]},
+                     "max_tile_list": stats["max_list"], "shape": shape},
         "e2e": e2e, "cpu_baseline": cpu,
         "density": None if not args.density_every else {
             "every": args.density_every, "r": round(float(dens_prm.r), 6), "events_timed_and_e2e": dens_log,
