@@ -23,7 +23,11 @@ METRICS = [
     ("launch__registers_per_thread", "regs"),
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem wavefronts"),
     ("smsp__inst_executed.sum", "warp inst"),
-    ("smsp__inst_executed_pipe_xu.sum", "xu (MUFU) inst"),
+    ("sm__inst_executed_pipe_xu.sum", "xu (MUFU) inst"),
+    ("sm__inst_executed_pipe_fma.sum", "fma-pipe inst"),
+    ("sm__inst_executed_pipe_alu.sum", "alu-pipe inst"),
+    ("sm__thread_inst_executed_pipe_fma_pred_on.sum", "fma-pipe lane ops"),
+    ("sm__thread_inst_executed_pipe_alu_pred_on.sum", "alu-pipe lane ops"),
     ("lts__t_sectors_op_red.sum", "L2 RED sectors"),
     ("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum", "L1 global ld sectors"),
     ("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "L1 global ld requests"),
