@@ -63,6 +63,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--one-frame", action="store_true",
                    help="diagnostic: one frame for all views (no per-view scheduling hint)")
+    p.add_argument("--pre-per-view", action="store_true",
+                   help="diagnostic: one preprocess launch per view instead of one per 16 views")
     p.add_argument("--no-stage-events", action="store_true", help="diagnostic: no per-stage events in the timed loop")
     p.add_argument("--thin", type=int, default=None,
                    help="oracle sample: every k-th Gaussian (default 64 for cpu_baseline, 256 for --impl reference)")
@@ -187,6 +189,8 @@ def run_ours(args, rank, world, local_rank):
     sharded = world > 1 and args.update == "sharded"
     # one GPU, one chain-rule launch: a10 and a11 fused (no collective between them)
     fused = world == 1 and not args.one_frame and args.fuse_adam and args.views <= 16
+    # the step's views share theta: one preprocess pass over it for all of them
+    batch_pre = not args.one_frame and not args.pre_per_view
     total = 59 * n
     if sharded:
         # reduce-scatter -> Adam on this rank's 1/G shard -> all-gather: theta
@@ -255,7 +259,7 @@ def run_ours(args, rank, world, local_rank):
         stage_names.append("density")
     # all timing events of the timed region are created up front (creating them inside the
     # loop adds host work between launches)
-    n_marks = args.steps * (7 * len(cam_structs) + 7)
+    n_marks = args.steps * (7 * len(cam_structs) + 9)
     pool = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
     step_no = [0]
 
@@ -345,6 +349,13 @@ def run_ours(args, rank, world, local_rank):
                 marks.append(e)
 
         gs, grad, frames = S["gs"], S["grad"], S["frames"]
+        if batch_pre:  # a1-a3 for all of the step's views in one pass over theta
+            marks = []
+            mark(marks)
+            bgs.bgs_preprocess_batch(gs, cam_structs, frames)
+            mark(marks)
+            if record is not None:
+                record["marks"].append(("pre", marks))
         if side:
             fork_ev.record(stream)
             for sj in side:
@@ -356,7 +367,8 @@ def run_ours(args, rank, world, local_rank):
             with torch.cuda.stream(sj):
                 marks = []
                 mark(marks)
-                bgs.bgs_preprocess(gs, cs, rj.frame)
+                if not batch_pre:
+                    bgs.bgs_preprocess(gs, cs, rj.frame)
                 mark(marks)
                 bgs.bgs_sort(rj.frame)
                 mark(marks)
@@ -450,7 +462,9 @@ def run_ours(args, rank, world, local_rank):
     # per-stage means
     sums = {s: 0.0 for s in stage_names}
     for kind, mk in record["marks"]:
-        if kind == "view":
+        if kind == "pre":
+            sums["preprocess"] += mk[0].elapsed_time(mk[1])
+        elif kind == "view":
             for s, a, b in zip(stage_names[:6], mk[:-1], mk[1:]):
                 sums[s] += a.elapsed_time(b)
         else:
@@ -579,7 +593,16 @@ def run_ours(args, rank, world, local_rank):
     def per_launch(stage):
         return max(per_step[stage] / steps_views / 1e3, 1e-12)  # seconds (0 with --no-stage-events)
 
-    frac("preprocess", (16 * n + 268 * V) / per_launch("preprocess") / 1e9, hbm, "GB/s", "hbm")
+    if batch_pre:  # per launch of <= 16 views: theta's geometry 44 B per Gaussian + SH 192 B per Gaussian
+        # some view sees (>= V: counted as V) once; per view radius + tiles_touched 8 B per Gaussian and
+        # depth 4 + rect 8 + record 48 + clamp bits 1 + zeroed blend-gradient slots 48 per visible
+        pre_launches = -(-steps_views // 16)
+        pre_bytes = (44 * n + 192 * V) * pre_launches + (8 * n + 109 * V) * steps_views
+        frac("preprocess", pre_bytes / max(per_step["preprocess"] / 1e3, 1e-12) / 1e9, hbm, "GB/s", "hbm")
+        roof["preprocess"]["ms_per_launch"] = per_step["preprocess"] / pre_launches
+        roof["preprocess"]["views_per_launch"] = min(16, steps_views)
+    else:
+        frac("preprocess", (16 * n + 268 * V) / per_launch("preprocess") / 1e9, hbm, "GB/s", "hbm")
     if frame_v.sort_mode == 1:  # 64-bit onesweep reference: dup 12 + hist 8 + 24/pass per key, rects 20/visible
         sort_bytes = (12 + 8 + 24 * passes) * K + 20 * V
     else:  # depth first: 128 B per Gaussian + 20 per visible + (8 + 16 per tile pass) per key

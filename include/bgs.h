@@ -148,6 +148,15 @@ bgs_status bgs_frame_init(bgs_frame* f /*host*/, void* workspace, size_t bytes, 
 bgs_status bgs_preprocess(const bgs_gaussians* g /*host*/, const bgs_camera* cam /*host*/, bgs_frame* f /*host*/,
                           void* stream);
 
+/* a1-a3 over a batch of views: cams[nframes] (host array) and frames[nframes] (host array
+ * of distinct host frame pointers, 1 <= nframes <= 4096, all of the same n, each
+ * cams[v] matching frames[v]'s w/h).  Bit-identical to calling bgs_preprocess(g, &cams[v],
+ * frames[v]) for each v, but theta is read once per 16 views instead of once per view
+ * (the views of a training batch share theta, R20).  Any invalid camera or frame ->
+ * BGS_ERR_INVALID before anything launches. */
+bgs_status bgs_preprocess_batch(const bgs_gaussians* g /*host*/, const bgs_camera* cams /*host*/,
+                                bgs_frame* const* frames /*host*/, int32_t nframes, void* stream);
+
 /* a4-a6: duplicate (tile | depth) keys (values = Gaussian index), stable 64-bit LSD
  * radix sort on bits [0, 32 + bit_width(tiles - 1)), tile ranges.  Result order =
  * (tile, depth bits, index): "N ... sorted by depth", ties by index

@@ -98,6 +98,8 @@ _SIGS = {
     "bgs_workspace_bytes": (C.c_size_t, [C.c_int64, C.c_int32, C.c_int32, C.c_int64]),
     "bgs_frame_init": (C.c_int, [C.POINTER(Frame), _P, C.c_size_t, C.c_int64, C.c_int32, C.c_int32, C.c_int64]),
     "bgs_preprocess": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Camera), C.POINTER(Frame), _P]),
+    "bgs_preprocess_batch": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Camera), C.POINTER(C.POINTER(Frame)),
+                                       C.c_int32, _P]),
     "bgs_sort": (C.c_int, [C.POINTER(Frame), _P]),
     "bgs_render_fwd": (C.c_int, [C.POINTER(Frame), _P, _P, _P, _P]),
     "bgs_render_bwd": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Frame), _P, _P, _P, _P, _P]),
@@ -198,6 +200,15 @@ def bgs_frame_init(frame: Frame, workspace: torch.Tensor, n, w, h, max_keys):
 
 def bgs_preprocess(g: Gaussians, cam: Camera, frame: Frame, stream=None):
     _check(_lib.bgs_preprocess(C.byref(g), C.byref(cam), C.byref(frame), _stream(stream)), "bgs_preprocess")
+
+
+def bgs_preprocess_batch(g: Gaussians, cams, frames, stream=None):
+    """a1-a3 for several views in one pass over theta: cams / frames are equal-length sequences."""
+    if len(cams) != len(frames):
+        raise ValueError("bgs_preprocess_batch: one camera per frame")
+    carr = (Camera * len(cams))(*cams)
+    farr = (C.POINTER(Frame) * len(frames))(*[C.pointer(f) for f in frames])
+    _check(_lib.bgs_preprocess_batch(C.byref(g), carr, farr, len(frames), _stream(stream)), "bgs_preprocess_batch")
 
 
 def bgs_sort(frame: Frame, stream=None):

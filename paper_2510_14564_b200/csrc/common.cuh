@@ -123,11 +123,13 @@ void set_error(const char* msg);
 
 // stage launchers (one .cu each)
 bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s);
+bgs_status launch_preprocess_batch(const bgs_gaussians* g, Frame* const* F, int nviews, cudaStream_t s);
 bgs_status launch_sort(Frame* F, cudaStream_t s);
 bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n_contrib, cudaStream_t s);
 bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
                             cudaStream_t s);
 bgs_status launch_preprocess_bwd(const bgs_gaussians* g, Frame* F, float* grad, cudaStream_t s);
+constexpr int kPreMaxViews = 16;     // views per k_preprocess launch (kernel-parameter cameras)
 constexpr int kPreBwdMaxViews = 16;  // views per k_preprocess_bwd launch (kernel-parameter cameras)
 bgs_status launch_preprocess_bwd_batch(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
                                        cudaStream_t s);

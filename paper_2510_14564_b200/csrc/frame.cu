@@ -276,6 +276,28 @@ bgs_status bgs_preprocess(const bgs_gaussians* g, const bgs_camera* cam, bgs_fra
   return launch_preprocess(g, F, (cudaStream_t)stream);
 }
 
+bgs_status bgs_preprocess_batch(const bgs_gaussians* g, const bgs_camera* cams, bgs_frame* const* frames,
+                                int32_t nframes, void* stream) {
+  if (!cams || !frames || nframes < 1 || nframes > 4096) return BGS_ERR_INVALID;
+  static thread_local Frame* F[4096];
+  for (int v = 0; v < nframes; ++v) {
+    if (!frame_ok(frames[v])) return BGS_ERR_INVALID;
+    F[v] = frame_of(frames[v]);
+    if (F[v]->n != F[0]->n) return BGS_ERR_INVALID;
+    for (int u = 0; u < v; ++u)
+      if (F[u] == F[v]) return BGS_ERR_INVALID;  // one frame twice would race on its outputs
+  }
+  bgs_status st = validate_gaussians(g, F[0]);
+  if (st != BGS_OK) return st;
+  for (int v = 0; v < nframes; ++v)
+    if ((st = validate_camera(&cams[v], F[v])) != BGS_OK) return st;
+  for (int v = 0; v < nframes; ++v) {
+    F[v]->cam = make_cam(cams[v], F[v]->tiles_x, F[v]->tiles_y);
+    F[v]->cam_valid = 1;
+  }
+  return launch_preprocess_batch(g, F, nframes, (cudaStream_t)stream);
+}
+
 bgs_status bgs_sort(bgs_frame* f, void* stream) {
   if (!frame_ok(f) || !frame_of(f)->cam_valid) return BGS_ERR_INVALID;
   return launch_sort(frame_of(f), (cudaStream_t)stream);

@@ -24,16 +24,9 @@ __constant__ float kC3[7] = {-0.5900435899266435f, 2.890611442640554f, -0.457045
                              0.3731763325901154f, -0.4570457994644658f, 1.445305721320277f,
                              -0.5900435899266435f};
 
-struct PreParams {
+// One view's camera and output buffers.
+struct PreView {
   Cam cam;
-  const float* means;
-  const float* log_scales;
-  const float* quats;
-  const float* ologits;
-  const float* sh;  // [n][16][3]
-  int64_t n;
-  int32_t deg;
-  bool quat_vec4, sh_vec4;  // 16-byte aligned segments -> vector loads
   int32_t* radius;
   float* depth;
   float4* record;
@@ -44,31 +37,33 @@ struct PreParams {
   const uint8_t* keep;      // NEXT-4 keep mask or null
 };
 
-__global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p.n) return;
-  const Cam& c = p.cam;
-  const float mx = p.means[3 * i], my = p.means[3 * i + 1], mz = p.means[3 * i + 2];
-  // camera space (O2) and near cull (R3)
-  const float t0 = fmaf(c.V[8], mz, fmaf(c.V[4], my, fmaf(c.V[0], mx, c.V[12])));
-  const float t1 = fmaf(c.V[9], mz, fmaf(c.V[5], my, fmaf(c.V[1], mx, c.V[13])));
-  const float t2 = fmaf(c.V[10], mz, fmaf(c.V[6], my, fmaf(c.V[2], mx, c.V[14])));
-  p.radius[i] = 0;
-  p.tiles_touched[i] = 0;
-  if (t2 <= c.near_plane) return;
-  if (p.keep && !p.keep[i]) return;  // NEXT-4: dropped by the importance keep rule (R40)
-  // clip, perspective divide (R4), pixel coordinates (R1)
-  const float c0 = fmaf(c.P[8], mz, fmaf(c.P[4], my, fmaf(c.P[0], mx, c.P[12])));
-  const float c1 = fmaf(c.P[9], mz, fmaf(c.P[5], my, fmaf(c.P[1], mx, c.P[13])));
-  const float c3 = fmaf(c.P[11], mz, fmaf(c.P[7], my, fmaf(c.P[3], mx, c.P[15])));
-  const float ndx = __fdiv_rn(c0, c3), ndy = __fdiv_rn(c1, c3);
-  const float px = 0.5f * fmaf(ndx + 1.0f, (float)c.W, -1.0f);
-  const float py = 0.5f * fmaf(ndy + 1.0f, (float)c.H, -1.0f);
+// Up to kPreMaxViews views per launch: theta is read once per Gaussian for all of them
+// (the views of a training batch share theta, R20), so HBM traffic per view is the
+// outputs plus 1/nviews of theta instead of all of theta.
+struct PreParams {
+  const float* means;
+  const float* log_scales;
+  const float* quats;
+  const float* ologits;
+  const float* sh;  // [n][16][3]
+  int64_t n;
+  int32_t deg, nviews;
+  bool quat_vec4, sh_vec4;  // 16-byte aligned segments -> vector loads
+  PreView view[kPreMaxViews];
+};
+
+// Sigma = (R diag s)(R diag s)^T (R5, R6) and the opacity, from theta: view independent.
+struct Sigma3 {
+  float S00, S01, S02, S11, S12, S22, o;
+};
+
+__device__ __forceinline__ Sigma3 sigma3(const PreParams& p, int64_t i) {
   // activations (R5): double transcendental, rounded once
   const float s0 = (float)exp((double)p.log_scales[3 * i]);
   const float s1 = (float)exp((double)p.log_scales[3 * i + 1]);
   const float s2 = (float)exp((double)p.log_scales[3 * i + 2]);
-  const float o = (float)(1.0 / (1.0 + exp(-(double)p.ologits[i])));
+  Sigma3 r;
+  r.o = (float)(1.0 / (1.0 + exp(-(double)p.ologits[i])));
   float4 q;
   if (p.quat_vec4) {
     q = __ldg(reinterpret_cast<const float4*>(p.quats) + i);
@@ -78,18 +73,33 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
   const float n2 = fmaf(q.x, q.x, fmaf(q.y, q.y, fmaf(q.z, q.z, q.w * q.w)));
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(n2));
   const float qw = q.x * inv, qx = q.y * inv, qy = q.z * inv, qz = q.w * inv;
-  // Sigma = (R diag s)(R diag s)^T (R6)
   const float xx = qx * qx, yy = qy * qy, zz = qz * qz, xy = qx * qy, xz = qx * qz, yz = qy * qz;
   const float wx = qw * qx, wy = qw * qy, wz = qw * qz;
   const float M00 = (1.0f - 2.0f * (yy + zz)) * s0, M01 = (2.0f * (xy - wz)) * s1, M02 = (2.0f * (xz + wy)) * s2;
   const float M10 = (2.0f * (xy + wz)) * s0, M11 = (1.0f - 2.0f * (xx + zz)) * s1, M12 = (2.0f * (yz - wx)) * s2;
   const float M20 = (2.0f * (xz - wy)) * s0, M21 = (2.0f * (yz + wx)) * s1, M22 = (1.0f - 2.0f * (xx + yy)) * s2;
-  const float S00 = fmaf(M02, M02, fmaf(M01, M01, M00 * M00));
-  const float S01 = fmaf(M02, M12, fmaf(M01, M11, M00 * M10));
-  const float S02 = fmaf(M02, M22, fmaf(M01, M21, M00 * M20));
-  const float S11 = fmaf(M12, M12, fmaf(M11, M11, M10 * M10));
-  const float S12 = fmaf(M12, M22, fmaf(M11, M21, M10 * M20));
-  const float S22 = fmaf(M22, M22, fmaf(M21, M21, M20 * M20));
+  r.S00 = fmaf(M02, M02, fmaf(M01, M01, M00 * M00));
+  r.S01 = fmaf(M02, M12, fmaf(M01, M11, M00 * M10));
+  r.S02 = fmaf(M02, M22, fmaf(M01, M21, M00 * M20));
+  r.S11 = fmaf(M12, M12, fmaf(M11, M11, M10 * M10));
+  r.S12 = fmaf(M12, M22, fmaf(M11, M21, M10 * M20));
+  r.S22 = fmaf(M22, M22, fmaf(M21, M21, M20 * M20));
+  return r;
+}
+
+// One view's geometry of a Gaussian in front of the near plane: pixel position, Sigma',
+// conic, radius, tile rect.  Writes every output but the colour (rec[2]) and the clamp
+// bits; returns the J clamp bits (CB_J*), or 0xffffffff when the Gaussian is culled.
+__device__ __forceinline__ uint32_t project_view(const PreView& pv, int64_t i, float mx, float my, float mz,
+                                                 float t0, float t1, float t2, const Sigma3& g, float tau) {
+  const Cam& c = pv.cam;
+  // clip, perspective divide (R4), pixel coordinates (R1)
+  const float c0 = fmaf(c.P[8], mz, fmaf(c.P[4], my, fmaf(c.P[0], mx, c.P[12])));
+  const float c1 = fmaf(c.P[9], mz, fmaf(c.P[5], my, fmaf(c.P[1], mx, c.P[13])));
+  const float c3 = fmaf(c.P[11], mz, fmaf(c.P[7], my, fmaf(c.P[3], mx, c.P[15])));
+  const float ndx = __fdiv_rn(c0, c3), ndy = __fdiv_rn(c1, c3);
+  const float px = 0.5f * fmaf(ndx + 1.0f, (float)c.W, -1.0f);
+  const float py = 0.5f * fmaf(ndy + 1.0f, (float)c.H, -1.0f);
   // EWA: T = J W3 (R7 clamp), Sigma' = T Sigma T^T + 0.3 I (R8)
   uint32_t cb = 0;
   float u = __fdiv_rn(t0, t2), v = __fdiv_rn(t1, t2);
@@ -111,18 +121,18 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
   const float T11 = fmaf(j12, c.V[6], j11 * c.V[5]);
   const float T12 = fmaf(j12, c.V[10], j11 * c.V[9]);
   // L = T Sigma (row i, column k): L_ik = fma(T_i2, S_2k, fma(T_i1, S_1k, T_i0 S_0k))
-  const float L00 = fmaf(T02, S02, fmaf(T01, S01, T00 * S00));
-  const float L01 = fmaf(T02, S12, fmaf(T01, S11, T00 * S01));
-  const float L02 = fmaf(T02, S22, fmaf(T01, S12, T00 * S02));
-  const float L10 = fmaf(T12, S02, fmaf(T11, S01, T10 * S00));
-  const float L11 = fmaf(T12, S12, fmaf(T11, S11, T10 * S01));
-  const float L12 = fmaf(T12, S22, fmaf(T11, S12, T10 * S02));
+  const float L00 = fmaf(T02, g.S02, fmaf(T01, g.S01, T00 * g.S00));
+  const float L01 = fmaf(T02, g.S12, fmaf(T01, g.S11, T00 * g.S01));
+  const float L02 = fmaf(T02, g.S22, fmaf(T01, g.S12, T00 * g.S02));
+  const float L10 = fmaf(T12, g.S02, fmaf(T11, g.S01, T10 * g.S00));
+  const float L11 = fmaf(T12, g.S12, fmaf(T11, g.S11, T10 * g.S01));
+  const float L12 = fmaf(T12, g.S22, fmaf(T11, g.S12, T10 * g.S02));
   const float a = fmaf(L02, T02, fmaf(L01, T01, L00 * T00)) + 0.3f;
   const float b = fmaf(L02, T12, fmaf(L01, T11, L00 * T10));
   const float cc = fmaf(L12, T12, fmaf(L11, T11, L10 * T10)) + 0.3f;
   // det, conic (R9), radius (R10)
   const float det = fmaf(a, cc, -(b * b));
-  if (det <= 0.0f) return;
+  if (det <= 0.0f) return 0xffffffffu;
   const float idet = __fdiv_rn(1.0f, det);
   const float conx = cc * idet, cony = -(b * idet), conz = a * idet;
   const float mid = 0.5f * (a + cc);
@@ -135,12 +145,35 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
   const int rx1 = (int)fminf(tx, fmaxf(0.0f, floorf((px + (float)(rad + 15)) * 0.0625f)));
   const int ry1 = (int)fminf(ty, fmaxf(0.0f, floorf((py + (float)(rad + 15)) * 0.0625f)));
   const uint32_t area = (uint32_t)(rx1 - rx0) * (uint32_t)(ry1 - ry0);
-  if (area == 0) return;
-  // SH colour (R12), free order
-  const float dxw = mx - c.campos[0], dyw = my - c.campos[1], dzw = mz - c.campos[2];
-  const float il = rsqrtf(dxw * dxw + dyw * dyw + dzw * dzw);
-  const float x = dxw * il, y = dyw * il, z = dzw * il;
-  float sh[48];
+  if (area == 0) return 0xffffffffu;
+  pv.radius[i] = rad;
+  pv.depth[i] = t2;
+  pv.tiles_touched[i] = area;
+  pv.rect[i] = make_uint2((uint32_t)rx0 | ((uint32_t)ry0 << 16), (uint32_t)(rx1 - rx0) | ((uint32_t)(ry1 - ry0) << 16));
+  float4* rec = pv.record + 3 * i;
+  rec[1] = make_float4(-0.5f * conx, -cony, -0.5f * conz, g.o);
+  // Conservative half-extents of the alpha >= 1/255 level set, d^T conic d <= 2 ln(255 o)
+  // (R14): AABB half-widths sqrt(2 tau a), sqrt(2 tau c) with tau = ln(255 o) raised by 1e-3
+  // (the threshold lowered by e^-1e-3) and a 1e-3 relative + 1e-3 px margin, so every pixel
+  // outside it gets alpha < 1/255 in the blend's own float arithmetic (its G error is ~2^-20
+  // relative).  The blend kernels use it to skip entries per warp block; it never changes a
+  // decision.
+  float ex = -1e30f, ey = -1e30f;
+  if (tau > 0.0f) {
+    ex = sqrtf(2.0f * tau * a) * 1.001f + 1e-3f;
+    ey = sqrtf(2.0f * tau * cc) * 1.001f + 1e-3f;
+  }
+  rec[0] = make_float4(px, py, ex, ey);  // everything the per-warp cull test reads
+  // this view's blend-gradient accumulator (render_bwd REDs into it)
+  float4* g2 = pv.grad2d + 3 * i;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  g2[0] = z4;
+  g2[1] = z4;
+  g2[2] = z4;
+  return cb;
+}
+
+__device__ __forceinline__ void load_sh(const PreParams& p, int64_t i, float* sh) {
   if (p.sh_vec4) {
     const float4* shp = reinterpret_cast<const float4*>(p.sh) + 12 * i;
 #pragma unroll
@@ -152,6 +185,16 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
 #pragma unroll
     for (int k = 0; k < 48; ++k) sh[k] = __ldg(p.sh + 48 * i + k);
   }
+}
+
+// SH colour (R12), free order, + 0.5, clamped below; writes rec[2] = {rgb, pthr} and the
+// clamp bits (cb = the view's J bits).
+__device__ __forceinline__ void colour_view(const PreView& pv, const PreParams& p, int64_t i, float mx, float my,
+                                            float mz, const float* sh, float tau, uint32_t cb) {
+  const Cam& c = pv.cam;
+  const float dxw = mx - c.campos[0], dyw = my - c.campos[1], dzw = mz - c.campos[2];
+  const float il = rsqrtf(dxw * dxw + dyw * dyw + dzw * dzw);
+  const float x = dxw * il, y = dyw * il, z = dzw * il;
   float rgb[3];
 #pragma unroll
   for (int ch = 0; ch < 3; ++ch) rgb[ch] = kC0 * sh[ch];
@@ -187,36 +230,81 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(PreParams p) {
       rgb[ch] = 0.0f;
     }
   }
-  p.radius[i] = rad;
-  p.depth[i] = t2;
-  p.tiles_touched[i] = area;
-  p.rect[i] = make_uint2((uint32_t)rx0 | ((uint32_t)ry0 << 16), (uint32_t)(rx1 - rx0) | ((uint32_t)(ry1 - ry0) << 16));
-  float4* rec = p.record + 3 * i;
-  rec[1] = make_float4(-0.5f * conx, -cony, -0.5f * conz, o);
-  // Conservative half-extents of the alpha >= 1/255 level set, d^T conic d <= 2 ln(255 o)
-  // (R14): AABB half-widths sqrt(2 tau a), sqrt(2 tau c) with tau raised by 1e-3 (the
-  // threshold lowered by e^-1e-3) and a
-  // 1e-3 relative + 1e-3 px margin, so every pixel outside it gets alpha < 1/255 in the
-  // blend's own float arithmetic (its G error is ~2^-20 relative).  The blend kernels use
-  // it to skip entries per warp block; it never changes a decision.
-  const float tau = logf(255.0f * o) + 1e-3f;
-  float ex = -1e30f, ey = -1e30f, pthr = 3.0e38f;
-  if (tau > 0.0f) {
-    ex = sqrtf(2.0f * tau * a) * 1.001f + 1e-3f;
-    ey = sqrtf(2.0f * tau * cc) * 1.001f + 1e-3f;
-    // the same bound per pixel: power < -tau  =>  o exp(power) < e^-1e-3 / 255, so the
-    // blend's alpha (G within 2^-20 relative) is < 1/255 -- skipped without evaluating G
-    pthr = -tau;
+  // the same bound as ex/ey per pixel: power < -tau  =>  o exp(power) < e^-1e-3 / 255, so
+  // the blend's alpha (G within 2^-20 relative) is < 1/255 -- skipped without evaluating G
+  const float pthr = tau > 0.0f ? -tau : 3.0e38f;
+  pv.record[3 * i + 2] = make_float4(rgb[0], rgb[1], rgb[2], pthr);
+  pv.cbits[i] = (uint8_t)cb;
+}
+
+// camera-space position (O2)
+__device__ __forceinline__ void to_camera(const Cam& c, float mx, float my, float mz, float& t0, float& t1,
+                                          float& t2) {
+  t0 = fmaf(c.V[8], mz, fmaf(c.V[4], my, fmaf(c.V[0], mx, c.V[12])));
+  t1 = fmaf(c.V[9], mz, fmaf(c.V[5], my, fmaf(c.V[1], mx, c.V[13])));
+  t2 = fmaf(c.V[10], mz, fmaf(c.V[6], my, fmaf(c.V[2], mx, c.V[14])));
+}
+
+// One view (view[0]).
+__global__ void __launch_bounds__(256, 4) k_preprocess(const __grid_constant__ PreParams p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  const PreView& pv = p.view[0];
+  const float mx = p.means[3 * i], my = p.means[3 * i + 1], mz = p.means[3 * i + 2];
+  float t0, t1, t2;
+  to_camera(pv.cam, mx, my, mz, t0, t1, t2);
+  pv.radius[i] = 0;
+  pv.tiles_touched[i] = 0;
+  if (t2 <= pv.cam.near_plane) return;  // near cull (R3)
+  if (pv.keep && !pv.keep[i]) return;   // NEXT-4: dropped by the importance keep rule (R40)
+  const Sigma3 g = sigma3(p, i);
+  const float tau = logf(255.0f * g.o) + 1e-3f;
+  const uint32_t cb = project_view(pv, i, mx, my, mz, t0, t1, t2, g, tau);
+  if (cb == 0xffffffffu) return;
+  float sh[48];
+  load_sh(p, i, sh);
+  colour_view(pv, p, i, mx, my, mz, sh, tau, cb);
+}
+
+// Up to kPreMaxViews views per thread: Sigma and the opacity once, the SH coefficients
+// loaded once -- at the first view that sees the Gaussian -- and held in registers across
+// the view loop; each view's record is written whole (its sectors complete in L2).
+// Measured alternatives: all geometry first and the colours after (records
+// written in two halves far apart: partial sectors leave L2) and re-reading the SH per view
+// from L1/L2 (fewer registers, more occupancy) were both slower.  Bit-identical to
+// k_preprocess per view.
+__global__ void __launch_bounds__(256, 2) k_preprocess_views(const __grid_constant__ PreParams p) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  const float mx = p.means[3 * i], my = p.means[3 * i + 1], mz = p.means[3 * i + 2];
+  bool have_S = false, have_sh = false;
+  Sigma3 g = {};
+  float tau = 0.f;
+  float sh[48];
+#pragma unroll
+  for (int k = 0; k < 48; ++k) sh[k] = 0.f;
+#pragma unroll 1
+  for (int v = 0; v < p.nviews; ++v) {
+    const PreView& pv = p.view[v];
+    float t0, t1, t2;
+    to_camera(pv.cam, mx, my, mz, t0, t1, t2);
+    pv.radius[i] = 0;
+    pv.tiles_touched[i] = 0;
+    if (t2 <= pv.cam.near_plane) continue;
+    if (pv.keep && !pv.keep[i]) continue;
+    if (!have_S) {
+      have_S = true;
+      g = sigma3(p, i);
+      tau = logf(255.0f * g.o) + 1e-3f;
+    }
+    const uint32_t cb = project_view(pv, i, mx, my, mz, t0, t1, t2, g, tau);
+    if (cb == 0xffffffffu) continue;
+    if (!have_sh) {
+      have_sh = true;
+      load_sh(p, i, sh);
+    }
+    colour_view(pv, p, i, mx, my, mz, sh, tau, cb);
   }
-  rec[0] = make_float4(px, py, ex, ey);  // everything the per-warp cull test reads
-  rec[2] = make_float4(rgb[0], rgb[1], rgb[2], pthr);
-  p.cbits[i] = (uint8_t)cb;
-  // this view's blend-gradient accumulator (render_bwd REDs into it)
-  float4* g2 = p.grad2d + 3 * i;
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  g2[0] = z4;
-  g2[1] = z4;
-  g2[2] = z4;
 }
 
 // ---------------------------------------------------------------------------
@@ -341,11 +429,11 @@ bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, b
   return check_launch("k_scan");
 }
 
-bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
-  if (cudaMemsetAsync(F->counters, 0, 4 * C_NUM, s) != cudaSuccess) return check_launch("preprocess memset");
-  if (F->n == 0) return BGS_OK;
+bgs_status launch_preprocess_batch(const bgs_gaussians* g, Frame* const* F, int nviews, cudaStream_t s) {
+  for (int v = 0; v < nviews; ++v)
+    if (cudaMemsetAsync(F[v]->counters, 0, 4 * C_NUM, s) != cudaSuccess) return check_launch("preprocess memset");
+  if (F[0]->n == 0) return BGS_OK;
   PreParams p;
-  p.cam = F->cam;
   p.means = g->means;
   p.log_scales = g->log_scales;
   p.quats = g->quats;
@@ -353,22 +441,39 @@ bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
   p.sh = g->sh;
   p.quat_vec4 = ((uintptr_t)g->quats & 15u) == 0;
   p.sh_vec4 = ((uintptr_t)g->sh & 15u) == 0;
-  p.n = F->n;
+  p.n = F[0]->n;
   p.deg = g->sh_degree;
-  p.radius = F->radius;
-  p.depth = F->depth;
-  p.record = F->record;
-  p.tiles_touched = F->tiles_touched;
-  p.rect = F->rect;
-  p.grad2d = F->grad2d;
-  p.cbits = F->cbits;
-  p.keep = F->keep;
-  const int64_t blocks = (F->n + 255) / 256;
-  k_preprocess<<<(unsigned)blocks, 256, 0, s>>>(p);
-  note_launch();
+  const int64_t blocks = (p.n + 255) / 256;
+  for (int v0 = 0; v0 < nviews; v0 += kPreMaxViews) {
+    p.nviews = nviews - v0 < kPreMaxViews ? nviews - v0 : kPreMaxViews;
+    for (int k = 0; k < p.nviews; ++k) {
+      const Frame* f = F[v0 + k];
+      PreView& pv = p.view[k];
+      pv.cam = f->cam;
+      pv.radius = f->radius;
+      pv.depth = f->depth;
+      pv.record = f->record;
+      pv.tiles_touched = f->tiles_touched;
+      pv.rect = f->rect;
+      pv.grad2d = f->grad2d;
+      pv.cbits = f->cbits;
+      pv.keep = f->keep;
+    }
+    if (p.nviews == 1)
+      k_preprocess<<<(unsigned)blocks, 256, 0, s>>>(p);
+    else
+      k_preprocess_views<<<(unsigned)blocks, 256, 0, s>>>(p);
+    note_launch();
+    bgs_status st = check_launch("k_preprocess");
+    if (st != BGS_OK) return st;
+  }
   // the key count K (and the capacity check) comes from the sort's scan: of tiles_touched
   // in index order (64-bit reference path), or of the tile counts in depth order
-  return check_launch("k_preprocess");
+  return BGS_OK;
+}
+
+bgs_status launch_preprocess(const bgs_gaussians* g, Frame* F, cudaStream_t s) {
+  return launch_preprocess_batch(g, &F, 1, s);
 }
 
 }  // namespace bgs

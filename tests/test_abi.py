@@ -118,5 +118,17 @@ def test_invalid_calls_launch_nothing(bgs):
     g.sh_degree = 3
     g.n = 5  # mismatch with the frame
     assert lib.bgs_preprocess(C.byref(g), C.byref(cam), C.byref(f), None) == bgs.BGS_ERR_INVALID
+    # the batched preprocess: same checks per view, plus no frame twice and nframes >= 1
+    g.n = 4
+    f2 = bgs.Frame()
+    assert lib.bgs_frame_init(C.byref(f2), C.c_void_p((1 << 40) + (1 << 30)), need, 4, 32, 32, 64) == bgs.BGS_OK
+    cams = (bgs.Camera * 2)(cam, cam)
+    twice = (C.POINTER(bgs.Frame) * 2)(C.pointer(f), C.pointer(f))
+    both = (C.POINTER(bgs.Frame) * 2)(C.pointer(f), C.pointer(f2))
+    assert lib.bgs_preprocess_batch(C.byref(g), cams, twice, 2, None) == bgs.BGS_ERR_INVALID
+    assert lib.bgs_preprocess_batch(C.byref(g), cams, both, 0, None) == bgs.BGS_ERR_INVALID
+    assert lib.bgs_preprocess_batch(C.byref(g), None, both, 2, None) == bgs.BGS_ERR_INVALID
+    cams[1].width = 40  # view 1 does not match frame 2
+    assert lib.bgs_preprocess_batch(C.byref(g), cams, both, 2, None) == bgs.BGS_ERR_INVALID
     assert bgs.launch_count() == before
     assert "invalid" in lib.bgs_status_string(bgs.BGS_ERR_INVALID).decode()

@@ -664,3 +664,46 @@ def test_parity_mode_is_bit_exact(bgs, name):
         if den == 0:
             continue
         assert np.linalg.norm(g[idx] - g_ref[idx]) / den <= GRAD_TOL, gname
+
+
+def test_batched_preprocess_is_bit_identical(bgs):
+    """bgs_preprocess_batch == bgs_preprocess per view, bit for bit (every preprocess output
+    of the visible Gaussians, radius / tiles_touched of all, and the rendered image): 18
+    views exercise the split into launches of <= 16 views; one frame carries a keep mask."""
+    s = gen.garden(seed=3, n=30000, n_cams=18)
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    g = bgs.gaussians(theta, s.n, 3)
+    w, h = s.cameras[0].width, s.cameras[0].height
+    keep = torch.from_numpy((np.random.default_rng(7).random(s.n) < 0.6).astype(np.uint8)).to(dev)
+    one = [bgs.Renderer(s.n, w, h, max_keys=1 << 22, device=dev) for _ in s.cameras]
+    bat = [bgs.Renderer(s.n, w, h, max_keys=1 << 22, device=dev) for _ in s.cameras]
+    for rs in (one, bat):
+        bgs.bgs_frame_set_keep(rs[5].frame, keep)
+    for r, cam in zip(one, s.cameras):
+        bgs.bgs_preprocess(g, bgs.camera(cam), r.frame)
+    bgs.bgs_preprocess_batch(g, [bgs.camera(c) for c in s.cameras], [r.frame for r in bat])
+    for rs in (one, bat):
+        for r in rs:
+            bgs.bgs_sort(r.frame)
+            bgs.bgs_render_fwd(r.frame, r.image, r.final_T, r.n_contrib)
+    torch.cuda.synchronize()
+    for j, (a, b) in enumerate(zip(one, bat)):
+        va, vb = a.views(), b.views()
+        ra, rb = dev_array(va.radius, s.n, torch.int32), dev_array(vb.radius, s.n, torch.int32)
+        assert np.array_equal(ra, rb), j
+        vis = ra > 0
+        assert vis.sum() > 100
+        for name, cnt, dt in (("depth", 1, torch.float32), ("record", 12, torch.float32),
+                              ("tiles_touched", 1, torch.int32)):
+            xa = dev_array(getattr(va, name), cnt * s.n, dt).reshape(s.n, cnt)
+            xb = dev_array(getattr(vb, name), cnt * s.n, dt).reshape(s.n, cnt)
+            sel = vis if name != "tiles_touched" else np.ones(s.n, bool)
+            assert np.array_equal(xa[sel].view(np.uint32), xb[sel].view(np.uint32)), (j, name)
+        ca = torch.as_tensor(_DevPtr(va.cbits, s.n, "|u1"), device="cuda").cpu().numpy()
+        cb = torch.as_tensor(_DevPtr(vb.cbits, s.n, "|u1"), device="cuda").cpu().numpy()
+        assert np.array_equal(ca[vis], cb[vis]), j
+        assert torch.equal(a.image, b.image) and torch.equal(a.n_contrib, b.n_contrib), j
+    # the keep mask took effect on frame 5 only
+    r5 = dev_array(bat[5].views().radius, s.n, torch.int32)
+    assert not (r5[keep.cpu().numpy() == 0] > 0).any()
