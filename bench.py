@@ -94,7 +94,7 @@ def arm_config(scene, args, world):
                         f"{scene.sh_degree}, batch of {args.views} views per step (fwd+bwd each, then "
                         f"{_update_desc(args, world)})",
             "views_per_step": args.views, "n_gaussians": scene.n, "width": cam.width, "height": cam.height,
-            "parallelism": f"view-dp{world}", "l2": "inputs larger than L2 (theta 1.37 GB, keys > 126 MB)",
+            "parallelism": f"view-dp{world}", "l2": f"inputs larger than L2 (theta {236 * scene.n / 1e9:.2f} GB, L2 126 MB)",
             "loss": "0.8 L1 + 0.2 D-SSIM (11x11 Gaussian window)" if args.loss == "l1dssim" else "L1",
             "density_every": args.density_every}
 

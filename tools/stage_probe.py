@@ -55,8 +55,11 @@ def main():
         vcams = [s.cameras[(a.view + 4 * j) % len(s.cameras)] for j in range(a.views)]
         rs = [r] + [bgs.Renderer(s.n, cam.width, cam.height, max_keys=r.max_keys, device=dev) for _ in vcams[1:]]
         for it in range(a.step):
+            if len(rs) > 1:  # as the bench: one preprocess pass over theta for the step's views
+                bgs.bgs_preprocess_batch(g, [bgs.camera(cj) for cj in vcams], [rj.frame for rj in rs])
             for rj, cj in zip(rs, vcams):
-                bgs.bgs_preprocess(g, bgs.camera(cj), rj.frame)
+                if len(rs) == 1:
+                    bgs.bgs_preprocess(g, bgs.camera(cj), rj.frame)
                 bgs.bgs_sort(rj.frame)
                 bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
                 bgs.bgs_l1_loss_grad(rj.image, tgt, cam.width, cam.height, 1.0 / (3 * cam.width * cam.height), dl,
