@@ -21,20 +21,35 @@
 
 namespace bgs {
 
-constexpr int kLTx = 32, kLTy = 16, kLR = 5, kLWin = 2 * kLR + 1;
-constexpr int kLHx = kLTx + 2 * kLR, kLHy = kLTy + 2 * kLR;  // tile + halo
+constexpr int kLTx = 32, kLTy = 32, kLR = 5, kLWin = 2 * kLR + 1;
+constexpr int kLHx = kLTx + 2 * kLR, kLHy = kLTy + 2 * kLR;  // tile + halo (42 x 42)
 constexpr int kLThreads = 256;
+// register blocking: the row pass gives each thread 4 consecutive outputs of one halo row
+// (14 inputs per map instead of 44), the column pass 4 consecutive outputs of one column
+constexpr int kLRun = 4, kLSegs = kLTx / kLRun, kLRowItems = kLHy * kLSegs, kLColRuns = kLTy / kLRun;
 constexpr float kC1 = 0.01f * 0.01f, kC2 = 0.03f * 0.03f;
+static_assert(kLColRuns * kLTx == kLThreads, "one column run per thread");
 
 struct LossWin {
   float w[kLWin];
 };
 
+// the 11-tap window over 14 consecutive values -> 4 outputs
+__device__ __forceinline__ void win4(const LossWin& win, const float* v, float* o) {
+#pragma unroll
+  for (int j = 0; j < kLRun; ++j) {
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < kLWin; ++k) acc = fmaf(win.w[k], v[j + k], acc);
+    o[j] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(kLThreads) k_ssim_fwd(const float* __restrict__ img, const uint8_t* __restrict__ tgt,
                                                         int W, int H, LossWin win, float* __restrict__ part,
                                                         float* __restrict__ acc) {
-  __shared__ float sx[kLHy][kLHx], sy[kLHy][kLHx];
-  __shared__ float hm[5][kLHy][kLTx];
+  __shared__ float sx[kLHy][kLHx + 1], sy[kLHy][kLHx + 1];  // odd strides: conflict-free
+  __shared__ float hm[5][kLHy][kLTx + 1];
   const int ch = blockIdx.z;
   const int x0 = blockIdx.x * kLTx, y0 = blockIdx.y * kLTy;
   const size_t plane = (size_t)W * H;
@@ -52,56 +67,71 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_fwd(const float* __restrict_
     sy[r][c] = yv;
   }
   __syncthreads();
-  // rows: the 11-tap pass along x for every halo row
-  for (int i = threadIdx.x; i < kLHy * kLTx; i += kLThreads) {
-    const int r = i / kLTx, c = i - r * kLTx;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f, a4 = 0.f;
+  // rows: the 11-tap pass along x of the five moment maps, 4 outputs per thread
+  for (int it = threadIdx.x; it < kLRowItems; it += kLThreads) {
+    const int r = it / kLSegs, c0 = (it - r * kLSegs) * kLRun;
+    float v[kLRun + kLWin - 1], o[kLRun];
 #pragma unroll
-    for (int k = 0; k < kLWin; ++k) {
-      const float wx = win.w[k], xv = sx[r][c + k], yv = sy[r][c + k];
-      a0 = fmaf(wx, xv, a0);
-      a1 = fmaf(wx, yv, a1);
-      a2 = fmaf(wx, xv * xv, a2);
-      a3 = fmaf(wx, yv * yv, a3);
-      a4 = fmaf(wx, xv * yv, a4);
-    }
-    hm[0][r][c] = a0;
-    hm[1][r][c] = a1;
-    hm[2][r][c] = a2;
-    hm[3][r][c] = a3;
-    hm[4][r][c] = a4;
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = sx[r][c0 + k];
+    win4(win, v, o);
+#pragma unroll
+    for (int j = 0; j < kLRun; ++j) hm[0][r][c0 + j] = o[j];
+#pragma unroll
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = v[k] * v[k];
+    win4(win, v, o);
+#pragma unroll
+    for (int j = 0; j < kLRun; ++j) hm[2][r][c0 + j] = o[j];
+#pragma unroll
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = sy[r][c0 + k];
+    win4(win, v, o);
+#pragma unroll
+    for (int j = 0; j < kLRun; ++j) hm[1][r][c0 + j] = o[j];
+    float u[kLRun + kLWin - 1];
+#pragma unroll
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) u[k] = sx[r][c0 + k] * v[k];
+    win4(win, u, o);
+#pragma unroll
+    for (int j = 0; j < kLRun; ++j) hm[4][r][c0 + j] = o[j];
+#pragma unroll
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = v[k] * v[k];
+    win4(win, v, o);
+#pragma unroll
+    for (int j = 0; j < kLRun; ++j) hm[3][r][c0 + j] = o[j];
   }
   __syncthreads();
-  // columns, then the per-pixel SSIM and its partials
-  float s_sum = 0.f, l1_sum = 0.f;
-  for (int i = threadIdx.x; i < kLTy * kLTx; i += kLThreads) {
-    const int r = i / kLTx, c = i - r * kLTx;
-    const int gx = x0 + c, gy = y0 + r;
-    if (gx >= W || gy >= H) continue;
-    float mx = 0.f, my = 0.f, exx = 0.f, eyy = 0.f, exy = 0.f;
+  // columns (4 consecutive rows of one column per thread), then per pixel SSIM and partials
+  const int c = threadIdx.x % kLTx, r0 = (threadIdx.x / kLTx) * kLRun;
+  float m[5][kLRun];
 #pragma unroll
-    for (int k = 0; k < kLWin; ++k) {
-      const float wy = win.w[k];
-      mx = fmaf(wy, hm[0][r + k][c], mx);
-      my = fmaf(wy, hm[1][r + k][c], my);
-      exx = fmaf(wy, hm[2][r + k][c], exx);
-      eyy = fmaf(wy, hm[3][r + k][c], eyy);
-      exy = fmaf(wy, hm[4][r + k][c], exy);
-    }
+  for (int q = 0; q < 5; ++q) {
+    float v[kLRun + kLWin - 1];
+#pragma unroll
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = hm[q][r0 + k][c];
+    win4(win, v, m[q]);
+  }
+  float s_sum = 0.f, l1_sum = 0.f;
+  const int gx = x0 + c;
+#pragma unroll
+  for (int j = 0; j < kLRun; ++j) {
+    const int gy = y0 + r0 + j;
+    if (gx >= W || gy >= H) continue;
+    const float mx = m[0][j], my = m[1][j], exx = m[2][j], eyy = m[3][j], exy = m[4][j];
     const float sxx = exx - mx * mx, syy = eyy - my * my, sxy = exy - mx * my;
     const float a1 = 2.f * mx * my + kC1, a2 = 2.f * sxy + kC2;
     const float b1 = mx * mx + my * my + kC1, b2 = sxx + syy + kC2;
-    const float ib = 1.0f / (b1 * b2);
+    // b1, b2 >= C1, C2 > 0: MUFU reciprocals (~1 ulp), far inside the loss tolerance
+    const float ib1 = __frcp_rn(b1), ib2 = __frcp_rn(b2);
+    const float ib = ib1 * ib2;
     const float s = a1 * a2 * ib;
-    const float d_e = -s / b2;
+    const float d_e = -s * ib2;
     const float d_p = 2.f * a1 * ib;
-    const float d_m = 2.f * my * a2 * ib - 2.f * mx * s / b1 + 2.f * mx * s / b2 - 2.f * my * a1 * ib;
+    const float d_m = 2.f * my * a2 * ib - 2.f * mx * s * ib1 + 2.f * mx * s * ib2 - 2.f * my * a1 * ib;
     const size_t p = (size_t)gy * W + gx;
     part[(0 * 3 + ch) * plane + p] = d_m;
     part[(1 * 3 + ch) * plane + p] = d_e;
     part[(2 * 3 + ch) * plane + p] = d_p;
     s_sum += s;
-    l1_sum += fabsf(sx[r + kLR][c + kLR] - sy[r + kLR][c + kLR]);
+    l1_sum += fabsf(sx[r0 + j + kLR][c + kLR] - sy[r0 + j + kLR][c + kLR]);
   }
   // block sums -> this block's slot of the partial-sum array (no same-address atomics)
   __shared__ float s_red[2][kLThreads / 32];
@@ -127,8 +157,8 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_bwd(const float* __restrict_
                                                         int W, int H, LossWin win, const float* __restrict__ part,
                                                         float lam, float scale, float* __restrict__ dl,
                                                         const float* __restrict__ acc, float* loss_sum) {
-  __shared__ float sg[3][kLHy][kLHx];
-  __shared__ float hg[3][kLHy][kLTx];
+  __shared__ float sg[3][kLHy][kLHx + 1];
+  __shared__ float hg[3][kLHy][kLTx + 1];
   const int ch = blockIdx.z;
   const int x0 = blockIdx.x * kLTx, y0 = blockIdx.y * kLTy;
   const size_t plane = (size_t)W * H;
@@ -170,39 +200,39 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_bwd(const float* __restrict_
     for (int q = 0; q < 3; ++q) sg[q][r][c] = in ? part[(q * 3 + ch) * plane + p] : 0.f;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < kLHy * kLTx; i += kLThreads) {
-    const int r = i / kLTx, c = i - r * kLTx;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+  for (int it = threadIdx.x; it < kLRowItems; it += kLThreads) {
+    const int r = it / kLSegs, c0 = (it - r * kLSegs) * kLRun;
 #pragma unroll
-    for (int k = 0; k < kLWin; ++k) {
-      const float wx = win.w[k];
-      a0 = fmaf(wx, sg[0][r][c + k], a0);
-      a1 = fmaf(wx, sg[1][r][c + k], a1);
-      a2 = fmaf(wx, sg[2][r][c + k], a2);
+    for (int q = 0; q < 3; ++q) {
+      float v[kLRun + kLWin - 1], o[kLRun];
+#pragma unroll
+      for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = sg[q][r][c0 + k];
+      win4(win, v, o);
+#pragma unroll
+      for (int j = 0; j < kLRun; ++j) hg[q][r][c0 + j] = o[j];
     }
-    hg[0][r][c] = a0;
-    hg[1][r][c] = a1;
-    hg[2][r][c] = a2;
   }
   __syncthreads();
-  const float inv_n = (float)(1.0 / n);
-  for (int i = threadIdx.x; i < kLTy * kLTx; i += kLThreads) {
-    const int r = i / kLTx, c = i - r * kLTx;
-    const int gx = x0 + c, gy = y0 + r;
-    if (gx >= W || gy >= H) continue;
-    float cm = 0.f, ce = 0.f, cp = 0.f;
+  const int c = threadIdx.x % kLTx, r0 = (threadIdx.x / kLTx) * kLRun;
+  float m[3][kLRun];
 #pragma unroll
-    for (int k = 0; k < kLWin; ++k) {
-      const float wy = win.w[k];
-      cm = fmaf(wy, hg[0][r + k][c], cm);
-      ce = fmaf(wy, hg[1][r + k][c], ce);
-      cp = fmaf(wy, hg[2][r + k][c], cp);
-    }
+  for (int q = 0; q < 3; ++q) {
+    float v[kLRun + kLWin - 1];
+#pragma unroll
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = hg[q][r0 + k][c];
+    win4(win, v, m[q]);
+  }
+  const float inv_n = (float)(1.0 / n);
+  const int gx = x0 + c;
+#pragma unroll
+  for (int j = 0; j < kLRun; ++j) {
+    const int gy = y0 + r0 + j;
+    if (gx >= W || gy >= H) continue;
     const size_t p = (size_t)gy * W + gx;
     const float xv = img[ch * plane + p], yv = (float)tgt[ch * plane + p] * (1.0f / 255.0f);
     const float d = xv - yv;
     const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-    const float dssim = cm + 2.f * xv * ce + yv * cp;
+    const float dssim = m[0][j] + 2.f * xv * m[1][j] + yv * m[2][j];
     dl[ch * plane + p] = scale * inv_n * ((1.0f - lam) * sgn - lam * dssim);
   }
 }

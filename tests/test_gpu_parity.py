@@ -386,6 +386,15 @@ def test_empty_scene(bgs):
     assert (img == cam.bg[:, None, None]).all() and (out["final_T"] == 1).all() and (out["n_contrib"] == 0).all()
     r.backward(theta, 3, torch.zeros_like(out["image"]), out, theta)
     torch.cuda.synchronize()
+    # the batched preprocess of an empty scene: a valid no-op, the frames render bg
+    r2 = bgs.Renderer(0, cam.width, cam.height, max_keys=1024, device=dev)
+    g = bgs.gaussians(theta, 0, 3)
+    bgs.bgs_preprocess_batch(g, [bgs.camera(cam)] * 2, [r.frame, r2.frame])
+    for rr in (r, r2):
+        bgs.bgs_sort(rr.frame)
+        bgs.bgs_render_fwd(rr.frame, rr.image, rr.final_T, rr.n_contrib)
+    torch.cuda.synchronize()
+    assert (r2.image.cpu().numpy() == cam.bg[:, None, None]).all() and (r2.n_contrib == 0).all()
 
 
 def test_all_culled_and_transparent(bgs):

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--fractions", default="1.0,0.9,0.75,0.5")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--per-view-preprocess", action="store_true",
+                    help="one preprocess launch per view instead of one per 16 views")
     a = ap.parse_args()
     s = gen.make(a.config)
     cams = [s.cameras[(4 * i) % len(s.cameras)] for i in range(a.views)]
@@ -35,9 +37,14 @@ def main():
     g = bgs.gaussians(theta, s.n, s.sh_degree)
     cs = [bgs.camera(c) for c in cams]
 
+    frames = [r.frame for r in rs]
+
     def render_all():
+        if not a.per_view_preprocess:  # the batch's views share theta: one pass over it
+            bgs.bgs_preprocess_batch(g, cs, frames)
         for r, c in zip(rs, cs):
-            bgs.bgs_preprocess(g, c, r.frame)
+            if a.per_view_preprocess:
+                bgs.bgs_preprocess(g, c, r.frame)
             bgs.bgs_sort(r.frame)
             bgs.bgs_render_fwd(r.frame, r.image, r.final_T, r.n_contrib)
 
@@ -77,6 +84,7 @@ def main():
         for r in rs:
             bgs.bgs_frame_set_keep(r.frame, None)
     line = {"workload": f"{s.name}-shaped {s.n} Gaussians, {W}x{H}, render-only (a2-a7), {len(rs)} views",
+            "preprocess": "one launch per view" if a.per_view_preprocess else "batched over the views",
             "keep_rule": "per-view importance I_g (R40)", "rows": rows}
     print(json.dumps(line))
     if a.out:
