@@ -41,6 +41,8 @@ def scenes():
         "deg1": lambda: gen.small_scene(9, 1500, 120, 72, sh_degree=1),
         "deg0": lambda: gen.small_scene(10, 1500, 64, 64, sh_degree=0),
         "odd_n": lambda: gen.small_scene(12, 1501, 70, 50),  # theta segments not 16-byte aligned
+        # depths over four orders of magnitude (0.3 .. 1500): every byte of the depth keys varies
+        "deep": lambda: gen.small_scene(13, 2500, 96, 64, depth=(0.3, 1500.0)),
     }
 
 
