@@ -1,0 +1,142 @@
+"""Full-size parity in the bench's configuration (BASELINE.json's garden workload: 5.8M
+Gaussians, 1237x822, SH degree 3): two views through bgs_preprocess_batch -> bgs_sort ->
+bgs_render_fwd, rendered twice so that the second render runs with the schedule hint and
+the split walks the bench times.  Checked against the oracle on outputs it computes one by
+one:
+  - preprocess (O1-O9) on every Gaussian: radius, tiles_touched, depth bits, xy, conic and
+    opacity bit-exact, rgb <= 1e-6 (R22);
+  - tile lists (O10-O13) on sampled tiles, the heaviest included: the Gaussians whose
+    oracle rect holds the tile, ordered by (depth bits, index) with a per-tile lexsort,
+    equal to the GPU's sorted values and ranges (R13);
+  - blend (O14) on every pixel of those tiles: oracle.render_fwd over the sampled tiles'
+    oracle lists alone; n_contrib exact and image <= 1e-4 where the oracle raises no R23
+    near-tie flag, final_T <= 1e-5 (R14-R16);
+  - gradients (O15-O16) with dL/dimage non-zero only on those tiles' unflagged pixels:
+    bgs_blend_bwd per view + bgs_preprocess_bwd_batch over both (as the bench) against the
+    oracle's backward over the same lists, summed over the views (R18, R20); per-group
+    rel-L2 <= 1e-3.
+"""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def bgs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2510_14564_b200 as m
+
+    return m
+
+
+class _DevPtr:
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2}
+
+
+def _dev(ptr, count, typestr):
+    return torch.as_tensor(_DevPtr(ptr, count, typestr), device="cuda")
+
+
+def test_garden_full_size_sampled_parity(bgs):
+    s = gen.garden()
+    cams = [s.cameras[0], s.cameras[4]]
+    W, H = cams[0].width, cams[0].height
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    g = bgs.gaussians(theta, s.n, s.sh_degree)
+    cs = [bgs.camera(c) for c in cams]
+    rs = [bgs.Renderer(s.n, W, H, max_keys=1 << 26, device=dev) for _ in cams]
+    for _ in range(2):  # the second pass renders with the first one's schedule hint
+        bgs.bgs_preprocess_batch(g, cs, [r.frame for r in rs])
+        for r in rs:
+            bgs.bgs_sort(r.frame)
+            bgs.bgs_render_fwd(r.frame, r.image, r.final_T, r.n_contrib)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(0)
+    tx, ty = (W + 15) // 16, (H + 15) // 16
+    nt = tx * ty
+    g_ref = np.zeros(59 * s.n)
+    dls = []
+    for j, (r, cam) in enumerate(zip(rs, cams)):
+        st, K = bgs.bgs_frame_status(r.frame)
+        assert st == bgs.BGS_OK and K > 10_000_000
+        pre = oracle.preprocess(s.theta, s.n, s.sh_degree, cam)
+        v = r.views()
+        n = s.n
+        # ---- preprocess, every Gaussian
+        radius = _dev(v.radius, n, "<i4").cpu().numpy()
+        assert np.array_equal(radius, pre["radius"])
+        assert np.array_equal(_dev(v.tiles_touched, n, "<u4").cpu().numpy(), pre["tiles_touched"])
+        vis = pre["radius"] > 0
+        depth = _dev(v.depth, n, "<f4").cpu().numpy()
+        assert np.array_equal(depth[vis].view(np.uint32), pre["depth"][vis].view(np.uint32))
+        rec = _dev(v.record, 12 * n, "<f4").cpu().numpy().reshape(n, 12)[vis]
+        assert np.array_equal(rec[:, 0:2], pre["xy"][vis])
+        assert np.array_equal(np.stack([-2 * rec[:, 4], -rec[:, 5], -2 * rec[:, 6]], 1), pre["conic"][vis])
+        assert np.array_equal(rec[:, 7], pre["opacity"][vis])
+        assert np.abs(rec[:, 8:11] - pre["rgb"][vis]).max() <= 1e-6
+        del rec
+        # ---- tile lists on sampled tiles (+ the heaviest), from the oracle's own rects
+        ranges = _dev(v.ranges, 2 * nt, "<u4").cpu().numpy().reshape(nt, 2).astype(np.int64)
+        vals = _dev(v.values_sorted, K, "<u4")
+        lens = ranges[:, 1] - ranges[:, 0]
+        tiles = np.unique(np.concatenate([rng.choice(nt, 40, replace=False), [int(np.argmax(lens))]]))
+        rect = pre["rect"]
+        dbits = pre["depth"].view(np.uint32)
+        sub_ranges = np.zeros((nt, 2), np.uint32)
+        sub_vals = []
+        off = 0
+        for t in tiles:
+            tyy, txx = divmod(int(t), tx)
+            ids = np.nonzero(vis & (rect[:, 0] <= txx) & (rect[:, 2] > txx) & (rect[:, 1] <= tyy)
+                             & (rect[:, 3] > tyy))[0]
+            ids = ids[np.lexsort((ids, dbits[ids]))]  # (depth bits, index)
+            assert lens[t] == len(ids), int(t)
+            got = vals[int(ranges[t, 0]):int(ranges[t, 1])].cpu().numpy()
+            assert np.array_equal(got, ids.astype(np.uint32)), int(t)
+            sub_ranges[t] = (off, off + len(ids))
+            sub_vals.append(ids.astype(np.uint32))
+            off += len(ids)
+        # ---- blend on every pixel of the sampled tiles, over the oracle's lists alone
+        srt = dict(ranges=sub_ranges, sorted_values=np.ascontiguousarray(np.concatenate(sub_vals)))
+        ref = oracle.render_fwd(pre, srt, cam)
+        img, fT = r.image.cpu().numpy(), r.final_T.cpu().numpy()
+        nc = r.n_contrib.cpu().numpy().view(np.uint32)
+        ys, xs = np.mgrid[0:H, 0:W]
+        sel = np.isin((ys // 16) * tx + xs // 16, tiles)
+        ok = sel & (ref["flags"] == 0)
+        assert ok.sum() > 0.9 * sel.sum()
+        assert np.array_equal(nc[ok], ref["n_contrib"][ok])
+        assert np.abs(img - ref["image"])[:, ok].max() <= IMG_TOL
+        assert np.abs(fT - ref["final_T"])[ok].max() <= 1e-5
+        # ---- backward: dL/dimage on the sampled tiles' unflagged pixels only
+        dl = gen.random_dl_dimage(70 + j, W, H, scale=1e-3)
+        dl[:, ~ok] = 0.0
+        dls.append(torch.from_numpy(dl).to(dev))
+        g_ref += oracle.backward(s.theta, s.n, s.sh_degree, cam, dict(pre=pre, srt=srt), dl)["grad"]
+        del ref, pre
+    for r, dl in zip(rs, dls):
+        bgs.bgs_blend_bwd(r.frame, dl, r.final_T, r.n_contrib)
+    grad = torch.zeros_like(theta)
+    bgs.bgs_preprocess_bwd_batch(g, [r.frame for r in rs], grad)
+    torch.cuda.synchronize()
+    gg = grad.cpu().numpy().astype(np.float64)
+    for gname, idx in oracle.group_slices(s.n).items():
+        den = np.linalg.norm(g_ref[idx])
+        assert den > 0, gname
+        err = np.linalg.norm(gg[idx] - g_ref[idx]) / den
+        assert err <= GRAD_TOL, (gname, err)
