@@ -635,7 +635,8 @@ def run_ours(args, rank, world, local_rank):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(dom)
+            # ncu_traffic.json is captured on the garden scene (tools/profile_round.sh)
+            traffic = json.load(f).get(dom) if args.config == "garden" else None
     except Exception:
         pass
     d = roof[dom]
