@@ -154,16 +154,31 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
     }
     float dmx = 0.f, dmy = 0.f, dmz = 0.f, gop = 0.f;
     float GS00 = 0.f, GS01 = 0.f, GS02 = 0.f, GS11 = 0.f, GS12 = 0.f, GS22 = 0.f;  // dL/dSigma (sym.)
+    // the next view's blend gradients and clamp bits are loaded one view ahead (in flight
+    // during this view's arithmetic)
+    float4 na = make_float4(0.f, 0.f, 0.f, 0.f), nb = na, nc = na;
+    uint32_t ncb = 0;
+    auto fetch = [&](int v) {
+      if (v < p.nviews && ((vmask >> v) & 1u)) {
+        const PreBwdView& q = p.view[v];
+        na = q.grad2d[3 * i];
+        nb = q.grad2d[3 * i + 1];
+        nc = q.grad2d[3 * i + 2];
+        ncb = q.cbits[i];
+      }
+    };
+    fetch(0);
     for (int vi = 0; vi < p.nviews; ++vi) {
+      const float4 ga4 = na, gb4 = nb, gc4 = nc;
+      const uint32_t cb = ncb;
+      fetch(vi + 1);
       if (!((vmask >> vi) & 1u)) continue;
       const PreBwdView& pv = p.view[vi];
       const Cam& c = pv.cam;
       const float* V = c.V;
       const float* P = c.P;
-      const float4 ga4 = pv.grad2d[3 * i], gb4 = pv.grad2d[3 * i + 1], gc4 = pv.grad2d[3 * i + 2];
       const float gx = ga4.x, gy = ga4.y;
       gop += gb4.y;
-      const uint32_t cb = pv.cbits[i];
       const float g_r = (cb & CB_R) ? 0.f : gb4.z, g_g = (cb & CB_G) ? 0.f : gb4.w, g_b = (cb & CB_B) ? 0.f : gc4.x;
       // ---- colour: per SH term, dL/dd from the coefficients, dL/dsh_k += Y_k dL/drgb
       //      (masked by the frozen clamp, R12)
