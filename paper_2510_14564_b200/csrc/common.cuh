@@ -154,7 +154,8 @@ bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* 
                             int shift, cudaStream_t s);
 bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
-                              int shift, int64_t count, cudaStream_t s);
+                              int shift, int64_t count, cudaStream_t s, const uint2* rect = nullptr,
+                              uint32_t* rank_cnt = nullptr, uint2* rank_rect = nullptr);
 bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, bool publish_k, cudaStream_t s);
 
 // ---------------------------------------------------------------- device helpers

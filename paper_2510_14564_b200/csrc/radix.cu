@@ -45,7 +45,9 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
                                                             const uint32_t* __restrict__ vin, KT* kout,
                                                             uint32_t* vout, const uint32_t* __restrict__ hist,
                                                             uint32_t* status, uint32_t* ticket,
-                                                            const uint32_t* counters, int shift, int64_t count) {
+                                                            const uint32_t* counters, int shift, int64_t count,
+                                                            const uint2* __restrict__ rect, uint32_t* rank_cnt,
+                                                            uint2* rank_rect) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<KT>& S = *reinterpret_cast<SortSmem<KT>*>(smem_raw);
   if (counters[C_OVERFLOW]) return;
@@ -185,8 +187,21 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
       const KT k2 = S.keys[j];
       const uint32_t d = (uint32_t)((k2 >> shift) & 0xff);
       const uint32_t g = S.global_base[d] + (uint32_t)j - S.tile_start[d];
+      const uint32_t v = S.vals[j];
       kout[g] = k2;
-      vout[g] = S.vals[j];
+      vout[g] = v;
+      if (rank_rect) {  // the depth sort's last pass: per-rank tile count and packed rect
+        uint32_t t = 0;
+        uint2 packed = make_uint2(0u, 0u);
+        if ((uint32_t)k2 != 0xffffffffu) {  // visible: the preprocess's rect (R11)
+          const uint2 q = rect[v];
+          const uint32_t w = q.y & 0xffffu;
+          t = w * (q.y >> 16);
+          packed = make_uint2(q.x, w);
+        }
+        rank_cnt[g] = t;
+        rank_rect[g] = packed;
+      }
     }
     __syncthreads();
   }
@@ -211,16 +226,17 @@ bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* 
                             const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                             int shift, cudaStream_t s) {
   k_sort_pass<uint64_t><<<pass_grid<uint64_t>(), kSortThreads, sizeof(SortSmem<uint64_t>), s>>>(
-      kin, vin, kout, vout, hist, status, ticket, counters, shift, -1);
+      kin, vin, kout, vout, hist, status, ticket, counters, shift, -1, nullptr, nullptr, nullptr);
   note_launch();
   return check_launch("k_sort_pass<u64>");
 }
 
 bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
-                              int shift, int64_t count, cudaStream_t s) {
+                              int shift, int64_t count, cudaStream_t s, const uint2* rect, uint32_t* rank_cnt,
+                              uint2* rank_rect) {
   k_sort_pass<uint32_t><<<pass_grid<uint32_t>(), kSortThreads, sizeof(SortSmem<uint32_t>), s>>>(
-      kin, vin, kout, vout, hist, status, ticket, counters, shift, count);
+      kin, vin, kout, vout, hist, status, ticket, counters, shift, count, rect, rank_cnt, rank_rect);
   note_launch();
   return check_launch("k_sort_pass<u32>");
 }

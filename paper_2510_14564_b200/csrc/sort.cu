@@ -158,27 +158,9 @@ __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const float* __re
   }
 }
 
-// step 2: per depth rank, gather the Gaussian's tile count and rect once, with every rank
-// independent (full memory-level parallelism), packed as {x0 | y0 << 16, w | h << 16} so
-// the emission reads contiguous data instead of dependent random gathers
-__global__ void __launch_bounds__(256) k_rank_info(int64_t n, const uint32_t* __restrict__ sigma,
-                                                   const uint32_t* __restrict__ dkey_sorted,
-                                                   const uint2* __restrict__ rect, const uint32_t* counters,
-                                                   uint32_t* rank_cnt, uint2* rank_rect) {
-  if (counters[C_OVERFLOW]) return;
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t t = 0;
-    uint2 packed = make_uint2(0u, 0u);
-    if (dkey_sorted[r] != 0xffffffffu) {  // visible: the preprocess's rect (R11)
-      const uint2 q = rect[sigma[r]];
-      const uint32_t w = q.y & 0xffffu;
-      t = w * (q.y >> 16);
-      packed = make_uint2(q.x, w);
-    }
-    rank_cnt[r] = t;
-    rank_rect[r] = packed;
-  }
-}
+// step 2: per depth rank, the Gaussian's tile count and rect, packed as {x0 | y0 << 16, w}
+// so the emission reads contiguous data instead of dependent random gathers -- written by
+// the depth sort's last pass as it places each rank (radix.cu)
 
 // step 3: emission of the (tile, Gaussian) items in depth order, from the packed rank info.
 // Balanced by items, not ranks: warp w emits the item positions [w L, (w + 1) L) (the nearest
@@ -625,14 +607,13 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
   for (int p = 0; p < 4; ++p) {
     if ((st = memset_status(F, s, F->n)) != BGS_OK) return st;
     const int a = p & 1, b = (p + 1) & 1;
+    // (2) the last pass also writes the per-rank tile counts and packed rects
+    const bool last = p == 3;
     st = launch_sort_pass32(F->dkey[a], F->dval[a], F->dkey[b], F->dval[b], F->sort_hist + p * kRadixBins,
-                            F->sort_status, F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, F->n, s);
+                            F->sort_status, F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, F->n, s,
+                            last ? F->rect : nullptr, last ? F->rank_cnt : nullptr, last ? F->rank_rect : nullptr);
     if (st != BGS_OK) return st;
   }
-  // (2) per-rank tile counts and rects, item offsets in depth order
-  k_rank_info<<<grid, 256, 0, s>>>(F->n, F->dval[0], F->dkey[0], F->rect, F->counters, F->rank_cnt, F->rank_rect);
-  note_launch();
-  if ((st = check_launch("k_rank_info")) != BGS_OK) return st;
   // K (published with the capacity check) = the total of the depth-order scan
   if ((st = launch_scan(F->rank_cnt, F->item_off, F->n, F, true, s)) != BGS_OK) return st;
   if (F->chunk_cnt && !(F->debug_flags & BGS_DEBUG_SORT_RADIX_SPLIT)) {
