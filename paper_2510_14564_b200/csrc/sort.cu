@@ -482,12 +482,24 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
           vals[p] = g_id;
         }
       } else {
-        // a Gaussian's items have distinct tiles, so the batch takes its positions one
-        // Gaussian at a time, in depth order (lanes of a Gaussian are contiguous)
-        uint32_t pending = __ballot_sync(0xffffffffu, valid);
+        // mark the contended tiles (the losers overwrite their tile's byte with 0xff: every
+        // lane of a tile that two items of the batch share then sees it); the items of
+        // uncontended tiles take their positions at once
+        if (clash) scratch[tile] = 0xffu;
+        __syncwarp();
+        const bool contended = valid && scratch[tile] == 0xffu;
+        if (valid && !contended) {
+          const uint32_t p = nxt[tile];
+          nxt[tile] = p + 1u;
+          vals[p] = g_id;
+        }
+        __syncwarp();
+        // a Gaussian's items have distinct tiles, so the contended items take their
+        // positions one Gaussian at a time, in depth order (lanes of a Gaussian are contiguous)
+        uint32_t pending = __ballot_sync(0xffffffffu, contended);
         while (pending) {
           const int gcur = __shfl_sync(0xffffffffu, g, __ffs(pending) - 1);
-          const bool mine = valid && g == gcur;
+          const bool mine = contended && g == gcur;
           pending &= ~__ballot_sync(0xffffffffu, mine);
           if (mine) {
             const uint32_t p = nxt[tile];
