@@ -350,20 +350,33 @@ __global__ void __launch_bounds__(kFwdPlanThreads) k_fwd_plan(const uint32_t* __
   __syncthreads();
   const bool overflow = counters[C_OVERFLOW] != 0;
   const int seg_b = cost_bucket((uint32_t)seg_len);
-  for (int t0 = 0; t0 < n_items; t0 += blockDim.x) {
-    const int t = t0 + threadIdx.x;
-    if (t >= n_items) continue;
-    const uint32_t h = overflow ? 0u : cost[t >> shift];
-    uint32_t ns = 1, base = 0;
-    if (hinted && h > 2u * (uint32_t)seg_len) {
-      ns = min((h + (uint32_t)seg_len - 1u) / (uint32_t)seg_len, (uint32_t)kCkMax + 1u);
-      base = atomicAdd(&s_bump, ns);
-      if (base + ns > cap) ns = 1;
+  // kPlanPF items per thread per round, their loads issued together: one global round trip
+  // per round instead of one per item (a lone CTA is latency-bound)
+  constexpr int kPlanPF = 8;
+  const int stride = kPlanPF * blockDim.x;
+  for (int t0 = 0; t0 < n_items; t0 += stride) {
+    uint32_t hq[kPlanPF];
+#pragma unroll
+    for (int q = 0; q < kPlanPF; ++q) {
+      const int t = t0 + q * blockDim.x + threadIdx.x;
+      hq[q] = (t < n_items && !overflow) ? cost[t >> shift] : 0u;
     }
-    spec_base[t] = base;
-    spec_n[t] = ns;
-    arrive[t] = 0;
-    atomicAdd(&s_b[ns > 1 ? seg_b : cost_bucket(h)], ns);
+#pragma unroll
+    for (int q = 0; q < kPlanPF; ++q) {
+      const int t = t0 + q * blockDim.x + threadIdx.x;
+      if (t >= n_items) continue;
+      const uint32_t h = hq[q];
+      uint32_t ns = 1, base = 0;
+      if (hinted && h > 2u * (uint32_t)seg_len) {
+        ns = min((h + (uint32_t)seg_len - 1u) / (uint32_t)seg_len, (uint32_t)kCkMax + 1u);
+        base = atomicAdd(&s_bump, ns);
+        if (base + ns > cap) ns = 1;
+      }
+      spec_base[t] = base;
+      spec_n[t] = ns;
+      arrive[t] = 0;
+      atomicAdd(&s_b[ns > 1 ? seg_b : cost_bucket(h)], ns);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -376,14 +389,25 @@ __global__ void __launch_bounds__(kFwdPlanThreads) k_fwd_plan(const uint32_t* __
     counters[C_FWD_UNITS] = run;
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < n_items; t += blockDim.x) {
-    const uint32_t ns = spec_n[t];
-    const uint32_t h = overflow ? 0u : cost[t >> shift];
-    const uint32_t pos = atomicAdd(&s_b[ns > 1 ? seg_b : cost_bucket(h)], ns);
-    if (ns > 1)
-      for (uint32_t k = 0; k < ns; ++k) units[pos + k] = (uint32_t)t | (k << 25) | (1u << 31);
-    else
-      units[pos] = (uint32_t)t;
+  for (int t0 = 0; t0 < n_items; t0 += stride) {
+    uint32_t nq[kPlanPF], hq[kPlanPF];
+#pragma unroll
+    for (int q = 0; q < kPlanPF; ++q) {
+      const int t = t0 + q * blockDim.x + threadIdx.x;
+      nq[q] = t < n_items ? spec_n[t] : 0u;
+      hq[q] = (t < n_items && !overflow) ? cost[t >> shift] : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < kPlanPF; ++q) {
+      const int t = t0 + q * blockDim.x + threadIdx.x;
+      if (t >= n_items) continue;
+      const uint32_t ns = nq[q];
+      const uint32_t pos = atomicAdd(&s_b[ns > 1 ? seg_b : cost_bucket(hq[q])], ns);
+      if (ns > 1)
+        for (uint32_t k = 0; k < ns; ++k) units[pos + k] = (uint32_t)t | (k << 25) | (1u << 31);
+      else
+        units[pos] = (uint32_t)t;
+    }
   }
 }
 
