@@ -373,8 +373,10 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(uint32_t* chunk_cnt, int32_
   const int per = (n_chunks + 31) / 32;
   const int c0 = ty * per, c1 = min(n_chunks, c0 + per);
   uint32_t sum = 0;
-  if (t < nt)
-    for (int c = c0; c < c1; ++c) sum += chunk_cnt[(size_t)c * nt + t];
+  if (t < nt) {
+#pragma unroll 8
+    for (int c = c0; c < c1; ++c) sum += chunk_cnt[(size_t)c * nt + t];  // loads in flight together
+  }
   s[ty][tx] = sum;
   __syncthreads();
   if (ty == 0) {
@@ -389,7 +391,18 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(uint32_t* chunk_cnt, int32_
   __syncthreads();
   if (t < nt) {
     uint32_t run = s[ty][tx];
-    for (int c = c0; c < c1; ++c) {
+    int c = c0;
+    for (; c + 8 <= c1; c += 8) {  // 8 loads in flight, then the 8 stores
+      uint32_t v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = chunk_cnt[(size_t)(c + q) * nt + t];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        chunk_cnt[(size_t)(c + q) * nt + t] = run;
+        run += v[q];
+      }
+    }
+    for (; c < c1; ++c) {
       uint32_t* p = chunk_cnt + (size_t)c * nt + t;
       const uint32_t v = *p;
       *p = run;
