@@ -435,6 +435,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
   uint32_t* nxt = s_dyn + warp * (nt_pad + nt_pad / 4);  // nt u32 positions + nt u8 scratch
   uint8_t* scratch = reinterpret_cast<uint8_t*>(nxt + nt_pad);
   const uint32_t* row = chunk_cnt + (size_t)c * nt;
+#pragma unroll 8
   for (int t = lane; t < nt; t += 32) nxt[t] = ranges[t].x + row[t];
   __syncwarp();
   const uint32_t a = c * CI, b = min(K, a + CI);
