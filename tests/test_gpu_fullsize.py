@@ -1,5 +1,5 @@
 """Full-size parity in the bench's configuration (BASELINE.json's garden workload: 5.8M
-Gaussians, 1237x822, SH degree 3): two views through bgs_preprocess_batch -> bgs_sort ->
+Gaussians, 1237x822, SH degree 3; and the T&T-train / DB-playroom shapes): two views through bgs_preprocess_batch -> bgs_sort ->
 bgs_render_fwd, rendered twice so that the second render runs with the schedule hint and
 the split walks the bench times.  Checked against the oracle on outputs it computes one by
 one:
@@ -51,15 +51,21 @@ def _dev(ptr, count, typestr):
     return torch.as_tensor(_DevPtr(ptr, count, typestr), device="cuda")
 
 
-def test_garden_full_size_sampled_parity(bgs):
-    s = gen.garden()
+FLAG_FRAC_MAX = 0.01  # R23: at most 1 % of the sampled pixels may carry a near-tie flag
+
+
+@pytest.mark.parametrize("config", ["garden", "tandt_train", "db_playroom"])
+def test_full_size_sampled_parity(bgs, config):
+    """BASELINE.json configs[1..3] at their full sizes (T&T-train 1.1M 980x545 with a 1-pixel
+    last tile row, DB-playroom 2.3M 1264x832, garden 5.8M 1237x822)."""
+    s = {"garden": gen.garden, "tandt_train": gen.tandt_train, "db_playroom": gen.db_playroom}[config]()
     cams = [s.cameras[0], s.cameras[4]]
     W, H = cams[0].width, cams[0].height
     dev = torch.device("cuda")
     theta = torch.from_numpy(s.theta).to(dev)
     g = bgs.gaussians(theta, s.n, s.sh_degree)
     cs = [bgs.camera(c) for c in cams]
-    rs = [bgs.Renderer(s.n, W, H, max_keys=1 << 26, device=dev) for _ in cams]
+    rs = [bgs.Renderer(s.n, W, H, max_keys=1 << 27, device=dev) for _ in cams]
     for _ in range(2):  # the second pass renders with the first one's schedule hint
         bgs.bgs_preprocess_batch(g, cs, [r.frame for r in rs])
         for r in rs:
@@ -73,7 +79,7 @@ def test_garden_full_size_sampled_parity(bgs):
     dls = []
     for j, (r, cam) in enumerate(zip(rs, cams)):
         st, K = bgs.bgs_frame_status(r.frame)
-        assert st == bgs.BGS_OK and K > 10_000_000
+        assert st == bgs.BGS_OK and K > 1_000_000
         pre = oracle.preprocess(s.theta, s.n, s.sh_degree, cam)
         v = r.views()
         n = s.n
@@ -119,7 +125,9 @@ def test_garden_full_size_sampled_parity(bgs):
         ys, xs = np.mgrid[0:H, 0:W]
         sel = np.isin((ys // 16) * tx + xs // 16, tiles)
         ok = sel & (ref["flags"] == 0)
-        assert ok.sum() > 0.9 * sel.sum()
+        flagged = int((sel & (ref["flags"] != 0)).sum())
+        print(f"{config} view {j}: {flagged} of {int(sel.sum())} sampled pixels flagged (R23)")
+        assert flagged <= FLAG_FRAC_MAX * sel.sum(), flagged
         assert np.array_equal(nc[ok], ref["n_contrib"][ok])
         assert np.abs(img - ref["image"])[:, ok].max() <= IMG_TOL
         assert np.abs(fT - ref["final_T"])[ok].max() <= 1e-5

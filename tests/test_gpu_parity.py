@@ -614,6 +614,50 @@ def test_l1_dssim_loss_parity(bgs, hw):
     assert np.abs(g - g_ref).max() <= 1e-3 * np.abs(g_ref).max()
 
 
+@pytest.mark.parametrize("hw", [(16, 16), (37, 53), (822, 1237)])
+def test_l1_loss_grad_parity(bgs, hw):
+    """bgs_l1_loss_grad (R19) against oracle/ssim.py at lambda = 0 (pure L1): dL/dimage =
+    scale * sign(x - t/255) bit for bit (inputs off the kink), loss_sum += sum |x - t/255|
+    = 3hw * loss(lambda = 0) within float summation error."""
+    from oracle import ssim as S
+
+    h, w = hw
+    x, t = _loss_inputs(3 + w, h, w)
+    dev = torch.device("cuda")
+    xd, td = torch.from_numpy(x).to(dev), torch.from_numpy(t).to(dev)
+    dl = torch.full_like(xd, float("nan"))
+    loss = torch.zeros(1, device=dev)
+    scale = 1.0 / (3 * h * w * 16)
+    bgs.bgs_l1_loss_grad(xd, td, w, h, scale, dl, loss)
+    torch.cuda.synchronize()
+    n = 3 * h * w
+    g_ref = S.loss_grad(x.astype(np.float64), t, lam=0.0) * n  # sign(x - y)
+    assert set(np.unique(g_ref)) <= {-1.0, 1.0}
+    np.testing.assert_array_equal(dl.cpu().numpy(), (np.float32(scale) * g_ref).astype(np.float32))
+    ref = n * S.loss(x.astype(np.float64), t, lam=0.0)
+    assert abs(loss.item() - ref) <= 1e-5 * ref
+
+
+def test_early_stop_equality_case(bgs):
+    """R15 equality on the GPU (tests/test_oracle_thresholds.py builds the fixture): at the
+    Gaussians' common centre G = 1 exactly, T (1 - alpha) == 1e-4 exactly continues (3
+    blended, final_T = 1e-4) and one float more opacity stops before the third."""
+    from types import SimpleNamespace
+
+    from tests import test_oracle_thresholds as TT
+
+    for logit, n_c, t_fin in ((TT.LOGITS["a3"], 3, TT.T_STOP),
+                              (TT.LOGITS["a3_up"], 2, np.float32(np.float32(1 - TT.A1) * np.float32(1 - TT.A2)))):
+        cam, th, n = TT.r15_scene(logit)
+        s = SimpleNamespace(theta=th, n=n, sh_degree=0)
+        for flags in (0, bgs.BGS_DEBUG_PARITY_EXP):
+            _, _, out = run_gpu(bgs, s, cam, max_keys=1 << 12, flags=flags)
+            assert int(out["n_contrib"][TT.C, TT.C].item()) == n_c, (logit, flags)
+            assert np.float32(out["final_T"][TT.C, TT.C].item()) == t_fin, (logit, flags)
+        ref = oracle.forward(th, n, 0, cam)
+        assert ref["n_contrib"][TT.C, TT.C] == n_c
+
+
 @pytest.mark.parametrize("repeat", [1, 5])
 def test_fused_chain_rule_adam_equals_unfused(bgs, repeat):
     """bgs_preprocess_bwd_batch_adam == bgs_preprocess_bwd_batch into a zero grad followed by

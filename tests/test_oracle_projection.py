@@ -194,6 +194,50 @@ def test_sh_degree1_signs():
     np.testing.assert_allclose(Y[:, 1:4], [[0, 0, -c1], [-c1, 0, 0], [0, c1, 0]], atol=2e-6)
 
 
+def _real_sh_scipy(d):
+    """Real spherical harmonics Y_k(d), k = l^2 + l + m (l <= 3), built from scipy's complex
+    Y_l^m (scipy.special.sph_harm_y, Condon-Shortley phase included) -- a library evaluation
+    independent of the oracle's hand-expanded polynomials.  [3DGS] real form (R12, the
+    convention of the SH coefficients PAPER.md l.59 names): m < 0 -> sqrt2 Im Y_l^|m|,
+    m = 0 -> Y_l^0, m > 0 -> sqrt2 Re Y_l^m (the CS phase kept, which gives Y_1 = -C1 y,
+    Y_3 = -C1 x)."""
+    from scipy.special import sph_harm_y
+
+    x, y, z = (float(v) for v in d)
+    theta = math.acos(max(-1.0, min(1.0, z)))  # polar
+    phi = math.atan2(y, x)                      # azimuth
+    out = np.zeros(16)
+    for l in range(4):
+        for m in range(-l, l + 1):
+            c = complex(sph_harm_y(l, abs(m), theta, phi))
+            if m < 0:
+                v = math.sqrt(2.0) * c.imag
+            elif m == 0:
+                v = c.real
+            else:
+                v = math.sqrt(2.0) * c.real
+            out[l * l + l + m] = v
+    return out
+
+
+def test_sh_basis_every_coefficient_against_scipy():
+    # R12 (PAPER.md l.59, §I: colour from SH coefficients): every Y_k, k < 16, value AND sign,
+    # at 40 directions (random + the axes + diagonals) against scipy's complex SH turned into
+    # the real form; a flipped sign or swapped polynomial in any Y_k fails here (the
+    # orthonormality quadrature above is blind to a single sign flip).
+    r = np.random.default_rng(11)
+    dirs = list(r.standard_normal((30, 3)))
+    dirs += [np.array(v, float) for v in ([1, 0, 0], [0, 1, 0], [0, 0, 1], [-1, 0, 0], [0, -1, 0], [0, 0, -1],
+                                          [1, 1, 1], [-1, 2, 0.5], [0.3, -0.2, -1], [2, -1, 1])]
+    dirs = [d / np.linalg.norm(d) for d in dirs]
+    got = _basis_values(dirs)
+    want = np.array([_real_sh_scipy(d) for d in dirs])
+    np.testing.assert_allclose(got, want, atol=3e-6)
+    # and the pin is not vacuous: every coefficient takes values of both signs over the set
+    for k in range(1, 16):
+        assert (want[:, k] > 1e-3).any() and (want[:, k] < -1e-3).any(), k
+
+
 def test_sh_clamped_below_only():
     # R12: rgb clamped below at 0, never above (R17)
     sh = np.zeros((2, 16, 3), np.float32)
