@@ -9,7 +9,8 @@ the G ranks (strong scaling: total work per step is fixed).  Every stage runs in
 libbgs.so kernels through the C ABI; torch provides memory, streams and NCCL.
 
 Prints ONE JSON line (rank 0).  `--impl reference` times the CPU oracle instead (the
-reference arm of this tier), on a bounded, thinned sample of the same workload.
+reference arm of this tier) on a bounded sample of the same workload (one full view per step,
+its per-pixel walks on a stratified 1/8 of the tiles).
 """
 from __future__ import annotations
 
@@ -66,8 +67,6 @@ def parse():
     p.add_argument("--pre-per-view", action="store_true",
                    help="diagnostic: one preprocess launch per view instead of one per 16 views")
     p.add_argument("--no-stage-events", action="store_true", help="diagnostic: no per-stage events in the timed loop")
-    p.add_argument("--thin", type=int, default=None,
-                   help="oracle sample: every k-th Gaussian (default 64 for cpu_baseline, 256 for --impl reference)")
     return p.parse_args()
 
 
@@ -671,48 +670,105 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ---------------------------------------------------------------------------- oracle
-def _thinned(args):
-    import gen
+# The oracle (oracle/bgs_oracle.cpp) as it stands -- the plain CPU program, OpenMP over
+# independent units with fixed-order reductions -- timed on this host's cores.  Only here
+# (the cpu_baseline leg and --impl reference) does bench.py execute oracle/.
 
-    scene = gen.make(args.config)
-    n = scene.n
-    keep = np.arange(0, n, args.thin)
-    seg = gen.segments(scene.theta, n)
-    th = gen.pack(seg["means"][keep], seg["log_scales"][keep], seg["quats"][keep], seg["opacity_logits"][keep],
-                  seg["sh"][keep])
-    return scene, th, len(keep)
+ADAM_SLICE = 16  # Adam is timed on 1/16 of theta (its cost is exactly linear per element) and scaled
 
 
-def _oracle_view(th, n, deg, cam, dl):
+def _oracle_adam_seconds(n):
+    """One O17 Adam step over 59 n elements: timed on the first 59 n / ADAM_SLICE, scaled."""
+    import ctypes as C
+
     import oracle
 
-    f = oracle.forward(th, n, deg, cam)
-    b = oracle.backward(th, n, deg, cam, f, dl)
-    return b
+    ns = max(1, n // ADAM_SLICE)
+    r = np.random.default_rng(0)
+    th, g, m, v = (r.standard_normal(59 * ns) for _ in range(4))
+    v = np.abs(v)
+    lr = np.array([1e-4, 5e-3, 1e-3, 0.05, 2.5e-3, 1.25e-4])
+    p = [a.ctypes.data_as(C.c_void_p) for a in (th, g, m, v, lr)]
+    t = time.perf_counter()
+    oracle.lib().orc_adam(ns, *p, 0.9, 0.999, 1e-15, 1)
+    return (time.perf_counter() - t) * n / ns
+
+
+def _oracle_view_stages(scene, cam, dl, tile_mod=1, tile_phase=0):
+    """One view through the oracle: O1-O9 preprocess, O10-O13 keys/sort/ranges over the whole
+    scene, then the per-pixel walks (O14 forward, O15 backward) and O16 chain rule.  With
+    tile_mod > 1 only the tile ROWS ty with ty % tile_mod == tile_phase are walked (a stratified
+    1/tile_mod sample of the view's real tile lists, whole rows so that the oracle's parallel
+    loops over rows / tile batches stay as busy as on the full view); the per-Gaussian parts of the backward
+    (double preprocess + chain rule) are timed separately with every tile list emptied, so
+    that only the walks are scaled.  Returns seconds per stage (walks already scaled)."""
+    import oracle
+
+    deg = scene.sh_degree
+    T = {}
+    t = time.perf_counter()
+    pre = oracle.preprocess(scene.theta, scene.n, deg, cam)
+    T["preprocess"] = time.perf_counter() - t
+    t = time.perf_counter()
+    srt = oracle.sort_keys(pre, cam)
+    T["sort"] = time.perf_counter() - t
+    ranges = srt["ranges"]
+    if tile_mod > 1:
+        ranges = ranges.copy()
+        tiles_x = (cam.width + 15) // 16
+        ranges[((np.arange(len(ranges)) // tiles_x) % tile_mod) != tile_phase] = 0
+    sub = dict(srt, ranges=np.ascontiguousarray(ranges))
+    t = time.perf_counter()
+    oracle.render_fwd(pre, sub, cam)
+    T["render_fwd"] = (time.perf_counter() - t) * tile_mod
+    if tile_mod > 1:  # per-Gaussian part first (it also warms the allocator), then the sample
+        empty = dict(srt, ranges=np.zeros_like(ranges))
+        t = time.perf_counter()
+        oracle.backward(scene.theta, scene.n, deg, cam, dict(pre=pre, srt=empty), dl)
+        t_gauss = time.perf_counter() - t
+    t = time.perf_counter()
+    oracle.backward(scene.theta, scene.n, deg, cam, dict(pre=pre, srt=sub), dl)
+    t_bwd = time.perf_counter() - t
+    T["backward"] = t_gauss + max(0.0, t_bwd - t_gauss) * tile_mod if tile_mod > 1 else t_bwd
+    T["K"] = srt["K"]
+    return T
 
 
 def cpu_baseline(args):
-    if args.thin is None:
-        args.thin = 64
-    return _cpu_baseline(args)
-
-
-def _cpu_baseline(args):
-    """The oracle as it stands (single thread) on a bounded sample: one view of the scene
-    thinned to every `thin`-th Gaussian, full preprocess -> sort -> fwd -> bwd; the view
-    time is scaled by `thin` to the full scene (assumes cost linear in N)."""
+    """cpu_baseline of the main bench line (rank 0, N = 1): the oracle on ONE FULL view of
+    the configured scene (camera 0: every Gaussian, every tile, every pixel; fwd + bwd) on all
+    host cores, + the batch's Adam step amortised over its views; beside it BASELINE.json
+    configs[0] (tiny: 4096 Gaussians, 128x128) fwd + bwd + Adam on one core."""
     import gen
+    import oracle
 
-    scene, th, ns = _thinned(args)
+    scene = gen.make(args.config)
     cam = scene.cameras[0]
     dl = gen.random_dl_dimage(0, cam.width, cam.height, scale=1e-6)
+    cores = oracle.set_threads(0)
+    T = _oracle_view_stages(scene, cam, dl)
+    t_adam = _oracle_adam_seconds(scene.n)
+    view_s = sum(v for k, v in T.items() if k != "K") + t_adam / args.views
+    # tiny (configs[0]) on one core: preprocess -> sort -> fwd -> bwd -> Adam, the whole iteration
+    tiny = gen.tiny()
+    oracle.set_threads(1)
+    tc = tiny.cameras[0]
     t = time.perf_counter()
-    _oracle_view(th, ns, scene.sh_degree, cam, dl)
-    sec = time.perf_counter() - t
-    return {"value": round(1.0 / (sec * args.thin), 6), "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"1 view (camera 0) of the {scene.name} scene thinned to every {args.thin}th Gaussian "
-                      f"({ns} of {scene.n}); oracle fwd+bwd took {sec:.2f} s on 1 core; scaled x{args.thin} to "
-                      f"the full scene (cost assumed linear in N)", "cpu": _cpu_model()}
+    f = oracle.forward(tiny.theta, tiny.n, tiny.sh_degree, tc)
+    b = oracle.backward(tiny.theta, tiny.n, tiny.sh_degree, tc, f, gen.random_dl_dimage(1, tc.width, tc.height))
+    oracle.adam(tiny.theta, b["grad"], np.zeros(59 * tiny.n), np.zeros(59 * tiny.n), tiny.n,
+                [1e-4, 5e-3, 1e-3, 0.05, 2.5e-3, 1.25e-4])
+    tiny_s = time.perf_counter() - t
+    oracle.set_threads(0)
+    return {"value": round(1.0 / view_s, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"full scene, {cores} cores: 1 view (camera 0) of the {scene.name} scene, all {scene.n} "
+                      f"Gaussians, {cam.width}x{cam.height}, K = {T['K']} keys, fwd+bwd {view_s - t_adam / args.views:.2f} s "
+                      f"+ Adam over 59N ({t_adam:.2f} s per batch, timed on 1/{ADAM_SLICE} of theta and scaled) / "
+                      f"{args.views} views",
+            "stages_s": {k: round(v, 3) for k, v in T.items() if k != "K"},
+            "tiny_1core": {"config": "tiny: 4096 Gaussians, 128x128, SH 3 (BASELINE.json configs[0])",
+                           "fwd_bwd_adam_s": round(tiny_s, 4), "cores": 1},
+            "cpu": _cpu_model()}
 
 
 def _cpu_model():
@@ -726,43 +782,43 @@ def _cpu_model():
 
 
 def run_reference(args, rank, world):
+    """The reference arm of this tier: the oracle, as it stands, on this host's cores, on the
+    same config / metric / unit as our arm.  Each step is a bounded sample of one step's
+    workload: one full view of the scene (camera of that step, every Gaussian) through the
+    per-Gaussian stages and the sort, a stratified 1/tile_mod of its tile rows (rotating with
+    the step, so 8 steps cover every tile once) through the per-pixel walks, scaled to the whole
+    view, and the batch's Adam; the step's time = views x (one view) + Adam."""
     if rank != 0:
         return
     import gen
     import oracle
 
-    if args.thin is None:
-        args.thin = 256
-    scene, th, ns = _thinned(args)
+    tile_mod = 8
+    scene = gen.make(args.config)
     cams = [scene.cameras[v] for v in batch_views(args.views, len(scene.cameras))]
-    deg = scene.sh_degree
+    cores = oracle.set_threads(0)
     cam0 = cams[0]
     dl = gen.random_dl_dimage(0, cam0.width, cam0.height, scale=1e-6)
-    m = np.zeros(59 * ns)
-    vv = np.zeros(59 * ns)
-    thd = th.astype(np.float64)
-    lr6 = [1.6e-4 * scene.extent, 5e-3, 1e-3, 0.05, 2.5e-3, 1.25e-4]
+    t_adam = _oracle_adam_seconds(scene.n)
 
     def step(i):
-        cam = cams[i % len(cams)]
-        b = _oracle_view(th, ns, deg, cam, dl)
-        return oracle.adam(thd, b["grad"], m, vv, ns, lr6, step=i + 1)
+        T = _oracle_view_stages(scene, cams[i % len(cams)], dl, tile_mod, i % tile_mod)
+        return args.views * sum(v for k, v in T.items() if k != "K") + t_adam
 
     for i in range(args.warmup):
         step(i)
-    t = time.perf_counter()
-    for i in range(args.steps):
-        step(i)
-    sec = (time.perf_counter() - t) / args.steps
-    value = 1.0 / (sec * args.thin)
+    sec = sum(step(args.warmup + i) for i in range(args.steps)) / args.steps
+    value = args.views / sec
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3 * args.thin * args.views, 3),  # a step = args.views views
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32",
             "data": "synthetic", "config": arm_config(scene, args, world),
-            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"each step: 1 view of the scene thinned to every {args.thin}th Gaussian "
-                                       f"({ns} of {scene.n}), fwd+bwd+Adam with a supplied dL/dimage (the "
-                                       f"loss is not timed), scaled x{args.thin}",
+            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"each step: one full view of the {scene.name} scene ({scene.n} Gaussians, "
+                                       f"the step's camera) through preprocess, keys and sort on {cores} cores; "
+                                       f"the per-pixel blend walks (fwd + bwd) on a stratified 1/{tile_mod} of "
+                                       f"its tile rows, scaled x{tile_mod}; x{args.views} views + one Adam over 59N "
+                                       f"(timed on 1/{ADAM_SLICE} of theta, scaled); supplied dL/dimage",
                              "cpu": _cpu_model()},
             "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

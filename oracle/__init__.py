@@ -37,7 +37,7 @@ CB_R, CB_G, CB_B, CB_JX, CB_JX_NEG, CB_JY, CB_JY_NEG = 1, 2, 4, 8, 16, 32, 64
 DELTA_ALPHA = 2.0 ** -18
 DELTA_T = 2.0 ** -11
 
-CFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+CFLAGS = ["-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared"]
 
 _lock = threading.Lock()
 _lib = None
@@ -99,8 +99,16 @@ def lib():
                 fn.argtypes = args
                 fn.restype = None
             l.orc_scan.restype = C.c_int64
+            l.orc_set_threads.argtypes = [C.c_int32]
+            l.orc_set_threads.restype = C.c_int32
             _lib = l
     return _lib
+
+
+def set_threads(k: int = 0) -> int:
+    """Host threads for the oracle's parallel loops (0 = all cores, 1 = serial); results do
+    not depend on it (bgs_oracle.cpp: fixed-order reductions).  Returns the count in effect."""
+    return int(lib().orc_set_threads(int(k)))
 
 
 def _p(a: np.ndarray):

@@ -31,6 +31,16 @@
 //
 // Pinned by tests/test_oracle_*.py (closed forms, brute force, P:146 evaluated
 // literally, orthonormality quadrature, central finite differences, torch Adam).
+//
+// Threading (SURVEY.md §8(d) "std::thread over all host cores ... fixed-order reductions"):
+// OpenMP over independent units only -- Gaussians (preprocess, key emission, chain rule),
+// pixel rows (blend forward), sorted chunks (stable sort = chunk std::stable_sort + stable
+// std::merge rounds), tiles (blend backward).  The per-unit arithmetic is unchanged, and the
+// one cross-unit sum (the blend backward's per-Gaussian sums over pixels) is reduced in a
+// fixed order -- per tile, then tiles in index order -- so results do not depend on the
+// thread count.  orc_set_threads(k) fixes k (1 = the plain serial program).
+
+#include <omp.h>
 
 #include <algorithm>
 #include <cmath>
@@ -361,7 +371,7 @@ WalkOut walk_pixel(const Gauss2D& g, const uint32_t* values, uint32_t start, uin
     w.T = tT;
     w.last = (int32_t)(pos - start + 1);
     ++w.blended;
-    on_blend(id, aclamp);
+    on_blend(id, aclamp, pos);
   }
   return w;
 }
@@ -455,13 +465,20 @@ struct PixelList {  // frozen per-pixel decisions: blended Gaussians in order, a
 // ===========================================================================
 extern "C" {
 
-int32_t orc_version(void) { return 1; }
+int32_t orc_version(void) { return 2; }
+
+// Threads used by the parallel loops (k <= 0: all host cores); returns the count in effect.
+int32_t orc_set_threads(int32_t k) {
+  omp_set_num_threads(k > 0 ? k : omp_get_num_procs());
+  return omp_get_max_threads();
+}
 
 // O1-O9 for every Gaussian.  Outputs for culled Gaussians: radius 0, tiles 0, rest 0.
 void orc_preprocess(int64_t n, int32_t deg, const float* theta, const orc_camera* cam, uint32_t mode,
                     int32_t* radius, float* depth, float* xy, float* conic, float* opacity, float* rgb,
                     uint8_t* cbits, int32_t* rect, uint32_t* tiles_touched) {
   Theta th{n, theta};
+#pragma omp parallel for schedule(static, 4096)
   for (int64_t i = 0; i < n; ++i) {
     const PreF p = preprocess_one(th, i, deg, *cam, mode);
     radius[i] = p.visible ? p.radius : 0;
@@ -492,6 +509,7 @@ int64_t orc_scan(int64_t n, const uint32_t* tiles_touched, uint64_t* offsets) {
 // O11: keys in index order, each rect ty-major (R13).
 void orc_duplicate(int64_t n, const uint32_t* tiles_touched, const float* depth, const int32_t* rect,
                    const uint64_t* offsets, int32_t tiles_x, uint64_t* keys, uint32_t* values) {
+#pragma omp parallel for schedule(static, 4096)
   for (int64_t i = 0; i < n; ++i) {
     if (tiles_touched[i] == 0) continue;
     uint64_t o = offsets[i];
@@ -504,14 +522,33 @@ void orc_duplicate(int64_t n, const uint32_t* tiles_touched, const float* depth,
   }
 }
 
-// O12: stable ascending sort by the 64-bit key (library routine: std::stable_sort).
+// O12: stable ascending sort by the 64-bit key (library routines: std::stable_sort on
+// contiguous chunks, then rounds of std::merge of neighbouring sorted runs -- std::merge
+// takes the left run's element first on equal keys, so the result is the stable order).
 void orc_sort(int64_t k, uint64_t* keys, uint32_t* values) {
-  std::vector<std::pair<uint64_t, uint32_t>> kv((size_t)k);
+  typedef std::pair<uint64_t, uint32_t> KV;
+  auto by_key = [](const KV& a, const KV& b) { return a.first < b.first; };
+  std::vector<KV> kv((size_t)k), tmp;
+#pragma omp parallel for schedule(static, 65536)
   for (int64_t i = 0; i < k; ++i) kv[i] = {keys[i], values[i]};
-  std::stable_sort(kv.begin(), kv.end(),
-                   [](const std::pair<uint64_t, uint32_t>& a, const std::pair<uint64_t, uint32_t>& b) {
-                     return a.first < b.first;
-                   });
+  const int64_t chunks = k < (1 << 16) ? 1 : std::max<int64_t>(1, omp_get_max_threads());
+  const int64_t len = (k + chunks - 1) / std::max<int64_t>(1, chunks);
+#pragma omp parallel for schedule(static, 1)
+  for (int64_t c = 0; c < chunks; ++c) {
+    const int64_t lo = std::min(k, c * len), hi = std::min(k, lo + len);
+    std::stable_sort(kv.begin() + lo, kv.begin() + hi, by_key);
+  }
+  if (chunks > 1) tmp.resize((size_t)k);
+  for (int64_t w = len; w < k; w *= 2) {  // merge runs [lo, lo+w) and [lo+w, lo+2w)
+    const int64_t pairs = (k + 2 * w - 1) / (2 * w);
+#pragma omp parallel for schedule(static, 1)
+    for (int64_t pi = 0; pi < pairs; ++pi) {
+      const int64_t lo = pi * 2 * w, mid = std::min(k, lo + w), hi = std::min(k, lo + 2 * w);
+      std::merge(kv.begin() + lo, kv.begin() + mid, kv.begin() + mid, kv.begin() + hi, tmp.begin() + lo, by_key);
+    }
+    kv.swap(tmp);
+  }
+#pragma omp parallel for schedule(static, 65536)
   for (int64_t i = 0; i < k; ++i) {
     keys[i] = kv[i].first;
     values[i] = kv[i].second;
@@ -539,27 +576,34 @@ void orc_render_fwd(const orc_camera* cam, uint32_t mode, const uint32_t* ranges
   const int W = cam->width, H = cam->height;
   const int tiles_x = (W + TILE - 1) / TILE;
   const Gauss2D g{xy, conic, opacity, rgb};
-  int64_t cursor = 0;
-  for (int py = 0; py < H; ++py)
-    for (int px = 0; px < W; ++px) {
-      const int t = (py / TILE) * tiles_x + (px / TILE);
-      const int64_t pix = (int64_t)py * W + px;
-      if (list_ptr) list_ptr[pix] = cursor;
-      const WalkOut w = walk_pixel(g, values, ranges[2 * t], ranges[2 * t + 1], (float)px, (float)py, mode,
-                                   delta_alpha, delta_T, [&](uint32_t id, bool ac) {
-                                     if (list_ptr) {
-                                       list_gid[cursor] = (int32_t)id;
-                                       list_aclamp[cursor] = ac ? 1 : 0;
-                                       ++cursor;
-                                     }
-                                   });
-      for (int ch = 0; ch < 3; ++ch) image[(int64_t)ch * H * W + pix] = std::fma(w.T, cam->bg[ch], w.C[ch]);
-      final_T[pix] = w.T;
-      n_contrib[pix] = (uint32_t)w.last;
-      if (walked) walked[pix] = (uint32_t)w.walked;
-      if (blended) blended[pix] = (uint32_t)w.blended;
-      if (flags) flags[pix] = w.flagged ? 1 : 0;
-    }
+  int64_t cursor = 0;  // list outputs (frozen decisions) are written in pixel order: serial
+  auto pixel = [&](int px, int py) {
+    const int t = (py / TILE) * tiles_x + (px / TILE);
+    const int64_t pix = (int64_t)py * W + px;
+    if (list_ptr) list_ptr[pix] = cursor;
+    const WalkOut w = walk_pixel(g, values, ranges[2 * t], ranges[2 * t + 1], (float)px, (float)py, mode,
+                                 delta_alpha, delta_T, [&](uint32_t id, bool ac, uint32_t) {
+                                   if (list_ptr) {
+                                     list_gid[cursor] = (int32_t)id;
+                                     list_aclamp[cursor] = ac ? 1 : 0;
+                                     ++cursor;
+                                   }
+                                 });
+    for (int ch = 0; ch < 3; ++ch) image[(int64_t)ch * H * W + pix] = std::fma(w.T, cam->bg[ch], w.C[ch]);
+    final_T[pix] = w.T;
+    n_contrib[pix] = (uint32_t)w.last;
+    if (walked) walked[pix] = (uint32_t)w.walked;
+    if (blended) blended[pix] = (uint32_t)w.blended;
+    if (flags) flags[pix] = w.flagged ? 1 : 0;
+  };
+  if (list_ptr) {
+    for (int py = 0; py < H; ++py)
+      for (int px = 0; px < W; ++px) pixel(px, py);
+  } else {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int py = 0; py < H; ++py)
+      for (int px = 0; px < W; ++px) pixel(px, py);
+  }
   if (list_ptr) list_ptr[(int64_t)H * W] = cursor;
 }
 
@@ -585,7 +629,7 @@ void orc_render_bruteforce(const orc_camera* cam, uint32_t mode, int64_t n, cons
         return da != db ? da < db : a < b;
       });
       const WalkOut w = walk_pixel(g, lst.data(), 0, (uint32_t)lst.size(), (float)px, (float)py, mode, 0.0, 0.0,
-                                   [](uint32_t, bool) {});
+                                   [](uint32_t, bool, uint32_t) {});
       const int64_t pix = (int64_t)py * W + px;
       for (int ch = 0; ch < 3; ++ch) image[(int64_t)ch * H * W + pix] = std::fma(w.T, cam->bg[ch], w.C[ch]);
       final_T[pix] = w.T;
@@ -621,71 +665,117 @@ void orc_render_frozen(int64_t n, int32_t deg, const double* theta_d, const orc_
 // O15: blend backward per pixel (double, decisions frozen from the float walk).
 // Outputs per-Gaussian sums (double, +=): g_xy[2n] (pixel units), g_conic[3n]
 // (w.r.t. conic = Sigma'^-1 entries (xx, xy, yy)), g_opac[n], g_rgb[3n].
+// Sum order (fixed, thread-count independent): within a tile over its pixels in row-major
+// order into per-list-position partials, then the tiles' partials in tile index order.
+namespace {
+struct Blend2D {  // what the double backward reads per Gaussian (from preprocess_double)
+  double xy[2], conic[3], o, rgb[3];
+};
+}  // namespace
+
 void orc_render_bwd(int64_t n, int32_t deg, const float* theta, const orc_camera* cam, uint32_t mode,
                     const int32_t* radius, const uint8_t* cbits, const uint32_t* ranges, const uint32_t* values,
                     const float* xy, const float* conic, const float* opacity, const float* rgb,
                     const float* dl_dimage, double* g_xy, double* g_conic, double* g_opac, double* g_rgb) {
   std::vector<double> thd((size_t)59 * n);
-  for (size_t k = 0; k < thd.size(); ++k) thd[k] = theta[k];
+#pragma omp parallel for schedule(static, 65536)
+  for (int64_t k = 0; k < 59 * n; ++k) thd[k] = theta[k];
   ThetaD th{n, thd.data()};
-  std::vector<PreD> pre((size_t)n);
-  for (int64_t i = 0; i < n; ++i)
-    if (radius[i] > 0) preprocess_double(th, i, deg, *cam, mode, cbits[i], pre[i]);
+  std::vector<Blend2D> pre((size_t)n);
+#pragma omp parallel for schedule(static, 4096)
+  for (int64_t i = 0; i < n; ++i) {
+    if (radius[i] <= 0) continue;
+    PreD p;
+    preprocess_double(th, i, deg, *cam, mode, cbits[i], p);
+    Blend2D& b = pre[i];
+    for (int k = 0; k < 2; ++k) b.xy[k] = p.xy[k];
+    for (int k = 0; k < 3; ++k) { b.conic[k] = p.conic[k]; b.rgb[k] = p.rgb[k]; }
+    b.o = p.o;
+  }
   const int W = cam->width, H = cam->height;
-  const int tiles_x = (W + TILE - 1) / TILE;
+  const int tiles_x = (W + TILE - 1) / TILE, tiles_y = (H + TILE - 1) / TILE;
+  const int num_tiles = tiles_x * tiles_y;
   const Gauss2D g{xy, conic, opacity, rgb};
-  std::vector<uint32_t> ids;
-  std::vector<uint8_t> acl;
-  std::vector<double> al, Tb, Gv;
-  for (int py = 0; py < H; ++py)
-    for (int px = 0; px < W; ++px) {
-      const int t = (py / TILE) * tiles_x + (px / TILE);
-      ids.clear();
-      acl.clear();
-      walk_pixel(g, values, ranges[2 * t], ranges[2 * t + 1], (float)px, (float)py, mode, 0.0, 0.0,
-                 [&](uint32_t id, bool ac) {
-                   ids.push_back(id);
-                   acl.push_back(ac ? 1 : 0);
-                 });
-      const int m = (int)ids.size();
-      if (m == 0) continue;
-      const int64_t pix = (int64_t)py * W + px;
-      double dLdC[3];
-      for (int ch = 0; ch < 3; ++ch) dLdC[ch] = dl_dimage[(int64_t)ch * H * W + pix];
-      al.assign(m, 0.0);
-      Tb.assign(m + 1, 0.0);
-      Gv.assign(m, 0.0);
-      Tb[0] = 1.0;
-      for (int j = 0; j < m; ++j) {
-        const PreD& p = pre[ids[j]];
-        const double dx = p.xy[0] - px, dy = p.xy[1] - py;
-        const double power = -0.5 * (p.conic[0] * dx * dx + p.conic[2] * dy * dy) - p.conic[1] * dx * dy;
-        Gv[j] = std::exp(power);
-        al[j] = acl[j] ? 0.99 : p.o * Gv[j];
-        Tb[j + 1] = Tb[j] * (1.0 - al[j]);
-      }
-      double S[3];
-      for (int ch = 0; ch < 3; ++ch) S[ch] = Tb[m] * (double)cam->bg[ch];
-      for (int j = m - 1; j >= 0; --j) {
-        const uint32_t id = ids[j];
-        const PreD& p = pre[id];
-        double dLda = 0.0;
-        for (int ch = 0; ch < 3; ++ch) {
-          g_rgb[3 * id + ch] += dLdC[ch] * al[j] * Tb[j];
-          dLda += dLdC[ch] * (p.rgb[ch] * Tb[j] - S[ch] / (1.0 - al[j]));
-          S[ch] += p.rgb[ch] * al[j] * Tb[j];
+  enum { NACC = 9 };  // per list position: xy 2, conic 3, opacity 1, rgb 3
+  // one tile: every pixel's walk and double backward, partials per list position
+  auto tile_partials = [&](int t, std::vector<double>& acc) {
+    const uint32_t start = ranges[2 * t], end = ranges[2 * t + 1];
+    acc.assign((size_t)(end - start) * NACC, 0.0);
+    std::vector<uint32_t> ids, pos;
+    std::vector<uint8_t> acl;
+    std::vector<double> al, Tb, Gv;
+    const int ty = t / tiles_x, tx = t % tiles_x;
+    for (int py = ty * TILE; py < std::min(H, ty * TILE + TILE); ++py)
+      for (int px = tx * TILE; px < std::min(W, tx * TILE + TILE); ++px) {
+        ids.clear();
+        pos.clear();
+        acl.clear();
+        walk_pixel(g, values, start, end, (float)px, (float)py, mode, 0.0, 0.0,
+                   [&](uint32_t id, bool ac, uint32_t ps) {
+                     ids.push_back(id);
+                     pos.push_back(ps - start);
+                     acl.push_back(ac ? 1 : 0);
+                   });
+        const int m = (int)ids.size();
+        if (m == 0) continue;
+        const int64_t pix = (int64_t)py * W + px;
+        double dLdC[3];
+        for (int ch = 0; ch < 3; ++ch) dLdC[ch] = dl_dimage[(int64_t)ch * H * W + pix];
+        al.assign(m, 0.0);
+        Tb.assign(m + 1, 0.0);
+        Gv.assign(m, 0.0);
+        Tb[0] = 1.0;
+        for (int j = 0; j < m; ++j) {
+          const Blend2D& p = pre[ids[j]];
+          const double dx = p.xy[0] - px, dy = p.xy[1] - py;
+          const double power = -0.5 * (p.conic[0] * dx * dx + p.conic[2] * dy * dy) - p.conic[1] * dx * dy;
+          Gv[j] = std::exp(power);
+          al[j] = acl[j] ? 0.99 : p.o * Gv[j];
+          Tb[j + 1] = Tb[j] * (1.0 - al[j]);
         }
-        if (acl[j]) continue;  // clamped alpha: zero gradient to o and G (R18)
-        const double dx = p.xy[0] - px, dy = p.xy[1] - py;
-        g_opac[id] += dLda * Gv[j];
-        const double dLdp = dLda * p.o * Gv[j];
-        g_xy[2 * id + 0] += dLdp * (-p.conic[0] * dx - p.conic[1] * dy);
-        g_xy[2 * id + 1] += dLdp * (-p.conic[2] * dy - p.conic[1] * dx);
-        g_conic[3 * id + 0] += dLdp * (-0.5 * dx * dx);
-        g_conic[3 * id + 1] += dLdp * (-dx * dy);
-        g_conic[3 * id + 2] += dLdp * (-0.5 * dy * dy);
+        double S[3];
+        for (int ch = 0; ch < 3; ++ch) S[ch] = Tb[m] * (double)cam->bg[ch];
+        for (int j = m - 1; j >= 0; --j) {
+          const Blend2D& p = pre[ids[j]];
+          double* a = acc.data() + (size_t)pos[j] * NACC;  // [xy 0-1 | conic 2-4 | opac 5 | rgb 6-8]
+          double dLda = 0.0;
+          for (int ch = 0; ch < 3; ++ch) {
+            a[6 + ch] += dLdC[ch] * al[j] * Tb[j];
+            dLda += dLdC[ch] * (p.rgb[ch] * Tb[j] - S[ch] / (1.0 - al[j]));
+            S[ch] += p.rgb[ch] * al[j] * Tb[j];
+          }
+          if (acl[j]) continue;  // clamped alpha: zero gradient to o and G (R18)
+          const double dx = p.xy[0] - px, dy = p.xy[1] - py;
+          a[5] += dLda * Gv[j];
+          const double dLdp = dLda * p.o * Gv[j];
+          a[0] += dLdp * (-p.conic[0] * dx - p.conic[1] * dy);
+          a[1] += dLdp * (-p.conic[2] * dy - p.conic[1] * dx);
+          a[2] += dLdp * (-0.5 * dx * dx);
+          a[3] += dLdp * (-dx * dy);
+          a[4] += dLdp * (-0.5 * dy * dy);
+        }
+      }
+  };
+  const int batch = std::max(1, 8 * omp_get_max_threads());
+  std::vector<std::vector<double>> accs((size_t)batch);
+  for (int t0 = 0; t0 < num_tiles; t0 += batch) {
+    const int t1 = std::min(num_tiles, t0 + batch);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int t = t0; t < t1; ++t) tile_partials(t, accs[t - t0]);
+    for (int t = t0; t < t1; ++t) {  // fixed order: tiles in index order, positions in list order
+      const std::vector<double>& acc = accs[t - t0];
+      const uint32_t start = ranges[2 * t];
+      for (size_t q = 0; q < acc.size() / NACC; ++q) {
+        const uint32_t id = values[start + q];
+        const double* a = acc.data() + q * NACC;
+        g_xy[2 * id] += a[0];
+        g_xy[2 * id + 1] += a[1];
+        for (int k = 0; k < 3; ++k) g_conic[3 * id + k] += a[2 + k];
+        g_opac[id] += a[5];
+        for (int k = 0; k < 3; ++k) g_rgb[3 * id + k] += a[6 + k];
       }
     }
+  }
 }
 
 // O16: preprocess backward (double, decisions frozen), grad59[59n] +=.
@@ -693,11 +783,13 @@ void orc_preprocess_bwd(int64_t n, int32_t deg, const float* theta, const orc_ca
                         const int32_t* radius, const uint8_t* cbits, const double* g_xy, const double* g_conic,
                         const double* g_opac, const double* g_rgb, double* grad) {
   std::vector<double> thd((size_t)59 * n);
-  for (size_t k = 0; k < thd.size(); ++k) thd[k] = theta[k];
+#pragma omp parallel for schedule(static, 65536)
+  for (int64_t k = 0; k < 59 * n; ++k) thd[k] = theta[k];
   ThetaD th{n, thd.data()};
   double V[16], P[16];
   for (int k = 0; k < 16; ++k) { V[k] = cam->view[k]; P[k] = cam->proj[k]; }
   const int ncf = n_coeffs(deg);
+#pragma omp parallel for schedule(static, 1024)
   for (int64_t i = 0; i < n; ++i) {
     if (radius[i] <= 0) continue;
     PreD p;
@@ -858,6 +950,7 @@ void orc_canon_exp(int64_t n, const float* x, float* out) {
 void orc_adam(int64_t n, double* theta, double* grad, double* m, double* v, const double* lr, double b1, double b2,
               double eps, int64_t step) {
   const double bc1 = 1.0 - std::pow(b1, (double)step), bc2 = 1.0 - std::pow(b2, (double)step);
+#pragma omp parallel for schedule(static, 65536)
   for (int64_t e = 0; e < 59 * n; ++e) {
     int grp;
     if (e < 3 * n) grp = 0;
