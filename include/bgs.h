@@ -349,6 +349,12 @@ bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contri
 /* Kept selectable: the blend backward on 8x4-pixel units (one pixel per lane) instead of
  * the default 8x8 units (two pixels per lane). */
 #define BGS_DEBUG_BWD_8X4 8
+/* Depth-first path with the row split (rowsplit.cu: the (row, Gaussian) entries stably
+ * split by tile row, then each row's items by tile column, one warp per chunk with a
+ * position counter per row / column in shared memory) instead of the default one-pass
+ * direct tile split (a position counter per tile of the image per warp); same values and
+ * ranges; measured slower. */
+#define BGS_DEBUG_SORT_ROWSPLIT 16
 /* Parity mode (R23): the blend kernels evaluate exp with the canonical expression tree the
  * oracle also uses (instead of MUFU.EX2) and the forward does not split walks, so every
  * blend decision, n_contrib and the image are bit-identical to the oracle's. */

@@ -26,6 +26,7 @@ BGS_DEBUG_SKIP_SORT = 1
 BGS_DEBUG_SORT_ONESWEEP64 = 2
 BGS_DEBUG_SORT_RADIX_SPLIT = 4
 BGS_DEBUG_BWD_8X4 = 8
+BGS_DEBUG_SORT_ROWSPLIT = 16
 BGS_DEBUG_PARITY_EXP = 64
 
 

@@ -25,6 +25,17 @@ __host__ __device__ __forceinline__ uint32_t chunk_items_of(uint32_t K) {
   while (c > (uint32_t)kChunkItemsMin && K / c < (uint32_t)kChunkTarget) c >>= 1;
   return c;
 }
+// row split (rowsplit.cu): entry chunks of kRsPairChunk (row, rank) pairs; item units of
+// unit_items_of(K) items inside one tile row (a power of two in [1024, 8192], >= 2048 units
+// when K allows)
+constexpr int kRsPairChunk = 4096;
+constexpr uint32_t kRsUnitMin = 1024, kRsUnitMax = 8192, kRsUnitTarget = 2048;
+__host__ __device__ __forceinline__ uint32_t unit_items_of(uint32_t K) {
+  uint32_t c = kRsUnitMax;
+  while (c > kRsUnitMin && K / c < kRsUnitTarget) c >>= 1;
+  return c;
+}
+constexpr int kRsMaxTiles = 4096;  // tiles_x, tiles_y bound of the row split (else the radix split)
 constexpr int kDirectMaxCells = 12800;  // (tiles_x + 1)(tiles_y + 1) bound  // the checkpoint / state pools are sized for seg_len >= this
 
 // blend work-unit planning (k_*_plan_*): 128 cost buckets (4 per octave, costliest first),
@@ -45,6 +56,9 @@ enum : int {
   C_SORT32_TICKET = 17,       // 8 slots: the depth-first path's 32-bit passes
   C_BWD_UNITS = 25,           // number of backward work units (k_bwd_plan)
   C_FWD_UNITS = 26,           // number of forward work units (k_fwd_plan)
+  C_PAIRS = C_SCAN_TOTAL,     // row split: number of (row, rank) entries (the height scan's total)
+  C_UNITS = 27,               // row split: number of item units
+  C_RS_TICKET = 28,           // row split: tile ticket of the width scan
   C_NUM = 32
 };
 
@@ -109,6 +123,15 @@ struct Frame {
   uint2* rank_rect;        // [n] packed tile rect per depth rank
   uint8_t* cbits;          // [n] frozen clamp decisions (rgb / J) for the backward (R18)
   const uint8_t* keep;     // [n] NEXT-4 keep mask (device, caller-owned) or null: keep[i] == 0 culls i
+  // row split (rowsplit.cu)
+  uint32_t* rank_h;        // [n] tile rows of each depth rank's rect
+  uint32_t* rs_tabA;       // [rs_max_chunks][tiles_y] entry counts, then offsets, per (pair chunk, row)
+  uint32_t* rs_chunk_r0;   // [rs_max_chunks] first rank of each pair chunk
+  uint32_t* rs_rows;       // [3 tiles_y + 2] row entry totals, row entry starts, row unit starts
+  uint4* rs_units;         // [rs_max_units] {row, first item, end item, first entry}
+  uint32_t* rs_tabB;       // [rs_max_units][tiles_x] item counts, then offsets, per (unit, x)
+  unsigned long long* rs_status;  // [rs_scan_tiles] look-back words of the width scan
+  int64_t rs_max_units, rs_scan_tiles;
 };
 static_assert(sizeof(Frame) <= sizeof(bgs_frame), "Frame must fit in bgs_frame::opaque");
 constexpr uint64_t kFrameMagic = 0xB6500F7A3E5ull;
@@ -155,8 +178,11 @@ bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* 
 bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                               int shift, int64_t count, cudaStream_t s, const uint2* rect = nullptr,
-                              uint32_t* rank_cnt = nullptr, uint2* rank_rect = nullptr);
+                              uint32_t* rank_cnt = nullptr, uint2* rank_rect = nullptr,
+                              uint32_t* rank_h = nullptr);
 bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, bool publish_k, cudaStream_t s);
+bgs_status launch_rowsplit(Frame* F, cudaStream_t s);
+bgs_status launch_tile_scan(Frame* F, cudaStream_t s);
 
 // ---------------------------------------------------------------- device helpers
 __device__ __forceinline__ float fast_exp(float x) {

@@ -44,7 +44,9 @@ struct Layout {
   size_t radius, depth, record, tiles_touched, rect, offsets, keys0, keys1, vals0, vals1, ranges, scan_status, sort_hist,
       sort_status, counters, plan, grad2d, tile_count, order_fwd, order_bwd, block_cost, ck_table, ck_pool, spec_base, spec_n,
       arrive, spec_state, spec_last, chunk_cnt, dkey0, dkey1,
-      dval0, dval1, rank_cnt, item_off, rank_rect, cbits, total;
+      dval0, dval1, rank_cnt, item_off, rank_rect, cbits, rank_h, rs_tabA, rs_chunk_r0, rs_rows, rs_units, rs_tabB,
+      rs_status, total;
+  int64_t rs_max_chunks, rs_max_units, rs_scan_tiles;
   int64_t ck_cap;
   int32_t tiles_x, tiles_y, num_tiles, sort_bits, sort_passes, scan_tiles;
   int64_t sort_tiles_max;
@@ -118,6 +120,16 @@ static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layou
   L.item_off = take(4 * N);
   L.rank_rect = take(8 * N);
   L.cbits = take(N);
+  L.rank_h = take(4 * N);
+  L.rs_max_chunks = (max_keys + kRsPairChunk - 1) / kRsPairChunk + 1;
+  L.rs_max_units = max_keys / kRsUnitMin + L.tiles_y + 1;
+  L.rs_scan_tiles = (max_keys + 4095) / 4096 + 1;
+  L.rs_tabA = take(4 * (size_t)L.rs_max_chunks * L.tiles_y);
+  L.rs_chunk_r0 = take(4 * (size_t)L.rs_max_chunks);
+  L.rs_rows = take(4 * (3 * (size_t)L.tiles_y + 2));
+  L.rs_units = take(16 * (size_t)L.rs_max_units);
+  L.rs_tabB = take(4 * (size_t)L.rs_max_units * L.tiles_x);
+  L.rs_status = take(8 * (size_t)L.rs_scan_tiles);
   L.total = o;
   return true;
 }
@@ -261,6 +273,15 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->item_off = (uint32_t*)(base + L.item_off);
   F->rank_rect = (uint2*)(base + L.rank_rect);
   F->cbits = (uint8_t*)(base + L.cbits);
+  F->rank_h = (uint32_t*)(base + L.rank_h);
+  F->rs_tabA = (uint32_t*)(base + L.rs_tabA);
+  F->rs_chunk_r0 = (uint32_t*)(base + L.rs_chunk_r0);
+  F->rs_rows = (uint32_t*)(base + L.rs_rows);
+  F->rs_units = (uint4*)(base + L.rs_units);
+  F->rs_tabB = (uint32_t*)(base + L.rs_tabB);
+  F->rs_status = (unsigned long long*)(base + L.rs_status);
+  F->rs_max_units = L.rs_max_units;
+  F->rs_scan_tiles = L.rs_scan_tiles;
   F->final_buf = L.sort_passes & 1;  // pass p reads buf p&1, writes buf (p+1)&1
   return BGS_OK;
 }

@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
                                                             uint32_t* status, uint32_t* ticket,
                                                             const uint32_t* counters, int shift, int64_t count,
                                                             const uint2* __restrict__ rect, uint32_t* rank_cnt,
-                                                            uint2* rank_rect) {
+                                                            uint2* rank_rect, uint32_t* rank_h) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<KT>& S = *reinterpret_cast<SortSmem<KT>*>(smem_raw);
   if (counters[C_OVERFLOW]) return;
@@ -191,16 +191,18 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
       kout[g] = k2;
       vout[g] = v;
       if (rank_rect) {  // the depth sort's last pass: per-rank tile count and packed rect
-        uint32_t t = 0;
+        uint32_t t = 0, hh = 0;
         uint2 packed = make_uint2(0u, 0u);
         if ((uint32_t)k2 != 0xffffffffu) {  // visible: the preprocess's rect (R11)
           const uint2 q = rect[v];
           const uint32_t w = q.y & 0xffffu;
-          t = w * (q.y >> 16);
+          hh = q.y >> 16;
+          t = w * hh;
           packed = make_uint2(q.x, w);
         }
         rank_cnt[g] = t;
         rank_rect[g] = packed;
+        rank_h[g] = hh;
       }
     }
     __syncthreads();
@@ -226,7 +228,7 @@ bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* 
                             const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                             int shift, cudaStream_t s) {
   k_sort_pass<uint64_t><<<pass_grid<uint64_t>(), kSortThreads, sizeof(SortSmem<uint64_t>), s>>>(
-      kin, vin, kout, vout, hist, status, ticket, counters, shift, -1, nullptr, nullptr, nullptr);
+      kin, vin, kout, vout, hist, status, ticket, counters, shift, -1, nullptr, nullptr, nullptr, nullptr);
   note_launch();
   return check_launch("k_sort_pass<u64>");
 }
@@ -234,9 +236,9 @@ bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* 
 bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                               int shift, int64_t count, cudaStream_t s, const uint2* rect, uint32_t* rank_cnt,
-                              uint2* rank_rect) {
+                              uint2* rank_rect, uint32_t* rank_h) {
   k_sort_pass<uint32_t><<<pass_grid<uint32_t>(), kSortThreads, sizeof(SortSmem<uint32_t>), s>>>(
-      kin, vin, kout, vout, hist, status, ticket, counters, shift, count, rect, rank_cnt, rank_rect);
+      kin, vin, kout, vout, hist, status, ticket, counters, shift, count, rect, rank_cnt, rank_rect, rank_h);
   note_launch();
   return check_launch("k_sort_pass<u32>");
 }

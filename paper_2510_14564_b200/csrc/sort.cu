@@ -584,6 +584,12 @@ __global__ void __launch_bounds__(kOrderThreads) k_tile_scan(const uint32_t* __r
     hist[4 * kRadixBins + k] = (&s_h[0][0])[k];
 }
 
+bgs_status launch_tile_scan(Frame* F, cudaStream_t s) {
+  k_tile_scan<<<1, kOrderThreads, 0, s>>>(F->tile_count, F->num_tiles, F->counters, F->ranges, F->sort_hist, 4);
+  note_launch();
+  return check_launch("k_tile_scan");
+}
+
 // look-back status words of a pass over at most `count` keys
 static bgs_status memset_status(Frame* F, cudaStream_t s, int64_t count = -1) {
   const int64_t tiles = count < 0 ? F->sort_tiles_max : (count + 4095) / 4096;
@@ -637,11 +643,20 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
     const bool last = p == 3;
     st = launch_sort_pass32(F->dkey[a], F->dval[a], F->dkey[b], F->dval[b], F->sort_hist + p * kRadixBins,
                             F->sort_status, F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, F->n, s,
-                            last ? F->rect : nullptr, last ? F->rank_cnt : nullptr, last ? F->rank_rect : nullptr);
+                            last ? F->rect : nullptr, last ? F->rank_cnt : nullptr, last ? F->rank_rect : nullptr,
+                            last ? F->rank_h : nullptr);
     if (st != BGS_OK) return st;
   }
   // K (published with the capacity check) = the total of the depth-order scan
   if ((st = launch_scan(F->rank_cnt, F->item_off, F->n, F, true, s)) != BGS_OK) return st;
+  const bool rowsplit_ok = F->tiles_x <= kRsMaxTiles && F->tiles_y <= kRsMaxTiles;
+  if (rowsplit_ok && (F->debug_flags & BGS_DEBUG_SORT_ROWSPLIT)) {
+    // (3'') row split (rowsplit.cu, measured slower than the direct split: DESIGN.md §6):
+    // the ranks' heights scanned for the entry count
+    F->final_buf = 0;
+    if ((st = launch_scan(F->rank_h, F->offsets, F->n, F, false, s)) != BGS_OK) return st;
+    return launch_rowsplit(F, s);
+  }
   if (F->chunk_cnt && !(F->debug_flags & BGS_DEBUG_SORT_RADIX_SPLIT)) {
     // (3') direct tile split: per-(chunk, tile) counts, column scan, ranges, emission
     F->final_buf = 0;

@@ -150,11 +150,11 @@ def test_unsorted_keys_parity(bgs, name):
 
 
 @pytest.mark.parametrize("name", list(scenes()))
-@pytest.mark.parametrize("path", ["depth_first", "radix_split", "onesweep64"])
+@pytest.mark.parametrize("path", ["depth_first", "rowsplit", "radix_split", "onesweep64"])
 def test_sort_and_ranges_parity(bgs, name, path):
     s = scenes()[name]()
     cam = s.cameras[0]
-    flags = {"depth_first": 0, "radix_split": bgs.BGS_DEBUG_SORT_RADIX_SPLIT,
+    flags = {"depth_first": 0, "rowsplit": bgs.BGS_DEBUG_SORT_ROWSPLIT, "radix_split": bgs.BGS_DEBUG_SORT_RADIX_SPLIT,
              "onesweep64": bgs.BGS_DEBUG_SORT_ONESWEEP64}[path]
     r, _, _ = run_gpu(bgs, s, cam, flags=flags)
     ref = oracle.forward(s.theta, s.n, s.sh_degree, cam)
@@ -168,13 +168,14 @@ def test_sort_and_ranges_parity(bgs, name, path):
 
 
 def test_sort_paths_identical_at_garden_scale(bgs):
-    """The depth-first paths (direct and radix tile split) and the 64-bit onesweep reference
+    """The depth-first paths (direct tile split, row split, radix tile split) and the 64-bit
+    onesweep reference
     give bit-identical tile lists
     on a full-size garden view (K ~ 4.8e7), where exact depth ties do occur."""
     s = gen.garden()
     cam = s.cameras[8]
     outs = []
-    for flags in (0, bgs.BGS_DEBUG_SORT_ONESWEEP64, bgs.BGS_DEBUG_SORT_RADIX_SPLIT):
+    for flags in (0, bgs.BGS_DEBUG_SORT_ONESWEEP64, bgs.BGS_DEBUG_SORT_RADIX_SPLIT, bgs.BGS_DEBUG_SORT_ROWSPLIT):
         r, _, out = run_gpu(bgs, s, cam, max_keys=1 << 26, flags=flags)
         K = r.num_keys
         v = r.views()
