@@ -32,10 +32,38 @@ UNIT = "views/s"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
 FP32_LANES_PER_SM = 128
 
-# Algorithmic work per unit (DESIGN.md §6 restates each):
-OPS_FWD_VISIT = 13      # FP32-pipe lane-ops per visited (pixel, entry) pair
-OPS_FWD_BLEND = 7       # extra lane-ops when the entry is blended (20 total)
-OPS_BWD_EVAL = 57       # lane-ops per evaluated pair in the blend backward
+# Algorithmic work per unit (DESIGN.md §6 restates each): FP32-pipe
+# lane-ops per (pixel, list entry) pair of the per-pixel walk, by outcome
+OPS_SKIPPED = 13        # power + exp + alpha test of an entry that is not blended
+OPS_FWD_BLENDED = 20    # ... and the blend of one that is (forward)
+OPS_BWD_BLENDED = 57    # backward: recompute, T division, colour / bg / geometric terms, 9 outputs
+
+
+def _ncu_hw(config):
+    """Hardware counters of the blend kernels from the committed ncu capture (garden camera 0,
+    tools/profile_round.sh -> profiles/ncu_hw.json): FP32+ALU lane-ops executed and shared-memory
+    wavefronts per launch, as fractions of the FP32-issue and shared-memory peaks at the SM
+    clock ncu measured (148 SMs x 128 lanes; 1 wavefront per SM per clock)."""
+    if config != "garden":
+        return {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_hw.json")) as f:
+            raw = json.load(f)
+    except Exception:
+        return {}
+    out = {}
+    for stage, d in raw.items():
+        if not isinstance(d, dict) or not d.get("time_s"):
+            continue
+        clk = d["sm_hz"]
+        e = {"hw_source": raw.get("_source", "profiles/ncu_hw.json")}
+        if d.get("lane_ops"):
+            e["hw_lane_op_frac"] = round(d["lane_ops"] / (d["time_s"] * 148 * FP32_LANES_PER_SM * clk), 4)
+            e["hw_lane_ops_per_launch"] = d["lane_ops"]
+        if d.get("smem_wavefronts"):
+            e["smem_wavefront_frac"] = round(d["smem_wavefronts"] / (d["time_s"] * 148 * clk), 4)
+        out[stage] = e
+    return out
 
 
 def parse():
@@ -64,6 +92,14 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--one-frame", action="store_true",
                    help="diagnostic: one frame for all views (no per-view scheduling hint)")
+    p.add_argument("--fixed-batch", action="store_true",
+                   help="every step renders the same 16 cameras (views 4i mod 64), each frame hinted by its own "
+                        "previous forward (round-1 bench); default: the batch rotates over the scene's cameras "
+                        "(step s renders views 4i + s mod 64), each view hinted by its camera's last forward")
+    p.add_argument("--sort-path", default="direct", choices=["direct", "radix_split", "rowsplit", "onesweep64"],
+                   help="a4-a6 implementation (default: the direct tile split; the others are bit-identical)")
+    p.add_argument("--no-variants", action="store_true",
+                   help="skip the extra timed loops (fixed batch; rotating batch without scheduling hints)")
     p.add_argument("--pre-per-view", action="store_true",
                    help="diagnostic: one preprocess launch per view instead of one per 16 views")
     p.add_argument("--no-stage-events", action="store_true", help="diagnostic: no per-stage events in the timed loop")
@@ -104,9 +140,10 @@ def _device_index(local_rank):
     return int(forced) if forced is not None else local_rank
 
 
-def batch_views(n_views, n_cams):
-    """views 4i mod n_cams for i < n_views."""
-    return [(4 * i) % n_cams for i in range(n_views)]
+def batch_views(n_views, n_cams, step=0):
+    """views 4i + step mod n_cams for i < n_views (SURVEY §8(d) at step 0; the batch rotates
+    with the step so that a 16-view batch visits each of 64 cameras every 4 steps)."""
+    return [(4 * i + step) % n_cams for i in range(n_views)]
 
 
 class ClockSampler:
@@ -181,10 +218,16 @@ def run_ours(args, rank, world, local_rank):
     scene = gen.make(args.config, **kw)
     n = scene.n
     cams_all = scene.cameras
-    views = batch_views(args.views, len(cams_all))
-    mine = dp.views_for_rank(views, rank, world)
-    cams = [cams_all[v] for v in mine]
-    W, H = cams[0].width, cams[0].height
+    n_cams = len(cams_all)
+
+    def rank_cams(step, fixed=None):
+        """camera indices of this rank's views at training step `step` (1-based)"""
+        fixed = args.fixed_batch if fixed is None else fixed
+        return dp.views_for_rank(batch_views(args.views, n_cams, 0 if fixed else step - 1), rank, world)
+
+    n_mine = len(rank_cams(1))
+    used = sorted(set(rank_cams(1, True)) if args.fixed_batch else range(n_cams))  # cameras any step renders
+    W, H = cams_all[0].width, cams_all[0].height
     sharded = world > 1 and args.update == "sharded"
     # one GPU, one chain-rule launch: a10 and a11 fused (no collective between them)
     fused = world == 1 and not args.one_frame and args.fuse_adam and args.views <= 16
@@ -208,18 +251,28 @@ def run_ours(args, rank, world, local_rank):
     hp = bgs.AdamHParams(lr_means=1.6e-4 * scene.extent)
     deg = scene.sh_degree
 
-    # size the key capacity once (overflow -> re-run with a larger workspace, R25)
-    rend = bgs.Renderer(n, W, H, max_keys=1 << 24, device=dev)
+    # size the key capacity once over every camera a step may render (overflow -> re-run
+    # with a larger workspace, R25); each camera's scheduling hint (its forward's per-block
+    # walk costs) is saved as a trainer keeps it, so every view is hinted by its camera's
+    # last forward (bgs_frame_save_hint / bgs_frame_load_hint)
+    dflags = {"direct": 0, "radix_split": bgs.BGS_DEBUG_SORT_RADIX_SPLIT, "rowsplit": bgs.BGS_DEBUG_SORT_ROWSPLIT,
+              "onesweep64": bgs.BGS_DEBUG_SORT_ONESWEEP64}[args.sort_path]
+    rend = bgs.Renderer(n, W, H, max_keys=1 << 24, device=dev, debug_flags=dflags)
     kmax = 0
-    for cam in cams:
-        rend.forward(theta, cam, deg)
+    for c in used:
+        rend.forward(theta, cams_all[c], deg)
         kmax = max(kmax, rend.num_keys)
     if int(kmax * 1.1) + 4096 > rend.max_keys:
         rend.alloc(int(kmax * 1.1) + 4096)
-    # one frame per view (as a trainer keeps per-camera state): a frame that re-renders its
-    # view orders the blend work items by its previous forward's per-block costs
-    rends = [rend] + [rend if args.one_frame else bgs.Renderer(n, W, H, max_keys=rend.max_keys, device=dev)
-                      for _ in cams[1:]]
+    hint_bytes = bgs.bgs_frame_hint_bytes(rend.frame)
+    hints = {}
+    for c in used:
+        rend.forward(theta, cams_all[c], deg, check=False)
+        hints[c] = torch.empty(hint_bytes, dtype=torch.uint8, device=dev)
+        bgs.bgs_frame_save_hint(rend.frame, hints[c])
+    # one frame per view slot of the batch
+    rends = [rend] + [rend if args.one_frame else bgs.Renderer(n, W, H, max_keys=rend.max_keys, device=dev, debug_flags=dflags)
+                      for _ in range(n_mine - 1)]
 
     # targets: a perturbed copy of theta rendered once, 8-bit (R19)
     r = gen.rng(1234)
@@ -228,20 +281,20 @@ def run_ours(args, rank, world, local_rank):
     seg["sh"][:, 0, :] += 0.05 * r.standard_normal((n, 3)).astype(np.float32)
     seg["means"][:] += (0.01 * scene.extent * r.standard_normal((n, 3))).astype(np.float32)
     th_t_dev = torch.from_numpy(th_t).to(dev)
-    targets = []
-    for cam in cams:
-        out = rend.forward(th_t_dev, cam, deg)
-        targets.append((out["image"].clamp(0, 1) * 255 + 0.5).to(torch.uint8).contiguous())
+    targets = {}
+    for c in used:
+        out = rend.forward(th_t_dev, cams_all[c], deg)
+        targets[c] = (out["image"].clamp(0, 1) * 255 + 0.5).to(torch.uint8).contiguous()
     del th_t_dev
-    targets_host = [t.cpu().pin_memory() for t in targets]
-    targets_e2e = [torch.empty_like(t) for t in targets]
+    targets_host = {c: t.cpu().pin_memory() for c, t in targets.items()}
+    targets_e2e = [torch.empty_like(targets[used[0]]) for _ in range(n_mine)]
     dl = torch.empty((3, H, W), dtype=torch.float32, device=dev)
     loss = torch.zeros(1, dtype=torch.float32, device=dev)
     loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
     scale = 1.0 / (3.0 * W * H * args.views)
     loss_ws = (torch.empty(bgs.bgs_loss_workspace_bytes(W, H), dtype=torch.uint8, device=dev)
                if args.loss == "l1dssim" else None)
-    cam_structs = [bgs.camera(c) for c in cams]
+    cam_structs_all = {c: bgs.camera(cams_all[c]) for c in used}
     stream = torch.cuda.current_stream()
     # views run round-robin on S streams (their frames, dL/dimage and loss workspaces are
     # independent): one view's single-CTA planning kernels and kernel tails overlap another
@@ -258,7 +311,7 @@ def run_ours(args, rank, world, local_rank):
         stage_names.append("density")
     # all timing events of the timed region are created up front (creating them inside the
     # loop adds host work between launches)
-    n_marks = args.steps * (7 * len(cam_structs) + 9)
+    n_marks = args.steps * (7 * n_mine + 9)
     pool = [torch.cuda.Event(enable_timing=True) for _ in range(n_marks)]
     step_no = [0]
 
@@ -308,9 +361,11 @@ def run_ours(args, rank, world, local_rank):
             S["m"], S["v"] = m_full.clone(), v_full.clone()
             S["lo"], S["hi"] = 0, tot
         S["theta"], S["grad"], S["n"] = th, torch.zeros_like(th), n_new
-        r0 = bgs.Renderer(n_new, W, H, max_keys=max_keys, device=dev)
-        S["rends"] = [r0] + [r0 if args.one_frame else bgs.Renderer(n_new, W, H, max_keys=max_keys, device=dev)
-                             for _ in cams[1:]]
+        r0 = bgs.Renderer(n_new, W, H, max_keys=max_keys, device=dev, debug_flags=dflags)
+        S["rends"] = [r0] + [r0 if args.one_frame else bgs.Renderer(n_new, W, H, max_keys=max_keys, device=dev, debug_flags=dflags)
+                             for _ in range(n_mine - 1)]
+        for c in hints:  # a new scene: no camera has a hint for it yet
+            hint_ok[c] = False
         derive()
 
     def full_moments():
@@ -337,8 +392,15 @@ def run_ours(args, rank, world, local_rank):
         dens_log.append({"step": step_no[0], "n_before": n0, "n_after": n2, "pairs": int(rep.n_pairs),
                          "children": int(rep.n_children)})
 
-    def one_step(tgts, record=None, tgt_events=None):
+    hint_ok = {c: True for c in hints}
+
+    def one_step(tgts, record=None, tgt_events=None, hint_mode="camera"):
+        """one training step; tgts(j, c) -> the target of view slot j (camera c).  hint_mode:
+        "camera" (each view hinted by its camera's last forward), "slot" (by its frame's
+        previous forward), "none" (no hint: work ordered by list length)"""
         step_no[0] += 1
+        cams_idx = rank_cams(step_no[0])
+        cam_structs = [cam_structs_all[c] for c in cams_idx]
 
         def mark(marks):
             if record is not None:
@@ -371,14 +433,23 @@ def run_ours(args, rank, world, local_rank):
                 mark(marks)
                 bgs.bgs_sort(rj.frame)
                 mark(marks)
+                c = cams_idx[j]
+                if hint_mode == "camera":
+                    bgs.bgs_frame_load_hint(rj.frame, hints[c] if hint_ok[c] else None)
+                elif hint_mode == "none":
+                    bgs.bgs_frame_load_hint(rj.frame, None)
                 bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
+                if hint_mode == "camera":
+                    bgs.bgs_frame_save_hint(rj.frame, hints[c])
+                    hint_ok[c] = True
                 mark(marks)
                 if tgt_events is not None:  # this view's target has arrived (H2D on the copy stream)
                     sj.wait_event(tgt_events[j])
+                tg = tgts(j, c)
                 if loss_ws is not None:  # the 3DGS loss 0.8 L1 + 0.2 D-SSIM (NEXT-2), batch mean
-                    bgs.bgs_l1_dssim_loss_grad(rj.image, tgts[j], W, H, 0.2, 1.0 / args.views, dl, loss, loss_ws)
+                    bgs.bgs_l1_dssim_loss_grad(rj.image, tg, W, H, 0.2, 1.0 / args.views, dl, loss, loss_ws)
                 else:  # L1 (R19)
-                    bgs.bgs_l1_loss_grad(rj.image, tgts[j], W, H, scale, dl, loss)
+                    bgs.bgs_l1_loss_grad(rj.image, tg, W, H, scale, dl, loss)
                 mark(marks)
                 bgs.bgs_blend_bwd(rj.frame, dl, rj.final_T, rj.n_contrib)
                 mark(marks)
@@ -424,19 +495,41 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
+    dev_targets = lambda j, c: targets[c]  # noqa: E731  (device-resident inputs)
+
     # warm-up
     for _ in range(args.warmup):
-        one_step(targets)
+        one_step(dev_targets)
     torch.cuda.synchronize()
 
-    # the step trains theta (Adam), which changes the workload; the e2e loop restarts from
-    # this snapshot so both loops time the same sequence of training states
-    snap = None
-    if not args.no_e2e:
-        mf, vf = full_moments()
-        snap = (S["theta"][:59 * S["n"]].clone(), mf.clone(), vf.clone(), S["n"], step_no[0],
-                S["rends"][0].max_keys)
+    # the step trains theta (Adam), which changes the workload; the e2e loop and the variants
+    # restart from this snapshot so every loop times the same sequence of training states
+    mf, vf = full_moments()
+    snap = (S["theta"][:59 * S["n"]].clone(), mf.clone(), vf.clone(), S["n"], step_no[0], S["rends"][0].max_keys)
+    del mf, vf
+    hints_snap = {c: (h.clone(), hint_ok[c]) for c, h in hints.items()}
 
+    def restore():
+        rebuild(snap[0], snap[1], snap[2], snap[3], snap[5])
+        step_no[0] = snap[4]
+        for c, (h, ok) in hints_snap.items():
+            hints[c].copy_(h)
+            hint_ok[c] = ok
+        torch.cuda.synchronize()
+
+    def check_overflow(what):
+        for rj in S["rends"]:  # the sticky flag covers every step since the last check
+            st, _ = bgs.bgs_frame_status(rj.frame)
+            assert st == bgs.BGS_OK, f"key capacity overflow in the {what}"
+
+    def max_over_ranks(ms):
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    check_overflow("warm-up")
     # ---- device-resident timed region (inputs larger than L2: theta 1.37 GB, keys GBs)
     record = {"next": 0, "marks": []}
     barrier()
@@ -444,20 +537,19 @@ def run_ours(args, rank, world, local_rank):
     launches0 = bgs.launch_count()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    hint_mode = "slot" if args.fixed_batch else "camera"
     with ClockSampler(_device_index(local_rank)) as clk:
         torch.cuda.nvtx.range_push("bench_timed")  # ncu --nvtx --nvtx-include "bench_timed/"
         t0.record(stream)
         for _ in range(args.steps):
-            one_step(targets, None if args.no_stage_events else record)
+            one_step(dev_targets, None if args.no_stage_events else record, hint_mode=hint_mode)
         t1.record(stream)
         torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
     barrier()
     launches = bgs.launch_count() - launches0
     ms_local = t0.elapsed_time(t1)
-    for rj in S["rends"]:
-        st, k_last = bgs.bgs_frame_status(rj.frame)
-        assert st == bgs.BGS_OK, "key capacity overflow in the timed region"
+    check_overflow("timed region")
     # per-stage means
     sums = {s: 0.0 for s in stage_names}
     for kind, mk in record["marks"]:
@@ -474,30 +566,26 @@ def run_ours(args, rank, world, local_rank):
                 sums["density"] += mk[4].elapsed_time(mk[5])
     per_step = {s: sums[s] / args.steps for s in stage_names}
 
-
     # ---- end-to-end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
         copy_stream = torch.cuda.Stream(device=dev)
-        tgt_events = [torch.cuda.Event() for _ in cams]
+        tgt_events = [torch.cuda.Event() for _ in range(n_mine)]
 
         def e2e_step():
-            # the step's 16 targets go H2D on a copy stream (after the previous step released
+            # the step's targets go H2D on a copy stream (after the previous step released
             # the buffers); view j's loss waits for target j only, so the copies overlap the
             # earlier views' work
             copy_stream.wait_stream(stream)
             with torch.cuda.stream(copy_stream):
-                for j in range(len(cams)):
-                    targets_e2e[j].copy_(targets_host[j], non_blocking=True)
+                for j, c in enumerate(rank_cams(step_no[0] + 1)):
+                    targets_e2e[j].copy_(targets_host[c], non_blocking=True)
                     tgt_events[j].record(copy_stream)
-            one_step(targets_e2e, tgt_events=tgt_events)
+            one_step(lambda j, c: targets_e2e[j], tgt_events=tgt_events, hint_mode=hint_mode)
             loss_host.copy_(loss, non_blocking=True)
 
         e2e_step()  # warm-up of the copy path
-        rebuild(snap[0], snap[1], snap[2], snap[3], snap[5])  # the pre-timing training state
-        step_no[0] = snap[4]
-        del snap
-        torch.cuda.synchronize()
+        restore()  # the pre-timing training state
         barrier()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -507,21 +595,48 @@ def run_ours(args, rank, world, local_rank):
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
-        e2e_ms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = float(t.item())
+        check_overflow("e2e loop")
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1))
         e2e = {"value": args.views * args.steps / (e2e_ms / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(sum(t.numel() for t in targets_host)) * (world if world > 1 else 1),
+               "h2d_bytes_per_step": int(targets_e2e[0].numel()) * args.views,
                "d2h_bytes_per_step": 4 * world}
 
-    # ---- workload counters (not timed) for the roofline numerators
+    # ---- variants of the schedule (same work, same results; device-resident, timed alike)
+    variants = None
+    if not args.no_variants and not args.one_frame and not args.density_every:
+        variants = {}
+        runs = [("unhinted", "none", args.fixed_batch)]
+        if not args.fixed_batch:
+            runs.insert(0, ("fixed_batch", "slot", True))
+        for name, mode, fixed in runs:
+            restore()
+            saved = args.fixed_batch
+            args.fixed_batch = fixed  # rank_cams' default
+            barrier()
+            v0 = torch.cuda.Event(enable_timing=True)
+            v1 = torch.cuda.Event(enable_timing=True)
+            v0.record(stream)
+            for _ in range(args.steps):
+                one_step(dev_targets, hint_mode=mode)
+            v1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            check_overflow(f"{name} loop")
+            args.fixed_batch = saved
+            vms = max_over_ranks(v0.elapsed_time(v1)) / args.steps
+            variants[name] = {"value": round(args.views / (vms / 1e3), 3), "ms_per_step": round(vms, 3),
+                              "batch": "views 4i mod 64 every step" if fixed else "views 4i + s mod 64 at step s",
+                              "scheduling_hint": {"slot": "the frame's previous forward (same camera)",
+                                                  "none": "none (work ordered by list length)",
+                                                  "camera": "the camera's last forward"}[mode]}
+
+    # ---- workload counters (not timed) for the roofline numerators: this rank's views of
+    # the step after the timed loop's last
     stats = {"visible": 0, "num_keys": 0, "evals_fwd": 0, "evals_bwd": 0, "evals_slot": 0, "max_list": 0,
              "blended": 0, "evals_fwd_culled": 0, "evals_bwd_culled": 0}
     gs, n = S["gs"], S["n"]
-    for rj, cs in zip(S["rends"], cam_structs):
-        bgs.bgs_preprocess(gs, cs, rj.frame)
+    for rj, c in zip(S["rends"], rank_cams(step_no[0] + 1)):
+        bgs.bgs_preprocess(gs, cam_structs_all[c], rj.frame)
         bgs.bgs_sort(rj.frame)
         bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
         s = bgs.bgs_frame_stats(rj.frame, rj.n_contrib)
@@ -552,15 +667,18 @@ def run_ours(args, rank, world, local_rank):
                  "local_density_r": r8, "local_density_quantiles_p5_p50_p95_p99": rq,
                  "density_contrast_p99_over_p5": rq[3] / max(rq[0], 1.0)}
 
-    # ---- max over ranks
+    # ---- max over ranks; the workload counters summed over ranks, per view of the step
     t = torch.tensor([ms_local], device=dev)
+    views_counted = n_mine
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        for key in ("visible", "num_keys", "evals_fwd", "evals_bwd", "evals_slot", "blended", "evals_fwd_culled",
-                    "evals_bwd_culled"):
-            tt = torch.tensor([stats[key]], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt)
-            stats[key] = int(tt.item())
+        keys = ("visible", "num_keys", "evals_fwd", "evals_bwd", "evals_slot", "blended", "evals_fwd_culled",
+                "evals_bwd_culled")
+        tt = torch.tensor([float(stats[k]) for k in keys] + [float(n_mine)], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt)
+        for k, v_ in zip(keys, tt.tolist()):
+            stats[k] = int(v_)
+        views_counted = int(tt[-1].item())
     ms_total = float(t.item())
     ms_step = ms_total / args.steps
     value = args.views / (ms_step / 1e3)
@@ -572,22 +690,23 @@ def run_ours(args, rank, world, local_rank):
     sm_mhz_max = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = 148 * FP32_LANES_PER_SM * sm_mhz_max * 1e6 / 1e12  # T lane-ops/s
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    K = stats["num_keys"] / len(cams) if cams else 0
-    steps_views = len(cams)  # views per step on rank 0
+    steps_views = n_mine  # views per step on rank 0 (its per-launch stage times)
     roof = {}
-    # per-view per-launch numerators (rank 0's views)
-    V = stats["visible"] / steps_views
-    Ef, Eb, Ebl = (stats["evals_fwd"] / steps_views, stats["evals_bwd"] / steps_views,
-                   stats["blended"] / steps_views)
-    # what the blend kernels must evaluate: list entries whose alpha >= 1/255 box reaches the
-    # pixel's warp block (exact skip of the rest)
-    Efc, Ebc = stats["evals_fwd_culled"] / steps_views, stats["evals_bwd_culled"] / steps_views
+    # per-view numerators: averages over every rank's views of one step
+    V = stats["visible"] / views_counted
+    K = stats["num_keys"] / views_counted
+    Ef, Eb, Ebl = (stats["evals_fwd"] / views_counted, stats["evals_bwd"] / views_counted,
+                   stats["blended"] / views_counted)
+    # what the blend kernels evaluate: list entries whose alpha >= 1/255 box reaches the
+    # pixel's warp block (the exact skip of the rest)
+    Efc, Ebc = stats["evals_fwd_culled"] / views_counted, stats["evals_bwd_culled"] / views_counted
     frame_v = S["rends"][0].views()
     passes = frame_v.sort_passes
 
-    def frac(stage, achieved, peak, unit, bound):
+    def frac(stage, achieved, peak, unit, bound, **extra):
         roof[stage] = {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                       "frac": achieved / peak if peak else None, "ms_per_launch": per_step[stage] / steps_views}
+                       "frac": achieved / peak if peak else None, "ms_per_launch": per_step[stage] / steps_views,
+                       **extra}
 
     def per_launch(stage):
         return max(per_step[stage] / steps_views / 1e3, 1e-12)  # seconds (0 with --no-stage-events)
@@ -602,14 +721,29 @@ def run_ours(args, rank, world, local_rank):
         roof["preprocess"]["views_per_launch"] = min(16, steps_views)
     else:
         frac("preprocess", (16 * n + 268 * V) / per_launch("preprocess") / 1e9, hbm, "GB/s", "hbm")
+    # sort: the algorithmic bytes of the path that runs
     if frame_v.sort_mode == 1:  # 64-bit onesweep reference: dup 12 + hist 8 + 24/pass per key, rects 20/visible
-        sort_bytes = (12 + 8 + 24 * passes) * K + 20 * V
-    else:  # depth first: 128 B per Gaussian + 20 per visible + (8 + 16 per tile pass) per key
-        sort_bytes = 128 * n + 20 * V + (8 + 16 * (passes - 4)) * K
-    frac("sort", sort_bytes / per_launch("sort") / 1e9, hbm, "GB/s", "hbm")
-    frac("render_fwd", (OPS_FWD_VISIT * Efc + OPS_FWD_BLEND * Ebl) / per_launch("render_fwd") / 1e12, fp32_peak,
-         "T lane-ops/s", "alu")
-    frac("blend_bwd", OPS_BWD_EVAL * Ebc / per_launch("blend_bwd") / 1e12, fp32_peak, "T lane-ops/s", "alu")
+        sort_bytes, sort_def = (12 + 8 + 24 * passes) * K + 20 * V, "(12 + 8 + 24 p) B per key + 20 B per visible"
+    elif args.sort_path == "radix_split":
+        sort_bytes = 92 * V + (8 + 16 * (passes - 4)) * K
+        sort_def = "92 B per visible (depth sort) + (8 + 16 per tile pass) B per key"
+    else:  # depth sort of the visible Gaussians + the values written once by the direct split
+        sort_bytes, sort_def = 92 * V + 4 * K, "92 B per visible + 4 B per key (SURVEY §8(d) a5 alternative, lower end)"
+    frac("sort", sort_bytes / per_launch("sort") / 1e9, hbm, "GB/s", "hbm", work=sort_def)
+    # blend: SURVEY §8(d) lane-ops per (pixel, list entry) pair by outcome over E_f / E_b (each
+    # pixel's walk to its early stop, plain, before the exact block cull), and beside it the
+    # same per-outcome counts over the pairs the kernels evaluate after the cull
+    fwd_ops = OPS_FWD_BLENDED * Ebl + OPS_SKIPPED * (Ef - Ebl)
+    bwd_ops = OPS_BWD_BLENDED * Ebl + OPS_SKIPPED * (Eb - Ebl)
+    hw = _ncu_hw(args.config)
+    for stage, ops, ops_c in (("render_fwd", fwd_ops, OPS_FWD_BLENDED * Ebl + OPS_SKIPPED * (Efc - Ebl)),
+                              ("blend_bwd", bwd_ops, OPS_BWD_BLENDED * Ebl + OPS_SKIPPED * (Ebc - Ebl))):
+        extra = {"work": f"SURVEY 8(d): {OPS_FWD_BLENDED if stage == 'render_fwd' else OPS_BWD_BLENDED} lane-ops "
+                         f"per blended pair + {OPS_SKIPPED} per skipped pair over the plain walk",
+                 "frac_after_cull": ops_c / per_launch(stage) / 1e12 / fp32_peak}
+        if hw.get(stage):
+            extra.update(hw[stage])
+        frac(stage, ops / per_launch(stage) / 1e12, fp32_peak, "T lane-ops/s", "alu", **extra)
     if fused:  # a10 + a11: theta 236 read + 708 written (theta, m, v) + m, v 472 read per Gaussian, + per
         # (view, visible Gaussian) blend gradients 36 + radius 4 + clamp bits 1; radius 4 per (view, culled)
         pb_bytes = 1416 * n + (37 * V + 4 * n) * steps_views
@@ -628,6 +762,8 @@ def run_ours(args, rank, world, local_rank):
         roof["adam"] = {"bound": "hbm", "achieved": adam_bytes / max(per_step["adam"] / 1e3, 1e-12) / 1e9,
                         "peak": hbm, "unit": "GB/s", "ms_per_launch": per_step["adam"]}
         roof["adam"]["frac"] = roof["adam"]["achieved"] / hbm
+    for k2, v2 in roof.items():
+        assert v2["frac"] is None or v2["frac"] <= 1.5, f"roofline fraction of {k2} above 1: {v2}"
     # the dominant KERNEL: stages that are one kernel launch (the sort stage is 13 kernels;
     # it is reported in stages_roofline)
     dom = max((s for s in roof if s != "sort"), key=lambda s: per_step[s])
@@ -643,6 +779,9 @@ def run_ours(args, rank, world, local_rank):
                 "unit": d["unit"], "frac": round(d["frac"], 4), "traffic": traffic, "kernel": dom,
                 "peak_source": f"{peaks_src} (FP32: 148 SMs x 128 lanes x {sm_mhz_max:.0f} MHz)"
                 if d["bound"] == "alu" else f"{peaks_src} MEASURED_PEAKS.json hbm_gbs"}
+    for k2 in ("work", "frac_after_cull", "hw_lane_op_frac", "smem_wavefront_frac", "hw_source"):
+        if k2 in d:
+            roofline[k2] = round(d[k2], 4) if isinstance(d[k2], float) else d[k2]
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args)
@@ -662,6 +801,12 @@ def run_ours(args, rank, world, local_rank):
                      "E_slot_over_E_f_culled": stats["evals_slot"] / max(1, stats["evals_fwd_culled"]),
                      "max_tile_list": stats["max_list"], "shape": shape},
         "e2e": e2e, "cpu_baseline": cpu,
+        "schedule": {"batch": "views 4i mod 64 every step" if args.fixed_batch else
+                     "rotating: step s renders views 4i + s mod 64 (each camera every 4 steps)",
+                     "scheduling_hint": "each frame's previous forward (same camera)" if args.fixed_batch else
+                     "each view hinted by its camera's last forward (bgs_frame_save_hint / load_hint)",
+                     "sort_path": args.sort_path},
+        "variants": variants,
         "density": None if not args.density_every else {
             "every": args.density_every, "r": round(float(dens_prm.r), 6), "events_timed_and_e2e": dens_log,
             "n_final": S["n"]},

@@ -328,9 +328,21 @@ bgs_status bgs_importance_keep(const float* importance, int64_t n, float fractio
 bgs_status bgs_frame_set_keep(bgs_frame* f /*host*/, const uint8_t* keep);
 
 /* ---------------------------------------------------------------- status / debug */
-/* After the caller synchronised the frame's stream: K (host out) and BGS_OK, or
- * BGS_ERR_CAPACITY when K > max_keys (re-run with a larger workspace). */
+/* After the caller synchronised the frame's stream: K of the last preprocess (host out)
+ * and BGS_OK, or BGS_ERR_CAPACITY when K > max_keys in ANY preprocess of this frame since
+ * the previous bgs_frame_status call (a sticky device flag, cleared by this call: a
+ * training loop can check once per many steps without losing an overflowed view, whose
+ * image is background and gradient zero); re-run with a larger workspace. */
 bgs_status bgs_frame_status(const bgs_frame* f /*host*/, int64_t* num_keys /*host*/);
+/* Per-camera scheduling hint: the per-(tile, 8x4 block) walk costs of the frame's last
+ * forward, which order (heaviest first) and split the next forward's work items.  A
+ * trainer rendering many cameras through a few frames saves a camera's hint after its
+ * forward and loads it before that camera's next render (src NULL: no hint, work ordered
+ * by list length).  Results are identical with any hint; only the schedule changes.
+ * dst / src: device, bgs_frame_hint_bytes(f) bytes, caller-owned; asynchronous. */
+size_t bgs_frame_hint_bytes(const bgs_frame* f /*host*/);
+bgs_status bgs_frame_save_hint(const bgs_frame* f /*host*/, void* dst, void* stream);
+bgs_status bgs_frame_load_hint(bgs_frame* f /*host*/, const void* src, void* stream);
 bgs_status bgs_frame_debug(const bgs_frame* f /*host*/, bgs_frame_views* out /*host*/);
 /* Workload counters of the last fwd (runs a counting kernel and synchronises). */
 bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contrib, bgs_stats* out /*host*/,

@@ -122,6 +122,9 @@ _SIGS = {
     "bgs_frame_stats": (C.c_int, [C.POINTER(Frame), _P, C.POINTER(Stats), _P]),
     "bgs_frame_set_debug": (C.c_int, [C.POINTER(Frame), C.c_int32]),
     "bgs_frame_set_seg_len": (C.c_int, [C.POINTER(Frame), C.c_int32]),
+    "bgs_frame_hint_bytes": (C.c_size_t, [C.POINTER(Frame)]),
+    "bgs_frame_save_hint": (C.c_int, [C.POINTER(Frame), _P, _P]),
+    "bgs_frame_load_hint": (C.c_int, [C.POINTER(Frame), _P, _P]),
     "bgs_density_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "bgs_local_density": (C.c_int, [_P, C.c_int64, C.c_float, C.c_float, C.c_float, _P, _P, _P, C.c_size_t, _P]),
     "bgs_density_step_workspace_bytes": (C.c_size_t, [C.c_int64]),
@@ -389,8 +392,30 @@ def bgs_importance_keep(importance, fraction, invert=False, workspace=None, stre
     return keep
 
 
+# device buffers a frame keeps pointers to (the keep mask): held here until replaced or
+# cleared, so the caching allocator cannot reuse them while the frame may read them
+_FRAME_REFS: dict = {}
+
+
 def bgs_frame_set_keep(frame: Frame, keep):
     _check(_lib.bgs_frame_set_keep(C.byref(frame), None if keep is None else _ptr(keep)), "bgs_frame_set_keep")
+    if keep is None:
+        _FRAME_REFS.pop(C.addressof(frame), None)
+    else:
+        _FRAME_REFS[C.addressof(frame)] = keep
+
+
+def bgs_frame_hint_bytes(frame: Frame) -> int:
+    return int(_lib.bgs_frame_hint_bytes(C.byref(frame)))
+
+
+def bgs_frame_save_hint(frame: Frame, dst, stream=None):
+    _check(_lib.bgs_frame_save_hint(C.byref(frame), _ptr(dst), _stream(stream)), "bgs_frame_save_hint")
+
+
+def bgs_frame_load_hint(frame: Frame, src, stream=None):
+    _check(_lib.bgs_frame_load_hint(C.byref(frame), None if src is None else _ptr(src), _stream(stream)),
+           "bgs_frame_load_hint")
 
 
 def launch_count() -> int:

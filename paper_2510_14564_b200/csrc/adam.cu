@@ -29,9 +29,11 @@ __device__ __forceinline__ int adam_group(int64_t e, int64_t n) {
   if (e < 6 * n) return 1;
   if (e < 10 * n) return 2;
   if (e < 11 * n) return 3;
-  // 32-bit offset inside the SH segment (48n < 2^32 for n < 89M): a constant-divisor
-  // modulo becomes a multiply-shift instead of a 64-bit division per element
-  return ((uint32_t)(e - 11 * n) % 48u) < 3u ? 4 : 5;
+  // offset inside the SH segment: in 32 bits while 48n < 2^32 (n < 89.4M; a constant-divisor
+  // modulo becomes a multiply-shift instead of a 64-bit division per element), else 64
+  const int64_t o = e - 11 * n;
+  const uint32_t k = n < (int64_t)(0xffffffffull / 48) ? (uint32_t)o % 48u : (uint32_t)((uint64_t)o % 48u);
+  return k < 3u ? 4 : 5;
 }
 
 __device__ __forceinline__ void adam_one(float& th, float& g, float& m, float& v, float ss, const AdamParams& p) {

@@ -59,6 +59,7 @@ enum : int {
   C_PAIRS = C_SCAN_TOTAL,     // row split: number of (row, rank) entries (the height scan's total)
   C_UNITS = 27,               // row split: number of item units
   C_RS_TICKET = 28,           // row split: tile ticket of the width scan
+  C_OVF_STICKY = 31,          // set by any overflow since the last bgs_frame_status (not reset by preprocess)
   C_NUM = 32
 };
 
@@ -105,6 +106,7 @@ struct Frame {
   uint32_t* order_bwd;     // [8 tiles] backward work items, longest first
   uint32_t* block_cost;    // [8 tiles] each block's largest n_contrib in the last forward
   int32_t have_cost, seg_len;  // block_cost holds this frame's previous forward; list segment length
+  int32_t counters_init;   // the sticky overflow word has been zeroed (first preprocess)
   uint32_t* ck_table;      // [8 tiles][kCkMax] pool slot of boundary b = 1..kCkMax of each block's walk
   float4* ck_pool;         // [ck_cap][32 lanes] {T, colour behind r, g, b} at a boundary
   int64_t ck_cap;          // slots of ck_pool, and of spec_state / spec_last

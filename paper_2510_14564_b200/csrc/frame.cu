@@ -447,11 +447,40 @@ bgs_status bgs_l1_dssim_loss_grad(const float* image, const uint8_t* target, int
 bgs_status bgs_frame_status(const bgs_frame* f, int64_t* num_keys) {
   if (!frame_ok(f) || !num_keys) return BGS_ERR_INVALID;
   const Frame* F = frame_of(f);
-  uint32_t c[3];
+  uint32_t c[C_NUM];
   if (cudaMemcpy(c, F->counters, sizeof(c), cudaMemcpyDeviceToHost) != cudaSuccess)
     return check_launch("bgs_frame_status");
   *num_keys = (int64_t)(((uint64_t)c[C_K_HI] << 32) | c[C_K_LO]);
-  return c[C_OVERFLOW] ? BGS_ERR_CAPACITY : BGS_OK;
+  const bool sticky = F->counters_init && c[C_OVF_STICKY];
+  if (sticky && cudaMemset(F->counters + C_OVF_STICKY, 0, 4) != cudaSuccess) return check_launch("bgs_frame_status");
+  return (c[C_OVERFLOW] || sticky) ? BGS_ERR_CAPACITY : BGS_OK;
+}
+
+size_t bgs_frame_hint_bytes(const bgs_frame* f) {
+  return frame_ok(f) ? 4 * 8 * (size_t)frame_of(f)->num_tiles : 0;
+}
+
+bgs_status bgs_frame_save_hint(const bgs_frame* f, void* dst, void* stream) {
+  if (!frame_ok(f) || !dst) return BGS_ERR_INVALID;
+  const Frame* F = frame_of(f);
+  if (cudaMemcpyAsync(dst, F->block_cost, bgs_frame_hint_bytes(f), cudaMemcpyDeviceToDevice,
+                      (cudaStream_t)stream) != cudaSuccess)
+    return check_launch("bgs_frame_save_hint");
+  return BGS_OK;
+}
+
+bgs_status bgs_frame_load_hint(bgs_frame* f, const void* src, void* stream) {
+  if (!frame_ok(f)) return BGS_ERR_INVALID;
+  Frame* F = frame_of(f);
+  if (!src) {
+    F->have_cost = 0;
+    return BGS_OK;
+  }
+  if (cudaMemcpyAsync(F->block_cost, src, bgs_frame_hint_bytes(f), cudaMemcpyDeviceToDevice,
+                      (cudaStream_t)stream) != cudaSuccess)
+    return check_launch("bgs_frame_load_hint");
+  F->have_cost = 1;
+  return BGS_OK;
 }
 
 bgs_status bgs_frame_debug(const bgs_frame* f, bgs_frame_views* out) {

@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
       counters[C_K_LO] = (uint32_t)K;
       counters[C_K_HI] = (uint32_t)(K >> 32);
       counters[C_OVERFLOW] = K > (unsigned long long)max_keys ? 1u : 0u;
+      if (K > (unsigned long long)max_keys) counters[C_OVF_STICKY] = 1u;
     }
     counters[C_SCAN_TOTAL] = (uint32_t)K;
   }
@@ -421,8 +422,11 @@ bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, b
 }
 
 bgs_status launch_preprocess_batch(const bgs_gaussians* g, Frame* const* F, int nviews, cudaStream_t s) {
-  for (int v = 0; v < nviews; ++v)
-    if (cudaMemsetAsync(F[v]->counters, 0, 4 * C_NUM, s) != cudaSuccess) return check_launch("preprocess memset");
+  for (int v = 0; v < nviews; ++v) {  // every word but the sticky overflow flag (zeroed once)
+    if (cudaMemsetAsync(F[v]->counters, 0, 4 * (F[v]->counters_init ? C_OVF_STICKY : C_NUM), s) != cudaSuccess)
+      return check_launch("preprocess memset");
+    F[v]->counters_init = 1;
+  }
   if (F[0]->n == 0) return BGS_OK;
   PreParams p;
   p.means = g->means;

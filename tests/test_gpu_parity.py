@@ -432,6 +432,49 @@ def test_capacity_overflow_is_reported_and_recovers(bgs):
     assert np.abs(out["image"].cpu().numpy() - ref["image"])[:, ok].max() <= IMG_TOL
 
 
+def test_overflow_flag_is_sticky_across_preprocesses(bgs):
+    """An overflowed view is reported by bgs_frame_status even after later preprocesses of
+    the frame that fit (the sticky flag); the call clears it."""
+    big = scenes()["dense"]()
+    cam = big.cameras[0]
+    dev = torch.device("cuda")
+    K_big = ref_K(big, cam)
+    r = bgs.Renderer(big.n, cam.width, cam.height, max_keys=K_big - 1, device=dev)
+    theta = torch.from_numpy(big.theta).to(dev)
+    r.forward(theta, cam, big.sh_degree, check=False)  # overflows
+    th2 = big.theta.copy()
+    gen.segments(th2, big.n)["means"][:, 2] = -1.0  # all culled: K = 0 fits
+    r.forward(torch.from_numpy(th2).to(dev), cam, big.sh_degree, check=False)
+    torch.cuda.synchronize()
+    st, k = bgs.bgs_frame_status(r.frame)
+    assert k == 0 and st == bgs.BGS_ERR_CAPACITY  # the earlier overflow is not lost
+    st, k = bgs.bgs_frame_status(r.frame)
+    assert st == bgs.BGS_OK  # cleared by the previous call
+
+
+def test_scheduling_hint_save_load_keeps_results(bgs):
+    """Rendering with the view's own saved hint, with none, or with a garbage one gives
+    bit-identical images and n_contrib (the hint only orders the work; the lists here are
+    shorter than 2 seg_len, so no walk is split)."""
+    s = scenes()["dense"]()
+    cams = [s.cameras[0]]
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    r = bgs.Renderer(s.n, cams[0].width, cams[0].height, max_keys=1 << 21, device=dev)
+    hb = bgs.bgs_frame_hint_bytes(r.frame)
+    assert hb == 4 * 8 * r.views().tiles_x * r.views().tiles_y
+    h = torch.empty(hb, dtype=torch.uint8, device=dev)
+    ref = r.forward(theta, cams[0], s.sh_degree)
+    img0, nc0 = ref["image"].clone(), ref["n_contrib"].clone()
+    bgs.bgs_frame_save_hint(r.frame, h)
+    garbage = torch.randint(0, 1 << 20, (hb // 4,), dtype=torch.int32, device=dev)
+    for src in (None, h, garbage):
+        bgs.bgs_frame_load_hint(r.frame, src)
+        out = r.forward(theta, cams[0], s.sh_degree)
+        torch.cuda.synchronize()
+        assert torch.equal(out["image"], img0) and torch.equal(out["n_contrib"], nc0)
+
+
 @pytest.mark.parametrize("wh", [(1, 1), (17, 3), (16, 16), (33, 250)])
 def test_odd_image_sizes(bgs, wh):
     W, H = wh
