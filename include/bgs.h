@@ -269,12 +269,13 @@ typedef struct {
   float alpha_sigma;  /* densification spread sigma_p = alpha_sigma d_bar_p (> 1) */
   float delta;        /* jitter half-width */
   int32_t k;          /* neighbours for d_bar_p and mu_d / sigma_d (1..16; 8) */
-  int32_t max_new;    /* children per sparse point cap (0..64; 4) */
+  int32_t max_new;    /* children per sparse point cap per round (0..64; 4) */
 } bgs_density_params;
 
 typedef struct {      /* filled on the device by bgs_density_plan */
   int64_t n_in, n_out, n_pairs, n_children;
   double mu_rho, sigma_rho, rho_low, rho_high, mu_d, sigma_d, d_merge;
+  int64_t n_sparse;   /* points with rho < rho_low (rho_low > 0): the densification parents */
 } bgs_density_report;
 
 /* Workspace bytes for the density step over n Gaussians (0 on invalid n: 1 <= n < 2^30). */
@@ -300,6 +301,32 @@ bgs_status bgs_density_apply(const float* theta, const float* exp_avg, const flo
                              const void* workspace, const bgs_density_params* p /*host*/, const float* normals,
                              const float* uniforms, int64_t n_children, float* theta_out, float* exp_avg_out,
                              float* exp_avg_sq_out, int64_t n_out, void* stream);
+/* Further densification rounds (R35'; §III-C2 l.206 "This process is repeated
+ * iteratively until the desired density is achieved"; SPEC.md l.247 max_rounds).
+ * bgs_density_parents (asynchronous, after bgs_density_plan): the report's n_sparse sparse
+ * points as parents[n_sparse] (device u32, out) = their indices in bgs_density_apply's
+ * output (index order; sparse points are never merged) and sigma[n_sparse] (device double,
+ * out) = alpha_sigma d_bar_p (R35).  A round on the current scene of n_t points: the
+ * caller counts rho of every point (bgs_local_density on its means, radius p->r), then
+ * bgs_density_round_plan: parent p below rho_low spawns min(max_new, ceil(rho_low - rho_p))
+ * children (exclusive offsets in the round workspace, device, >=
+ * bgs_density_round_workspace_bytes(n_parents) bytes, 256-byte aligned);
+ * bgs_density_round_result (after the caller synchronised): the round's child count (0: the
+ * desired density is reached, stop); bgs_density_round_apply: the n_t points (moments kept)
+ * then the children in (parent, j) order, child at p + sigma_p z + delta u (z, u: device
+ * [n_children][3] N(0,1) / U(-1,1) variates), attributes copied from the parent, zero
+ * moments; outputs [59 (n_t + n_children)]. */
+bgs_status bgs_density_parents(const void* workspace, int64_t n, const bgs_density_params* p /*host*/,
+                               uint32_t* parents, double* sigma, void* stream);
+size_t bgs_density_round_workspace_bytes(int64_t n_parents);
+bgs_status bgs_density_round_plan(const uint32_t* rho, int64_t n_t, const uint32_t* parents, int64_t n_parents,
+                                  double rho_low, int32_t max_new, void* workspace, size_t bytes, void* stream);
+bgs_status bgs_density_round_result(const void* workspace, int64_t n_parents, int64_t* n_children /*host*/);
+bgs_status bgs_density_round_apply(const float* theta, const float* exp_avg, const float* exp_avg_sq, int64_t n_t,
+                                   const uint32_t* parents, const double* sigma, int64_t n_parents,
+                                   const void* workspace, float delta, const float* normals, const float* uniforms,
+                                   int64_t n_children, float* theta_out, float* exp_avg_out, float* exp_avg_sq_out,
+                                   void* stream);
 
 /* ---------------------------------------------------------------- NEXT-3 / NEXT-4: T2 sampling */
 /* PAPER.md §IV-C1 (l.253-268): per 16x16 tile, each pixel's rendered colour (clamped to

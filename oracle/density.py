@@ -24,12 +24,18 @@ Readings (R31-R36):
        units), rotation = the higher-opacity member's quaternion (ties: lower index), opacity =
        min(0.999, o_p + o_q) (S:262's clamped sum, capped so the logit stays finite), SH =
        opacity-weighted mean.  Computed in double, rounded once to float.
-  R35  densification: each point with rho < max(rho_low, 0) spawns c = min(max_new,
-       ceil(rho_low - rho)) children (one round; S:247's "until the density is achieved" is
-       approximated by the deficit), child j at p + sigma_p z + delta u with sigma_p =
+  R35  densification, round 1: each point with rho < max(rho_low, 0) spawns c = min(max_new,
+       ceil(rho_low - rho)) children, child j at p + sigma_p z + delta u with sigma_p =
        alpha_sigma d_bar_p, z ~ N(0, I3), u ~ U(-1, 1)^3, scale,
        rotation, opacity and SH copied from the parent.  Children are numbered in
        (parent index, j) order; z and u are indexed by that number.
+  R35' rounds 2 .. max_rounds ("This process is repeated iteratively until the desired
+       density is achieved"; until the point's recomputed local density
+       >= rho_low or max_rounds): the parents are round 1's sparse points (at their indices
+       in the round-1 output, sigma_p and rho_low of the step's statistics kept); each round
+       re-counts rho over the whole current scene (children included) and a parent still
+       below rho_low spawns min(max_new, ceil(rho_low - rho)) more children, appended in
+       (parent, j) order; the loop ends early when no parent is below rho_low.
   R36  output order: survivors in index order (a merged pair's result at the lower index),
        then the children; Adam moments are kept for unmerged survivors and zero for merged
        Gaussians and children.
@@ -174,6 +180,57 @@ def apply(theta, m, v, n, st, pairs, counts, normals, uniforms, alpha_sigma=1.5,
         return np.concatenate([a[:, 0:3].ravel(), a[:, 3:6].ravel(), a[:, 6:10].ravel(), a[:, 10], a[:, 11:59].ravel()])
 
     return pack(rows), pack(mrows), pack(vrows), nn
+
+
+def sparse_parents(theta, n, st, pairs, alpha_sigma=1.5):
+    """R35': round 1's sparse points (rho < rho_low, rho_low > 0) as (index in apply's
+    output, sigma_p) -- sparse points are never merged, so their output index is their rank
+    among the survivors."""
+    removed = np.zeros(n, bool)
+    for _, q in pairs:
+        removed[q] = True
+    out_idx = np.cumsum(~removed) - 1
+    lo = st["rho_low"]
+    sel = [i for i in range(n) if lo > 0 and st["rho"][i] < lo]
+    return np.asarray([out_idx[i] for i in sel], np.int64), \
+        np.asarray([alpha_sigma * st["d_bar"][i] for i in sel], np.float64)
+
+
+def densify_round(theta, m, v, n, r, parents, sigma, rho_low, normals, uniforms, max_new=4, delta=0.0):
+    """R35' one further round on the current scene (theta, m, v of n points): rho of every
+    point re-counted at radius r; parent p (index into the scene) below rho_low spawns
+    min(max_new, ceil(rho_low - rho_p)) children at p + sigma_p z + delta u, appended after
+    the n points in (parent, j) order (zero moments).  Returns (theta', m', v', n', children)."""
+    s = _seg(theta, n)
+    rho = oracle.local_density(s["means"], r).astype(np.int64)
+    counts = [min(max_new, math.ceil(rho_low - rho[p])) if rho[p] < rho_low else 0 for p in parents]
+    nc = int(sum(counts))
+    if nc == 0:
+        return theta, m, v, n, 0
+    sm, sv = _seg(m, n), _seg(v, n)
+
+    def rows(seg):
+        return [np.concatenate([seg["means"][i], seg["log_scales"][i], seg["quats"][i], [seg["opacity"][i]],
+                                seg["sh"][i]]) for i in range(n)]
+
+    R, Mr, Vr = rows(s), rows(sm), rows(sv)
+    c = 0
+    for p, sg, cnt in zip(parents, sigma, counts):
+        for _ in range(cnt):
+            base = R[p].astype(np.float64)
+            base[0:3] = s["means"][p].astype(np.float64) + sg * np.asarray(normals[c], np.float64) + \
+                delta * np.asarray(uniforms[c], np.float64)
+            R.append(base.astype(np.float32))
+            Mr.append(np.zeros(59, np.float32))
+            Vr.append(np.zeros(59, np.float32))
+            c += 1
+    nn = n + nc
+
+    def pack(rs):
+        a = np.asarray(rs, np.float32).reshape(nn, 59)
+        return np.concatenate([a[:, 0:3].ravel(), a[:, 3:6].ravel(), a[:, 6:10].ravel(), a[:, 10], a[:, 11:59].ravel()])
+
+    return pack(R), pack(Mr), pack(Vr), nn, nc
 
 
 def normalized_deviation(means, r):

@@ -72,7 +72,8 @@ class DensityParams(C.Structure):
 class DensityReport(C.Structure):
     _fields_ = [("n_in", C.c_int64), ("n_out", C.c_int64), ("n_pairs", C.c_int64), ("n_children", C.c_int64),
                 ("mu_rho", C.c_double), ("sigma_rho", C.c_double), ("rho_low", C.c_double),
-                ("rho_high", C.c_double), ("mu_d", C.c_double), ("sigma_d", C.c_double), ("d_merge", C.c_double)]
+                ("rho_high", C.c_double), ("mu_d", C.c_double), ("sigma_d", C.c_double), ("d_merge", C.c_double),
+                ("n_sparse", C.c_int64)]
 
 
 class Frame(C.Structure):
@@ -132,6 +133,12 @@ _SIGS = {
     "bgs_density_result": (C.c_int, [_P, C.c_int64, C.POINTER(DensityReport), C.POINTER(C.c_uint32)]),
     "bgs_density_apply": (C.c_int, [_P, _P, _P, C.c_int64, _P, C.POINTER(DensityParams), _P, _P, C.c_int64, _P, _P,
                                     _P, C.c_int64, _P]),
+    "bgs_density_parents": (C.c_int, [_P, C.c_int64, C.POINTER(DensityParams), _P, _P, _P]),
+    "bgs_density_round_workspace_bytes": (C.c_size_t, [C.c_int64]),
+    "bgs_density_round_plan": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.c_double, C.c_int32, _P, C.c_size_t, _P]),
+    "bgs_density_round_result": (C.c_int, [_P, C.c_int64, C.POINTER(C.c_int64)]),
+    "bgs_density_round_apply": (C.c_int, [_P, _P, _P, C.c_int64, _P, _P, C.c_int64, _P, C.c_float, _P, _P, C.c_int64,
+                                          _P, _P, _P, _P]),
     "bgs_tile_buckets": (C.c_int, [_P, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P]),
     "bgs_importance_workspace_bytes": (C.c_size_t, [C.c_int64]),
     "bgs_importance": (C.c_int, [C.POINTER(Frame), _P, _P, _P, _P, C.c_size_t, _P]),
@@ -324,12 +331,17 @@ def bgs_local_density(means, r, alpha=1.0, beta=1.0, counts=None, stats=None, wo
     return counts, stats
 
 
-def density_control(theta, exp_avg, exp_avg_sq, n, params: DensityParams, generator=None, stream=None):
+def density_control(theta, exp_avg, exp_avg_sq, n, params: DensityParams, generator=None, stream=None,
+                    max_rounds=4):
     """One NEXT-1 density-control step (§III-C2-C4): plan on the device, one host
     read of the report (n_out sizes the new buffers), the method's random draws
-    (N(0,1) / U(-1,1) variates, torch generator on the device), apply.  Returns
-    (theta', exp_avg', exp_avg_sq', n', report, short_knn, (normals, uniforms)), short_knn =
-    points with fewer than k neighbours within 3 r (R32)."""
+    (N(0,1) / U(-1,1) variates, torch generator on the device), apply; then up to
+    max_rounds - 1 further densification rounds (R35', "repeated iteratively until the
+    desired density is achieved", l.206): the sparse points' local densities re-counted over
+    the grown scene, more children for those still below rho_low.  Returns (theta',
+    exp_avg', exp_avg_sq', n', report, short_knn, draws), short_knn = points with fewer than
+    k neighbours within 3 r (R32), draws = [(normals, uniforms)] per round, and sets
+    report.rounds / report.children_per_round (Python attributes)."""
     dev = theta.device
     nbytes = int(_lib.bgs_density_step_workspace_bytes(n))
     if nbytes == 0:
@@ -339,17 +351,59 @@ def density_control(theta, exp_avg, exp_avg_sq, n, params: DensityParams, genera
            "bgs_density_plan")
     rep = DensityReport()
     short = C.c_uint32(0)
-    torch.cuda.current_stream(dev).synchronize() if stream is None else stream.synchronize()
+
+    def sync():
+        torch.cuda.current_stream(dev).synchronize() if stream is None else stream.synchronize()
+
+    sync()
     _check(_lib.bgs_density_result(_ptr(ws), n, C.byref(rep), C.byref(short)), "bgs_density_result")
     nc, n_out = int(rep.n_children), int(rep.n_out)
-    normals = torch.randn((max(nc, 1), 3), generator=generator, device=dev)
-    uniforms = torch.rand((max(nc, 1), 3), generator=generator, device=dev) * 2.0 - 1.0
+
+    def draws(count):
+        z = torch.randn((max(count, 1), 3), generator=generator, device=dev)
+        u = torch.rand((max(count, 1), 3), generator=generator, device=dev) * 2.0 - 1.0
+        return z, u
+
+    normals, uniforms = draws(nc)
     th2 = torch.empty(59 * n_out, dtype=torch.float32, device=dev)
     m2, v2 = torch.empty_like(th2), torch.empty_like(th2)
     _check(_lib.bgs_density_apply(_ptr(theta), _ptr(exp_avg), _ptr(exp_avg_sq), n, _ptr(ws), C.byref(params),
                                   _ptr(normals), _ptr(uniforms), nc, _ptr(th2), _ptr(m2), _ptr(v2), n_out,
                                   _stream(stream)), "bgs_density_apply")
-    return th2, m2, v2, n_out, rep, int(short.value), (normals[:nc], uniforms[:nc])
+    rounds = [(normals[:nc], uniforms[:nc])]
+    per_round = [nc]
+    npar = int(rep.n_sparse)
+    if max_rounds > 1 and npar > 0 and params.max_new > 0:
+        parents = torch.empty(npar, dtype=torch.int32, device=dev)
+        sigma = torch.empty(npar, dtype=torch.float64, device=dev)
+        _check(_lib.bgs_density_parents(_ptr(ws), n, C.byref(params), _ptr(parents), _ptr(sigma), _stream(stream)),
+               "bgs_density_parents")
+        rws = torch.empty(max(int(_lib.bgs_density_round_workspace_bytes(npar)), 256), dtype=torch.uint8, device=dev)
+        for _ in range(max_rounds - 1):
+            rho, _st = bgs_local_density(th2[:3 * n_out].view(n_out, 3), params.r, params.alpha, params.beta,
+                                         stream=stream)
+            _check(_lib.bgs_density_round_plan(_ptr(rho), n_out, _ptr(parents), npar, float(rep.rho_low),
+                                               params.max_new, _ptr(rws), rws.numel(), _stream(stream)),
+                   "bgs_density_round_plan")
+            sync()
+            kc = C.c_int64(0)
+            _check(_lib.bgs_density_round_result(_ptr(rws), npar, C.byref(kc)), "bgs_density_round_result")
+            kc = int(kc.value)
+            if kc == 0:  # every sparse point reached rho_low
+                break
+            z, u = draws(kc)
+            n3 = n_out + kc
+            th3 = torch.empty(59 * n3, dtype=torch.float32, device=dev)
+            m3, v3 = torch.empty_like(th3), torch.empty_like(th3)
+            _check(_lib.bgs_density_round_apply(_ptr(th2), _ptr(m2), _ptr(v2), n_out, _ptr(parents), _ptr(sigma), npar,
+                                                _ptr(rws), params.delta, _ptr(z), _ptr(u), kc, _ptr(th3), _ptr(m3),
+                                                _ptr(v3), _stream(stream)), "bgs_density_round_apply")
+            th2, m2, v2, n_out = th3, m3, v3, n3
+            rounds.append((z[:kc], u[:kc]))
+            per_round.append(kc)
+    rep.rounds = len(per_round)
+    rep.children_per_round = per_round
+    return th2, m2, v2, n_out, rep, int(short.value), rounds
 
 
 def bgs_tile_buckets(image, final_T, w, h, stream=None):

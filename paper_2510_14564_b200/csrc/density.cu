@@ -451,14 +451,17 @@ __global__ void __launch_bounds__(kStepThreads) k_merge_nn(int64_t n, const floa
 // packed as keep << 32 | children for one scan.
 __global__ void __launch_bounds__(kStepThreads) k_step_flags(int64_t n, const int32_t* __restrict__ nn,
                                                              const uint32_t* __restrict__ rho,
-                                                             const bgs_density_report* rep, int max_new,
+                                                             bgs_density_report* rep, int max_new,
                                                              unsigned long long* packed) {
   const double lo = rep->rho_low;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t q = nn[i];
     const bool removed = q >= 0 && q < i && nn[q] == (int32_t)i;
     uint32_t c = 0;
-    if (lo > 0.0 && (double)rho[i] < lo) c = (uint32_t)min((double)max_new, ceil(lo - (double)rho[i]));
+    if (lo > 0.0 && (double)rho[i] < lo) {
+      c = (uint32_t)min((double)max_new, ceil(lo - (double)rho[i]));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&rep->n_sparse), 1ull);
+    }
     packed[i] = ((unsigned long long)(removed ? 0u : 1u) << 32) | c;
   }
 }
@@ -581,6 +584,136 @@ __global__ void __launch_bounds__(kStepThreads) k_step_emit(int64_t n, int64_t n
       put(0, oc, mean, I.ls + 3 * i, I.q + 4 * i, I.op[i], I.sh + 48 * i);
       put(1, oc, zero, zero, zero, 0.f, zero);
       put(2, oc, zero, zero, zero, 0.f, zero);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- R35': further rounds
+// exclusive scan of u32 values in place (1024-value blocks, block totals scanned by one
+// thread, then added); total to *total
+__global__ void __launch_bounds__(1024) k_u32_scan_blocks(int64_t n, uint32_t* v, uint32_t* blk) {
+  __shared__ uint32_t s_w[32];
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  const uint32_t x = i < n ? v[i] : 0u;
+  uint32_t inc = x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) s_w[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    uint32_t t = s_w[lane], ti = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, ti, o);
+      if (lane >= o) ti += y;
+    }
+    s_w[lane] = ti - t;
+    if (lane == 31) blk[blockIdx.x] = ti;
+  }
+  __syncthreads();
+  if (i < n) v[i] = inc - x + s_w[w];
+}
+
+__global__ void k_u32_scan_top(int64_t nb, uint32_t* blk, uint32_t* total) {
+  if (threadIdx.x != 0) return;
+  uint32_t run = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    const uint32_t t = blk[b];
+    blk[b] = run;
+    run += t;
+  }
+  *total = run;
+}
+
+__global__ void __launch_bounds__(1024) k_u32_scan_add(int64_t n, uint32_t* v, const uint32_t* blk) {
+  const int64_t i = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+  if (i < n) v[i] += blk[blockIdx.x];
+}
+
+static bgs_status u32_scan(uint32_t* v, int64_t n, uint32_t* blk, uint32_t* total, cudaStream_t s) {
+  const int64_t nb = (n + 1023) / 1024;
+  if (nb > 0) {
+    k_u32_scan_blocks<<<(int)nb, 1024, 0, s>>>(n, v, blk);
+    note_launch();
+  }
+  k_u32_scan_top<<<1, 32, 0, s>>>(nb, blk, total);
+  note_launch();
+  if (nb > 0) {
+    k_u32_scan_add<<<(int)nb, 1024, 0, s>>>(n, v, blk);
+    note_launch();
+  }
+  return check_launch("density u32 scan");
+}
+
+// the sparse points of the plan, in index order: their apply-output index (the keep scan)
+// and sigma_p = alpha_sigma d_bar_p; slot = the sparse flags' exclusive scan
+__global__ void __launch_bounds__(256) k_sparse_flags(int64_t n, const uint32_t* __restrict__ rho,
+                                                      const bgs_density_report* rep, uint32_t* flag) {
+  const double lo = rep->rho_low;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flag[i] = (lo > 0.0 && (double)rho[i] < lo) ? 1u : 0u;
+}
+
+__global__ void __launch_bounds__(256) k_sparse_emit(int64_t n, const uint32_t* __restrict__ rho,
+                                                     const bgs_density_report* rep,
+                                                     const uint32_t* __restrict__ slot,
+                                                     const unsigned long long* __restrict__ packed,
+                                                     const double* __restrict__ dbar, float alpha_sigma,
+                                                     uint32_t* parents, double* sigma) {
+  const double lo = rep->rho_low;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    if (lo > 0.0 && (double)rho[i] < lo) {
+      parents[slot[i]] = (uint32_t)(packed[i] >> 32);  // survivors before i = its output index
+      sigma[slot[i]] = (double)alpha_sigma * dbar[i];  // k_step_emit's spread
+    }
+}
+
+__global__ void __launch_bounds__(256) k_round_counts(int64_t np, const uint32_t* __restrict__ parents,
+                                                      const uint32_t* __restrict__ rho, double lo, int max_new,
+                                                      uint32_t* cnt) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (int64_t)gridDim.x * blockDim.x) {
+    const double r = (double)rho[parents[i]];
+    cnt[i] = r < lo ? (uint32_t)min((double)max_new, ceil(lo - r)) : 0u;
+  }
+}
+
+// the n_t points copied into the n_out layout (moments kept), then each parent's children
+__global__ void __launch_bounds__(256) k_round_emit(int64_t n_t, int64_t n_out, const float* __restrict__ th,
+                                                    const float* __restrict__ m, const float* __restrict__ v,
+                                                    int64_t np, const uint32_t* __restrict__ parents,
+                                                    const double* __restrict__ sigma,
+                                                    const uint32_t* __restrict__ off, const uint32_t* total,
+                                                    float delta, const float* normals, const float* uniforms,
+                                                    float* th_o, float* m_o, float* v_o) {
+  const float* src[3] = {th, m, v};
+  float* dst[3] = {th_o, m_o, v_o};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // segment s of a buffer: [s_off(n) .. + width n); widths 3, 3, 4, 1, 48
+  const int wid[5] = {3, 3, 4, 1, 48}, at[5] = {0, 3, 6, 10, 11};
+  for (int b = 0; b < 3; ++b)
+    for (int sg = 0; sg < 5; ++sg)
+      for (int64_t e = t0; e < wid[sg] * n_t; e += stride) dst[b][at[sg] * n_out + e] = src[b][at[sg] * n_t + e];
+  const uint32_t nc = *total;
+  for (int64_t i = t0; i < np; i += stride) {
+    const uint32_t c0 = off[i], c1 = i + 1 < np ? off[i + 1] : nc;
+    const int64_t p = parents[i];
+    for (uint32_t c = c0; c < c1; ++c) {
+      const int64_t o = n_t + c;
+      for (int a = 0; a < 3; ++a)
+        th_o[3 * o + a] = (float)((double)th[3 * p + a] + sigma[i] * (double)normals[3 * (int64_t)c + a] +
+                                  (double)delta * (double)uniforms[3 * (int64_t)c + a]);
+      for (int a = 0; a < 3; ++a) th_o[3 * n_out + 3 * o + a] = th[3 * n_t + 3 * p + a];
+      for (int a = 0; a < 4; ++a) th_o[6 * n_out + 4 * o + a] = th[6 * n_t + 4 * p + a];
+      th_o[10 * n_out + o] = th[10 * n_t + p];
+      for (int a = 0; a < 48; ++a) th_o[11 * n_out + 48 * o + a] = th[11 * n_t + 48 * p + a];
+      for (int b = 1; b < 3; ++b)
+        for (int sg = 0; sg < 5; ++sg)
+          for (int a = 0; a < wid[sg]; ++a) dst[b][at[sg] * n_out + wid[sg] * o + a] = 0.0f;
     }
   }
 }
@@ -740,6 +873,75 @@ bgs_status bgs_density_apply(const float* theta, const float* exp_avg, const flo
                                                      exp_avg_sq_out);
   note_launch();
   return check_launch("k_step_emit");
+}
+
+bgs_status bgs_density_parents(const void* workspace, int64_t n, const bgs_density_params* p, uint32_t* parents,
+                               double* sigma, void* stream) {
+  StepWs w;
+  if (!workspace || !params_ok(p) || !parents || !sigma || !step_layout(n, (char*)workspace, &w, nullptr))
+    return BGS_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  // the grid's key buffers are free after the plan: flags / slots and the block totals
+  uint32_t* slot = w.g.key[0];
+  uint32_t* blk = w.g.key[1];
+  const int grid = 4 * num_sms();
+  k_sparse_flags<<<grid, 256, 0, s>>>(n, w.rho, w.rep, slot);
+  note_launch();
+  bgs_status st = u32_scan(slot, n, blk, blk + (n + 1023) / 1024 + 1, s);
+  if (st != BGS_OK) return st;
+  k_sparse_emit<<<grid, 256, 0, s>>>(n, w.rho, w.rep, slot, w.packed, w.dbar, p->alpha_sigma, parents, sigma);
+  note_launch();
+  return check_launch("k_sparse_emit");
+}
+
+// round workspace: counts / offsets [np], block totals [np / 1024 + 1], total [1]
+static size_t round_bytes(int64_t np) { return dens_align(4 * (size_t)np) + dens_align(4 * (size_t)(np / 1024 + 2)); }
+
+size_t bgs_density_round_workspace_bytes(int64_t n_parents) { return n_parents < 0 ? 0 : round_bytes(n_parents); }
+
+bgs_status bgs_density_round_plan(const uint32_t* rho, int64_t n_t, const uint32_t* parents, int64_t n_parents,
+                                  double rho_low, int32_t max_new, void* workspace, size_t bytes, void* stream) {
+  if (!rho || n_t < 1 || n_parents < 0 || (n_parents > 0 && !parents) || !workspace ||
+      ((uintptr_t)workspace & 255u) || bytes < round_bytes(n_parents) || max_new < 0 || max_new > 64)
+    return BGS_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  uint32_t* cnt = (uint32_t*)workspace;
+  uint32_t* blk = (uint32_t*)((char*)workspace + dens_align(4 * (size_t)n_parents));
+  if (n_parents > 0) {
+    k_round_counts<<<4 * num_sms(), 256, 0, s>>>(n_parents, parents, rho, rho_low, max_new, cnt);
+    note_launch();
+  }
+  return u32_scan(cnt, n_parents, blk, blk + n_parents / 1024 + 1, s);
+}
+
+bgs_status bgs_density_round_result(const void* workspace, int64_t n_parents, int64_t* n_children) {
+  if (!workspace || n_parents < 0 || !n_children) return BGS_ERR_INVALID;
+  const uint32_t* blk = (const uint32_t*)((const char*)workspace + dens_align(4 * (size_t)n_parents));
+  uint32_t t = 0;
+  if (cudaMemcpy(&t, blk + n_parents / 1024 + 1, 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return check_launch("bgs_density_round_result");
+  *n_children = t;
+  return BGS_OK;
+}
+
+bgs_status bgs_density_round_apply(const float* theta, const float* exp_avg, const float* exp_avg_sq, int64_t n_t,
+                                   const uint32_t* parents, const double* sigma, int64_t n_parents,
+                                   const void* workspace, float delta, const float* normals, const float* uniforms,
+                                   int64_t n_children, float* theta_out, float* exp_avg_out, float* exp_avg_sq_out,
+                                   void* stream) {
+  if (!theta || !exp_avg || !exp_avg_sq || n_t < 1 || n_parents < 0 || (n_parents > 0 && (!parents || !sigma)) ||
+      !workspace || !(delta >= 0.0f) || n_children < 0 || (n_children > 0 && (!normals || !uniforms)) ||
+      !theta_out || !exp_avg_out || !exp_avg_sq_out)
+    return BGS_ERR_INVALID;
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint32_t* off = (const uint32_t*)workspace;
+  const uint32_t* total = (const uint32_t*)((const char*)workspace + dens_align(4 * (size_t)n_parents)) +
+                          n_parents / 1024 + 1;
+  k_round_emit<<<4 * num_sms(), 256, 0, s>>>(n_t, n_t + n_children, theta, exp_avg, exp_avg_sq, n_parents, parents,
+                                             sigma, off, total, delta, normals, uniforms, theta_out, exp_avg_out,
+                                             exp_avg_sq_out);
+  note_launch();
+  return check_launch("k_round_emit");
 }
 
 }  // extern "C"

@@ -83,8 +83,10 @@ def test_density_step_parity(bgs, name):
     dev = torch.device("cuda")
     g = torch.Generator(device=dev)
     g.manual_seed(5)
-    th2, m2, v2, n2, rep, short, (z, u) = bgs.density_control(
-        torch.from_numpy(theta).to(dev), torch.from_numpy(m).to(dev), torch.from_numpy(v).to(dev), n, prm, g)
+    th2, m2, v2, n2, rep, short, rounds = bgs.density_control(
+        torch.from_numpy(theta).to(dev), torch.from_numpy(m).to(dev), torch.from_numpy(v).to(dev), n, prm, g,
+        max_rounds=1)
+    (z, u), = rounds
     torch.cuda.synchronize()
     print(name, "points with < 8 neighbours within 3 r:", short)
     st = D.stats(theta, n, r=float(np.float32(rad)), k=8)
@@ -103,3 +105,57 @@ def test_density_step_parity(bgs, name):
     np.testing.assert_allclose(th2.cpu().numpy(), th_ref, rtol=2e-6, atol=1e-6)
     np.testing.assert_array_equal(m2.cpu().numpy(), m_ref)
     np.testing.assert_array_equal(v2.cpu().numpy(), v_ref)
+
+
+@pytest.mark.parametrize("name", ["contrast", "clustered"])
+def test_density_rounds_parity(bgs, name):
+    """R35' ("repeated iteratively until the desired density is achieved"): up to four
+    densification rounds, each re-counting rho over the grown scene; every round's child
+    count and the final scene equal the oracle's loop fed the GPU's variates; the normalized
+    deviation before / after (Fig. 5(a)) is printed."""
+    from oracle import density as D
+
+    pts, rad = _step_fixtures()[name]
+    pts = np.ascontiguousarray(pts, np.float32)
+    r = np.random.default_rng(13)
+    n = pts.shape[0]
+    theta = np.concatenate([pts.ravel(), r.normal(np.log(0.01), 0.1, 3 * n), r.normal(0, 1, 4 * n),
+                            r.normal(0, 2, n), r.normal(0, 0.2, 48 * n)]).astype(np.float32)
+    m = r.normal(0, 1, 59 * n).astype(np.float32)
+    v = r.random(59 * n).astype(np.float32)
+    if rad is None:
+        rad = float(np.median(D.knn(pts, 8)[0][:, -1]))
+    rad = float(np.float32(rad))
+    prm = bgs.DensityParams(rad)
+    delta = float(np.float32(0.1 * np.float32(rad)))
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(7)
+    th2, m2, v2, n2, rep, _, rounds = bgs.density_control(
+        torch.from_numpy(theta).to(dev), torch.from_numpy(m).to(dev), torch.from_numpy(v).to(dev), n, prm, g,
+        max_rounds=4)
+    torch.cuda.synchronize()
+    st = D.stats(theta, n, r=rad, k=8)
+    pairs = D.merge_pairs(theta, n, st)
+    c = D.child_counts(st, n, max_new=4)
+    z, u = rounds[0]
+    th_r, m_r, v_r, n_r = D.apply(theta, m, v, n, st, pairs, c, z.cpu().numpy().astype(np.float64),
+                                  u.cpu().numpy().astype(np.float64), alpha_sigma=1.5, delta=delta)
+    parents, sigma = D.sparse_parents(theta, n, st, pairs, alpha_sigma=1.5)
+    assert rep.n_sparse == len(parents) > 0
+    per_round = [int(c.sum())]
+    for z, u in rounds[1:]:
+        th_r, m_r, v_r, n_r, kc = D.densify_round(th_r, m_r, v_r, n_r, rad, parents, sigma, st["rho_low"],
+                                                  z.cpu().numpy().astype(np.float64),
+                                                  u.cpu().numpy().astype(np.float64), max_new=4, delta=delta)
+        per_round.append(kc)
+    if len(rounds) < 4:  # the GPU stopped early: the oracle's next round spawns nothing either
+        assert D.densify_round(th_r, m_r, v_r, n_r, rad, parents, sigma, st["rho_low"], [], [], 4, delta)[4] == 0
+    assert rep.children_per_round == per_round and n2 == n_r
+    np.testing.assert_allclose(th2.cpu().numpy(), th_r, rtol=2e-6, atol=1e-6)
+    np.testing.assert_array_equal(m2.cpu().numpy(), m_r)
+    np.testing.assert_array_equal(v2.cpu().numpy(), v_r)
+    d0 = D.normalized_deviation(pts, rad)
+    d1 = D.normalized_deviation(D._seg(th_r, n_r)["means"], rad)
+    print(f"{name}: n {n} -> {n2}, children per round {per_round}, sigma/mu {d0:.3f} -> {d1:.3f} "
+          f"({d1 / d0:.2f}x; the paper's Fig. 5(a): 0.51x)")

@@ -165,3 +165,51 @@ def test_merging_thins_the_dense_region_on_a_100x_contrast_fixture():
     assert (rho2 > st["rho_high"]).sum() < (st["rho"] > st["rho_high"]).sum()
     c = D.child_counts(st, n)
     assert (c[2500:] > 0).all()  # every sparse point is below rho_low and spawns
+
+
+def test_densify_rounds_reach_the_desired_density_spec_example():
+    """SPEC.md l.250's example for the iterated densification (R35'): a single isolated point
+    with rho_low = 2 and enough rounds ends with >= 2 neighbours within r; with one child per
+    round and children within r that takes exactly two rounds, and a third round spawns
+    nothing (the desired density is achieved)."""
+    pts = np.zeros((1, 3), np.float32)
+    th, n = _theta(pts, seed=3)
+    m = np.zeros_like(th)
+    r = 1.0
+    z = np.array([[0.1, 0.0, 0.0]])
+    counts = []
+    for t in range(3):
+        th, m, m2, n, kc = D.densify_round(th, m, m, n, r, np.array([0]), np.array([1.0]), 2.0,
+                                           z * (t + 1), np.zeros((1, 3)), max_new=1, delta=0.0)
+        counts.append(kc)
+    assert counts == [1, 1, 0] and n == 3
+    mu = D._seg(th, n)["means"]
+    assert np.allclose(mu[1], [0.1, 0, 0]) and np.allclose(mu[2], [0.2, 0, 0])  # p + sigma z, exact
+    assert oracle.local_density(mu, r)[0] >= 2
+    assert not m.any()  # children have zero Adam moments
+
+
+def test_densify_round_appends_in_parent_order_and_keeps_the_scene():
+    """R35': the n points are unchanged (moments kept), children follow in (parent, j) order
+    with the parent's attributes; parents at or above rho_low spawn nothing."""
+    r = np.random.default_rng(5)
+    pts = np.concatenate([r.uniform(0, 0.2, (40, 3)), [[5.0, 5.0, 5.0], [-5.0, 0.0, 0.0]]]).astype(np.float32)
+    th, n = _theta(pts, seed=5)
+    m = r.normal(0, 1, th.shape).astype(np.float32)
+    parents = np.array([40, 41, 0])  # two isolated points and one inside the cluster
+    rho = oracle.local_density(pts, 0.05)
+    lo = 0.5 * (rho[0] + 1) if rho[0] > 0 else 0.5  # parent 0 is at or above it
+    lo = min(lo, float(rho[0]))
+    z = r.normal(0, 1, (8, 3))
+    th2, m2, _, n2, kc = D.densify_round(th, m, m, n, 0.05, parents, np.array([0.01, 0.02, 0.03]), max(lo, 1.0),
+                                         z, np.zeros((8, 3)), max_new=3, delta=0.0)
+    c40 = min(3, math.ceil(max(lo, 1.0) - rho[40]))
+    c41 = min(3, math.ceil(max(lo, 1.0) - rho[41]))
+    c0 = min(3, math.ceil(max(lo, 1.0) - rho[0])) if rho[0] < max(lo, 1.0) else 0
+    assert kc == c40 + c41 + c0 and n2 == n + kc
+    s1, s2 = D._seg(th, n), D._seg(th2, n2)
+    for key in ("means", "log_scales", "quats", "opacity", "sh"):
+        assert np.array_equal(s2[key][:n], s1[key][:n])
+    assert np.array_equal(D._seg(m2, n2)["sh"][:n], D._seg(m, n)["sh"])
+    assert np.allclose(s2["means"][n], pts[40] + 0.01 * z[0]) and np.array_equal(s2["sh"][n], s1["sh"][40])
+    assert np.allclose(s2["means"][n + c40], pts[41] + 0.02 * z[c40])
