@@ -207,7 +207,6 @@ constexpr int kRsRing = 4;
 __device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_ring() {
   asm volatile("cp.async.wait_group %0;" ::"n"(kRsRing - 1) : "memory");
 }
@@ -312,6 +311,7 @@ __device__ __forceinline__ void rs_emit_range(const Src& src, int64_t sb, uint32
         got = s_rs_dyn[ctr_at + bin];
         s_rs_dyn[ctr_at + bin] = got + __popc(pm);
       }
+      __syncwarp();  // the next batch's leaders read these counters
       const uint32_t base = __shfl_sync(0xffffffffu, got, leader);
       if (valid) emit(base + __popc(pm & lt), q0, q1);
       bin = bin_n;

@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(uint32_t* chunk_cnt, int32_
 }
 
 // (c) items of each chunk, in depth order, to their final positions.  Per warp: the next
-// final position of each tile's items (u32) and a per-tile lane scratch (u8) that detects
+// final position of each tile's items (u32) and a per-tile item count (u8) that detects
 // two items of a 32-item batch falling into the same tile.
 constexpr int kEmitWarps = 2;
 
@@ -432,11 +432,12 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
   const uint32_t c = blockIdx.x * kEmitWarps + warp;
   if (c >= n_chunks) return;
   const int nt_pad = (nt + 3) & ~3;
-  uint32_t* nxt = s_dyn + warp * (nt_pad + nt_pad / 4);  // nt u32 positions + nt u8 scratch
-  uint8_t* scratch = reinterpret_cast<uint8_t*>(nxt + nt_pad);
+  uint32_t* nxt = s_dyn + warp * (nt_pad + nt_pad / 4);  // the next position of each tile's items
+  uint32_t* cnt8 = nxt + nt_pad;                          // a batch's items per tile, one byte each
   const uint32_t* row = chunk_cnt + (size_t)c * nt;
 #pragma unroll 8
   for (int t = lane; t < nt; t += 32) nxt[t] = ranges[t].x + row[t];
+  for (int t = lane; t < nt_pad / 4; t += 32) cnt8[t] = 0u;
   __syncwarp();
   const uint32_t a = c * CI, b = min(K, a + CI);
   int64_t rb = rank_of_item(item_off, n, a, lane);
@@ -483,34 +484,26 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
       const uint32_t rowi = (uint32_t)(((float)local + 0.5f) * g_iw);
       tile = ((g_xy >> 16) + rowi) * (uint32_t)tiles_x + (g_xy & 0xffffu) + (local - rowi * g_w);
     };
-    // commit one 32-item batch in order
+    // commit one 32-item batch in order: items of tiles no other item of the batch shares
+    // take their positions at once; a Gaussian's items have distinct tiles, so the items of
+    // contended tiles take theirs one Gaussian at a time, in depth order (lanes of a Gaussian
+    // are contiguous).  The batch's items per tile are counted in a byte per tile with shared
+    // atomics (4 tiles per word), and the counts are taken back after the commit: no two
+    // lanes store to one shared-memory word in the same instruction (racecheck-clean,
+    // tests/test_gpu_sanitizer.py; MATCH.ANY peer sets instead: 0.58 -> 0.65 ms per view).
     auto commit = [&](bool valid, int g, uint32_t tile, uint32_t g_id) {
-      // fast path: the batch's items are in distinct tiles
-      if (valid) scratch[tile] = (uint8_t)lane;
+      const uint32_t one = 1u << (8u * (tile & 3u));
+      if (valid) atomicAdd(&cnt8[tile >> 2], one);
       __syncwarp();
-      const bool clash = valid && scratch[tile] != (uint8_t)lane;
-      if (!__any_sync(0xffffffffu, clash)) {
-        if (valid) {
-          const uint32_t p = nxt[tile];
-          nxt[tile] = p + 1u;
-          vals[p] = g_id;
-        }
-      } else {
-        // mark the contended tiles (the losers overwrite their tile's byte with 0xff: every
-        // lane of a tile that two items of the batch share then sees it); the items of
-        // uncontended tiles take their positions at once
-        if (clash) scratch[tile] = 0xffu;
+      const bool contended = valid && ((cnt8[tile >> 2] >> (8u * (tile & 3u))) & 0xffu) > 1u;
+      if (valid && !contended) {
+        const uint32_t p = nxt[tile];
+        nxt[tile] = p + 1u;
+        vals[p] = g_id;
+      }
+      uint32_t pending = __ballot_sync(0xffffffffu, contended);
+      if (pending) {
         __syncwarp();
-        const bool contended = valid && scratch[tile] == 0xffu;
-        if (valid && !contended) {
-          const uint32_t p = nxt[tile];
-          nxt[tile] = p + 1u;
-          vals[p] = g_id;
-        }
-        __syncwarp();
-        // a Gaussian's items have distinct tiles, so the contended items take their
-        // positions one Gaussian at a time, in depth order (lanes of a Gaussian are contiguous)
-        uint32_t pending = __ballot_sync(0xffffffffu, contended);
         while (pending) {
           const int gcur = __shfl_sync(0xffffffffu, g, __ffs(pending) - 1);
           const bool mine = contended && g == gcur;
@@ -524,6 +517,7 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
         }
       }
       __syncwarp();
+      if (valid) atomicSub(&cnt8[tile >> 2], one);
     };
     // two batches per round: their lookups are independent (ILP), commits stay in order
     for (uint32_t kb = pos; kb < end; kb += 64) {
