@@ -83,9 +83,11 @@ def parse():
                    help="CUDA streams the step's views are spread over (round-robin; measured at garden: 1 -> 239.3, 2 -> 242.0, 3 -> 220.3 views/s, so 1 by default)")
     p.add_argument("--density-every", type=int, default=0,
                    help="run the NEXT-1 density-control step every D training steps (configs[4]; 0 = off)")
-    p.add_argument("--update", default="sharded", choices=["sharded", "allreduce"],
-                   help="G > 1: reduce-scatter + Adam on a 1/G shard + all-gather (default), or all-reduce + "
-                        "full Adam on every rank")
+    p.add_argument("--update", default="sharded", choices=["sharded", "allreduce", "overlap"],
+                   help="G > 1: reduce-scatter + Adam on a 1/G shard + all-gather (default); all-reduce + "
+                        "full Adam on every rank; or 'overlap': the chain rule in Gaussian chunks, each chunk's "
+                        "gradient all-reduced on a communication stream while the next computes (SURVEY 8(e) 1)")
+    p.add_argument("--overlap-chunks", type=int, default=4, help="--update overlap: Gaussian chunks")
     p.add_argument("--loss", default="l1dssim", choices=["l1dssim", "l1"],
                    help="per-view loss: the 3DGS 0.8 L1 + 0.2 D-SSIM (default) or L1 alone (R19)")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -106,6 +108,27 @@ def parse():
     return p.parse_args()
 
 
+def nccl_summary():
+    """The lines of this process's NCCL log (NCCL_DEBUG_FILE) that identify the communicator:
+    ranks, NVLS (in-switch reduction) support, channels / rings."""
+    import glob
+
+    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    files = glob.glob(path.replace("%h", "*").replace("%p", str(os.getpid()))) if path else []
+    keep = []
+    for fn in files[:1]:
+        try:
+            for ln in open(fn, errors="replace"):
+                if any(k in ln for k in ("NVLS", "nRanks", "Init COMPLETE", "NCCL version", "Channel 00", "Trees",
+                                          "P2P/CUMEM", "via P2P", "NVLink")):
+                    keep.append(ln.strip()[-200:])
+                if len(keep) >= 24:
+                    break
+        except OSError:
+            pass
+    return {"log": files[:1], "lines": keep}
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -116,7 +139,9 @@ def load_peaks():
 
 def _update_desc(args, world):
     if world > 1:
-        return "reduce-scatter + sharded Adam + all-gather" if args.update == "sharded" else "all-reduce + Adam"
+        return {"sharded": "reduce-scatter + sharded Adam + all-gather", "allreduce": "all-reduce + Adam",
+                "overlap": f"chain rule in {args.overlap_chunks} Gaussian chunks, each chunk's all-reduce overlapped "
+                           "with the next, + Adam"}[args.update]
     if args.fuse_adam and not args.one_frame and args.views <= 16:
         return "chain rule fused with Adam"
     return "all-reduce (none at G = 1) + Adam"
@@ -229,6 +254,9 @@ def run_ours(args, rank, world, local_rank):
     used = sorted(set(rank_cams(1, True)) if args.fixed_batch else range(n_cams))  # cameras any step renders
     W, H = cams_all[0].width, cams_all[0].height
     sharded = world > 1 and args.update == "sharded"
+    overlap = world > 1 and args.update == "overlap" and not args.one_frame
+    comm_stream = torch.cuda.Stream(device=dev) if overlap else None
+    chunk_ev = [torch.cuda.Event() for _ in range(max(1, args.overlap_chunks))]
     # one GPU, one chain-rule launch: a10 and a11 fused (no collective between them)
     fused = world == 1 and not args.one_frame and args.fuse_adam and args.views <= 16
     # the step's views share theta: one preprocess pass over it for all of them
@@ -466,11 +494,23 @@ def run_ours(args, rank, world, local_rank):
         theta, m, v, n, lo, hi = S["theta"], S["m"], S["v"], S["n"], S["lo"], S["hi"]
         if fused:  # a10 + a11 in one pass per Gaussian: the gradient never reaches memory
             bgs.bgs_preprocess_bwd_batch_adam(gs, frames, theta, None, m, v, hp, step_no[0])
+        elif overlap:  # a10 in Gaussian chunks; chunk k's all-reduce runs while chunk k+1 computes
+            for ci, (b, e) in enumerate(dp.gaussian_chunks(n, args.overlap_chunks)):
+                bgs.bgs_preprocess_bwd_batch_range(gs, frames, grad, b, e - b)
+                chunk_ev[ci].record(stream)
+                comm_stream.wait_event(chunk_ev[ci])
+                with torch.cuda.stream(comm_stream):
+                    dp.allreduce_chunk(grad, n, b, e, world)
         elif not args.one_frame:  # a10 once over the batch's views: theta/grad cross HBM once
             bgs.bgs_preprocess_bwd_batch(gs, frames, grad)
         mark(marks)
         if fused:
             mark(marks)
+            mark(marks)
+        elif overlap:
+            stream.wait_stream(comm_stream)  # the last chunk's exchange
+            mark(marks)
+            bgs.bgs_adam_step(theta, grad, m, v, n, hp, step_no[0])
             mark(marks)
         elif sharded:  # NCCL over NVLink: reduce-scatter, Adam on the shard, all-gather
             g_shard = dp.reduce_scatter_grads(grad, rank, world)
@@ -807,6 +847,7 @@ def run_ours(args, rank, world, local_rank):
                      "each view hinted by its camera's last forward (bgs_frame_save_hint / load_hint)",
                      "sort_path": args.sort_path},
         "variants": variants,
+        "nccl": (nccl_summary() if world > 1 and os.environ.get("BGS_DIST_BACKEND", "nccl") == "nccl" else None),
         "density": None if not args.density_every else {
             "every": args.density_every, "r": round(float(dens_prm.r), 6), "events_timed_and_e2e": dens_log,
             "n_final": S["n"]},
@@ -984,6 +1025,11 @@ def main():
         backend = os.environ.get("BGS_DIST_BACKEND", "nccl")
         torch.cuda.set_device(_device_index(local_rank))
         if backend == "nccl":
+            # NCCL's own log (init, topology, NVLS) to a per-process file; rank 0 quotes the
+            # lines that confirm the ranks, transport and algorithm in its JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,GRAPH,NVLS")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/bgs_nccl.%h.%p.log")
             dist.init_process_group("nccl", device_id=torch.device("cuda", _device_index(local_rank)))
         else:  # test-only: several ranks sharing one GPU (NCCL refuses duplicate GPUs)
             dist.init_process_group(backend)

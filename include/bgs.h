@@ -189,6 +189,17 @@ bgs_status bgs_preprocess_bwd(const bgs_gaussians* g /*host*/, bgs_frame* f /*ho
 bgs_status bgs_preprocess_bwd_batch(const bgs_gaussians* g /*host*/, bgs_frame* const* frames /*host*/,
                                     int32_t nframes, float* grad, void* stream);
 
+/* bgs_preprocess_bwd_batch restricted to the Gaussians [begin, begin + count): grad +=
+ * their 59 elements (in each theta segment the sub-range of those Gaussians) and nothing
+ * else.  Consecutive ranges covering [0, n) sum to bgs_preprocess_bwd_batch's gradient
+ * (bit-identical: each element is written by one Gaussian's thread).  A multi-GPU caller
+ * processes the Gaussians in chunks and starts each chunk's gradient exchange (an
+ * all-reduce of its five segment sub-ranges) while the next chunk
+ * computes.  BGS_ERR_INVALID if the range is not inside [0, n). */
+bgs_status bgs_preprocess_bwd_batch_range(const bgs_gaussians* g /*host*/, bgs_frame* const* frames /*host*/,
+                                          int32_t nframes, float* grad, int64_t begin, int64_t count,
+                                          void* stream);
+
 /* a10 + a11 fused for one GPU (no collective between them): the batched chain rule of
  * bgs_preprocess_bwd_batch, then -- in the same kernel, per Gaussian -- the Adam update of
  * bgs_adam_step with the batch's gradient, which is never written to memory (dense: a

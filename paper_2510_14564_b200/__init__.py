@@ -108,6 +108,8 @@ _SIGS = {
     "bgs_blend_bwd": (C.c_int, [C.POINTER(Frame), _P, _P, _P, _P]),
     "bgs_preprocess_bwd": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Frame), _P, _P]),
     "bgs_preprocess_bwd_batch": (C.c_int, [C.POINTER(Gaussians), C.POINTER(C.POINTER(Frame)), C.c_int32, _P, _P]),
+    "bgs_preprocess_bwd_batch_range": (C.c_int, [C.POINTER(Gaussians), C.POINTER(C.POINTER(Frame)), C.c_int32, _P, C.c_int64,
+                                                C.c_int64, _P]),
     "bgs_preprocess_bwd_batch_adam": (C.c_int, [C.POINTER(Gaussians), C.POINTER(C.POINTER(Frame)), C.c_int32, _P, _P,
                                                 _P, _P, C.POINTER(AdamHParams), C.c_int64, _P]),
     "bgs_adam_step": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(AdamHParams), C.c_int64, _P]),
@@ -250,6 +252,13 @@ def bgs_preprocess_bwd_batch(g: Gaussians, frames, grad, stream=None):
     arr = (C.POINTER(Frame) * len(frames))(*[C.pointer(f) for f in frames])
     _check(_lib.bgs_preprocess_bwd_batch(C.byref(g), arr, len(frames), _ptr(grad), _stream(stream)),
            "bgs_preprocess_bwd_batch")
+
+
+def bgs_preprocess_bwd_batch_range(g: Gaussians, frames, grad, begin, count, stream=None):
+    """The batched chain rule for the Gaussians [begin, begin + count) only."""
+    arr = (C.POINTER(Frame) * len(frames))(*[C.pointer(f) for f in frames])
+    _check(_lib.bgs_preprocess_bwd_batch_range(C.byref(g), arr, len(frames), _ptr(grad), int(begin), int(count),
+                                               _stream(stream)), "bgs_preprocess_bwd_batch_range")
 
 
 def bgs_preprocess_bwd_batch_adam(g: Gaussians, frames, theta, grad, exp_avg, exp_avg_sq, hp: AdamHParams,

@@ -160,7 +160,7 @@ bgs_status launch_preprocess_bwd_batch(const bgs_gaussians* g, Frame* const* fra
                                        cudaStream_t s);
 bgs_status launch_preprocess_bwd_batch_impl(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
                                             float* theta, float* m, float* v, const bgs_adam_hparams* hp,
-                                            int64_t step, cudaStream_t s);
+                                            int64_t step, cudaStream_t s, int64_t i0 = 0, int64_t i1 = -1);
 bgs_status launch_render_bwd(const bgs_gaussians* g, Frame* F, const float* dL_dimage, const float* final_T,
                              const uint32_t* n_contrib, float* grad, cudaStream_t s);
 bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, int64_t begin, int64_t count,

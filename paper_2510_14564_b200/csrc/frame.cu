@@ -369,6 +369,23 @@ bgs_status bgs_preprocess_bwd_batch(const bgs_gaussians* g, bgs_frame* const* fr
   return launch_preprocess_bwd_batch(g, F, nframes, grad, (cudaStream_t)stream);
 }
 
+bgs_status bgs_preprocess_bwd_batch_range(const bgs_gaussians* g, bgs_frame* const* frames, int32_t nframes,
+                                          float* grad, int64_t begin, int64_t count, void* stream) {
+  if (!frames || nframes < 1 || nframes > 4096 || begin < 0 || count < 0) return BGS_ERR_INVALID;
+  static thread_local Frame* F[4096];
+  for (int v = 0; v < nframes; ++v) {
+    if (!frame_ok(frames[v]) || !frame_of(frames[v])->cam_valid) return BGS_ERR_INVALID;
+    F[v] = frame_of(frames[v]);
+    if (F[v]->n != F[0]->n) return BGS_ERR_INVALID;
+  }
+  if (begin + count > F[0]->n) return BGS_ERR_INVALID;
+  bgs_status st = validate_gaussians(g, F[0]);
+  if (st != BGS_OK) return st;
+  if (count > 0 && (!grad || ((uintptr_t)grad & 3u))) return BGS_ERR_INVALID;
+  return launch_preprocess_bwd_batch_impl(g, F, nframes, grad, nullptr, nullptr, nullptr, nullptr, 0,
+                                          (cudaStream_t)stream, begin, begin + count);
+}
+
 bgs_status bgs_preprocess_bwd_batch_adam(const bgs_gaussians* g, bgs_frame* const* frames, int32_t nframes,
                                          float* theta, float* grad, float* exp_avg, float* exp_avg_sq,
                                          const bgs_adam_hparams* hp, int64_t step, void* stream) {

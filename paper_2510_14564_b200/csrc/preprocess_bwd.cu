@@ -40,6 +40,7 @@ struct PreBwdParams {
   const float* ologits;
   const float* sh;  // [n][16][3]
   int64_t n;
+  int64_t i0, i1;  // the Gaussians [i0, i1) this launch processes
   int32_t deg, nviews;
   bool quat_vec4, sh_vec4, gq_vec4, gsh_vec4;  // 16-byte aligned -> vector paths
   float* grad;  // theta layout (fused Adam: the partial sums of earlier launches, or null)
@@ -94,17 +95,17 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
   __shared__ int s_vis[kBwdThreads / 32][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = p.n;
-  const int64_t wbase = ((int64_t)blockIdx.x * kBwdThreads) + warp * 32;
+  const int64_t wbase = p.i0 + ((int64_t)blockIdx.x * kBwdThreads) + warp * 32;
   const int64_t i = wbase + lane;
   uint32_t vmask = 0;  // views in which Gaussian i is visible
-  if (i < n)
+  if (i < p.i1)
     for (int v = 0; v < p.nviews; ++v) vmask |= (p.view[v].radius[i] > 0 ? 1u : 0u) << v;
   const bool valid = vmask != 0;
   s_vis[warp][lane] = valid;
   float* row = &s_sh[warp][lane * kRow];
   float* drow = &s_dsh[warp][lane * kRow];
   const int ncoef = (p.deg + 1) * (p.deg + 1);
-  const int64_t nvalid = n - wbase < 32 ? n - wbase : 32;
+  const int64_t nvalid = p.i1 - wbase < 32 ? p.i1 - wbase : 32;
   for (int k = 0; k < 48; ++k) drow[k] = 0.f;
   __syncwarp();
   // ---- coalesced load of the warp's SH block into shared memory
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
       gq[3] += d3;
     }
   }
-  else if (p.adam && i < n) {
+  else if (p.adam && i < p.i1) {
     // fused Adam is dense (R26): a Gaussian no view sees still takes g = 0
     for (int e = 0; e < 3; ++e) put_grad(p, 3 * i + e, 0.0f, 0);
     for (int e = 0; e < 3; ++e) put_grad(p, 3 * n + 3 * i + e, 0.0f, 1);
@@ -404,9 +405,10 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
 // null when one launch covers all views).
 bgs_status launch_preprocess_bwd_batch_impl(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
                                             float* theta, float* m, float* v, const bgs_adam_hparams* hp,
-                                            int64_t step, cudaStream_t s) {
+                                            int64_t step, cudaStream_t s, int64_t i0, int64_t i1) {
   const int64_t n = frames[0]->n;
-  if (n == 0) return BGS_OK;
+  if (i1 < 0) i1 = n;
+  if (n == 0 || i1 <= i0) return BGS_OK;
   PreBwdParams p;
   p.adam = false;
   p.theta = theta;
@@ -429,6 +431,8 @@ bgs_status launch_preprocess_bwd_batch_impl(const bgs_gaussians* g, Frame* const
   p.ologits = g->opacity_logits;
   p.sh = g->sh;
   p.n = n;
+  p.i0 = i0;
+  p.i1 = i1;
   p.deg = g->sh_degree;
   auto al16 = [](const void* q) { return ((uintptr_t)q & 15u) == 0; };
   p.quat_vec4 = al16(g->quats);
@@ -446,7 +450,7 @@ bgs_status launch_preprocess_bwd_batch_impl(const bgs_gaussians* g, Frame* const
       p.view[v].cbits = F->cbits;
       p.view[v].grad2d = F->grad2d;
     }
-    k_preprocess_bwd<<<(unsigned)((n + kBwdThreads - 1) / kBwdThreads), kBwdThreads, 0, s>>>(p);
+    k_preprocess_bwd<<<(unsigned)((i1 - i0 + kBwdThreads - 1) / kBwdThreads), kBwdThreads, 0, s>>>(p);
     note_launch();
     bgs_status st = check_launch("k_preprocess_bwd");
     if (st != BGS_OK) return st;

@@ -74,3 +74,41 @@ def all_gather_params(theta_padded: torch.Tensor, rank: int, world: int) -> None
     if world > 1:
         shard = theta_padded.numel() // world
         dist.all_gather_into_tensor(theta_padded, theta_padded.narrow(0, rank * shard, shard))
+
+
+# ---------------------------------------------------------------- overlapped all-reduce (§8(e) 1)
+# The chain rule (a10) runs over the Gaussians in chunks; a chunk's gradient -- in each of
+# theta's five segments the sub-range of its Gaussians -- is all-reduced on a communication
+# stream while the next chunk computes, so the exchange hides behind a10 except for the last
+# chunk.
+
+SEGMENT_WIDTHS = (3, 3, 4, 1, 48)  # means, log_scales, quats, opacity logit, sh (theta layout)
+
+
+def gaussian_chunks(n: int, chunks: int) -> list[tuple[int, int]]:
+    """[begin, end) Gaussian ranges of ~equal size covering [0, n)."""
+    if n < 0 or chunks < 1:
+        raise ValueError(f"bad chunking n={n} chunks={chunks}")
+    step = -(-n // chunks) if n else 0
+    return [(b, min(n, b + step)) for b in range(0, n, step)] if n else []
+
+
+def segment_slices(n: int, begin: int, end: int) -> list[tuple[int, int]]:
+    """The theta elements of Gaussians [begin, end): one [lo, hi) per segment."""
+    out, base = [], 0
+    for w in SEGMENT_WIDTHS:
+        out.append((base + w * begin, base + w * end))
+        base += w * n
+    return out
+
+
+def allreduce_chunk(grad: torch.Tensor, n: int, begin: int, end: int, world: int, async_op: bool = False):
+    """All-reduce (SUM) of the gradient elements of Gaussians [begin, end) -- five contiguous
+    collectives; returns their work handles when async_op."""
+    works = []
+    if world > 1:
+        for lo, hi in segment_slices(n, begin, end):
+            w = dist.all_reduce(grad.narrow(0, lo, hi - lo), op=dist.ReduceOp.SUM, async_op=async_op)
+            if async_op:
+                works.append(w)
+    return works

@@ -194,3 +194,60 @@ def test_two_rank_allreduce_matches_single_process():
         g = results[r][1]
         assert np.linalg.norm(g - ref) <= 1e-12 * max(np.linalg.norm(ref), 1.0)
     assert np.array_equal(results[0][2], results[1][2])  # replicas bit-identical after Adam
+
+
+def test_gaussian_chunks_cover_theta_once():
+    """§8(e) 1: the chunks' segment sub-ranges tile theta[59n] exactly once."""
+    dp = _load_dp_module()
+    for n in (1, 7, 300, 5_800_000):
+        for chunks in (1, 3, 4, 16):
+            cover = np.zeros(59 * n, np.int8) if n < 10_000 else None
+            total = 0
+            for b, e in dp.gaussian_chunks(n, chunks):
+                for lo, hi in dp.segment_slices(n, b, e):
+                    assert 0 <= lo <= hi <= 59 * n
+                    total += hi - lo
+                    if cover is not None:
+                        cover[lo:hi] += 1
+            assert total == 59 * n
+            if cover is not None:
+                assert (cover == 1).all()
+
+
+def _worker_chunked(rank, port, q):
+    _load_dp_module()
+    from paper_2510_14564_b200_dp import dp
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    s, cams = _scene()
+    grad = torch.zeros(59 * s.n, dtype=torch.float64)
+    for v in dp.views_for_rank(list(range(N_VIEWS)), rank, WORLD):
+        grad += torch.from_numpy(_view_grad(s, cams[v], 100 + v))
+    works = []
+    for b, e in dp.gaussian_chunks(s.n, 4):  # as the chain rule finishes each chunk
+        works += dp.allreduce_chunk(grad, s.n, b, e, WORLD, async_op=True)
+    for w in works:
+        w.wait()
+    q.put((rank, grad.numpy().copy()))
+    dist.destroy_process_group()
+
+
+def test_two_rank_chunked_allreduce_matches_single_process():
+    """The overlapped exchange (five async all-reduces per Gaussian chunk) sums the same
+    gradient as one all-reduce of grad[59n]: both ranks hold the 4-view sum."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_chunked, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(WORLD))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    s, cams = _scene()
+    ref = sum(_view_grad(s, cams[v], 100 + v) for v in range(N_VIEWS))
+    for r in range(WORLD):
+        assert np.linalg.norm(res[r] - ref) <= 1e-12 * max(np.linalg.norm(ref), 1.0)
+    assert np.array_equal(res[0], res[1])

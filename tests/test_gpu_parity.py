@@ -321,6 +321,15 @@ def test_batched_preprocess_bwd(bgs):
         for gname, idx in oracle.group_slices(s.n).items():
             err = np.linalg.norm(gg[idx] - mult * g_ref[idx]) / np.linalg.norm(mult * g_ref[idx])
             assert err <= GRAD_TOL, (mult, gname, err)
+    # the chain rule in Gaussian chunks (the overlapped multi-GPU exchange):
+    # ragged ranges covering [0, n) give the one-pass gradient bit for bit
+    grad_c = torch.zeros_like(theta)
+    for b, e in ((0, 1), (1, 4097), (4097, 12000), (12000, 12000), (12000, s.n)):
+        bgs.bgs_preprocess_bwd_batch_range(g, [r.frame for r in rs], grad_c, b, e - b)
+    torch.cuda.synchronize()
+    assert torch.equal(grad_c, grad1)
+    with pytest.raises(bgs.BgsError):
+        bgs.bgs_preprocess_bwd_batch_range(g, [r.frame for r in rs], grad_c, s.n - 1, 2)
 
 
 def test_adam_parity(bgs):
