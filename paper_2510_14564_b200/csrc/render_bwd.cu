@@ -156,6 +156,11 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
         DS[h] = dLr[h] * c.y + dLg[h] * c.z + dLb[h] * c.w;
       }
     }
+    // PPL == 2: the two pixels' state as pairs for the FP32x2 instructions (FFMA2 / FMUL2 /
+    // FADD2 of sm_100: one instruction, two separately rounded results)
+    float2 T2 = make_float2(T[0], T[PPL - 1]), DS2 = make_float2(DS[0], DS[PPL - 1]);
+    const float2 dLr2 = make_float2(dLr[0], dLr[PPL - 1]), dLg2 = make_float2(dLg[0], dLg[PPL - 1]),
+                 dLb2 = make_float2(dLb[0], dLb[PPL - 1]), npy2 = make_float2(-pyf[0], -pyf[PPL - 1]);
     const int nst = (top - lo + 31) / 32;
     // lane's list position in step s (back to front; below lo = no entry)
     auto pos_of = [&](int s) { return top - 32 * (s + 1) + lane; };
@@ -208,6 +213,73 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
         const uint32_t pos = spos[k];
         bool any_act = false;
         float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
+        if constexpr (PPL == 2) {
+          // both pixels of the lane at once, without per-pixel branches: a pixel that does not
+          // take the entry gets alpha = 0 (1 / (1 - 0) = 1 exactly, weight 0), so its T, DS and
+          // partials are unchanged; an entry no pixel of the warp takes is skipped uniformly
+          const bool a0 = pos < my_last[0], a1 = pos < my_last[1];
+          if (!__any_sync(0xffffffffu, a0 | a1)) goto reduce;
+          {
+            const float4 r0 = sr0[k];
+            const float4 r1 = sr1[k];
+            const float4 r2 = sr2[k];
+            const float dx = r0.x - pxf;
+            const float dxx = dx * dx;
+            const float2 dx2 = make_float2(dx, dx);
+            const float2 dy2 = __fadd2_rn(make_float2(r0.y, r0.y), npy2);
+            const float2 dyy2 = __fmul2_rn(dy2, dy2), dxy2 = __fmul2_rn(dx2, dy2);
+            const float2 pw = __ffma2_rn(make_float2(r1.x, r1.x), make_float2(dxx, dxx),
+                                         __ffma2_rn(make_float2(r1.z, r1.z), dyy2,
+                                                    __fmul2_rn(make_float2(r1.y, r1.y), dxy2)));
+            // power below the exact alpha < 1/255 bound (pthr) or R14's power > 0 guard
+            const bool c0 = a0 & !(pw.x > 0.0f) & !(pw.x < r2.w), c1 = a1 & !(pw.y > 0.0f) & !(pw.y < r2.w);
+            if (!__any_sync(0xffffffffu, c0 | c1)) goto reduce;
+            const float G0 = canon ? canon_exp(pw.x) : fast_exp(pw.x);
+            const float G1 = canon ? canon_exp(pw.y) : fast_exp(pw.y);
+            const float2 og2 = __fmul2_rn(make_float2(r1.w, r1.w), make_float2(G0, G1));
+            const float al0 = fminf(0.99f, og2.x), al1 = fminf(0.99f, og2.y);
+            const bool t0 = c0 & (al0 >= (1.0f / 255.0f)), t1 = c1 & (al1 >= (1.0f / 255.0f));
+            any_act = t0 | t1;
+            const float2 al2 = make_float2(t0 ? al0 : 0.0f, t1 ? al1 : 0.0f);
+            const float2 om2 = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al2.x, -al2.y));
+            // MUFU reciprocal (1 - alpha >= 0.01): ~2^-22 relative per step, far inside the
+            // 1e-3 gradient tolerance, instead of the multi-instruction IEEE division
+            const float2 io2 = make_float2(__fdividef(1.0f, om2.x), __fdividef(1.0f, om2.y));
+            T2 = __fmul2_rn(T2, io2);  // transmittance in front of this Gaussian
+            const float2 w2 = __fmul2_rn(al2, T2);
+            const float2 p6 = __fmul2_rn(w2, dLr2), p7 = __fmul2_rn(w2, dLg2), p8 = __fmul2_rn(w2, dLb2);
+            g6 = p6.x + p6.y;
+            g7 = p7.x + p7.y;
+            g8 = p8.x + p8.y;
+            // dL/dalpha = T (dL . c) - DS / (1 - alpha); DS += (dL . c) w
+            const float2 dLc2 = __ffma2_rn(dLb2, make_float2(r2.z, r2.z),
+                                           __ffma2_rn(dLg2, make_float2(r2.y, r2.y),
+                                                      __fmul2_rn(dLr2, make_float2(r2.x, r2.x))));
+            const float2 dsi = __fmul2_rn(DS2, io2);
+            const float2 dLda2 = __ffma2_rn(T2, dLc2, make_float2(-dsi.x, -dsi.y));
+            DS2 = __ffma2_rn(dLc2, w2, DS2);
+            // unclamped alpha: gradient to opacity and G (R18)
+            // (the factors of pixels that do not take the entry are zeroed, not just dL/dalpha:
+            // G and o G of a skipped power > 0 may be infinite)
+            const bool u0 = t0 & (og2.x <= 0.99f), u1 = t1 & (og2.y <= 0.99f);
+            const float2 dl2 = make_float2(u0 ? dLda2.x : 0.0f, u1 ? dLda2.y : 0.0f);
+            const float2 p5 = __fmul2_rn(dl2, make_float2(u0 ? G0 : 0.0f, u1 ? G1 : 0.0f));
+            g5 = p5.x + p5.y;
+            const float2 dp2 = __fmul2_rn(dl2, make_float2(u0 ? og2.x : 0.0f, u1 ? og2.y : 0.0f));  // dL/dpower
+            const float2 e0 = __ffma2_rn(make_float2(2.0f * r1.x, 2.0f * r1.x), dx2,
+                                         __fmul2_rn(make_float2(r1.y, r1.y), dy2));
+            const float2 e1 = __ffma2_rn(make_float2(2.0f * r1.z, 2.0f * r1.z), dy2,
+                                         __fmul2_rn(make_float2(r1.y, r1.y), dx2));
+            const float2 p0 = __fmul2_rn(dp2, e0), p1 = __fmul2_rn(dp2, e1);
+            const float2 p2 = __fmul2_rn(dp2, make_float2(dxx, dxx)), p3 = __fmul2_rn(dp2, dxy2),
+                         p4 = __fmul2_rn(dp2, dyy2);
+            g0 = p0.x + p0.y;
+            g1 = p1.x + p1.y;
+            g2 = p2.x + p2.y;
+            g3 = p3.x + p3.y;
+            g4 = p4.x + p4.y;
+          }
+        } else {
         bool act[PPL];
 #pragma unroll
         for (int h = 0; h < PPL; ++h) act[h] = pos < my_last[h];
@@ -256,6 +328,8 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
             }
           }
         }
+        }
+      reduce:;
         const uint32_t actm = __ballot_sync(0xffffffffu, any_act);
         if (__popc(actm) > 8) {
           const float gv[9] = {g0, g1, g2, g3, g4, g5, g6, g7, g8};
