@@ -1,1 +1,2 @@
-timeout 2400 python -m pytest tests/test_gpu_sanitizer.py -q -rs --durations=10 2>&1 | tail -15 > gpurun_out/r2v_sanitizer.log; tail -15 gpurun_out/r2v_sanitizer.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py -x -q 2>&1 | tail -2
+timeout 300 python tools/stage_probe.py --only render_fwd,blend_bwd --reps 20 2>&1 | grep -v "^{"

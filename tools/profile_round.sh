@@ -10,7 +10,7 @@ OUT=gpurun_out
 mkdir -p $OUT
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --nvtx --nvtx-include "bench_timed/" --csv --log-file $OUT/launches_$TAG.csv \
-    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $OUT/launches_$TAG.log 2>&1
+    python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-variants > $OUT/launches_$TAG.log 2>&1
 python tools/launch_shares.py $OUT/launches_$TAG.csv $OUT/launch_shares_$TAG.md \
     --title "Launch list $TAG: one bench step (16 garden views + batched chain rule + Adam)" \
     --note "ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none over the NVTX range of one timed bench step. Cold-cache, serialised launches: compare SHARES, not absolutes." \
@@ -32,6 +32,10 @@ ncu --set full --clock-control none --import-source on -f -o /tmp/prof_pb_$TAG -
 python tools/ncu_summary.py /tmp/prof_pb_$TAG.ncu-rep $OUT/ncu_summary_pb_$TAG.md --title "$TAG, batched a10 over 16 garden views" \
     --traffic $OUT/ncu_traffic_$TAG.json --stage 'preprocess_bwd=^k_preprocess_bwd$' >> $OUT/ncu_full_$TAG.log 2>&1
 ncu -i /tmp/prof_pb_$TAG.ncu-rep --page source --csv --print-source cuda,sass > $OUT/src_k_preprocess_bwd_$TAG.csv 2>&1
+# the blend kernels' hardware lane-ops and shared-memory wavefronts (bench.py's hw fractions)
+ncu --metrics gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second,sm__thread_inst_executed_pipe_fma_pred_on.sum,sm__thread_inst_executed_pipe_alu_pred_on.sum,sm__sass_thread_inst_executed_ops_fadd2_fmul2_ffma2_pred_on.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum \
+    --clock-control none -k regex:"k_render_fwd|render_bwd" -c 5 --csv python tools/stage_probe.py --step 2 > $OUT/ncu_hw_$TAG.csv 2>> $OUT/ncu_full_$TAG.log
+python tools/ncu_hw.py $OUT/ncu_hw_$TAG.csv $OUT/ncu_hw_$TAG.json $TAG >> $OUT/ncu_full_$TAG.log 2>&1
 for k in k_render_fwd k_render_bwd k_emit_direct; do
   ncu -i /tmp/prof_$TAG.ncu-rep --page source --csv --print-source cuda,sass -k regex:$k -s 1 -c 1 \
       > $OUT/src_${k}_$TAG.csv 2>&1
