@@ -464,22 +464,23 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
     const uint32_t incl = off + t;
     const float inv_w = 1.0f / (float)rc.y;
     const uint32_t end = min(b, __shfl_sync(0xffffffffu, incl, 31));
-    // item kk -> (owning lane g of the window, tile, Gaussian)
-    auto locate = [&](uint32_t kk, int& g, uint32_t& tile, uint32_t& g_id) {
-      int l = 0, h = 31;  // smallest lane g with incl_g > kk
-#pragma unroll
-      for (int it = 0; it < 5; ++it) {
-        const int mid = (l + h) >> 1;
-        const uint32_t v = __shfl_sync(0xffffffffu, incl, mid);
-        if (v > kk) h = mid; else l = mid + 1;
-      }
-      g = l;
+    // item kb + lane -> (owning lane g of the window, tile, Gaussian): the owner of item kb + j
+    // is the owner of item kb - 1 plus the ranks of the window starting in [kb, kb + j] (one
+    // OR-reduction of their start bits; the 5-step shuffle search it replaces was a quarter
+    // of the kernel's instructions)
+    const uint32_t le = lanemask_lt() | (1u << lane);
+    int g_prev = __shfl_sync(0xffffffffu, off, 0) == pos ? -1 : 0;  // owner of item pos - 1
+    auto locate = [&](uint32_t kb, int& g, uint32_t& tile, uint32_t& g_id) {
+      const uint32_t rel = off - kb;
+      const uint32_t heads = __reduce_or_sync(0xffffffffu, (t && rel < 32u) ? 1u << rel : 0u);
+      g = g_prev + __popc(heads & le);
+      g_prev += __popc(heads);
       const uint32_t g_off = __shfl_sync(0xffffffffu, off, g);
       const uint32_t g_xy = __shfl_sync(0xffffffffu, rc.x, g);
       const uint32_t g_w = __shfl_sync(0xffffffffu, rc.y, g);
       const float g_iw = __shfl_sync(0xffffffffu, inv_w, g);
       g_id = __shfl_sync(0xffffffffu, gid, g);
-      const uint32_t local = kk - g_off;
+      const uint32_t local = kb + (uint32_t)lane - g_off;
       // exact row split: see k_emit_ranked
       const uint32_t rowi = (uint32_t)(((float)local + 0.5f) * g_iw);
       tile = ((g_xy >> 16) + rowi) * (uint32_t)tiles_x + (g_xy & 0xffffu) + (local - rowi * g_w);
@@ -525,8 +526,8 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
       const bool v0 = k0 < end, v1 = k1 < end;
       int g0, g1;
       uint32_t t0, t1, id0, id1;
-      locate(v0 ? k0 : end - 1, g0, t0, id0);
-      locate(v1 ? k1 : end - 1, g1, t1, id1);
+      locate(kb, g0, t0, id0);
+      locate(kb + 32, g1, t1, id1);
       commit(v0, g0, t0, id0);
       if (__any_sync(0xffffffffu, v1)) commit(v1, g1, t1, id1);
     }
