@@ -195,6 +195,13 @@ __device__ __forceinline__ float fast_exp(float x) {
   return y;
 }
 
+// MUFU.RCP alone (rcp.approx: ~1 ulp; __fdividef(1, x) adds a multiply by the numerator)
+__device__ __forceinline__ float fast_rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // The parity mode's exponential (BGS_DEBUG_PARITY_EXP; R23): a fixed expression tree that
 // the oracle evaluates identically (oracle/bgs_oracle.cpp, canon_exp), so alpha -- and every
 // blend decision -- is bit-identical on both sides: 2^x with x = power * log2(e) (one float

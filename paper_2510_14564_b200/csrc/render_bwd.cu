@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
             const float2 om2 = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al2.x, -al2.y));
             // MUFU reciprocal (1 - alpha >= 0.01): ~2^-22 relative per step, far inside the
             // 1e-3 gradient tolerance, instead of the multi-instruction IEEE division
-            const float2 io2 = make_float2(__fdividef(1.0f, om2.x), __fdividef(1.0f, om2.y));
+            const float2 io2 = make_float2(fast_rcp(om2.x), fast_rcp(om2.y));
             T2 = __fmul2_rn(T2, io2);  // transmittance in front of this Gaussian
             const float2 w2 = __fmul2_rn(al2, T2);
             const float2 p6 = __fmul2_rn(w2, dLr2), p7 = __fmul2_rn(w2, dLg2), p8 = __fmul2_rn(w2, dLb2);
