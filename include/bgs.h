@@ -227,6 +227,22 @@ bgs_status bgs_adam_step_range(float* theta, float* grad, float* exp_avg, float*
                                int64_t begin, int64_t count, const bgs_adam_hparams* hp /*host*/, int64_t step,
                                void* stream);
 
+/* SURVEY.md §8(e) 3, the exchange fused with Adam over NVSwitch multicast (NVLink SHARP):
+ * theta_mc / grad_mc are multicast addresses (CUDA driver cuMulticastCreate / BindMem /
+ * MemMap; the caller owns the objects) of every rank's theta[59n] and grad[59n]; theta is
+ * this rank's replica.  For the theta elements [begin, begin + count) of this rank's shard:
+ * g = the sum of all ranks' grad (one multimem.ld_reduce per 4 elements, reduced in the
+ * switch), Adam with the shard's exp_avg / exp_avg_sq [count] (as bgs_adam_step_range), the
+ * new theta stored to every rank's replica (multimem.st) and every rank's grad over the
+ * shard zeroed (multimem.st) -- reduce-scatter + Adam + all-gather in one pass.  The caller
+ * orders it between device-wide barriers across the ranks (every grad complete before,
+ * every store visible after).  begin and count multiples of 4 (elements past 59n are not
+ * touched), pointers 16-byte aligned, else BGS_ERR_INVALID.  One rank's call updates only
+ * its shard; all ranks' calls together update every replica. */
+bgs_status bgs_adam_step_multimem(float* theta, float* theta_mc, float* grad_mc, float* exp_avg, float* exp_avg_sq,
+                                  int64_t n, int64_t begin, int64_t count, const bgs_adam_hparams* hp /*host*/,
+                                  int64_t step, void* stream);
+
 /* Zero `count` floats at device pointer p (cudaMemsetAsync on `stream`): resets a gradient
  * buffer whose shard bgs_adam_step_range consumed after a reduce-scatter (the rest of the
  * buffer still holds this rank's partial sums).  BGS_ERR_INVALID on p = NULL with count > 0. */

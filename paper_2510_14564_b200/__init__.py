@@ -115,6 +115,8 @@ _SIGS = {
     "bgs_adam_step": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(AdamHParams), C.c_int64, _P]),
     "bgs_adam_step_range": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.POINTER(AdamHParams),
                                       C.c_int64, _P]),
+    "bgs_adam_step_multimem": (C.c_int, [_P, _P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.POINTER(AdamHParams),
+                                         C.c_int64, _P]),
     "bgs_zero": (C.c_int, [_P, C.c_int64, _P]),
     "bgs_loss_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),
     "bgs_l1_dssim_loss_grad": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_float, C.c_float, _P, _P, _P, C.c_size_t,
@@ -279,6 +281,15 @@ def bgs_adam_step_range(theta, grad, exp_avg, exp_avg_sq, n, begin, count, hp: A
                         stream=None):
     _check(_lib.bgs_adam_step_range(_ptr(theta), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), n, begin, count,
                                     C.byref(hp), step, _stream(stream)), "bgs_adam_step_range")
+
+
+def bgs_adam_step_multimem(theta, theta_mc_ptr: int, grad_mc_ptr: int, exp_avg, exp_avg_sq, n, begin, count,
+                           hp: AdamHParams, step: int, stream=None):
+    """the exchange fused with Adam over NVSwitch multicast addresses
+    (theta_mc_ptr / grad_mc_ptr: raw device addresses of the caller's multicast mappings)."""
+    _check(_lib.bgs_adam_step_multimem(_ptr(theta), C.c_void_p(theta_mc_ptr), C.c_void_p(grad_mc_ptr), _ptr(exp_avg),
+                                       _ptr(exp_avg_sq), n, begin, count, C.byref(hp), step, _stream(stream)),
+           "bgs_adam_step_multimem")
 
 
 def bgs_zero(t, stream=None):

@@ -118,6 +118,76 @@ bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n,
   return BGS_OK;
 }
 
+// ---------------------------------------------------------------- fused exchange + Adam (§8(e) 3)
+// NVSwitch multicast: grad_mc / theta_mc are multicast addresses of every rank's grad and
+// theta (one NVLink-SHARP object each).  Per 4 elements of this rank's shard: the sum of
+// all ranks' gradients in one in-switch reduction load (multimem.ld_reduce), the Adam
+// update with the shard's moments, the new theta stored to every rank's replica in one
+// multicast store (multimem.st), and the shard of every rank's grad zeroed the same way --
+// reduce-scatter, Adam and all-gather in a single pass over the shard.
+__device__ __forceinline__ float4 mm_ld_reduce_add(const float* mc) {
+  float4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(mc)
+               : "memory");
+  return r;
+}
+__device__ __forceinline__ void mm_st(float* mc, float4 v) {
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc), "f"(v.x), "f"(v.y),
+               "f"(v.z), "f"(v.w)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_adam_multimem(AdamParams p, float* grad_mc, float* theta_mc) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.total4; i += stride) {
+    const int64_t e = p.base + 4 * i;
+    float4 g = mm_ld_reduce_add(grad_mc + e);
+    float4 th = p.theta[i], m = p.m[i], v = p.v[i];
+    adam_one(th.x, g.x, m.x, v.x, p.step_size[adam_group(e, p.n)], p);
+    adam_one(th.y, g.y, m.y, v.y, p.step_size[adam_group(e + 1, p.n)], p);
+    adam_one(th.z, g.z, m.z, v.z, p.step_size[adam_group(e + 2, p.n)], p);
+    adam_one(th.w, g.w, m.w, v.w, p.step_size[adam_group(e + 3, p.n)], p);
+    mm_st(theta_mc + e, th);
+    mm_st(grad_mc + e, z4);
+    p.m[i] = m;
+    p.v[i] = v;
+  }
+}
+
+bgs_status launch_adam_multimem(float* theta, float* theta_mc, float* grad_mc, float* m, float* v, int64_t n,
+                                int64_t begin, int64_t count, const bgs_adam_hparams* hp, int64_t step,
+                                cudaStream_t s) {
+  const int64_t total = std::max<int64_t>(0, std::min<int64_t>(count, 59 * n - begin));
+  if (total == 0) return BGS_OK;
+  AdamParams p;
+  p.theta = (float4*)(theta + begin);  // this rank's replica, read; the new values go out by multicast
+  p.grad = nullptr;
+  p.m = (float4*)m;
+  p.v = (float4*)v;
+  p.n = n;
+  p.base = begin;
+  p.total4 = total / 4;
+  const float lr[6] = {hp->lr_means, hp->lr_log_scales, hp->lr_quats, hp->lr_opacity, hp->lr_sh_dc, hp->lr_sh_rest};
+  const double bc1 = 1.0 - pow((double)hp->beta1, (double)step);
+  const double bc2 = 1.0 - pow((double)hp->beta2, (double)step);
+  for (int k = 0; k < 6; ++k) {
+    p.lr[k] = lr[k];
+    p.step_size[k] = (float)((double)lr[k] / bc1);
+  }
+  p.b1 = hp->beta1;
+  p.b2 = hp->beta2;
+  p.eps = hp->eps;
+  p.inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+  const int64_t work = p.total4 > 0 ? p.total4 : 1;
+  const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)num_sms() * 8);
+  k_adam_multimem<<<blocks, 256, 0, s>>>(p, grad_mc, theta_mc);
+  note_launch();
+  return check_launch("k_adam_multimem");
+}
+
 // ---------------------------------------------------------------- K15 L1 loss gradient
 __global__ void __launch_bounds__(256) k_l1(const float* __restrict__ image, const uint8_t* __restrict__ target,
                                             int64_t count, float scale, float* __restrict__ dl, float* loss_sum) {

@@ -184,6 +184,9 @@ bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t
                               uint32_t* rank_h = nullptr);
 bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, bool publish_k, cudaStream_t s);
 bgs_status launch_rowsplit(Frame* F, cudaStream_t s);
+bgs_status launch_adam_multimem(float* theta, float* theta_mc, float* grad_mc, float* m, float* v, int64_t n,
+                                int64_t begin, int64_t count, const bgs_adam_hparams* hp, int64_t step,
+                                cudaStream_t s);
 bgs_status launch_tile_scan(Frame* F, cudaStream_t s);
 
 // ---------------------------------------------------------------- device helpers

@@ -431,6 +431,21 @@ bgs_status bgs_adam_step_range(float* theta, float* grad, float* exp_avg, float*
   return launch_adam(theta, grad, exp_avg, exp_avg_sq, n, begin, count, hp, step, (cudaStream_t)stream);
 }
 
+bgs_status bgs_adam_step_multimem(float* theta, float* theta_mc, float* grad_mc, float* exp_avg, float* exp_avg_sq,
+                                  int64_t n, int64_t begin, int64_t count, const bgs_adam_hparams* hp,
+                                  int64_t step, void* stream) {
+  if (n < 0 || begin < 0 || count < 0 || (begin & 3) || (count & 3) || !hp || step < 1) return BGS_ERR_INVALID;
+  if (n == 0 || count == 0 || begin >= 59 * n) return BGS_OK;
+  if (!theta || !theta_mc || !grad_mc || !exp_avg || !exp_avg_sq) return BGS_ERR_INVALID;
+  if (!aligned16(theta) || !aligned16(theta_mc) || !aligned16(grad_mc) || !aligned16(exp_avg) ||
+      !aligned16(exp_avg_sq) || ((59 * n - begin) < count && ((59 * n - begin) & 3)))
+    return BGS_ERR_INVALID;
+  if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f && hp->beta2 >= 0.0f && hp->beta2 < 1.0f && hp->eps >= 0.0f))
+    return BGS_ERR_INVALID;
+  return launch_adam_multimem(theta, theta_mc, grad_mc, exp_avg, exp_avg_sq, n, begin, count, hp, step,
+                              (cudaStream_t)stream);
+}
+
 bgs_status bgs_zero(float* p, int64_t count, void* stream) {
   if (count < 0 || (count > 0 && !p)) return BGS_ERR_INVALID;
   if (count == 0) return BGS_OK;
