@@ -5,7 +5,9 @@
 // C2 = 0.03^2 (Wang et al. 2004, the quality metric of PAPER.md §VI-A l.394; window per
 // SPEC.md l.171; readings R28-R30 in DESIGN.md §3).
 //
-// k_ssim_fwd: per (32x16 tile, channel): x and y = target/255 with a 5-pixel halo staged in
+// The 11-tap passes run two maps at once where they pair ({x, y}, {x^2, y^2}; {dS/dm, dS/dE})
+// as paired FP32 (FFMA2): the same rounding per map, half the instructions.
+// k_ssim_fwd: per (32x32 tile, channel): x and y = target/255 with a 5-pixel halo staged in
 // shared memory, the five window moments {w*x, w*y, w*x^2, w*y^2, w*xy} by a separable
 // 11-tap pass (rows, then columns), then per pixel SSIM, |x - y| and the three partials of
 // SSIM w.r.t. the raw moments (dS/dm, dS/dE, dS/dP) written to the workspace; each block
@@ -45,11 +47,24 @@ __device__ __forceinline__ void win4(const LossWin& win, const float* v, float* 
   }
 }
 
+// the same over two maps at once (paired FP32: one FFMA2 per tap, separately rounded halves)
+__device__ __forceinline__ void win4x2(const LossWin& win, const float2* v, float2* o) {
+#pragma unroll
+  for (int j = 0; j < kLRun; ++j) {
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < kLWin; ++k) acc = __ffma2_rn(make_float2(win.w[k], win.w[k]), v[j + k], acc);
+    o[j] = acc;
+  }
+}
+
 __global__ void __launch_bounds__(kLThreads) k_ssim_fwd(const float* __restrict__ img, const uint8_t* __restrict__ tgt,
                                                         int W, int H, LossWin win, float* __restrict__ part,
                                                         float* __restrict__ acc) {
-  __shared__ float sx[kLHy][kLHx + 1], sy[kLHy][kLHx + 1];  // odd strides: conflict-free
-  __shared__ float hm[5][kLHy][kLTx + 1];
+  // x and y interleaved (the paired window passes load both with one 8-byte access)
+  __shared__ float2 s_xy[kLHy][kLHx + 1];
+  __shared__ float2 h01[kLHy][kLTx + 1], h23[kLHy][kLTx + 1];  // {w*x, w*y}, {w*x^2, w*y^2} along rows
+  __shared__ float h4[kLHy][kLTx + 1];                         // w*xy along rows
   const int ch = blockIdx.z;
   const int x0 = blockIdx.x * kLTx, y0 = blockIdx.y * kLTy;
   const size_t plane = (size_t)W * H;
@@ -63,51 +78,57 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_fwd(const float* __restrict_
       xv = xc[(size_t)gy * W + gx];
       yv = (float)yc[(size_t)gy * W + gx] * (1.0f / 255.0f);
     }
-    sx[r][c] = xv;
-    sy[r][c] = yv;
+    s_xy[r][c] = make_float2(xv, yv);
   }
   __syncthreads();
-  // rows: the 11-tap pass along x of the five moment maps, 4 outputs per thread
+  // rows: the 11-tap pass along x of the five moment maps, 4 outputs per thread; (x, y) and
+  // (x^2, y^2) as pairs
   for (int it = threadIdx.x; it < kLRowItems; it += kLThreads) {
     const int r = it / kLSegs, c0 = (it - r * kLSegs) * kLRun;
-    float v[kLRun + kLWin - 1], o[kLRun];
+    float2 v[kLRun + kLWin - 1], o[kLRun];
 #pragma unroll
-    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = sx[r][c0 + k];
-    win4(win, v, o);
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = s_xy[r][c0 + k];
+    win4x2(win, v, o);
 #pragma unroll
-    for (int j = 0; j < kLRun; ++j) hm[0][r][c0 + j] = o[j];
+    for (int j = 0; j < kLRun; ++j) h01[r][c0 + j] = o[j];
+    float u[kLRun + kLWin - 1], ou[kLRun];
 #pragma unroll
-    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = v[k] * v[k];
-    win4(win, v, o);
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) u[k] = v[k].x * v[k].y;
+    win4(win, u, ou);
 #pragma unroll
-    for (int j = 0; j < kLRun; ++j) hm[2][r][c0 + j] = o[j];
+    for (int j = 0; j < kLRun; ++j) h4[r][c0 + j] = ou[j];
 #pragma unroll
-    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = sy[r][c0 + k];
-    win4(win, v, o);
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = __fmul2_rn(v[k], v[k]);
+    win4x2(win, v, o);
 #pragma unroll
-    for (int j = 0; j < kLRun; ++j) hm[1][r][c0 + j] = o[j];
-    float u[kLRun + kLWin - 1];
-#pragma unroll
-    for (int k = 0; k < kLRun + kLWin - 1; ++k) u[k] = sx[r][c0 + k] * v[k];
-    win4(win, u, o);
-#pragma unroll
-    for (int j = 0; j < kLRun; ++j) hm[4][r][c0 + j] = o[j];
-#pragma unroll
-    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = v[k] * v[k];
-    win4(win, v, o);
-#pragma unroll
-    for (int j = 0; j < kLRun; ++j) hm[3][r][c0 + j] = o[j];
+    for (int j = 0; j < kLRun; ++j) h23[r][c0 + j] = o[j];
   }
   __syncthreads();
   // columns (4 consecutive rows of one column per thread), then per pixel SSIM and partials
   const int c = threadIdx.x % kLTx, r0 = (threadIdx.x / kLTx) * kLRun;
   float m[5][kLRun];
+  {
+    float2 v[kLRun + kLWin - 1], o[kLRun];
 #pragma unroll
-  for (int q = 0; q < 5; ++q) {
-    float v[kLRun + kLWin - 1];
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = h01[r0 + k][c];
+    win4x2(win, v, o);
 #pragma unroll
-    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = hm[q][r0 + k][c];
-    win4(win, v, m[q]);
+    for (int j = 0; j < kLRun; ++j) {
+      m[0][j] = o[j].x;
+      m[1][j] = o[j].y;
+    }
+#pragma unroll
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = h23[r0 + k][c];
+    win4x2(win, v, o);
+#pragma unroll
+    for (int j = 0; j < kLRun; ++j) {
+      m[2][j] = o[j].x;
+      m[3][j] = o[j].y;
+    }
+    float u[kLRun + kLWin - 1];
+#pragma unroll
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) u[k] = h4[r0 + k][c];
+    win4(win, u, m[4]);
   }
   float s_sum = 0.f, l1_sum = 0.f;
   const int gx = x0 + c;
@@ -131,7 +152,8 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_fwd(const float* __restrict_
     part[(1 * 3 + ch) * plane + p] = d_e;
     part[(2 * 3 + ch) * plane + p] = d_p;
     s_sum += s;
-    l1_sum += fabsf(sx[r0 + j + kLR][c + kLR] - sy[r0 + j + kLR][c + kLR]);
+    const float2 q = s_xy[r0 + j + kLR][c + kLR];
+    l1_sum += fabsf(q.x - q.y);
   }
   // block sums -> this block's slot of the partial-sum array (no same-address atomics)
   __shared__ float s_red[2][kLThreads / 32];
@@ -157,8 +179,11 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_bwd(const float* __restrict_
                                                         int W, int H, LossWin win, const float* __restrict__ part,
                                                         float lam, float scale, float* __restrict__ dl,
                                                         const float* __restrict__ acc, float* loss_sum) {
-  __shared__ float sg[3][kLHy][kLHx + 1];
-  __shared__ float hg[3][kLHy][kLTx + 1];
+  // the partial maps dS/dm, dS/dE (paired) and dS/dP
+  __shared__ float2 sg01[kLHy][kLHx + 1];
+  __shared__ float sg2[kLHy][kLHx + 1];
+  __shared__ float2 hg01[kLHy][kLTx + 1];
+  __shared__ float hg2[kLHy][kLTx + 1];
   const int ch = blockIdx.z;
   const int x0 = blockIdx.x * kLTx, y0 = blockIdx.y * kLTy;
   const size_t plane = (size_t)W * H;
@@ -196,31 +221,43 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_bwd(const float* __restrict_
     const int gx = x0 + c - kLR, gy = y0 + r - kLR;
     const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
     const size_t p = (size_t)gy * W + gx;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) sg[q][r][c] = in ? part[(q * 3 + ch) * plane + p] : 0.f;
+    sg01[r][c] = in ? make_float2(part[(0 * 3 + ch) * plane + p], part[(1 * 3 + ch) * plane + p])
+                    : make_float2(0.f, 0.f);
+    sg2[r][c] = in ? part[(2 * 3 + ch) * plane + p] : 0.f;
   }
   __syncthreads();
   for (int it = threadIdx.x; it < kLRowItems; it += kLThreads) {
     const int r = it / kLSegs, c0 = (it - r * kLSegs) * kLRun;
+    float2 v2[kLRun + kLWin - 1], o2[kLRun];
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
-      float v[kLRun + kLWin - 1], o[kLRun];
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v2[k] = sg01[r][c0 + k];
+    win4x2(win, v2, o2);
 #pragma unroll
-      for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = sg[q][r][c0 + k];
-      win4(win, v, o);
+    for (int j = 0; j < kLRun; ++j) hg01[r][c0 + j] = o2[j];
+    float v[kLRun + kLWin - 1], o[kLRun];
 #pragma unroll
-      for (int j = 0; j < kLRun; ++j) hg[q][r][c0 + j] = o[j];
-    }
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = sg2[r][c0 + k];
+    win4(win, v, o);
+#pragma unroll
+    for (int j = 0; j < kLRun; ++j) hg2[r][c0 + j] = o[j];
   }
   __syncthreads();
   const int c = threadIdx.x % kLTx, r0 = (threadIdx.x / kLTx) * kLRun;
   float m[3][kLRun];
+  {
+    float2 v2[kLRun + kLWin - 1], o2[kLRun];
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v2[k] = hg01[r0 + k][c];
+    win4x2(win, v2, o2);
+#pragma unroll
+    for (int j = 0; j < kLRun; ++j) {
+      m[0][j] = o2[j].x;
+      m[1][j] = o2[j].y;
+    }
     float v[kLRun + kLWin - 1];
 #pragma unroll
-    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = hg[q][r0 + k][c];
-    win4(win, v, m[q]);
+    for (int k = 0; k < kLRun + kLWin - 1; ++k) v[k] = hg2[r0 + k][c];
+    win4(win, v, m[2]);
   }
   const float inv_n = (float)(1.0 / n);
   const int gx = x0 + c;
