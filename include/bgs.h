@@ -425,6 +425,10 @@ bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contri
  * oracle also uses (instead of MUFU.EX2) and the forward does not split walks, so every
  * blend decision, n_contrib and the image are bit-identical to the oracle's. */
 #define BGS_DEBUG_PARITY_EXP 64
+/* R10 / R11: 3DGS's square tile rect of half-width radius = ceil(3 sqrt(lambda_1)) instead of
+ * the default R11' rect (the tiles the alpha >= 1/255 box reaches): the 3DGS key
+ * set, longer lists, and images that cut opaque Gaussians at 3 sigma. */
+#define BGS_DEBUG_SQUARE_RECT 128
 bgs_status bgs_frame_set_debug(bgs_frame* f /*host*/, int32_t flags);
 
 /* Scheduling parameter of the blend kernels (default 4096): a (tile, 8x4 pixel block) work

@@ -25,6 +25,7 @@ NO_LOWPASS, NO_JCLAMP, FULL_RECT = 1, 2, 4
 NO_ALPHA_CLAMP, NO_ALPHA_CUTOFF, NO_EARLY_STOP, NO_POWER_GUARD = 8, 16, 32, 64
 PLAIN = 127
 CANON_EXP = 128  # R23 parity mode: the canonical exponential the GPU's parity mode also uses
+SQUARE_RECT = 256  # R10/R11: 3DGS's square rect of half-width radius instead of R11' (the alpha box)
 # clamp bits
 CB_R, CB_G, CB_B, CB_JX, CB_JX_NEG, CB_JY, CB_JY_NEG = 1, 2, 4, 8, 16, 32, 64
 

@@ -14,7 +14,8 @@
 //   O5  Sigma' = J W Sigma W^T J^T (+0.3 I)                             (R7, R8)
 //   O6  det, conic = Sigma'^-1                                          (R9)
 //   O7  radius = ceil(3 sqrt(lambda_1))                                 (R10)
-//   O8  16x16 tile rect                                                 (R11)
+//   O8  16x16 tile rect: the tiles the alpha >= 1/255 level set's
+//       conservative box reaches (R11'; R10's square rect: SQUARE_RECT)  (R11)
 //   O9  SH degree <= 3 colour                                           (R12)
 //   O10 offsets = exclusive scan of tiles_touched                       (R13)
 //   O11 (tile | depth) keys, O12 std::stable_sort, O13 tile ranges      (R13)
@@ -62,6 +63,7 @@ enum : uint32_t {
   ORC_NO_EARLY_STOP = 32u,   // R15
   ORC_NO_POWER_GUARD = 64u,  // R14 skip power > 0
   ORC_CANON_EXP = 128u,      // R23 parity mode: G from canon_exp instead of std::exp
+  ORC_SQUARE_RECT = 256u,    // R10/R11: 3DGS's square rect of half-width radius (else R11')
 };
 
 // R23's optional parity mode: a canonical exponential both sides evaluate
@@ -217,7 +219,6 @@ PreF preprocess_one(const Theta& th, int64_t i, int deg, const orc_camera& cam, 
   // O1: activations (R5): transcendentals in double, rounded once
   float s[3];
   for (int k = 0; k < 3; ++k) s[k] = (float)std::exp((double)th.lscale(i)[k]);
-  const float o = (float)(1.0 / (1.0 + std::exp(-(double)th.ologit(i))));
   float qw = th.quat(i)[0], qx = th.quat(i)[1], qy = th.quat(i)[2], qz = th.quat(i)[3];
   const float n2 = std::fma(qw, qw, std::fma(qx, qx, std::fma(qy, qy, qz * qz)));
   const float inv = 1.0f / std::sqrt(n2);
@@ -273,17 +274,36 @@ PreF preprocess_one(const Theta& th, int64_t i, int deg, const orc_camera& cam, 
   const float mid = 0.5f * (ca + cc);
   const float lam = mid + std::sqrt(std::fmax(0.1f, mid * mid - det));
   const int32_t rad = (int32_t)std::ceil(3.0f * std::sqrt(lam));
-  // O8: tile rect (R11)
+  // O1 (opacity): o = sigmoid(ol), the transcendental in double, rounded once (R5)
+  const float o = (float)(1.0 / (1.0 + std::exp(-(double)th.ologit(i))));
+  // O8: tile rect (R11').  A pixel d away from the centre blends the Gaussian only if
+  // o exp(-d^T conic d / 2) >= 1/255 (R14), i.e. d^T Sigma'^-1 d <= 2 tau, tau = ln(255 o):
+  // inside the ellipse whose bounding box has half-widths sqrt(2 tau a), sqrt(2 tau c).  The
+  // extents e carry margins (tau + 1e-3, x 1.001, + 1e-3 px) for the float error of the
+  // blend's own power and alpha, so every pixel outside the box takes alpha < 1/255; the rect
+  // is the 16x16 tiles the box reaches (floor then clamp, as R11).  Tiles outside it never
+  // blend the Gaussian: the images, final T and every decision are R10's; the lists are
+  // shorter, so n_contrib (a list position, R16) is counted in them.  tau in double, rounded
+  // once (R5); a Gaussian with tau <= 0 (o < 1/255) blends nowhere and is culled.
   const int tiles_x = (cam.width + TILE - 1) / TILE, tiles_y = (cam.height + TILE - 1) / TILE;
   int32_t rect[4];
+  auto clampt = [](float f, int hi) { return (int32_t)std::fmin((float)hi, std::fmax(0.0f, f)); };
   if (mode & ORC_FULL_RECT) {
     rect[0] = 0; rect[1] = 0; rect[2] = tiles_x; rect[3] = tiles_y;
-  } else {
-    auto clampt = [](float f, int hi) { return (int32_t)std::fmin((float)hi, std::fmax(0.0f, f)); };
+  } else if ((mode & ORC_SQUARE_RECT) || (mode & ORC_NO_ALPHA_CUTOFF)) {  // R10 / R11
     rect[0] = clampt(std::floor((px - (float)rad) * 0.0625f), tiles_x);
     rect[1] = clampt(std::floor((py - (float)rad) * 0.0625f), tiles_y);
     rect[2] = clampt(std::floor((px + (float)(rad + 15)) * 0.0625f), tiles_x);
     rect[3] = clampt(std::floor((py + (float)(rad + 15)) * 0.0625f), tiles_y);
+  } else {
+    const float tau = (float)std::log((double)(255.0f * o)) + 1e-3f;
+    if (!(tau > 0.0f)) return p;
+    const float ex = std::sqrt(2.0f * tau * ca) * 1.001f + 1e-3f;
+    const float ey = std::sqrt(2.0f * tau * cc) * 1.001f + 1e-3f;
+    rect[0] = clampt(std::floor((px - ex) * 0.0625f), tiles_x);
+    rect[1] = clampt(std::floor((py - ey) * 0.0625f), tiles_y);
+    rect[2] = clampt(std::floor((px + ex) * 0.0625f) + 1.0f, tiles_x);
+    rect[3] = clampt(std::floor((py + ey) * 0.0625f) + 1.0f, tiles_y);
   }
   if ((int64_t)(rect[2] - rect[0]) * (rect[3] - rect[1]) == 0) return p;
   // O9: SH colour (R12) -- free evaluation order (float)

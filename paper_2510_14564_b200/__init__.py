@@ -28,6 +28,7 @@ BGS_DEBUG_SORT_RADIX_SPLIT = 4
 BGS_DEBUG_BWD_8X4 = 8
 BGS_DEBUG_SORT_ROWSPLIT = 16
 BGS_DEBUG_PARITY_EXP = 64
+BGS_DEBUG_SQUARE_RECT = 128
 
 
 class BgsError(RuntimeError):

@@ -35,6 +35,7 @@ struct PreView {
   float4* grad2d;
   uint8_t* cbits;
   const uint8_t* keep;      // NEXT-4 keep mask or null
+  int32_t square;           // R10 / R11's square rect instead of R11' (BGS_DEBUG_SQUARE_RECT)
 };
 
 // Up to kPreMaxViews views per launch: theta is read once per Gaussian for all of them
@@ -138,12 +139,36 @@ __device__ __forceinline__ uint32_t project_view(const PreView& pv, int64_t i, f
   const float mid = 0.5f * (a + cc);
   const float lam = mid + __fsqrt_rn(fmaxf(0.1f, mid * mid - det));
   const int rad = (int)ceilf(3.0f * __fsqrt_rn(lam));
-  // rect, floor then clamp (R11); culled if empty
+  // Conservative half-extents of the alpha >= 1/255 level set, d^T conic d <= 2 ln(255 o)
+  // (R14): AABB half-widths sqrt(2 tau a), sqrt(2 tau c) with tau = ln(255 o) raised by 1e-3
+  // (the threshold lowered by e^-1e-3) and a 1e-3 relative + 1e-3 px margin, so every pixel
+  // outside it gets alpha < 1/255 in the blend's own float arithmetic (its G error is ~2^-20
+  // relative).  The tile rect (R11') and the blend kernels' per-block skips use it; it never
+  // changes a blend decision.
+  float ex = -1e30f, ey = -1e30f;
+  if (tau > 0.0f) {
+    ex = __fsqrt_rn(2.0f * tau * a) * 1.001f + 1e-3f;
+    ey = __fsqrt_rn(2.0f * tau * cc) * 1.001f + 1e-3f;
+  }
+  // rect, floor then clamp; culled if empty.  R11' (default): the tiles the alpha box
+  // reaches -- every tile with a pixel that can blend the Gaussian, no other (a Gaussian with
+  // o < 1/255 blends nowhere).  R10 / R11 (BGS_DEBUG_SQUARE_RECT): 3DGS's square of half-width
+  // radius, which also holds tiles no pixel of which blends it and cuts the alpha set of an
+  // opaque Gaussian (sqrt(2 ln 255) = 3.33 sigma > 3 sigma).
   const float tx = (float)c.tiles_x, ty = (float)c.tiles_y;
-  const int rx0 = (int)fminf(tx, fmaxf(0.0f, floorf((px - (float)rad) * 0.0625f)));
-  const int ry0 = (int)fminf(ty, fmaxf(0.0f, floorf((py - (float)rad) * 0.0625f)));
-  const int rx1 = (int)fminf(tx, fmaxf(0.0f, floorf((px + (float)(rad + 15)) * 0.0625f)));
-  const int ry1 = (int)fminf(ty, fmaxf(0.0f, floorf((py + (float)(rad + 15)) * 0.0625f)));
+  int rx0, ry0, rx1, ry1;
+  if (pv.square) {
+    rx0 = (int)fminf(tx, fmaxf(0.0f, floorf((px - (float)rad) * 0.0625f)));
+    ry0 = (int)fminf(ty, fmaxf(0.0f, floorf((py - (float)rad) * 0.0625f)));
+    rx1 = (int)fminf(tx, fmaxf(0.0f, floorf((px + (float)(rad + 15)) * 0.0625f)));
+    ry1 = (int)fminf(ty, fmaxf(0.0f, floorf((py + (float)(rad + 15)) * 0.0625f)));
+  } else {
+    if (!(tau > 0.0f)) return 0xffffffffu;
+    rx0 = (int)fminf(tx, fmaxf(0.0f, floorf((px - ex) * 0.0625f)));
+    ry0 = (int)fminf(ty, fmaxf(0.0f, floorf((py - ey) * 0.0625f)));
+    rx1 = (int)fminf(tx, fmaxf(0.0f, floorf((px + ex) * 0.0625f) + 1.0f));
+    ry1 = (int)fminf(ty, fmaxf(0.0f, floorf((py + ey) * 0.0625f) + 1.0f));
+  }
   const uint32_t area = (uint32_t)(rx1 - rx0) * (uint32_t)(ry1 - ry0);
   if (area == 0) return 0xffffffffu;
   pv.radius[i] = rad;
@@ -152,17 +177,6 @@ __device__ __forceinline__ uint32_t project_view(const PreView& pv, int64_t i, f
   pv.rect[i] = make_uint2((uint32_t)rx0 | ((uint32_t)ry0 << 16), (uint32_t)(rx1 - rx0) | ((uint32_t)(ry1 - ry0) << 16));
   float4* rec = pv.record + 3 * i;
   rec[1] = make_float4(-0.5f * conx, -cony, -0.5f * conz, g.o);
-  // Conservative half-extents of the alpha >= 1/255 level set, d^T conic d <= 2 ln(255 o)
-  // (R14): AABB half-widths sqrt(2 tau a), sqrt(2 tau c) with tau = ln(255 o) raised by 1e-3
-  // (the threshold lowered by e^-1e-3) and a 1e-3 relative + 1e-3 px margin, so every pixel
-  // outside it gets alpha < 1/255 in the blend's own float arithmetic (its G error is ~2^-20
-  // relative).  The blend kernels use it to skip entries per warp block; it never changes a
-  // decision.
-  float ex = -1e30f, ey = -1e30f;
-  if (tau > 0.0f) {
-    ex = sqrtf(2.0f * tau * a) * 1.001f + 1e-3f;
-    ey = sqrtf(2.0f * tau * cc) * 1.001f + 1e-3f;
-  }
   rec[0] = make_float4(px, py, ex, ey);  // everything the per-warp cull test reads
   // this view's blend-gradient accumulator (render_bwd REDs into it)
   float4* g2 = pv.grad2d + 3 * i;
@@ -258,7 +272,7 @@ __global__ void __launch_bounds__(256, 4) k_preprocess(const __grid_constant__ P
   if (t2 <= pv.cam.near_plane) return;  // near cull (R3)
   if (pv.keep && !pv.keep[i]) return;   // NEXT-4: dropped by the importance keep rule (R40)
   const Sigma3 g = sigma3(p, i);
-  const float tau = logf(255.0f * g.o) + 1e-3f;
+  const float tau = (float)log((double)(255.0f * g.o)) + 1e-3f;  // double, rounded once (R5)
   const uint32_t cb = project_view(pv, i, mx, my, mz, t0, t1, t2, g, tau);
   if (cb == 0xffffffffu) return;
   float sh[48];
@@ -280,7 +294,7 @@ __global__ void __launch_bounds__(256, 2) k_preprocess_views(const __grid_consta
   // every theta load is issued up front (one DRAM round trip instead of three dependent
   // ones): across a batch of views almost every Gaussian is visible in some view
   const Sigma3 g = sigma3(p, i);
-  const float tau = logf(255.0f * g.o) + 1e-3f;
+  const float tau = (float)log((double)(255.0f * g.o)) + 1e-3f;  // double, rounded once (R5)
   float sh[48];
   load_sh(p, i, sh);
 #pragma unroll 1
@@ -453,6 +467,7 @@ bgs_status launch_preprocess_batch(const bgs_gaussians* g, Frame* const* F, int 
       pv.grad2d = f->grad2d;
       pv.cbits = f->cbits;
       pv.keep = f->keep;
+      pv.square = (f->debug_flags & BGS_DEBUG_SQUARE_RECT) ? 1 : 0;
     }
     if (p.nviews == 1)
       k_preprocess<<<(unsigned)blocks, 256, 0, s>>>(p);

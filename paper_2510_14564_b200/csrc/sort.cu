@@ -35,8 +35,7 @@ constexpr int kSmemTiles = 8192;  // tile counts kept in shared memory up to thi
 // shuffle binary search over the inclusive scan, so a 4000-tile background Gaussian does
 // not serialise one thread and the 32 writes of a round are consecutive.
 template <bool kByRank>
-__global__ void __launch_bounds__(kDupThreads) k_emit(int64_t n, const float4* __restrict__ record,
-                                                      const int32_t* __restrict__ radius,
+__global__ void __launch_bounds__(kDupThreads) k_emit(int64_t n, const uint2* __restrict__ rect,
                                                       const float* __restrict__ depth,
                                                       const uint32_t* __restrict__ offsets,  // index or rank order
                                                       const uint32_t* __restrict__ sigma,    // rank -> Gaussian
@@ -55,7 +54,6 @@ __global__ void __launch_bounds__(kDupThreads) k_emit(int64_t n, const float4* _
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int warps = kDupThreads / 32;
-  const float ftx = (float)tiles_x, fty = (float)tiles_y;
   for (int64_t base = ((int64_t)blockIdx.x * warps + warp) * 32; base < n; base += (int64_t)gridDim.x * warps * 32) {
     const int64_t r = base + lane;
     uint32_t t = 0, off = 0, dbits = 0, gid = 0;
@@ -65,13 +63,11 @@ __global__ void __launch_bounds__(kDupThreads) k_emit(int64_t n, const float4* _
       off = offsets[r];
       t = tiles_touched[gid];
       if (t) {
-        const float4 r0 = record[3 * gid];
-        const int rad = radius[gid];
-        // the preprocess's canonical rect expression (R11)
-        rx0 = (int)fminf(ftx, fmaxf(0.0f, floorf((r0.x - (float)rad) * 0.0625f)));
-        ry0 = (int)fminf(fty, fmaxf(0.0f, floorf((r0.y - (float)rad) * 0.0625f)));
-        const int rx1 = (int)fminf(ftx, fmaxf(0.0f, floorf((r0.x + (float)(rad + 15)) * 0.0625f)));
-        w = rx1 - rx0;
+        // the preprocess's rect (R11' or R11), packed {x0 | y0 << 16, w | h << 16}
+        const uint2 q = rect[gid];
+        rx0 = (int)(q.x & 0xffffu);
+        ry0 = (int)(q.x >> 16);
+        w = (int)(q.y & 0xffffu);
         if (!kByRank) {
           dbits = __float_as_uint(depth[gid]);
 #pragma unroll
@@ -609,7 +605,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
   bgs_status st;
   if (ref64) {
     if ((st = launch_scan(F->tiles_touched, F->offsets, F->n, F, true, s)) != BGS_OK) return st;  // a3, K
-    k_emit<false><<<grid, kDupThreads, 0, s>>>(F->n, F->record, F->radius, F->depth, F->offsets, nullptr,
+    k_emit<false><<<grid, kDupThreads, 0, s>>>(F->n, F->rect, F->depth, F->offsets, nullptr,
                                                F->tiles_touched, F->tiles_x, F->tiles_y, F->num_tiles, F->counters,
                                                F->keys[0], F->vals[0], F->tile_count, F->sort_hist);
     note_launch();

@@ -167,6 +167,32 @@ def test_sort_and_ranges_parity(bgs, name, path):
     assert np.array_equal(v["ranges"], ref["srt"]["ranges"])
 
 
+@pytest.mark.parametrize("name", ["tiny", "ragged", "dense", "deep"])
+def test_square_rect_mode_parity(bgs, name):
+    """BGS_DEBUG_SQUARE_RECT (R10 / R11: 3DGS's square rect) against the oracle's SQUARE_RECT
+    mode: tiles_touched, K, sorted values, ranges bit-exact; image and n_contrib on the
+    unflagged pixels; and the default R11' image equals the square one except where R10
+    cuts an opaque Gaussian beyond 3 sigma (more alpha >= 1/255 contributions, never fewer
+    blended entries per pixel)."""
+    s = scenes()[name]()
+    cam = s.cameras[0]
+    r, _, out = run_gpu(bgs, s, cam, flags=bgs.BGS_DEBUG_SQUARE_RECT)
+    ref = oracle.forward(s.theta, s.n, s.sh_degree, cam, mode=oracle.SQUARE_RECT)
+    K = ref["srt"]["K"]
+    v = views(bgs, r, s.n, K, len(ref["srt"]["ranges"]))
+    assert r.num_keys == K
+    assert np.array_equal(v["tiles_touched"], ref["pre"]["tiles_touched"])
+    assert np.array_equal(v["values_sorted"], ref["srt"]["sorted_values"])
+    assert np.array_equal(v["ranges"], ref["srt"]["ranges"])
+    ok = ref["flags"] == 0
+    img = out["image"].cpu().numpy()
+    assert np.abs(img - ref["image"])[:, ok].max() <= IMG_TOL
+    assert np.array_equal(out["n_contrib"].cpu().numpy().view(np.uint32)[ok], ref["n_contrib"][ok])
+    # the default (R11') lists are shorter
+    r2, _, _ = run_gpu(bgs, s, cam)
+    assert r2.num_keys <= K
+
+
 def test_sort_paths_identical_at_garden_scale(bgs):
     """The depth-first paths (direct tile split, row split, radix tile split) and the 64-bit
     onesweep reference

@@ -83,7 +83,8 @@ def test_opacity_and_scale_activations():
     # R5: o = sigmoid(logit)
     lg = np.array([-6.0, -1.0, 0.0, 0.5, 3.0, 9.0], np.float32)
     th, n = gaussians([[0, 0, 2.0]] * 6, ologits=lg)
-    pre = oracle.preprocess(th, n, 0, axis_camera(64, 64))
+    # R10's square rect: o < 1/255 (logit -6) blends nowhere and R11' would cull it
+    pre = oracle.preprocess(th, n, 0, axis_camera(64, 64), mode=oracle.SQUARE_RECT)
     np.testing.assert_allclose(pre["opacity"], 1 / (1 + np.exp(-lg.astype(np.float64))), rtol=1e-7)
     assert pre["opacity"][2] == 0.5
 
