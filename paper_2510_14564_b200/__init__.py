@@ -16,7 +16,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbgs.so")
+LIB_PATH = os.environ.get("BGS_LIB") or os.path.join(_HERE, "libbgs.so")  # BGS_LIB: A/B builds (tools/)
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"libbgs.so not built at {LIB_PATH}: run `python __graft_entry__.py` (build()) first")
 _lib = C.CDLL(LIB_PATH)

@@ -181,7 +181,7 @@ bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                               int shift, int64_t count, cudaStream_t s, const uint2* rect = nullptr,
                               uint32_t* rank_cnt = nullptr, uint2* rank_rect = nullptr,
-                              uint32_t* rank_h = nullptr);
+                              uint32_t* rank_h = nullptr, bool drop_culled = false, int64_t fill_to = 0);
 bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, bool publish_k, cudaStream_t s);
 bgs_status launch_rowsplit(Frame* F, cudaStream_t s);
 bgs_status launch_adam_multimem(float* theta, float* theta_mc, float* grad_mc, float* m, float* v, int64_t n,

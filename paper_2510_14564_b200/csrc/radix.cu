@@ -19,7 +19,10 @@ namespace bgs {
 constexpr int kSortThreads = 256, kSortItems = 16, kSortTile = kSortThreads * kSortItems, kRadix = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr uint32_t kStA = 1u << 30, kStP = 2u << 30, kStMask = (1u << 30) - 1;
-constexpr int kLookBatch = 8;
+#ifndef BGS_LOOK_BATCH
+#define BGS_LOOK_BATCH 8
+#endif
+constexpr int kLookBatch = BGS_LOOK_BATCH;
 
 __device__ __forceinline__ uint64_t load_k(const uint32_t* counters) {
   return ((uint64_t)counters[C_K_HI] << 32) | counters[C_K_LO];
@@ -36,10 +39,15 @@ struct SortSmem {
   uint32_t hist_excl[kRadix];              // exclusive scan of this pass's global histogram
   uint32_t scan_tmp[kSortWarps];
   uint32_t tile;
+  uint32_t tile_valid;
 };
 
-// Sorts `count` (key, value) pairs by the digit at `shift`; count < 0 means "read K from
-// counters" (the 64-bit tile|depth keys), otherwise it is the host-known length.
+// Sorts `count` (key, value) pairs by the digit at `shift`; count = -1 means "read K from
+// counters" (the 64-bit tile|depth keys), count = -2 "read the visible count" (the depth
+// sort after its first pass), otherwise it is the host-known length.  drop_culled: keys
+// ~0 (culled Gaussians) take no slot and are not written (the pass histogram excludes
+// them), so the depth sort's first pass compacts the visible Gaussians to [0, V).
+// fill_to > 0 (the depth sort's last pass): ranks [V, fill_to) get zero tile counts.
 template <typename KT>
 __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restrict__ kin,
                                                             const uint32_t* __restrict__ vin, KT* kout,
@@ -47,11 +55,12 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
                                                             uint32_t* status, uint32_t* ticket,
                                                             const uint32_t* counters, int shift, int64_t count,
                                                             const uint2* __restrict__ rect, uint32_t* rank_cnt,
-                                                            uint2* rank_rect, uint32_t* rank_h) {
+                                                            uint2* rank_rect, uint32_t* rank_h, bool drop_culled,
+                                                            int64_t fill_to) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<KT>& S = *reinterpret_cast<SortSmem<KT>*>(smem_raw);
   if (counters[C_OVERFLOW]) return;
-  const int64_t K = count >= 0 ? count : (int64_t)load_k(counters);
+  const int64_t K = count >= 0 ? count : count == -1 ? (int64_t)load_k(counters) : (int64_t)counters[C_VISIBLE];
   const int64_t ntiles = (K + kSortTile - 1) / kSortTile;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // exclusive scan of the pass histogram (thread = digit)
@@ -79,6 +88,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
     if (tile >= ntiles) break;
     const int64_t tbase = tile * kSortTile;
     const int tcount = (int)(K - tbase < kSortTile ? K - tbase : kSortTile);
+    const KT culled = (KT)~(KT)0;
     // load: warp w owns the contiguous slice [w*512, (w+1)*512) of the tile
     KT key[kSortItems];
     uint32_t val[kSortItems];
@@ -102,7 +112,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
 #pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
       const int idx = wbase + k * 32 + lane;
-      const bool valid = idx < tcount;
+      const bool valid = idx < tcount && !(drop_culled && key[k] == culled);
       const uint32_t d = (uint32_t)((key[k] >> shift) & 0xff);
       uint32_t peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
@@ -143,6 +153,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
       uint32_t off = 0;
       for (int w = 0; w < warp; ++w) off += S.scan_tmp[w];
       S.tile_start[tid] = off + incl - cnt;
+      if (tid == kRadix - 1) S.tile_valid = off + incl;  // the tile's keys that take a slot
     }
     // look-back for digit tid: the statuses of kLookBatch predecessors are loaded together
     // (independent loads in flight), then consumed in order until an inclusive prefix; an
@@ -175,7 +186,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
 #pragma unroll
     for (int k = 0; k < kSortItems; ++k) {
       const int idx = wbase + k * 32 + lane;
-      if (idx < tcount) {
+      if (idx < tcount && !(drop_culled && key[k] == culled)) {
         const uint32_t d = (uint32_t)((key[k] >> shift) & 0xff);
         const uint32_t pos = S.tile_start[d] + S.warp_hist[warp][d] + rank[k];
         S.keys[pos] = key[k];
@@ -183,7 +194,8 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
       }
     }
     __syncthreads();
-    for (int j = tid; j < tcount; j += kSortThreads) {
+    const int tvalid = (int)S.tile_valid;
+    for (int j = tid; j < tvalid; j += kSortThreads) {
       const KT k2 = S.keys[j];
       const uint32_t d = (uint32_t)((k2 >> shift) & 0xff);
       const uint32_t g = S.global_base[d] + (uint32_t)j - S.tile_start[d];
@@ -207,6 +219,12 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
     }
     __syncthreads();
   }
+  if (fill_to > K)  // ranks past the visible ones own no tiles
+    for (int64_t r = K + (int64_t)blockIdx.x * kSortThreads + tid; r < fill_to; r += (int64_t)gridDim.x * kSortThreads) {
+      rank_cnt[r] = 0u;
+      rank_rect[r] = make_uint2(0u, 0u);
+      rank_h[r] = 0u;
+    }
 }
 
 template <typename KT>
@@ -228,7 +246,7 @@ bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* 
                             const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                             int shift, cudaStream_t s) {
   k_sort_pass<uint64_t><<<pass_grid<uint64_t>(), kSortThreads, sizeof(SortSmem<uint64_t>), s>>>(
-      kin, vin, kout, vout, hist, status, ticket, counters, shift, -1, nullptr, nullptr, nullptr, nullptr);
+      kin, vin, kout, vout, hist, status, ticket, counters, shift, -1, nullptr, nullptr, nullptr, nullptr, false, 0);
   note_launch();
   return check_launch("k_sort_pass<u64>");
 }
@@ -236,9 +254,10 @@ bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* 
 bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                               int shift, int64_t count, cudaStream_t s, const uint2* rect, uint32_t* rank_cnt,
-                              uint2* rank_rect, uint32_t* rank_h) {
+                              uint2* rank_rect, uint32_t* rank_h, bool drop_culled, int64_t fill_to) {
   k_sort_pass<uint32_t><<<pass_grid<uint32_t>(), kSortThreads, sizeof(SortSmem<uint32_t>), s>>>(
-      kin, vin, kout, vout, hist, status, ticket, counters, shift, count, rect, rank_cnt, rank_rect, rank_h);
+      kin, vin, kout, vout, hist, status, ticket, counters, shift, count, rect, rank_cnt, rank_rect, rank_h,
+      drop_culled, fill_to);
   note_launch();
   return check_launch("k_sort_pass<u32>");
 }

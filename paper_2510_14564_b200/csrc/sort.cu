@@ -10,8 +10,8 @@
 //    load-balanced duplication (K9) and LSD-sorted on bits [0, 32 + bit_width(tiles-1))
 //    with the onesweep pass of radix.cu (K10): ~8 + 24 p bytes per key (p = 6 passes).
 //  * default, depth first (SURVEY.md §8(a) a5 alternative): (1) stable LSD sort of the N
-//    Gaussians by depth bits (4 passes of 32-bit keys over N, not K; culled Gaussians get
-//    the key 0xffffffff and sort last); (2) scan of their tile counts in that order;
+//    Gaussians by depth bits (4 passes of 32-bit keys, not K; the first pass over N drops
+//    the culled Gaussians, the other three see the V visible ones); (2) scan of their tile counts in that order;
 //    (3) emission of (tile, Gaussian) items in depth order; (4) a stable split of the
 //    items by tile id (ceil(bits/8) 32-bit passes).  A stable split of a depth-ordered
 //    (stable in index) sequence by tile is exactly the (tile, depth, index) order, so the
@@ -128,24 +128,42 @@ __global__ void __launch_bounds__(kDupThreads) k_emit(int64_t n, const uint2* __
 }
 
 // ---------------------------------------------------------------- depth-first path, step 1
-// 32-bit depth keys (culled: 0xffffffff, sorts last) + the 4 pass histograms.
+#ifdef BGS_NO_COMPACT  // A/B experiment: every pass over N, culled keys sorted last
+constexpr bool kNoCompact = true;
+#else
+constexpr bool kNoCompact = false;
+#endif
+// 32-bit depth keys (culled: 0xffffffff) + the 4 pass histograms of the VISIBLE keys and
+// their count V (counters[C_VISIBLE]): the first pass drops the culled keys, so the other
+// three run over [0, V), and the ranks [V, N) own no tiles.
 __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const float* __restrict__ depth,
                                                     const uint32_t* __restrict__ tiles_touched,
-                                                    const uint32_t* counters, uint32_t* dkey, uint32_t* dval,
+                                                    uint32_t* counters, uint32_t* dkey, uint32_t* dval,
                                                     uint32_t* hist) {
   __shared__ uint32_t s_h[8][4][kRadixBins];  // one copy per warp: conflicts stay inside a warp
+  __shared__ uint32_t s_vis;
   if (counters[C_OVERFLOW]) return;
   for (int k = threadIdx.x; k < 8 * 4 * kRadixBins; k += blockDim.x) (&s_h[0][0][0])[k] = 0;
+  if (threadIdx.x == 0) s_vis = 0;
   __syncthreads();
   uint32_t(*h)[kRadixBins] = s_h[threadIdx.x >> 5];
+  uint32_t vis = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t key = tiles_touched[i] ? __float_as_uint(depth[i]) : 0xffffffffu;
+    const bool visible = tiles_touched[i] != 0;
+    const uint32_t key = visible ? __float_as_uint(depth[i]) : 0xffffffffu;
     dkey[i] = key;
     dval[i] = (uint32_t)i;
+    if (visible || kNoCompact) {
+      ++vis;
 #pragma unroll
-    for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(key >> (8 * p)) & 0xff], 1u);
+      for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(key >> (8 * p)) & 0xff], 1u);
+    }
   }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) vis += __shfl_xor_sync(0xffffffffu, vis, d);
+  if ((threadIdx.x & 31) == 0 && vis) atomicAdd(&s_vis, vis);
   __syncthreads();
+  if (threadIdx.x == 0 && s_vis) atomicAdd(&counters[C_VISIBLE], s_vis);
   for (int k = threadIdx.x; k < 4 * kRadixBins; k += blockDim.x) {
     uint32_t v = 0;
 #pragma unroll
@@ -498,19 +516,18 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
         nxt[tile] = p + 1u;
         vals[p] = g_id;
       }
-      uint32_t pending = __ballot_sync(0xffffffffu, contended);
-      if (pending) {
+      if (__any_sync(0xffffffffu, contended)) {
+        // the items of a contended tile belong to distinct Gaussians, so lane order is their
+        // depth order: each takes the tile's next position plus its rank among the tile's
+        // lanes (one MATCH.ANY), and the tile's last lane advances the counter
         __syncwarp();
-        while (pending) {
-          const int gcur = __shfl_sync(0xffffffffu, g, __ffs(pending) - 1);
-          const bool mine = contended && g == gcur;
-          pending &= ~__ballot_sync(0xffffffffu, mine);
-          if (mine) {
-            const uint32_t p = nxt[tile];
-            nxt[tile] = p + 1u;
-            vals[p] = g_id;
-          }
-          __syncwarp();
+        const uint32_t peers = __match_any_sync(0xffffffffu, contended ? tile : 0x80000000u | (uint32_t)lane);
+        uint32_t p = 0;
+        if (contended) p = nxt[tile] + (uint32_t)__popc(peers & lanemask_lt());
+        __syncwarp();
+        if (contended) {
+          if ((peers >> lane) == 1u) nxt[tile] = p + 1u;
+          vals[p] = g_id;
         }
       }
       __syncwarp();
@@ -594,7 +611,8 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
       cudaMemsetAsync(F->tile_count, 0, 4 * (size_t)F->num_tiles, s) != cudaSuccess ||
       cudaMemsetAsync(F->sort_hist, 0, 4 * 8 * kRadixBins, s) != cudaSuccess ||
       cudaMemsetAsync(F->counters + C_SORT_TICKET, 0, 4 * 8, s) != cudaSuccess ||
-      cudaMemsetAsync(F->counters + C_SORT32_TICKET, 0, 4 * 8, s) != cudaSuccess)
+      cudaMemsetAsync(F->counters + C_SORT32_TICKET, 0, 4 * 8, s) != cudaSuccess ||
+      cudaMemsetAsync(F->counters + C_VISIBLE, 0, 4, s) != cudaSuccess)
     return check_launch("sort memset");
   const bool ref64 = (F->debug_flags & (BGS_DEBUG_SORT_ONESWEEP64 | BGS_DEBUG_SKIP_SORT)) != 0;
   const int P = F->sort_passes;
@@ -630,12 +648,13 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
   for (int p = 0; p < 4; ++p) {
     if ((st = memset_status(F, s, F->n)) != BGS_OK) return st;
     const int a = p & 1, b = (p + 1) & 1;
-    // (2) the last pass also writes the per-rank tile counts and packed rects
+    // the first pass compacts the visible Gaussians; (2) the last pass also writes the
+    // per-rank tile counts and packed rects (zero past V)
     const bool last = p == 3;
     st = launch_sort_pass32(F->dkey[a], F->dval[a], F->dkey[b], F->dval[b], F->sort_hist + p * kRadixBins,
-                            F->sort_status, F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, F->n, s,
+                            F->sort_status, F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, (p && !kNoCompact) ? -2 : F->n, s,
                             last ? F->rect : nullptr, last ? F->rank_cnt : nullptr, last ? F->rank_rect : nullptr,
-                            last ? F->rank_h : nullptr);
+                            last ? F->rank_h : nullptr, p == 0 && !kNoCompact, last ? F->n : 0);
     if (st != BGS_OK) return st;
   }
   // K (published with the capacity check) = the total of the depth-order scan
