@@ -398,6 +398,20 @@ size_t bgs_frame_hint_bytes(const bgs_frame* f /*host*/);
 bgs_status bgs_frame_save_hint(const bgs_frame* f /*host*/, void* dst, void* stream);
 bgs_status bgs_frame_load_hint(bgs_frame* f /*host*/, const void* src, void* stream);
 bgs_status bgs_frame_debug(const bgs_frame* f /*host*/, bgs_frame_views* out /*host*/);
+/* Failure detection, not on the hot path.  Structural check of the frame's
+ * last bgs_sort (a4-a6, §II-A, SPEC.md l.123 / R13): out (device,
+ * caller-owned, 8-byte aligned u64[5]) receives {range errors (a range outside [0, K),
+ * a non-empty tile not starting where the previous one ended, the last not ending at K,
+ * an empty tile not (0, 0)), membership errors (an entry that is not a visible Gaussian
+ * whose tile rect covers the tile), order errors (adjacent entries not strictly increasing
+ * in (depth bits, index)), count error (1 if sum tiles_touched != K), sum tiles_touched}.
+ * The first four all zero prove every tile list is exactly its Gaussians in order.
+ * Asynchronous on `stream`; BGS_ERR_INVALID on a bad frame or pointer. */
+bgs_status bgs_frame_validate(const bgs_frame* f /*host*/, uint64_t* out, void* stream);
+/* Non-finite check (e.g. of a gradient before Adam): out (device, caller-owned, 8-byte
+ * aligned u64[2]) receives {number of NaN / Inf entries of x[0, count), smallest such
+ * index or UINT64_MAX}.  x: device, 16-byte aligned.  Asynchronous on `stream`. */
+bgs_status bgs_nonfinite(const float* x, int64_t count, uint64_t* out, void* stream);
 /* Workload counters of the last fwd (runs a counting kernel and synchronises). */
 bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contrib, bgs_stats* out /*host*/,
                            void* stream);

@@ -126,6 +126,8 @@ _SIGS = {
     "bgs_frame_status": (C.c_int, [C.POINTER(Frame), C.POINTER(C.c_int64)]),
     "bgs_frame_debug": (C.c_int, [C.POINTER(Frame), C.POINTER(FrameViews)]),
     "bgs_frame_stats": (C.c_int, [C.POINTER(Frame), _P, C.POINTER(Stats), _P]),
+    "bgs_frame_validate": (C.c_int, [C.POINTER(Frame), _P, _P]),
+    "bgs_nonfinite": (C.c_int, [_P, C.c_int64, _P, _P]),
     "bgs_frame_set_debug": (C.c_int, [C.POINTER(Frame), C.c_int32]),
     "bgs_frame_set_seg_len": (C.c_int, [C.POINTER(Frame), C.c_int32]),
     "bgs_frame_hint_bytes": (C.c_size_t, [C.POINTER(Frame)]),
@@ -325,6 +327,36 @@ def bgs_frame_stats(frame: Frame, n_contrib, stream=None) -> dict:
     s = Stats()
     _check(_lib.bgs_frame_stats(C.byref(frame), _ptr(n_contrib), C.byref(s), _stream(stream)), "bgs_frame_stats")
     return {k: int(getattr(s, k)) for k, _ in Stats._fields_}
+
+
+VALIDATE_KEYS = ("range_errors", "member_errors", "order_errors", "count_error", "tiles_touched")
+
+
+def bgs_frame_validate(frame: Frame, out: torch.Tensor, stream=None):
+    """Asynchronous structural check of the frame's sorted lists into out (device int64[5])."""
+    assert out.dtype == torch.int64 and out.numel() >= 5
+    _check(_lib.bgs_frame_validate(C.byref(frame), _ptr(out), _stream(stream)), "bgs_frame_validate")
+
+
+def validate(frame: Frame, stream=None) -> dict:
+    """bgs_frame_validate, synchronised: the five counts by name (all errors 0: lists exact)."""
+    out = torch.empty(5, dtype=torch.int64, device="cuda")
+    bgs_frame_validate(frame, out, stream)
+    return dict(zip(VALIDATE_KEYS, (int(x) for x in out.cpu())))
+
+
+def bgs_nonfinite(x: torch.Tensor, out: torch.Tensor, stream=None):
+    """Asynchronous: out (device int64[2]) = {NaN/Inf count, smallest such index or -1}."""
+    assert x.dtype == torch.float32 and out.dtype == torch.int64 and out.numel() >= 2
+    _check(_lib.bgs_nonfinite(_ptr(x), x.numel(), _ptr(out), _stream(stream)), "bgs_nonfinite")
+
+
+def nonfinite(x: torch.Tensor, stream=None) -> tuple[int, int]:
+    """bgs_nonfinite, synchronised: (count, first index or -1)."""
+    out = torch.empty(2, dtype=torch.int64, device=x.device)
+    bgs_nonfinite(x, out, stream)
+    c, f = (int(v) for v in out.cpu())
+    return c, (f if c else -1)
 
 
 def bgs_frame_set_debug(frame: Frame, flags: int):

@@ -170,6 +170,7 @@ bgs_status launch_l1(const float* image, const uint8_t* target, int32_t w, int32
 size_t loss_workspace_bytes(int32_t w, int32_t h);
 bgs_status launch_l1_dssim(const float* image, const uint8_t* target, int32_t w, int32_t h, float lam, float scale,
                            float* dl, float* loss_sum, void* workspace, cudaStream_t s);
+bgs_status launch_validate(const Frame* F, unsigned long long* out, cudaStream_t s);
 bgs_status launch_stats(const Frame* F, const uint32_t* n_contrib, bgs_stats* out, cudaStream_t s);
 
 int num_sms();

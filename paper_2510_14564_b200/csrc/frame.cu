@@ -552,6 +552,11 @@ bgs_status bgs_frame_set_seg_len(bgs_frame* f, int32_t seg_len) {
   return BGS_OK;
 }
 
+bgs_status bgs_frame_validate(const bgs_frame* f, uint64_t* out, void* stream) {
+  if (!frame_ok(f) || !out || (reinterpret_cast<uintptr_t>(out) & 7u)) return BGS_ERR_INVALID;
+  return launch_validate(frame_of(f), reinterpret_cast<unsigned long long*>(out), (cudaStream_t)stream);
+}
+
 bgs_status bgs_frame_stats(const bgs_frame* f, const uint32_t* n_contrib, bgs_stats* out, void* stream) {
   if (!frame_ok(f) || !n_contrib || !out) return BGS_ERR_INVALID;
   return launch_stats(frame_of(f), n_contrib, out, (cudaStream_t)stream);

@@ -45,6 +45,9 @@ def main():
         for _ in range(2):  # the second forward is hinted (splits long walks)
             out = r.forward(theta, cam, s.sh_degree)
         r.backward(theta, s.sh_degree, dl, out, grad)
+        rep = bgs.validate(r.frame)  # failure detection: the list check ...
+        assert rep["member_errors"] == rep["order_errors"] == rep["range_errors"] == 0, rep
+    assert bgs.nonfinite(grad)[0] == 0  # ... and the non-finite check
     # the bench's batched form: one preprocess for two views, loss, blend bwd, batched chain rule
     rs = [bgs.Renderer(s.n, W, H, max_keys=1 << 20, device=dev) for _ in range(2)]
     cams = [bgs.camera(c) for c in s.cameras[:2]] if len(s.cameras) > 1 else [bgs.camera(cam)] * 2
