@@ -247,6 +247,10 @@ __device__ __forceinline__ void st_relaxed_u32(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
 // cp.async (LDGSTS): global -> shared copies that bypass the registers; completion per
 // thread by commit groups
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
@@ -258,28 +262,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// mbarrier (sm_90+) helpers for producer/consumer pipelines in shared memory
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
 }
 
 // Exact-up-to-margin cull of one list entry against an 8x4 pixel block: can any pixel
@@ -308,6 +290,21 @@ __device__ __forceinline__ bool ellipse_hits_block(float mx, float my, float A, 
   const float ex = fmaxf(-lx, hx), ey = fmaxf(-ly, hy);
   const float margin = 1e-3f + 1e-5f * (fabsf(A) * ex * ex + fabsf(C) * ey * ey);
   return best >= thr - margin;
+}
+
+// Cheaper conservative form of the same test: the power is a negative-definite quadratic
+// q, so over the block (centre c, half-extents hx, hy) q(mu - p) = q(d_c) - grad q(d_c) . e
+// + q(e) <= q(d_c) + hx |dq/dx| + hy |dq/dy| (q(e) <= 0).  When even that bound is below
+// thr (with the same rounding margin), no pixel of the block reaches the level set.
+__device__ __forceinline__ bool bound_hits_block(float mx, float my, float A, float B, float C, float thr,
+                                                 float cx, float cy, float hx, float hy) {
+  const float dx = mx - cx, dy = my - cy;
+  const float gx = fmaf(2.0f * A, dx, B * dy), gy = fmaf(2.0f * C, dy, B * dx);
+  const float q = fmaf(A, dx * dx, fmaf(C, dy * dy, B * (dx * dy)));
+  const float bound = fmaf(hx, fabsf(gx), fmaf(hy, fabsf(gy), q));
+  const float ex = fabsf(dx) + hx, ey = fabsf(dy) + hy;
+  const float margin = 1e-3f + 2e-5f * (fabsf(A) * ex * ex + fabsf(C) * ey * ey);
+  return bound >= thr - margin;
 }
 
 // work-unit ordering: bucket of a cost, 4 buckets per octave, costliest first (0..127)

@@ -38,6 +38,9 @@
 
 namespace bgs {
 
+#ifndef BGS_FWD_CULL
+#define BGS_FWD_CULL 0
+#endif
 constexpr int kFwdWarps = 4;
 // The forward keeps a one-CTA planner: it places a tile's eight blocks next to each other
 // inside their cost bucket, and the tile list they share stays hot in L2 (a grid-wide
@@ -157,6 +160,11 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const FwdArgs a, 
             ck_step = nck < kCkMax ? (nck + 1) * seg_steps : -1;
           }
           // (1) commit step s into the warp's shared-memory slice
+#if BGS_FWD_CULL == 1
+          if (h_c) h_c = ellipse_hits_block(a_c.x, a_c.y, r1_c.x, r1_c.y, r1_c.z, r2_c.w, bx0, by0, bx1, by1);
+#elif BGS_FWD_CULL == 2
+          if (h_c) h_c = bound_hits_block(a_c.x, a_c.y, r1_c.x, r1_c.y, r1_c.z, r2_c.w, bx0 + 3.5f, by0 + 1.5f, 3.5f, 1.5f);
+#endif
           const uint32_t bal = __ballot_sync(0xffffffffu, h_c);
           if (h_c) {
             const int q = __popc(bal & lt);
