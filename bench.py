@@ -99,6 +99,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--one-frame", action="store_true",
                    help="diagnostic: one frame for all views (no per-view scheduling hint)")
+    p.add_argument("--no-plan-ahead", action="store_true",
+                   help="with --sort-streams: build each view's forward schedule in bgs_render_fwd and its "
+                        "backward schedule in bgs_blend_bwd instead of ahead (with the sorts / beside the loss)")
     p.add_argument("--fixed-batch", action="store_true",
                    help="every step renders the same 16 cameras (views 4i mod 64), each frame hinted by its own "
                         "previous forward (round-1 bench); default: the batch rotates over the scene's cameras "
@@ -342,6 +345,12 @@ def run_ours(args, rank, world, local_rank):
     sort_ahead = args.sort_streams > 0 and not args.one_frame
     sort_streams = [torch.cuda.Stream(device=dev) for _ in range(args.sort_streams)] if sort_ahead else []
     sort_evs = [torch.cuda.Event() for _ in range(n_mine)] if sort_ahead else []
+    # the blend kernels' schedules built off the critical path: the forward's with the sorts,
+    # the backward's on a side stream while the view's loss runs
+    plan_ahead = sort_ahead and not args.no_plan_ahead
+    plan_stream = torch.cuda.Stream(device=dev) if plan_ahead else None
+    fwd_evs = [torch.cuda.Event() for _ in range(n_mine)] if plan_ahead else []
+    plan_evs = [torch.cuda.Event() for _ in range(n_mine)] if plan_ahead else []
     stage_names = ["preprocess", "sort", "render_fwd", "loss", "blend_bwd", "preprocess_bwd", "allreduce", "adam"]
     if args.density_every:
         stage_names.append("density")
@@ -456,12 +465,17 @@ def run_ours(args, rank, world, local_rank):
         if sort_ahead:  # a4-a6 of every view first, spread over the sort streams
             marks = []
             mark(marks)
+            if plan_ahead and hint_mode != "slot":  # the hints first: the plans follow them
+                for j, c in enumerate(cams_idx):
+                    bgs.bgs_frame_load_hint(frames[j], hints[c] if hint_mode == "camera" and hint_ok[c] else None)
             fork_ev.record(stream)
             for ss in sort_streams:
                 ss.wait_event(fork_ev)
             for j in range(len(cam_structs)):
                 with torch.cuda.stream(sort_streams[j % len(sort_streams)]):
                     bgs.bgs_sort(frames[j])
+                    if plan_ahead:
+                        bgs.bgs_render_fwd_plan(frames[j])
                     sort_evs[j].record()
             for ev in sort_evs[:len(cam_structs)]:
                 stream.wait_event(ev)
@@ -486,11 +500,19 @@ def run_ours(args, rank, world, local_rank):
                     bgs.bgs_sort(rj.frame)
                 mark(marks)
                 c = cams_idx[j]
-                if hint_mode == "camera":
+                if plan_ahead:
+                    pass  # loaded before the sorts
+                elif hint_mode == "camera":
                     bgs.bgs_frame_load_hint(rj.frame, hints[c] if hint_ok[c] else None)
                 elif hint_mode == "none":
                     bgs.bgs_frame_load_hint(rj.frame, None)
                 bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
+                if plan_ahead:  # the backward's schedule, beside the loss
+                    fwd_evs[j].record(sj)
+                    plan_stream.wait_event(fwd_evs[j])
+                    with torch.cuda.stream(plan_stream):
+                        bgs.bgs_blend_bwd_plan(rj.frame)
+                        plan_evs[j].record()
                 if hint_mode == "camera":
                     bgs.bgs_frame_save_hint(rj.frame, hints[c])
                     hint_ok[c] = True
@@ -503,6 +525,8 @@ def run_ours(args, rank, world, local_rank):
                 else:  # L1 (R19)
                     bgs.bgs_l1_loss_grad(rj.image, tg, W, H, scale, dl, loss)
                 mark(marks)
+                if plan_ahead:
+                    sj.wait_event(plan_evs[j])
                 bgs.bgs_blend_bwd(rj.frame, dl, rj.final_T, rj.n_contrib)
                 mark(marks)
                 if args.one_frame:  # the frame is reused by the next view: chain rule now
@@ -873,7 +897,9 @@ def run_ours(args, rank, world, local_rank):
                      "each view hinted by its camera's last forward (bgs_frame_save_hint / load_hint)",
                      "sort_path": args.sort_path,
                      "sorts": (f"all views' a4-a6 first, over {args.sort_streams} streams" if args.sort_streams > 0
-                               and not args.one_frame else "each view's a4-a6 inline before its forward")},
+                               and not args.one_frame else "each view's a4-a6 inline before its forward"),
+                     "plans": ("forward schedules built with the sorts, backward schedules beside the loss "
+                               "(bgs_render_fwd_plan / bgs_blend_bwd_plan)" if plan_ahead else "inline")},
         "variants": variants,
         "nccl": (nccl_summary() if world > 1 and os.environ.get("BGS_DIST_BACKEND", "nccl") == "nccl" else None),
         "density": None if not args.density_every else {

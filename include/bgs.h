@@ -168,6 +168,18 @@ bgs_status bgs_sort(bgs_frame* f /*host*/, void* stream);
  * §II-A; R14-R16).  Outputs planar image[3][h][w], final_T[h][w] and n_contrib[h][w] =
  * 1-based list position of the last blended Gaussian (0 if none). */
 bgs_status bgs_render_fwd(bgs_frame* f /*host*/, float* image, float* final_T, uint32_t* n_contrib, void* stream);
+/* Optional plan-ahead of the blend kernels' schedules (a launch-order aid; results are
+ * unchanged).  bgs_render_fwd_plan builds the work units of the frame's NEXT bgs_render_fwd
+ * (heaviest first and split by its scheduling hint, else ordered by tile list length): call
+ * it after bgs_sort and bgs_frame_load_hint, e.g. on another stream while other views blend.
+ * bgs_blend_bwd_plan builds the NEXT bgs_blend_bwd's units from the frame's last forward:
+ * call it after bgs_render_fwd, e.g. on another stream while the loss runs.  A plan is
+ * discarded by bgs_preprocess(_batch), bgs_sort, bgs_frame_load_hint, bgs_frame_set_debug,
+ * bgs_frame_set_seg_len (and a forward plan by the forward that uses it, a backward plan by
+ * the next bgs_render_fwd); without one, bgs_render_fwd / bgs_blend_bwd plan for themselves.
+ * The caller orders the plan before its kernel across streams (events).  Asynchronous. */
+bgs_status bgs_render_fwd_plan(bgs_frame* f /*host*/, void* stream);
+bgs_status bgs_blend_bwd_plan(bgs_frame* f /*host*/, void* stream);
 
 /* a9-a10: blend backward (back to front, decisions of the forward frozen, R18) and
  * the chain rule conic -> Sigma' -> Sigma/(s, q) and J -> t -> mu, xy -> mu,

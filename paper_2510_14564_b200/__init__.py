@@ -127,6 +127,8 @@ _SIGS = {
     "bgs_frame_debug": (C.c_int, [C.POINTER(Frame), C.POINTER(FrameViews)]),
     "bgs_frame_stats": (C.c_int, [C.POINTER(Frame), _P, C.POINTER(Stats), _P]),
     "bgs_frame_validate": (C.c_int, [C.POINTER(Frame), _P, _P]),
+    "bgs_render_fwd_plan": (C.c_int, [C.POINTER(Frame), _P]),
+    "bgs_blend_bwd_plan": (C.c_int, [C.POINTER(Frame), _P]),
     "bgs_nonfinite": (C.c_int, [_P, C.c_int64, _P, _P]),
     "bgs_frame_set_debug": (C.c_int, [C.POINTER(Frame), C.c_int32]),
     "bgs_frame_set_seg_len": (C.c_int, [C.POINTER(Frame), C.c_int32]),
@@ -327,6 +329,14 @@ def bgs_frame_stats(frame: Frame, n_contrib, stream=None) -> dict:
     s = Stats()
     _check(_lib.bgs_frame_stats(C.byref(frame), _ptr(n_contrib), C.byref(s), _stream(stream)), "bgs_frame_stats")
     return {k: int(getattr(s, k)) for k, _ in Stats._fields_}
+
+
+def bgs_render_fwd_plan(frame: Frame, stream=None):
+    _check(_lib.bgs_render_fwd_plan(C.byref(frame), _stream(stream)), "bgs_render_fwd_plan")
+
+
+def bgs_blend_bwd_plan(frame: Frame, stream=None):
+    _check(_lib.bgs_blend_bwd_plan(C.byref(frame), _stream(stream)), "bgs_blend_bwd_plan")
 
 
 VALIDATE_KEYS = ("range_errors", "member_errors", "order_errors", "count_error", "tiles_touched")

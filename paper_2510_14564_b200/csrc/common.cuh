@@ -106,6 +106,7 @@ struct Frame {
   uint32_t* order_bwd;     // [8 tiles] backward work items, longest first
   uint32_t* block_cost;    // [8 tiles] each block's largest n_contrib in the last forward
   int32_t have_cost, seg_len;  // block_cost holds this frame's previous forward; list segment length
+  int32_t fwd_planned, bwd_planned;  // the next fwd's / bwd's work units are already built (plan-ahead)
   int32_t counters_init;   // the sticky overflow word has been zeroed (first preprocess)
   uint32_t* ck_table;      // [8 tiles][kCkMax] pool slot of boundary b = 1..kCkMax of each block's walk
   float4* ck_pool;         // [ck_cap][32 lanes] {T, colour behind r, g, b} at a boundary
@@ -170,6 +171,8 @@ bgs_status launch_l1(const float* image, const uint8_t* target, int32_t w, int32
 size_t loss_workspace_bytes(int32_t w, int32_t h);
 bgs_status launch_l1_dssim(const float* image, const uint8_t* target, int32_t w, int32_t h, float lam, float scale,
                            float* dl, float* loss_sum, void* workspace, cudaStream_t s);
+bgs_status launch_fwd_plan(Frame* F, cudaStream_t s);
+bgs_status launch_bwd_plan(Frame* F, cudaStream_t s);
 bgs_status launch_validate(const Frame* F, unsigned long long* out, cudaStream_t s);
 bgs_status launch_stats(const Frame* F, const uint32_t* n_contrib, bgs_stats* out, cudaStream_t s);
 

@@ -255,6 +255,7 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->order_bwd = (uint32_t*)(base + L.order_bwd);
   F->block_cost = (uint32_t*)(base + L.block_cost);
   F->have_cost = 0;
+  F->fwd_planned = F->bwd_planned = 0;
   F->seg_len = kSegLenDefault;
   F->ck_table = (uint32_t*)(base + L.ck_table);
   F->ck_pool = (float4*)(base + L.ck_pool);
@@ -294,6 +295,7 @@ bgs_status bgs_preprocess(const bgs_gaussians* g, const bgs_camera* cam, bgs_fra
   if ((st = validate_camera(cam, F)) != BGS_OK) return st;
   F->cam = make_cam(*cam, F->tiles_x, F->tiles_y);
   F->cam_valid = 1;
+  F->fwd_planned = F->bwd_planned = 0;
   return launch_preprocess(g, F, (cudaStream_t)stream);
 }
 
@@ -315,13 +317,25 @@ bgs_status bgs_preprocess_batch(const bgs_gaussians* g, const bgs_camera* cams, 
   for (int v = 0; v < nframes; ++v) {
     F[v]->cam = make_cam(cams[v], F[v]->tiles_x, F[v]->tiles_y);
     F[v]->cam_valid = 1;
+    F[v]->fwd_planned = F[v]->bwd_planned = 0;
   }
   return launch_preprocess_batch(g, F, nframes, (cudaStream_t)stream);
 }
 
 bgs_status bgs_sort(bgs_frame* f, void* stream) {
   if (!frame_ok(f) || !frame_of(f)->cam_valid) return BGS_ERR_INVALID;
+  frame_of(f)->fwd_planned = frame_of(f)->bwd_planned = 0;
   return launch_sort(frame_of(f), (cudaStream_t)stream);
+}
+
+bgs_status bgs_render_fwd_plan(bgs_frame* f, void* stream) {
+  if (!frame_ok(f) || !frame_of(f)->cam_valid) return BGS_ERR_INVALID;
+  return launch_fwd_plan(frame_of(f), (cudaStream_t)stream);
+}
+
+bgs_status bgs_blend_bwd_plan(bgs_frame* f, void* stream) {
+  if (!frame_ok(f) || !frame_of(f)->cam_valid) return BGS_ERR_INVALID;
+  return launch_bwd_plan(frame_of(f), (cudaStream_t)stream);
 }
 
 bgs_status bgs_render_fwd(bgs_frame* f, float* image, float* final_T, uint32_t* n_contrib, void* stream) {
@@ -504,6 +518,7 @@ bgs_status bgs_frame_save_hint(const bgs_frame* f, void* dst, void* stream) {
 bgs_status bgs_frame_load_hint(bgs_frame* f, const void* src, void* stream) {
   if (!frame_ok(f)) return BGS_ERR_INVALID;
   Frame* F = frame_of(f);
+  F->fwd_planned = 0;
   if (!src) {
     F->have_cost = 0;
     return BGS_OK;
@@ -543,12 +558,14 @@ bgs_status bgs_frame_debug(const bgs_frame* f, bgs_frame_views* out) {
 bgs_status bgs_frame_set_debug(bgs_frame* f, int32_t flags) {
   if (!frame_ok(f)) return BGS_ERR_INVALID;
   frame_of(f)->debug_flags = flags;
+  frame_of(f)->fwd_planned = frame_of(f)->bwd_planned = 0;
   return BGS_OK;
 }
 
 bgs_status bgs_frame_set_seg_len(bgs_frame* f, int32_t seg_len) {
   if (!frame_ok(f) || seg_len < 32 || seg_len > 65536 || (seg_len & 31)) return BGS_ERR_INVALID;
   frame_of(f)->seg_len = seg_len;
+  frame_of(f)->fwd_planned = frame_of(f)->bwd_planned = 0;
   return BGS_OK;
 }
 

@@ -454,10 +454,8 @@ __global__ void __launch_bounds__(256) k_bwd_plan_place(const uint32_t* __restri
   }
 }
 
-bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
-                            cudaStream_t s) {
+bgs_status launch_bwd_plan(Frame* F, cudaStream_t s) {
   const uint32_t cap = (uint32_t)(F->ck_cap < 0xffffffffll ? F->ck_cap : 0xffffffffll);
-  // 8x8 units (two pixels per lane) unless BGS_DEBUG_BWD_8X4 asks for the 8x4 ones
   const int ppl = (F->debug_flags & BGS_DEBUG_BWD_8X4) ? 1 : 2;
   const int n_units = 8 / ppl * F->num_tiles;
   const int pgrid = (n_units + 255) / 256 < 2 * num_sms() ? (n_units + 255) / 256 : 2 * num_sms();
@@ -468,8 +466,21 @@ bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final
   k_bwd_plan_place<<<pgrid, 256, 0, s>>>(F->block_cost, n_units, ppl, F->ck_table, cap, F->seg_len, F->counters,
                                          F->plan, F->order_bwd);
   note_launch(3);
-  bgs_status st = check_launch("k_bwd_plan");
-  if (st != BGS_OK) return st;
+  const bgs_status st = check_launch("k_bwd_plan");
+  F->bwd_planned = st == BGS_OK;
+  return st;
+}
+
+bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final_T, const uint32_t* n_contrib,
+                            cudaStream_t s) {
+  // 8x8 units (two pixels per lane) unless BGS_DEBUG_BWD_8X4 asks for the 8x4 ones; the work
+  // units built ahead by bgs_blend_bwd_plan, else now
+  const int ppl = (F->debug_flags & BGS_DEBUG_BWD_8X4) ? 1 : 2;
+  if (!F->bwd_planned) {
+    const bgs_status st = launch_bwd_plan(F, s);
+    if (st != BGS_OK) return st;
+  }
+  F->bwd_planned = 0;
   if (ppl == 2)
     k_render_bwd<2><<<bwd_grid<2>(), kBwdWarpsPerCta * 32, 0, s>>>(
         F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,

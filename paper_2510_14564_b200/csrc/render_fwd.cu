@@ -454,7 +454,7 @@ static int fwd_grid() {
   return grid;
 }
 
-bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n_contrib, cudaStream_t s) {
+bgs_status launch_fwd_plan(Frame* F, cudaStream_t s) {
   const int n_items = 8 * F->num_tiles;
   const uint32_t cap = (uint32_t)(F->ck_cap < 0xffffffffll ? F->ck_cap : 0xffffffffll);
   // parity mode: no speculative segments (their merges re-associate T, R23)
@@ -465,7 +465,20 @@ bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n
                                            F->spec_n, F->arrive);
   note_launch();
   bgs_status st = check_launch("k_fwd_plan");
-  if (st != BGS_OK) return st;
+  F->fwd_planned = st == BGS_OK;
+  return st;
+}
+
+bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n_contrib, cudaStream_t s) {
+  // the work units: built ahead by bgs_render_fwd_plan, else now
+  if (!F->fwd_planned) {
+    const bgs_status st = launch_fwd_plan(F, s);
+    if (st != BGS_OK) return st;
+  }
+  F->fwd_planned = 0;
+  F->bwd_planned = 0;  // a new forward: the backward's plan follows it
+  const uint32_t cap = (uint32_t)(F->ck_cap < 0xffffffffll ? F->ck_cap : 0xffffffffll);
+  const bool parity = (F->debug_flags & BGS_DEBUG_PARITY_EXP) != 0;
   FwdArgs a;
   a.ranges = F->ranges;
   a.values = F->vals[F->final_buf];
