@@ -79,8 +79,9 @@ def parse():
     p.add_argument("--fuse-adam", action="store_true",
                    help="G = 1: the chain rule and Adam in one pass (bgs_preprocess_bwd_batch_adam; measured "
                         "slower at garden, 5.7 -> 8.3 ms per step, so off by default)")
-    p.add_argument("--streams", type=int, default=1,
-                   help="CUDA streams the step's views are spread over (round-robin; measured at garden: 1 -> 239.3, 2 -> 242.0, 3 -> 220.3 views/s, so 1 by default)")
+    p.add_argument("--streams", type=int, default=2,
+                   help="CUDA streams the step's views are spread over (round-robin; with the sorts and plans "
+                        "ahead, measured at garden: 1 -> 331.8, 2 -> 345.5, 3 -> 345.4 views/s)")
     p.add_argument("--density-every", type=int, default=0,
                    help="run the NEXT-1 density-control step every D training steps (configs[4]; 0 = off)")
     p.add_argument("--update", default="sharded", choices=["sharded", "allreduce", "overlap"],
@@ -99,6 +100,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--one-frame", action="store_true",
                    help="diagnostic: one frame for all views (no per-view scheduling hint)")
+    p.add_argument("--serial-steps", type=int, default=3,
+                   help="after the timed region, steps with every stage serialised on one stream, whose stage "
+                        "times feed the per-stage rooflines (the timed region's stages overlap across streams)")
     p.add_argument("--no-plan-ahead", action="store_true",
                    help="with --sort-streams: build each view's forward schedule in bgs_render_fwd and its "
                         "backward schedule in bgs_blend_bwd instead of ahead (with the sorts / beside the loss)")
@@ -439,17 +443,22 @@ def run_ours(args, rank, world, local_rank):
 
     hint_ok = {c: True for c in hints}
 
-    def one_step(tgts, record=None, tgt_events=None, hint_mode="camera"):
+    def one_step(tgts, record=None, tgt_events=None, hint_mode="camera", serial=False):
         """one training step; tgts(j, c) -> the target of view slot j (camera c).  hint_mode:
         "camera" (each view hinted by its camera's last forward), "slot" (by its frame's
-        previous forward), "none" (no hint: work ordered by list length)"""
+        previous forward), "none" (no hint: work ordered by list length).  serial: every
+        stage of every view in order on one stream (the per-stage timing pass)"""
+        n_st = 1 if serial else n_streams
+        side_ = [] if serial else side
+        s_ahead = sort_ahead and not serial
+        p_ahead = plan_ahead and not serial
         step_no[0] += 1
         cams_idx = rank_cams(step_no[0])
         cam_structs = [cam_structs_all[c] for c in cams_idx]
 
         def mark(marks):
             if record is not None:
-                e = pool[record["next"]]
+                e = record["pool"][record["next"]]
                 record["next"] += 1
                 e.record()  # on the current stream (the view's)
                 marks.append(e)
@@ -462,10 +471,10 @@ def run_ours(args, rank, world, local_rank):
             mark(marks)
             if record is not None:
                 record["marks"].append(("pre", marks))
-        if sort_ahead:  # a4-a6 of every view first, spread over the sort streams
+        if s_ahead:  # a4-a6 of every view first, spread over the sort streams
             marks = []
             mark(marks)
-            if plan_ahead and hint_mode != "slot":  # the hints first: the plans follow them
+            if p_ahead and hint_mode != "slot":  # the hints first: the plans follow them
                 for j, c in enumerate(cams_idx):
                     bgs.bgs_frame_load_hint(frames[j], hints[c] if hint_mode == "camera" and hint_ok[c] else None)
             fork_ev.record(stream)
@@ -474,7 +483,7 @@ def run_ours(args, rank, world, local_rank):
             for j in range(len(cam_structs)):
                 with torch.cuda.stream(sort_streams[j % len(sort_streams)]):
                     bgs.bgs_sort(frames[j])
-                    if plan_ahead:
+                    if p_ahead:
                         bgs.bgs_render_fwd_plan(frames[j])
                     sort_evs[j].record()
             for ev in sort_evs[:len(cam_structs)]:
@@ -482,32 +491,32 @@ def run_ours(args, rank, world, local_rank):
             mark(marks)
             if record is not None:
                 record["marks"].append(("sort", marks))
-        if side:
+        if side_:
             fork_ev.record(stream)
-            for sj in side:
+            for sj in side_:
                 sj.wait_event(fork_ev)
         for j, cs in enumerate(cam_structs):
             rj = S["rends"][j]
-            sj = streams_all[j % n_streams]
-            dl, loss_ws = dls[j % n_streams], loss_wss[j % n_streams]
+            sj = streams_all[j % n_st]
+            dl, loss_ws = dls[j % n_st], loss_wss[j % n_st]
             with torch.cuda.stream(sj):
                 marks = []
                 mark(marks)
                 if not batch_pre:
                     bgs.bgs_preprocess(gs, cs, rj.frame)
                 mark(marks)
-                if not sort_ahead:
+                if not s_ahead:
                     bgs.bgs_sort(rj.frame)
                 mark(marks)
                 c = cams_idx[j]
-                if plan_ahead:
+                if p_ahead:
                     pass  # loaded before the sorts
                 elif hint_mode == "camera":
                     bgs.bgs_frame_load_hint(rj.frame, hints[c] if hint_ok[c] else None)
                 elif hint_mode == "none":
                     bgs.bgs_frame_load_hint(rj.frame, None)
                 bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
-                if plan_ahead:  # the backward's schedule, beside the loss
+                if p_ahead:  # the backward's schedule, beside the loss
                     fwd_evs[j].record(sj)
                     plan_stream.wait_event(fwd_evs[j])
                     with torch.cuda.stream(plan_stream):
@@ -525,7 +534,7 @@ def run_ours(args, rank, world, local_rank):
                 else:  # L1 (R19)
                     bgs.bgs_l1_loss_grad(rj.image, tg, W, H, scale, dl, loss)
                 mark(marks)
-                if plan_ahead:
+                if p_ahead:
                     sj.wait_event(plan_evs[j])
                 bgs.bgs_blend_bwd(rj.frame, dl, rj.final_T, rj.n_contrib)
                 mark(marks)
@@ -534,7 +543,7 @@ def run_ours(args, rank, world, local_rank):
                 mark(marks)
                 if record is not None:
                     record["marks"].append(("view", marks))
-        for sj, ev in zip(side, join_evs):
+        for sj, ev in zip(side_, join_evs):
             ev.record(sj)
             stream.wait_event(ev)
         marks = []
@@ -619,7 +628,7 @@ def run_ours(args, rank, world, local_rank):
 
     check_overflow("warm-up")
     # ---- device-resident timed region (inputs larger than L2: theta 1.37 GB, keys GBs)
-    record = {"next": 0, "marks": []}
+    record = {"next": 0, "marks": [], "pool": pool}
     barrier()
     torch.cuda.synchronize()
     launches0 = bgs.launch_count()
@@ -638,23 +647,43 @@ def run_ours(args, rank, world, local_rank):
     launches = bgs.launch_count() - launches0
     ms_local = t0.elapsed_time(t1)
     check_overflow("timed region")
-    # per-stage means
-    sums = {s: 0.0 for s in stage_names}
-    for kind, mk in record["marks"]:
-        if kind == "pre":
-            sums["preprocess"] += mk[0].elapsed_time(mk[1])
-        elif kind == "sort":
-            sums["sort"] += mk[0].elapsed_time(mk[1])
-        elif kind == "view":
-            for s, a, b in zip(stage_names[:6], mk[:-1], mk[1:]):
-                sums[s] += a.elapsed_time(b)
-        else:
-            sums["preprocess_bwd"] += mk[0].elapsed_time(mk[1])
-            sums["allreduce"] += mk[1].elapsed_time(mk[2]) + mk[3].elapsed_time(mk[4])
-            sums["adam"] += mk[2].elapsed_time(mk[3])
-            if args.density_every:
-                sums["density"] += mk[4].elapsed_time(mk[5])
-    per_step = {s: sums[s] / args.steps for s in stage_names}
+    def stage_means(rec, steps):
+        sums = {s: 0.0 for s in stage_names}
+        for kind, mk in rec["marks"]:
+            if kind == "pre":
+                sums["preprocess"] += mk[0].elapsed_time(mk[1])
+            elif kind == "sort":
+                sums["sort"] += mk[0].elapsed_time(mk[1])
+            elif kind == "view":
+                for s, a, b in zip(stage_names[:6], mk[:-1], mk[1:]):
+                    sums[s] += a.elapsed_time(b)
+            else:
+                sums["preprocess_bwd"] += mk[0].elapsed_time(mk[1])
+                sums["allreduce"] += mk[1].elapsed_time(mk[2]) + mk[3].elapsed_time(mk[4])
+                sums["adam"] += mk[2].elapsed_time(mk[3])
+                if args.density_every:
+                    sums["density"] += mk[4].elapsed_time(mk[5])
+        return {s: sums[s] / steps for s in stage_names}
+
+    # per-stage means of the timed region; with several streams the views' stages overlap, so
+    # these intervals include other views' concurrent kernels.  The per-stage roofline uses a
+    # serial pass instead: the same steps with every stage of every view in order on one
+    # stream (no overlap), timed alike, right after the timed region
+    per_step_concurrent = stage_means(record, args.steps)
+    per_step = per_step_concurrent
+    concurrent = n_streams > 1 or sort_ahead
+    serial_steps = 0
+    if concurrent and args.serial_steps > 0 and not args.no_stage_events and not args.density_every:
+        serial_steps = args.serial_steps
+        pool2 = [torch.cuda.Event(enable_timing=True) for _ in range(serial_steps * (7 * n_mine + 11))]
+        rec2 = {"next": 0, "marks": [], "pool": pool2}
+        barrier()
+        for _ in range(serial_steps):
+            one_step(dev_targets, rec2, hint_mode=hint_mode, serial=True)
+        torch.cuda.synchronize()
+        barrier()
+        check_overflow("serial stage pass")
+        per_step = stage_means(rec2, serial_steps)
 
     # ---- end-to-end through the public API with host buffers
     e2e = None
@@ -884,6 +913,12 @@ def run_ours(args, rank, world, local_rank):
         "config": arm_config(scene, args, world),
         "clocks": clocks, "gpu_launches": int(launches), "roofline": roofline,
         "stages_ms_per_step": {k2: round(v2, 4) for k2, v2 in per_step.items()},
+        "stages_timing": (f"serial pass: {serial_steps} steps after the timed region, every stage of every view in "
+                          "order on one stream (the timed region overlaps views on "
+                          f"{n_streams} streams and sorts on {args.sort_streams})" if serial_steps else
+                          "the timed region's own stage events"),
+        "stages_ms_per_step_concurrent": ({k2: round(v2, 4) for k2, v2 in per_step_concurrent.items()}
+                                          if serial_steps else None),
         "stages_roofline": {k2: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v2.items()}
                             for k2, v2 in roof.items()},
         "workload": {"V_per_view": V, "K_per_view": K, "E_f_per_view": Ef, "E_b_per_view": Eb,
