@@ -103,6 +103,9 @@ def parse():
     p.add_argument("--serial-steps", type=int, default=3,
                    help="after the timed region, steps with every stage serialised on one stream, whose stage "
                         "times feed the per-stage rooflines (the timed region's stages overlap across streams)")
+    p.add_argument("--no-consume", action="store_true",
+                   help="keep the preprocess's zeroing of the blend-gradient slots instead of letting the chain "
+                        "rule zero what it reads (bgs_frame_set_consume)")
     p.add_argument("--no-plan-ahead", action="store_true",
                    help="with --sort-streams: build each view's forward schedule in bgs_render_fwd and its "
                         "backward schedule in bgs_blend_bwd instead of ahead (with the sorts / beside the loss)")
@@ -372,6 +375,9 @@ def run_ours(args, rank, world, local_rank):
     def derive():
         S["gs"] = bgs.gaussians(S["theta"][:59 * S["n"]], S["n"], deg)  # (sharded: theta is padded)
         S["frames"] = [rj.frame for rj in S["rends"]]
+        if not args.one_frame and not args.no_consume:  # the batched chain rule zeroes what it reads
+            for f in S["frames"]:
+                bgs.bgs_frame_set_consume(f, True)
 
     derive()
     del theta, grad, m, v, rends
@@ -627,6 +633,11 @@ def run_ours(args, rank, world, local_rank):
         return ms
 
     check_overflow("warm-up")
+    # the stage times come from a serial pass after the timed region when the step overlaps
+    # views on streams; the timed region then records no stage events (their host calls
+    # would slow small configs' launch-bound steps)
+    concurrent = n_streams > 1 or sort_ahead
+    serial_pass = concurrent and args.serial_steps > 0 and not args.no_stage_events and not args.density_every
     # ---- device-resident timed region (inputs larger than L2: theta 1.37 GB, keys GBs)
     record = {"next": 0, "marks": [], "pool": pool}
     barrier()
@@ -639,7 +650,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.nvtx.range_push("bench_timed")  # ncu --nvtx --nvtx-include "bench_timed/"
         t0.record(stream)
         for _ in range(args.steps):
-            one_step(dev_targets, None if args.no_stage_events else record, hint_mode=hint_mode)
+            one_step(dev_targets, None if (args.no_stage_events or serial_pass) else record, hint_mode=hint_mode)
         t1.record(stream)
         torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
@@ -665,15 +676,12 @@ def run_ours(args, rank, world, local_rank):
                     sums["density"] += mk[4].elapsed_time(mk[5])
         return {s: sums[s] / steps for s in stage_names}
 
-    # per-stage means of the timed region; with several streams the views' stages overlap, so
-    # these intervals include other views' concurrent kernels.  The per-stage roofline uses a
-    # serial pass instead: the same steps with every stage of every view in order on one
-    # stream (no overlap), timed alike, right after the timed region
-    per_step_concurrent = stage_means(record, args.steps)
-    per_step = per_step_concurrent
-    concurrent = n_streams > 1 or sort_ahead
+    # per-stage means: with several streams the views' stages overlap (their intervals would
+    # include other views' kernels), so they come from a serial pass instead: the same steps
+    # with every stage of every view in order on one stream, right after the timed region
+    per_step = stage_means(record, args.steps)
     serial_steps = 0
-    if concurrent and args.serial_steps > 0 and not args.no_stage_events and not args.density_every:
+    if serial_pass:
         serial_steps = args.serial_steps
         pool2 = [torch.cuda.Event(enable_timing=True) for _ in range(serial_steps * (7 * n_mine + 11))]
         rec2 = {"next": 0, "marks": [], "pool": pool2}
@@ -915,10 +923,8 @@ def run_ours(args, rank, world, local_rank):
         "stages_ms_per_step": {k2: round(v2, 4) for k2, v2 in per_step.items()},
         "stages_timing": (f"serial pass: {serial_steps} steps after the timed region, every stage of every view in "
                           "order on one stream (the timed region overlaps views on "
-                          f"{n_streams} streams and sorts on {args.sort_streams})" if serial_steps else
-                          "the timed region's own stage events"),
-        "stages_ms_per_step_concurrent": ({k2: round(v2, 4) for k2, v2 in per_step_concurrent.items()}
-                                          if serial_steps else None),
+                          f"{n_streams} streams and sorts on {args.sort_streams}, and records no stage events)"
+                          if serial_steps else "the timed region's own stage events"),
         "stages_roofline": {k2: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v2.items()}
                             for k2, v2 in roof.items()},
         "workload": {"V_per_view": V, "K_per_view": K, "E_f_per_view": Ef, "E_b_per_view": Eb,

@@ -105,7 +105,8 @@ typedef struct {
   uint32_t* values_sorted;  /* [max_keys]                                            */
   uint32_t* ranges;         /* [tiles][2] [start, end) per tile, (0,0) if empty      */
   float* grad2d;            /* [n][12] per-view blend grads {dx, dy, dconic x,y,z, do,
-                               dr, dg, db, 0, 0, 0}; consumed and zeroed by render_bwd */
+                               dr, dg, db, 0, 0, 0}; zeroed by the preprocess (or, on a
+                               consuming frame, by the chain rule that reads it) */
   int64_t n, max_keys;
   int32_t tiles_x, tiles_y, sort_bits, sort_passes;
   int32_t sort_mode;        /* 0 depth-first (keys_* hold 32-bit tile ids), 1 onesweep64 */
@@ -464,6 +465,12 @@ bgs_status bgs_frame_set_debug(bgs_frame* f /*host*/, int32_t flags);
  * boundaries per item, as many as the frame's checkpoint pool holds; the rest of a walk
  * stays in its last segment).  Results agree with the unsplit walk to float rounding.
  * seg_len: multiple of 32 in [32, 65536].  BGS_ERR_INVALID otherwise. */
+/* Consuming frame (on != 0): every chain rule over all Gaussians (bgs_preprocess_bwd,
+ * _batch, _batch_adam, bgs_render_bwd) zeroes the frame's per-view blend gradients as it reads
+ * them, and the next bgs_preprocess of the frame then skips zeroing them (48 B per visible
+ * Gaussian of HBM writes).  A second chain rule over the same backward then sees zeros:
+ * leave it off (the default) to run several chain rules from one bgs_blend_bwd. */
+bgs_status bgs_frame_set_consume(bgs_frame* f /*host*/, int32_t on);
 bgs_status bgs_frame_set_seg_len(bgs_frame* f /*host*/, int32_t seg_len);
 
 const char* bgs_status_string(bgs_status s);

@@ -128,6 +128,7 @@ _SIGS = {
     "bgs_frame_stats": (C.c_int, [C.POINTER(Frame), _P, C.POINTER(Stats), _P]),
     "bgs_frame_validate": (C.c_int, [C.POINTER(Frame), _P, _P]),
     "bgs_render_fwd_plan": (C.c_int, [C.POINTER(Frame), _P]),
+    "bgs_frame_set_consume": (C.c_int, [C.POINTER(Frame), C.c_int32]),
     "bgs_blend_bwd_plan": (C.c_int, [C.POINTER(Frame), _P]),
     "bgs_nonfinite": (C.c_int, [_P, C.c_int64, _P, _P]),
     "bgs_frame_set_debug": (C.c_int, [C.POINTER(Frame), C.c_int32]),
@@ -329,6 +330,10 @@ def bgs_frame_stats(frame: Frame, n_contrib, stream=None) -> dict:
     s = Stats()
     _check(_lib.bgs_frame_stats(C.byref(frame), _ptr(n_contrib), C.byref(s), _stream(stream)), "bgs_frame_stats")
     return {k: int(getattr(s, k)) for k, _ in Stats._fields_}
+
+
+def bgs_frame_set_consume(frame: Frame, on: bool):
+    _check(_lib.bgs_frame_set_consume(C.byref(frame), 1 if on else 0), "bgs_frame_set_consume")
 
 
 def bgs_render_fwd_plan(frame: Frame, stream=None):

@@ -107,6 +107,10 @@ struct Frame {
   uint32_t* block_cost;    // [8 tiles] each block's largest n_contrib in the last forward
   int32_t have_cost, seg_len;  // block_cost holds this frame's previous forward; list segment length
   int32_t fwd_planned, bwd_planned;  // the next fwd's / bwd's work units are already built (plan-ahead)
+  // grad2d state of a consuming frame: 0 unknown (some slots may be non-zero), 1 all zero,
+  // 2 non-zero only in the slots of the last preprocess's visible Gaussians (one backward)
+  int32_t grad2d_clean;
+  int32_t consume_g2;    // bgs_frame_set_consume: the chain rule zeroes the blend gradients it reads
   int32_t counters_init;   // the sticky overflow word has been zeroed (first preprocess)
   uint32_t* ck_table;      // [8 tiles][kCkMax] pool slot of boundary b = 1..kCkMax of each block's walk
   float4* ck_pool;         // [ck_cap][32 lanes] {T, colour behind r, g, b} at a boundary
@@ -185,7 +189,8 @@ bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                               int shift, int64_t count, cudaStream_t s, const uint2* rect = nullptr,
                               uint32_t* rank_cnt = nullptr, uint2* rank_rect = nullptr,
-                              uint32_t* rank_h = nullptr, bool drop_culled = false, int64_t fill_to = 0);
+                              uint32_t* rank_h = nullptr, bool drop_culled = false, int64_t fill_to = 0,
+                              const uint32_t* gen_tt = nullptr);
 bgs_status launch_scan(const uint32_t* in, uint32_t* out, int64_t n, Frame* F, bool publish_k, cudaStream_t s);
 bgs_status launch_rowsplit(Frame* F, cudaStream_t s);
 bgs_status launch_adam_multimem(float* theta, float* theta_mc, float* grad_mc, float* m, float* v, int64_t n,

@@ -256,6 +256,8 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->block_cost = (uint32_t*)(base + L.block_cost);
   F->have_cost = 0;
   F->fwd_planned = F->bwd_planned = 0;
+  F->grad2d_clean = 0;
+  F->consume_g2 = 0;
   F->seg_len = kSegLenDefault;
   F->ck_table = (uint32_t*)(base + L.ck_table);
   F->ck_pool = (float4*)(base + L.ck_pool);
@@ -559,6 +561,13 @@ bgs_status bgs_frame_set_debug(bgs_frame* f, int32_t flags) {
   if (!frame_ok(f)) return BGS_ERR_INVALID;
   frame_of(f)->debug_flags = flags;
   frame_of(f)->fwd_planned = frame_of(f)->bwd_planned = 0;
+  return BGS_OK;
+}
+
+bgs_status bgs_frame_set_consume(bgs_frame* f, int32_t on) {
+  if (!frame_ok(f)) return BGS_ERR_INVALID;
+  frame_of(f)->consume_g2 = on ? 1 : 0;
+  frame_of(f)->grad2d_clean = 0;  // unknown until the next preprocess zeroes it
   return BGS_OK;
 }
 

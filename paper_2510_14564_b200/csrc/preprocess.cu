@@ -36,6 +36,7 @@ struct PreView {
   uint8_t* cbits;
   const uint8_t* keep;      // NEXT-4 keep mask or null
   int32_t square;           // R10 / R11's square rect instead of R11' (BGS_DEBUG_SQUARE_RECT)
+  int32_t zero_g2;          // zero the visible Gaussians' blend-gradient slots (not already zero)
 };
 
 // Up to kPreMaxViews views per launch: theta is read once per Gaussian for all of them
@@ -178,12 +179,15 @@ __device__ __forceinline__ uint32_t project_view(const PreView& pv, int64_t i, f
   float4* rec = pv.record + 3 * i;
   rec[1] = make_float4(-0.5f * conx, -cony, -0.5f * conz, g.o);
   rec[0] = make_float4(px, py, ex, ey);  // everything the per-warp cull test reads
-  // this view's blend-gradient accumulator (render_bwd REDs into it)
-  float4* g2 = pv.grad2d + 3 * i;
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  g2[0] = z4;
-  g2[1] = z4;
-  g2[2] = z4;
+  // this view's blend-gradient accumulator (render_bwd REDs into it), unless the frame's
+  // grad2d is known to be all zero (a consuming frame)
+  if (pv.zero_g2) {
+    float4* g2 = pv.grad2d + 3 * i;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    g2[0] = z4;
+    g2[1] = z4;
+    g2[2] = z4;
+  }
   return cb;
 }
 
@@ -453,6 +457,18 @@ bgs_status launch_preprocess_batch(const bgs_gaussians* g, Frame* const* F, int 
   p.n = F[0]->n;
   p.deg = g->sh_degree;
   const int64_t blocks = (p.n + 255) / 256;
+  for (int v = 0; v < nviews; ++v) {
+    // a consuming frame (bgs_frame_set_consume) keeps grad2d all zero between backwards: once
+    // it is in an unknown state, one memset restores that; a non-consuming frame has the
+    // kernel zero its visible Gaussians' slots every time
+    Frame* f = F[v];
+    if (f->consume_g2 && f->grad2d_clean != 1) {
+      if (cudaMemsetAsync(f->grad2d, 0, 48 * (size_t)f->n, s) != cudaSuccess) return check_launch("grad2d memset");
+      f->grad2d_clean = 1;
+    } else if (!f->consume_g2) {
+      f->grad2d_clean = 0;
+    }
+  }
   for (int v0 = 0; v0 < nviews; v0 += kPreMaxViews) {
     p.nviews = nviews - v0 < kPreMaxViews ? nviews - v0 : kPreMaxViews;
     for (int k = 0; k < p.nviews; ++k) {
@@ -468,6 +484,7 @@ bgs_status launch_preprocess_batch(const bgs_gaussians* g, Frame* const* F, int 
       pv.cbits = f->cbits;
       pv.keep = f->keep;
       pv.square = (f->debug_flags & BGS_DEBUG_SQUARE_RECT) ? 1 : 0;
+      pv.zero_g2 = f->grad2d_clean == 1 ? 0 : 1;
     }
     if (p.nviews == 1)
       k_preprocess<<<(unsigned)blocks, 256, 0, s>>>(p);

@@ -31,6 +31,7 @@ struct PreBwdView {
   const int32_t* radius;
   const uint8_t* cbits;
   const float4* grad2d;
+  float4* grad2d_zero;  // non-null: zero each slot after reading it (the frame's grad2d is then clean)
 };
 
 struct PreBwdParams {
@@ -398,6 +399,18 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
       dst[c] += s_dsh[warp][g * kRow + e];
     }
   }
+  // a consuming frame: the blend-gradient slots read above are left zero for its next
+  // backward (after all the arithmetic: the stores stay off the loads' pipeline; a warp's
+  // slots of one view are 1.5 KB contiguous)
+  for (int v = 0; v < p.nviews; ++v) {
+    float4* z = p.view[v].grad2d_zero;
+    if (z && ((vmask >> v) & 1u)) {
+      const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+      z[3 * i] = z4;
+      z[3 * i + 1] = z4;
+      z[3 * i + 2] = z4;
+    }
+  }
 }
 
 // a10 over a batch of views: grad += sum over the frames of each view's chain rule; with
@@ -449,11 +462,17 @@ bgs_status launch_preprocess_bwd_batch_impl(const bgs_gaussians* g, Frame* const
       p.view[v].radius = F->radius;
       p.view[v].cbits = F->cbits;
       p.view[v].grad2d = F->grad2d;
+      // a consuming frame (bgs_frame_set_consume): a launch over every Gaussian zeroes what it
+      // reads, so the next preprocess of the frame need not (a partial range leaves the frame
+      // to the preprocess's zeroing)
+      p.view[v].grad2d_zero = (F->consume_g2 && i0 == 0 && i1 == n) ? F->grad2d : nullptr;
     }
     k_preprocess_bwd<<<(unsigned)((i1 - i0 + kBwdThreads - 1) / kBwdThreads), kBwdThreads, 0, s>>>(p);
     note_launch();
     bgs_status st = check_launch("k_preprocess_bwd");
     if (st != BGS_OK) return st;
+    for (int v = 0; v < p.nviews; ++v)  // one backward's slots zeroed: all zero again
+      if (p.view[v].grad2d_zero) frames[v0 + v]->grad2d_clean = frames[v0 + v]->grad2d_clean == 2 ? 1 : 0;
   }
   return BGS_OK;
 }

@@ -16,7 +16,13 @@
 
 namespace bgs {
 
-constexpr int kSortThreads = 256, kSortItems = 16, kSortTile = kSortThreads * kSortItems, kRadix = 256;
+#ifndef BGS_SORT_ITEMS
+#define BGS_SORT_ITEMS 16
+#endif
+#ifndef BGS_SORT_MINB
+#define BGS_SORT_MINB 3
+#endif
+constexpr int kSortThreads = 256, kSortItems = BGS_SORT_ITEMS, kSortTile = kSortThreads * kSortItems, kRadix = 256;
 constexpr int kSortWarps = kSortThreads / 32;
 constexpr uint32_t kStA = 1u << 30, kStP = 2u << 30, kStMask = (1u << 30) - 1;
 #ifndef BGS_LOOK_BATCH
@@ -48,15 +54,17 @@ struct SortSmem {
 // ~0 (culled Gaussians) take no slot and are not written (the pass histogram excludes
 // them), so the depth sort's first pass compacts the visible Gaussians to [0, V).
 // fill_to > 0 (the depth sort's last pass): ranks [V, fill_to) get zero tile counts.
+// gen_tt != null (the depth sort's first pass): kin holds the depth bits of every Gaussian,
+// the key of Gaussian i is its depth bits if gen_tt[i] (tiles touched) else ~0, its value i.
 template <typename KT>
-__global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restrict__ kin,
+__global__ void __launch_bounds__(kSortThreads, BGS_SORT_MINB) k_sort_pass(const KT* __restrict__ kin,
                                                             const uint32_t* __restrict__ vin, KT* kout,
                                                             uint32_t* vout, const uint32_t* __restrict__ hist,
                                                             uint32_t* status, uint32_t* ticket,
                                                             const uint32_t* counters, int shift, int64_t count,
                                                             const uint2* __restrict__ rect, uint32_t* rank_cnt,
                                                             uint2* rank_rect, uint32_t* rank_h, bool drop_culled,
-                                                            int64_t fill_to) {
+                                                            int64_t fill_to, const uint32_t* __restrict__ gen_tt) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SortSmem<KT>& S = *reinterpret_cast<SortSmem<KT>*>(smem_raw);
   if (counters[C_OVERFLOW]) return;
@@ -98,8 +106,13 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_sort_pass(const KT* __restr
     for (int k = 0; k < kSortItems; ++k) {
       const int idx = wbase + k * 32 + lane;
       if (idx < tcount) {
-        key[k] = kin[tbase + idx];
-        val[k] = vin[tbase + idx];
+        if (gen_tt) {  // the depth sort's first pass: keys from the depths, values = indices
+          key[k] = gen_tt[tbase + idx] ? kin[tbase + idx] : culled;
+          val[k] = (uint32_t)(tbase + idx);
+        } else {
+          key[k] = kin[tbase + idx];
+          val[k] = vin[tbase + idx];
+        }
       } else {
         key[k] = (KT)~(KT)0;
         val[k] = 0;
@@ -246,7 +259,8 @@ bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* 
                             const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                             int shift, cudaStream_t s) {
   k_sort_pass<uint64_t><<<pass_grid<uint64_t>(), kSortThreads, sizeof(SortSmem<uint64_t>), s>>>(
-      kin, vin, kout, vout, hist, status, ticket, counters, shift, -1, nullptr, nullptr, nullptr, nullptr, false, 0);
+      kin, vin, kout, vout, hist, status, ticket, counters, shift, -1, nullptr, nullptr, nullptr, nullptr, false, 0,
+      nullptr);
   note_launch();
   return check_launch("k_sort_pass<u64>");
 }
@@ -254,10 +268,11 @@ bgs_status launch_sort_pass(const uint64_t* kin, const uint32_t* vin, uint64_t* 
 bgs_status launch_sort_pass32(const uint32_t* kin, const uint32_t* vin, uint32_t* kout, uint32_t* vout,
                               const uint32_t* hist, uint32_t* status, uint32_t* ticket, const uint32_t* counters,
                               int shift, int64_t count, cudaStream_t s, const uint2* rect, uint32_t* rank_cnt,
-                              uint2* rank_rect, uint32_t* rank_h, bool drop_culled, int64_t fill_to) {
+                              uint2* rank_rect, uint32_t* rank_h, bool drop_culled, int64_t fill_to,
+                              const uint32_t* gen_tt) {
   k_sort_pass<uint32_t><<<pass_grid<uint32_t>(), kSortThreads, sizeof(SortSmem<uint32_t>), s>>>(
       kin, vin, kout, vout, hist, status, ticket, counters, shift, count, rect, rank_cnt, rank_rect, rank_h,
-      drop_culled, fill_to);
+      drop_culled, fill_to, gen_tt);
   note_launch();
   return check_launch("k_sort_pass<u32>");
 }

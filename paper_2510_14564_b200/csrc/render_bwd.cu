@@ -481,6 +481,8 @@ bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final
     if (st != BGS_OK) return st;
   }
   F->bwd_planned = 0;
+  // the REDs below accumulate into the slots of this view's visible Gaussians
+  F->grad2d_clean = F->grad2d_clean == 1 ? 2 : 0;
   if (ppl == 2)
     k_render_bwd<2><<<bwd_grid<2>(), kBwdWarpsPerCta * 32, 0, s>>>(
         F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,

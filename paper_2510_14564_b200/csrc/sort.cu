@@ -133,13 +133,13 @@ constexpr bool kNoCompact = true;
 #else
 constexpr bool kNoCompact = false;
 #endif
-// 32-bit depth keys (culled: 0xffffffff) + the 4 pass histograms of the VISIBLE keys and
-// their count V (counters[C_VISIBLE]): the first pass drops the culled keys, so the other
-// three run over [0, V), and the ranks [V, N) own no tiles.
+// The 4 pass histograms of the VISIBLE Gaussians' 32-bit depth keys and their count V
+// (counters[C_VISIBLE]).  The first pass generates its (key, index) pairs from the depths
+// and tiles_touched itself (culled: key 0xffffffff, dropped), so the other three run over
+// [0, V), and the ranks [V, N) own no tiles.
 __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const float* __restrict__ depth,
                                                     const uint32_t* __restrict__ tiles_touched,
-                                                    uint32_t* counters, uint32_t* dkey, uint32_t* dval,
-                                                    uint32_t* hist) {
+                                                    uint32_t* counters, uint32_t* hist) {
   __shared__ uint32_t s_h[8][4][kRadixBins];  // one copy per warp: conflicts stay inside a warp
   __shared__ uint32_t s_vis;
   if (counters[C_OVERFLOW]) return;
@@ -150,10 +150,8 @@ __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const float* __re
   uint32_t vis = 0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const bool visible = tiles_touched[i] != 0;
-    const uint32_t key = visible ? __float_as_uint(depth[i]) : 0xffffffffu;
-    dkey[i] = key;
-    dval[i] = (uint32_t)i;
     if (visible || kNoCompact) {
+      const uint32_t key = visible ? __float_as_uint(depth[i]) : 0xffffffffu;
       ++vis;
 #pragma unroll
       for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(key >> (8 * p)) & 0xff], 1u);
@@ -163,7 +161,7 @@ __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const float* __re
   for (int d = 16; d > 0; d >>= 1) vis += __shfl_xor_sync(0xffffffffu, vis, d);
   if ((threadIdx.x & 31) == 0 && vis) atomicAdd(&s_vis, vis);
   __syncthreads();
-  if (threadIdx.x == 0 && s_vis) atomicAdd(&counters[C_VISIBLE], s_vis);
+  if (threadIdx.x == 0 && s_vis && !kNoCompact) atomicAdd(&counters[C_VISIBLE], s_vis);
   for (int k = threadIdx.x; k < 4 * kRadixBins; k += blockDim.x) {
     uint32_t v = 0;
 #pragma unroll
@@ -641,8 +639,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
     return BGS_OK;
   }
   // ---- depth first: (1) stable sort of the Gaussians by depth bits
-  k_depth_keys<<<grid, 256, 0, s>>>(F->n, F->depth, F->tiles_touched, F->counters, F->dkey[0], F->dval[0],
-                                    F->sort_hist);
+  k_depth_keys<<<grid, 256, 0, s>>>(F->n, F->depth, F->tiles_touched, F->counters, F->sort_hist);
   note_launch();
   if ((st = check_launch("k_depth_keys")) != BGS_OK) return st;
   for (int p = 0; p < 4; ++p) {
@@ -651,10 +648,13 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
     // the first pass compacts the visible Gaussians; (2) the last pass also writes the
     // per-rank tile counts and packed rects (zero past V)
     const bool last = p == 3;
-    st = launch_sort_pass32(F->dkey[a], F->dval[a], F->dkey[b], F->dval[b], F->sort_hist + p * kRadixBins,
+    // the first pass reads the depths and visibility directly (keys and values generated)
+    const uint32_t* kin = p ? F->dkey[a] : reinterpret_cast<const uint32_t*>(F->depth);
+    st = launch_sort_pass32(kin, p ? F->dval[a] : nullptr, F->dkey[b], F->dval[b], F->sort_hist + p * kRadixBins,
                             F->sort_status, F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, (p && !kNoCompact) ? -2 : F->n, s,
                             last ? F->rect : nullptr, last ? F->rank_cnt : nullptr, last ? F->rank_rect : nullptr,
-                            last ? F->rank_h : nullptr, p == 0 && !kNoCompact, last ? F->n : 0);
+                            last ? F->rank_h : nullptr, p == 0 && !kNoCompact, last ? F->n : 0,
+                            p ? nullptr : F->tiles_touched);
     if (st != BGS_OK) return st;
   }
   // K (published with the capacity check) = the total of the depth-order scan

@@ -105,3 +105,48 @@ def test_stale_plans_are_discarded(bgs):
     rel = float(torch.linalg.vector_norm(grad - ref[2]) / torch.linalg.vector_norm(ref[2]))
     assert rel <= 1e-5
     assert np.isfinite(grad.cpu().numpy()).all()
+
+
+def test_consuming_frame_equals_default(bgs):
+    """bgs_frame_set_consume: the chain rule zeroes the blend gradients it reads and the next
+    preprocess skips zeroing them -- two training steps give the same gradients as the
+    default frame, the slots are zero after each chain rule, and a second chain rule over
+    the same backward adds nothing."""
+    s = gen.small_scene(33, 5000, 160, 128, scale_mu=0.05)
+    cam = s.cameras[0]
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    g = bgs.gaussians(theta, s.n, s.sh_degree)
+    dl = torch.from_numpy(gen.random_dl_dimage(5, cam.width, cam.height)).to(dev)
+    outs = []
+    for consume in (False, True):
+        r = bgs.Renderer(s.n, cam.width, cam.height, max_keys=1 << 22, device=dev)
+        bgs.bgs_frame_set_consume(r.frame, consume)
+        grads = []
+        for it in range(2):
+            grad = torch.zeros_like(theta)
+            bgs.bgs_preprocess(g, bgs.camera(cam), r.frame)
+            bgs.bgs_sort(r.frame)
+            bgs.bgs_render_fwd(r.frame, r.image, r.final_T, r.n_contrib)
+            bgs.bgs_blend_bwd(r.frame, dl, r.final_T, r.n_contrib)
+            bgs.bgs_preprocess_bwd_batch(g, [r.frame], grad)
+            torch.cuda.synchronize()
+            grads.append(grad.clone())
+            v = r.views()
+            g2 = torch.as_tensor(_DevPtr(v.grad2d, 12 * s.n, "<f4"), device="cuda")
+            assert bool((g2 == 0).all()) == consume
+            if consume and it == 1:
+                again = torch.zeros_like(theta)
+                bgs.bgs_preprocess_bwd_batch(g, [r.frame], again)
+                torch.cuda.synchronize()
+                assert not bool(again.any())
+        outs.append(grads)
+    for a, b in zip(*outs):
+        rel = float(torch.linalg.vector_norm(a - b) / torch.linalg.vector_norm(a))
+        assert rel <= 1e-5
+
+
+class _DevPtr:
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": typestr, "data": (int(ptr), False),
+                                         "version": 2}
