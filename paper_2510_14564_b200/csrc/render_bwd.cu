@@ -32,30 +32,55 @@ constexpr int kBwdWarpsPerCta = 4;
 // return lane l holds the warp total of value `idx`, or idx = -1 (padding / duplicate).
 __device__ __forceinline__ float warp_reduce_scatter9(const float v[9], int lane, int& idx) {
   const bool a = lane & 16, b = lane & 8, c = lane & 4, d = lane & 2;
-  float s[5];
+  // each step: the lane keeps one half of its values and sends the other to its partner;
+  // the sums of a step go pairwise through FADD2
+  float k5[5], r5[5];
 #pragma unroll
   for (int j = 0; j < 5; ++j) {
     const float lo = v[j], hi = j < 4 ? v[5 + j] : 0.0f;
-    s[j] = (a ? hi : lo) + __shfl_xor_sync(0xffffffffu, a ? lo : hi, 16);
+    k5[j] = a ? hi : lo;
+    r5[j] = __shfl_xor_sync(0xffffffffu, a ? lo : hi, 16);
   }
-  float t[3];
+  const float2 s01 = __fadd2_rn(make_float2(k5[0], k5[1]), make_float2(r5[0], r5[1]));
+  const float2 s23 = __fadd2_rn(make_float2(k5[2], k5[3]), make_float2(r5[2], r5[3]));
+  const float s[5] = {s01.x, s01.y, s23.x, s23.y, k5[4] + r5[4]};
+  float k3[3], r3[3];
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
     const float lo = s[j], hi = j < 2 ? s[3 + j] : 0.0f;
-    t[j] = (b ? hi : lo) + __shfl_xor_sync(0xffffffffu, b ? lo : hi, 8);
+    k3[j] = b ? hi : lo;
+    r3[j] = __shfl_xor_sync(0xffffffffu, b ? lo : hi, 8);
   }
-  float u[2];
+  const float2 t01 = __fadd2_rn(make_float2(k3[0], k3[1]), make_float2(r3[0], r3[1]));
+  const float t[3] = {t01.x, t01.y, k3[2] + r3[2]};
+  float k2[2], r2[2];
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const float lo = t[j], hi = j < 1 ? t[2] : 0.0f;
-    u[j] = (c ? hi : lo) + __shfl_xor_sync(0xffffffffu, c ? lo : hi, 4);
+    k2[j] = c ? hi : lo;
+    r2[j] = __shfl_xor_sync(0xffffffffu, c ? lo : hi, 4);
   }
-  float w = (d ? u[1] : u[0]) + __shfl_xor_sync(0xffffffffu, d ? u[0] : u[1], 2);
+  const float2 u = __fadd2_rn(make_float2(k2[0], k2[1]), make_float2(r2[0], r2[1]));
+  float w = (d ? u.y : u.x) + __shfl_xor_sync(0xffffffffu, d ? u.x : u.y, 2);
   w += __shfl_xor_sync(0xffffffffu, w, 1);
   const int slot = (b ? 3 : 0) + (c ? 2 : 0) + (d ? 1 : 0);
   const bool valid = (b ? !c : !(c && d)) && !(a && slot == 4) && !(lane & 1);
   idx = valid ? (a ? 5 : 0) + slot : -1;
   return w;
+}
+
+__device__ __forceinline__ uint64_t f2_to_u64(float2 a) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(a.x), "f"(a.y));
+  return d;
+}
+__device__ __forceinline__ float2 f2_from_u64(uint64_t a) {
+  float2 d;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(a));
+  return d;
+}
+__device__ __forceinline__ void f2_mul_inplace(uint64_t& a, uint64_t b) {
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(a) : "l"(b));
 }
 
 __device__ __forceinline__ bool box_hits(const float4 a, float bx0, float by0, float bx1, float by1) {
@@ -66,24 +91,18 @@ __device__ __forceinline__ bool box_hits(const float4 a, float bx0, float by0, f
 // block (two vertically adjacent forward items, lane l on pixels (x, y) and (x, y + 4)):
 // each entry's staging, shared-memory record reads and 9-value warp reduction then serve
 // 64 pixels instead of 32.
-template <int PPL>
+template <int PPL, bool CANON>
 __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     const uint2* __restrict__ ranges, const uint32_t* __restrict__ values, const float4* __restrict__ record,
     const uint32_t* __restrict__ counters, Cam cam, const uint32_t* __restrict__ units, uint32_t* ticket,
     const float* __restrict__ dl_dimage, const float* __restrict__ final_T, const uint32_t* __restrict__ n_contrib,
     float4* __restrict__ grad2d, int32_t seg_len, const uint32_t* __restrict__ ck_table,
-    const float4* __restrict__ ck_pool, int32_t canon) {
-  __shared__ float4 s_rec[kBwdWarpsPerCta][3][32];
-  __shared__ uint32_t s_pos[kBwdWarpsPerCta][32];
-  __shared__ uint32_t s_id[kBwdWarpsPerCta][32];
+    const float4* __restrict__ ck_pool) {
+  __shared__ float4 s_rec[kBwdWarpsPerCta][32 * 3];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t lt = lanemask_lt();
   const bool overflow = counters[C_OVERFLOW] != 0;
-  float4* sr0 = s_rec[warp][0];
-  float4* sr1 = s_rec[warp][1];
-  float4* sr2 = s_rec[warp][2];
-  uint32_t* spos = s_pos[warp];
-  uint32_t* sid = s_id[warp];
+  float4* srec = s_rec[warp];
   const int64_t plane = (int64_t)cam.W * cam.H;
   const float4 none = make_float4(-1e30f, -1e30f, -1e30f, -1e30f);
   const uint32_t n_units = counters[C_BWD_UNITS];
@@ -158,7 +177,10 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     }
     // PPL == 2: the two pixels' state as pairs for the FP32x2 instructions (FFMA2 / FMUL2 /
     // FADD2 of sm_100: one instruction, two separately rounded results)
-    float2 T2 = make_float2(T[0], T[PPL - 1]), DS2 = make_float2(DS[0], DS[PPL - 1]);
+    // (T2 is carried as one 64-bit register pair: as a float2 the allocator split it over two
+    // unrelated registers and copied it into a pair around every entry)
+    uint64_t T2u = f2_to_u64(make_float2(T[0], T[PPL - 1]));
+    float2 DS2 = make_float2(DS[0], DS[PPL - 1]);
     const float2 dLr2 = make_float2(dLr[0], dLr[PPL - 1]), dLg2 = make_float2(dLg[0], dLg[PPL - 1]),
                  dLb2 = make_float2(dLb[0], dLb[PPL - 1]), npy2 = make_float2(-pyf[0], -pyf[PPL - 1]);
     const int nst = (top - lo + 31) / 32;
@@ -188,11 +210,9 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
       const uint32_t bal = __ballot_sync(0xffffffffu, h_c);
       if (h_c) {
         const int q = __popc(bal & lt);
-        sr0[q] = a_c;
-        sr1[q] = r1_c;
-        sr2[q] = r2_c;
-        spos[q] = (uint32_t)pos_of(s);
-        sid[q] = id_c;
+        srec[3 * q] = make_float4(a_c.x, a_c.y, __uint_as_float((uint32_t)pos_of(s)), __uint_as_float(id_c));
+        srec[3 * q + 1] = r1_c;
+        srec[3 * q + 2] = r2_c;
       }
       __syncwarp();
       // (2) step s+1: hit test and its full records; (3) step s+2 cull record, s+3 id
@@ -210,139 +230,127 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
       // are applied to the warp totals
       const int m = __popc(bal);
       for (int k = m - 1; k >= 0; --k) {
-        const uint32_t pos = spos[k];
+        // entry k of the step: {x, y, list position, id}, {A, B, C, o}, {r, g, b, pthr}
+        const float4 r0 = srec[3 * k];
+        const float4 r1 = srec[3 * k + 1];
+        const float4 r2 = srec[3 * k + 2];
+        const uint32_t pos = __float_as_uint(r0.z);
         bool any_act = false;
-        float g0 = 0.f, g1 = 0.f, g2 = 0.f, g3 = 0.f, g4 = 0.f, g5 = 0.f, g6 = 0.f, g7 = 0.f, g8 = 0.f;
+        float g0, g1, g2, g3, g4, g5, g6, g7, g8;
         if constexpr (PPL == 2) {
           // both pixels of the lane at once, without per-pixel branches: a pixel that does not
           // take the entry gets alpha = 0 (1 / (1 - 0) = 1 exactly, weight 0), so its T, DS and
           // partials are unchanged; an entry no pixel of the warp takes is skipped uniformly
-          const bool a0 = pos < my_last[0], a1 = pos < my_last[1];
-          if (!__any_sync(0xffffffffu, a0 | a1)) goto reduce;
-          {
-            const float4 r0 = sr0[k];
-            const float4 r1 = sr1[k];
-            const float4 r2 = sr2[k];
-            const float dx = r0.x - pxf;
-            const float dxx = dx * dx;
-            const float2 dx2 = make_float2(dx, dx);
-            const float2 dy2 = __fadd2_rn(make_float2(r0.y, r0.y), npy2);
-            const float2 dyy2 = __fmul2_rn(dy2, dy2), dxy2 = __fmul2_rn(dx2, dy2);
-            const float2 pw = __ffma2_rn(make_float2(r1.x, r1.x), make_float2(dxx, dxx),
-                                         __ffma2_rn(make_float2(r1.z, r1.z), dyy2,
-                                                    __fmul2_rn(make_float2(r1.y, r1.y), dxy2)));
-            // power below the exact alpha < 1/255 bound (pthr) or R14's power > 0 guard
-            const bool c0 = a0 & !(pw.x > 0.0f) & !(pw.x < r2.w), c1 = a1 & !(pw.y > 0.0f) & !(pw.y < r2.w);
-            if (!__any_sync(0xffffffffu, c0 | c1)) goto reduce;
-            const float G0 = canon ? canon_exp(pw.x) : fast_exp(pw.x);
-            const float G1 = canon ? canon_exp(pw.y) : fast_exp(pw.y);
-            const float2 og2 = __fmul2_rn(make_float2(r1.w, r1.w), make_float2(G0, G1));
-            const float al0 = fminf(0.99f, og2.x), al1 = fminf(0.99f, og2.y);
-            const bool t0 = c0 & (al0 >= (1.0f / 255.0f)), t1 = c1 & (al1 >= (1.0f / 255.0f));
-            any_act = t0 | t1;
-            const float2 al2 = make_float2(t0 ? al0 : 0.0f, t1 ? al1 : 0.0f);
-            const float2 om2 = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al2.x, -al2.y));
-            // MUFU reciprocal (1 - alpha >= 0.01): ~2^-22 relative per step, far inside the
-            // 1e-3 gradient tolerance, instead of the multi-instruction IEEE division
-            const float2 io2 = make_float2(fast_rcp(om2.x), fast_rcp(om2.y));
-            T2 = __fmul2_rn(T2, io2);  // transmittance in front of this Gaussian
-            const float2 w2 = __fmul2_rn(al2, T2);
-            const float2 p6 = __fmul2_rn(w2, dLr2), p7 = __fmul2_rn(w2, dLg2), p8 = __fmul2_rn(w2, dLb2);
-            g6 = p6.x + p6.y;
-            g7 = p7.x + p7.y;
-            g8 = p8.x + p8.y;
-            // dL/dalpha = T (dL . c) - DS / (1 - alpha); DS += (dL . c) w
-            const float2 dLc2 = __ffma2_rn(dLb2, make_float2(r2.z, r2.z),
-                                           __ffma2_rn(dLg2, make_float2(r2.y, r2.y),
-                                                      __fmul2_rn(dLr2, make_float2(r2.x, r2.x))));
-            const float2 dsi = __fmul2_rn(DS2, io2);
-            const float2 dLda2 = __ffma2_rn(T2, dLc2, make_float2(-dsi.x, -dsi.y));
-            DS2 = __ffma2_rn(dLc2, w2, DS2);
-            // unclamped alpha: gradient to opacity and G (R18)
-            // (the factors of pixels that do not take the entry are zeroed, not just dL/dalpha:
-            // G and o G of a skipped power > 0 may be infinite)
-            const bool u0 = t0 & (og2.x <= 0.99f), u1 = t1 & (og2.y <= 0.99f);
-            const float2 dl2 = make_float2(u0 ? dLda2.x : 0.0f, u1 ? dLda2.y : 0.0f);
-            const float2 p5 = __fmul2_rn(dl2, make_float2(u0 ? G0 : 0.0f, u1 ? G1 : 0.0f));
-            g5 = p5.x + p5.y;
-            const float2 dp2 = __fmul2_rn(dl2, make_float2(u0 ? og2.x : 0.0f, u1 ? og2.y : 0.0f));  // dL/dpower
-            const float2 e0 = __ffma2_rn(make_float2(2.0f * r1.x, 2.0f * r1.x), dx2,
-                                         __fmul2_rn(make_float2(r1.y, r1.y), dy2));
-            const float2 e1 = __ffma2_rn(make_float2(2.0f * r1.z, 2.0f * r1.z), dy2,
-                                         __fmul2_rn(make_float2(r1.y, r1.y), dx2));
-            const float2 p0 = __fmul2_rn(dp2, e0), p1 = __fmul2_rn(dp2, e1);
-            const float2 p2 = __fmul2_rn(dp2, make_float2(dxx, dxx)), p3 = __fmul2_rn(dp2, dxy2),
-                         p4 = __fmul2_rn(dp2, dyy2);
-            g0 = p0.x + p0.y;
-            g1 = p1.x + p1.y;
-            g2 = p2.x + p2.y;
-            g3 = p3.x + p3.y;
-            g4 = p4.x + p4.y;
-          }
-        } else {
-        bool act[PPL];
-#pragma unroll
-        for (int h = 0; h < PPL; ++h) act[h] = pos < my_last[h];
-        bool act_any = act[0];
-#pragma unroll
-        for (int h = 1; h < PPL; ++h) act_any |= act[h];
-        if (act_any) {
-          const float4 r0 = sr0[k];
-          const float4 r1 = sr1[k];
-          const float4 r2 = sr2[k];
           const float dx = r0.x - pxf;
           const float dxx = dx * dx;
-#pragma unroll
-          for (int h = 0; h < PPL; ++h) {
-            if (!act[h]) continue;
-            const float dy = r0.y - pyf[h];
+          const float2 dx2 = make_float2(dx, dx);
+          const float2 dy2 = __fadd2_rn(make_float2(r0.y, r0.y), npy2);
+          const float2 dyy2 = __fmul2_rn(dy2, dy2), dxy2 = __fmul2_rn(dx2, dy2);
+          const float2 pw = __ffma2_rn(make_float2(r1.x, r1.x), make_float2(dxx, dxx),
+                                       __ffma2_rn(make_float2(r1.z, r1.z), dyy2,
+                                                  __fmul2_rn(make_float2(r1.y, r1.y), dxy2)));
+          // the pixel's walk reaches the entry, and the power is neither below the exact
+          // alpha < 1/255 bound (pthr) nor above R14's power > 0 guard
+          const bool c0 = (pos < my_last[0]) & !(pw.x > 0.0f) & !(pw.x < r2.w);
+          const bool c1 = (pos < my_last[1]) & !(pw.y > 0.0f) & !(pw.y < r2.w);
+          if (!__any_sync(0xffffffffu, c0 | c1)) continue;
+          // min(power, 0): G <= 1 is finite for the pixels that skip the entry too, so their
+          // zeroed dL/dalpha zeroes every partial (power <= 0 wherever the entry is taken)
+          const float G0 = CANON ? canon_exp(fminf(pw.x, 0.0f)) : fast_exp(fminf(pw.x, 0.0f));
+          const float G1 = CANON ? canon_exp(fminf(pw.y, 0.0f)) : fast_exp(fminf(pw.y, 0.0f));
+          const float2 og2 = __fmul2_rn(make_float2(r1.w, r1.w), make_float2(G0, G1));
+          const float al0 = fminf(0.99f, og2.x), al1 = fminf(0.99f, og2.y);
+          const bool t0 = c0 & (al0 >= (1.0f / 255.0f)), t1 = c1 & (al1 >= (1.0f / 255.0f));
+          any_act = t0 | t1;
+          const float2 al2 = make_float2(t0 ? al0 : 0.0f, t1 ? al1 : 0.0f);
+          const float2 om2 = __fadd2_rn(make_float2(1.0f, 1.0f), make_float2(-al2.x, -al2.y));
+          // MUFU reciprocal (1 - alpha >= 0.01): ~2^-22 relative per step, far inside the
+          // 1e-3 gradient tolerance, instead of the multi-instruction IEEE division
+          const float2 io2 = make_float2(fast_rcp(om2.x), fast_rcp(om2.y));
+          f2_mul_inplace(T2u, f2_to_u64(io2));  // transmittance in front of this Gaussian
+          const float2 T2 = f2_from_u64(T2u);
+          const float2 w2 = __fmul2_rn(al2, T2);
+          const float2 p6 = __fmul2_rn(w2, dLr2), p7 = __fmul2_rn(w2, dLg2), p8 = __fmul2_rn(w2, dLb2);
+          // dL/dalpha = T (dL . c) - DS / (1 - alpha); DS += (dL . c) w
+          const float2 dLc2 = __ffma2_rn(dLb2, make_float2(r2.z, r2.z),
+                                         __ffma2_rn(dLg2, make_float2(r2.y, r2.y),
+                                                    __fmul2_rn(dLr2, make_float2(r2.x, r2.x))));
+          const float2 dsi = __fmul2_rn(DS2, io2);
+          const float2 dLda2 = __ffma2_rn(T2, dLc2, make_float2(-dsi.x, -dsi.y));
+          DS2 = __ffma2_rn(dLc2, w2, DS2);
+          // unclamped alpha: gradient to opacity and G (R18)
+          const bool u0 = t0 & (og2.x <= 0.99f), u1 = t1 & (og2.y <= 0.99f);
+          const float2 dl2 = make_float2(u0 ? dLda2.x : 0.0f, u1 ? dLda2.y : 0.0f);
+          const float2 p5 = __fmul2_rn(dl2, make_float2(G0, G1));
+          const float2 dp2 = __fmul2_rn(dl2, og2);  // dL/dpower
+          const float2 e0 = __ffma2_rn(make_float2(2.0f * r1.x, 2.0f * r1.x), dx2,
+                                       __fmul2_rn(make_float2(r1.y, r1.y), dy2));
+          const float2 e1 = __ffma2_rn(make_float2(2.0f * r1.z, 2.0f * r1.z), dy2,
+                                       __fmul2_rn(make_float2(r1.y, r1.y), dx2));
+          const float2 p0 = __fmul2_rn(dp2, e0), p1 = __fmul2_rn(dp2, e1);
+          const float2 p2 = __fmul2_rn(dp2, make_float2(dxx, dxx)), p3 = __fmul2_rn(dp2, dxy2),
+                       p4 = __fmul2_rn(dp2, dyy2);
+          g0 = p0.x + p0.y;
+          g1 = p1.x + p1.y;
+          g2 = p2.x + p2.y;
+          g3 = p3.x + p3.y;
+          g4 = p4.x + p4.y;
+          g5 = p5.x + p5.y;
+          g6 = p6.x + p6.y;
+          g7 = p7.x + p7.y;
+          g8 = p8.x + p8.y;
+        } else {
+          g0 = g1 = g2 = g3 = g4 = g5 = g6 = g7 = g8 = 0.0f;
+          if (pos < my_last[0]) {
+            const float dx = r0.x - pxf;
+            const float dxx = dx * dx;
+            const float dy = r0.y - pyf[0];
             const float dyy = dy * dy, dxy = dx * dy;
             const float power = fmaf(r1.x, dxx, fmaf(r1.z, dyy, r1.y * dxy));
             // power below the exact alpha < 1/255 bound (pthr): skipped without the MUFU path
-            if (power > 0.0f || power < r2.w) continue;
-            const float G = canon ? canon_exp(power) : fast_exp(power);
-            const float og = r1.w * G;
-            const float alpha = fminf(0.99f, og);
-            if (alpha < (1.0f / 255.0f)) continue;
-            any_act = true;
-            // MUFU reciprocal (1 - alpha >= 0.01): ~2^-22 relative per step, far inside the
-            // 1e-3 gradient tolerance, instead of the multi-instruction IEEE division
-            const float ioma = __fdividef(1.0f, 1.0f - alpha);
-            T[h] = T[h] * ioma;  // transmittance in front of this Gaussian
-            const float w = alpha * T[h];
-            g6 = fmaf(w, dLr[h], g6);
-            g7 = fmaf(w, dLg[h], g7);
-            g8 = fmaf(w, dLb[h], g8);
-            // dL/dalpha = sum_c dL_c (c_c T - S_c / (1 - alpha)) = T (dL . c) - DS / (1 - alpha)
-            const float dLc = fmaf(dLb[h], r2.z, fmaf(dLg[h], r2.y, dLr[h] * r2.x));
-            const float dLda = fmaf(T[h], dLc, -(DS[h] * ioma));
-            DS[h] = fmaf(dLc, w, DS[h]);  // S += c w
-            if (og <= 0.99f) {  // unclamped alpha: gradient to opacity and G (R18)
-              g5 = fmaf(dLda, G, g5);
-              const float dp = dLda * og;  // dL/dpower
-              g0 = fmaf(dp, fmaf(2.0f * r1.x, dx, r1.y * dy), g0);
-              g1 = fmaf(dp, fmaf(2.0f * r1.z, dy, r1.y * dx), g1);
-              g2 = fmaf(dp, dxx, g2);
-              g3 = fmaf(dp, dxy, g3);
-              g4 = fmaf(dp, dyy, g4);
+            if (!(power > 0.0f || power < r2.w)) {
+              const float G = CANON ? canon_exp(power) : fast_exp(power);
+              const float og = r1.w * G;
+              const float alpha = fminf(0.99f, og);
+              if (alpha >= (1.0f / 255.0f)) {
+                any_act = true;
+                const float ioma = __fdividef(1.0f, 1.0f - alpha);
+                T[0] = T[0] * ioma;  // transmittance in front of this Gaussian
+                const float w = alpha * T[0];
+                g6 = w * dLr[0];
+                g7 = w * dLg[0];
+                g8 = w * dLb[0];
+                // dL/dalpha = sum_c dL_c (c_c T - S_c / (1 - alpha)) = T (dL . c) - DS / (1 - alpha)
+                const float dLc = fmaf(dLb[0], r2.z, fmaf(dLg[0], r2.y, dLr[0] * r2.x));
+                const float dLda = fmaf(T[0], dLc, -(DS[0] * ioma));
+                DS[0] = fmaf(dLc, w, DS[0]);  // S += c w
+                if (og <= 0.99f) {  // unclamped alpha: gradient to opacity and G (R18)
+                  g5 = dLda * G;
+                  const float dp = dLda * og;  // dL/dpower
+                  g0 = dp * fmaf(2.0f * r1.x, dx, r1.y * dy);
+                  g1 = dp * fmaf(2.0f * r1.z, dy, r1.y * dx);
+                  g2 = dp * dxx;
+                  g3 = dp * dxy;
+                  g4 = dp * dyy;
+                }
+              }
             }
           }
         }
-        }
-      reduce:;
         const uint32_t actm = __ballot_sync(0xffffffffu, any_act);
+        const uint32_t id = __float_as_uint(r0.w);
         if (__popc(actm) > 8) {
           const float gv[9] = {g0, g1, g2, g3, g4, g5, g6, g7, g8};
           int idx;
           const float tot = warp_reduce_scatter9(gv, lane, idx);
           // 9 lanes, 9 consecutive floats of grad2d[id]: one RED instruction (the conic
           // partials take their constant factor here, once per entry)
-          if (idx >= 0) atomicAdd(reinterpret_cast<float*>(grad2d + 3 * sid[k]) + idx, tot * red_mul);
+          if (idx >= 0) atomicAdd(reinterpret_cast<float*>(grad2d + 3 * id) + idx, tot * red_mul);
         } else if (any_act) {
           // at most 8 active lanes (an entry at the edge of its footprint): 9 REDs from each
           // instead of the 12-shuffle reduce-scatter.  Garden: blend bwd 20.65 -> 20.4 ms per
           // step at <= 8; <= 16 lanes is slower (22.6 ms: same-address L2 atomics)
-          float* dst = reinterpret_cast<float*>(grad2d + 3 * sid[k]);
+          float* dst = reinterpret_cast<float*>(grad2d + 3 * id);
           atomicAdd(dst + 0, g0);
           atomicAdd(dst + 1, g1);
           atomicAdd(dst + 2, -0.5f * g2);
@@ -368,12 +376,12 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
   }
 }
 
-template <int PPL>
+template <int PPL, bool CANON>
 static int bwd_grid() {
   static int grid = 0;
   if (!grid) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_bwd<PPL>, kBwdWarpsPerCta * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_bwd<PPL, CANON>, kBwdWarpsPerCta * 32, 0);
     grid = (per_sm < 1 ? 1 : per_sm) * num_sms();
   }
   return grid;
@@ -483,16 +491,19 @@ bgs_status launch_blend_bwd(Frame* F, const float* dL_dimage, const float* final
   F->bwd_planned = 0;
   // the REDs below accumulate into the slots of this view's visible Gaussians
   F->grad2d_clean = F->grad2d_clean == 1 ? 2 : 0;
-  if (ppl == 2)
-    k_render_bwd<2><<<bwd_grid<2>(), kBwdWarpsPerCta * 32, 0, s>>>(
-        F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,
-        dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool,
-        (F->debug_flags & BGS_DEBUG_PARITY_EXP) ? 1 : 0);
-  else
-    k_render_bwd<1><<<bwd_grid<1>(), kBwdWarpsPerCta * 32, 0, s>>>(
-        F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET,
-        dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool,
-        (F->debug_flags & BGS_DEBUG_PARITY_EXP) ? 1 : 0);
+  const bool canon = (F->debug_flags & BGS_DEBUG_PARITY_EXP) != 0;
+#define BGS_BWD_LAUNCH(P, C)                                                                                    \
+  k_render_bwd<P, C><<<bwd_grid<P, C>(), kBwdWarpsPerCta * 32, 0, s>>>(                                         \
+      F->ranges, F->vals[F->final_buf], F->record, F->counters, F->cam, F->order_bwd, F->counters + C_BWD_TICKET, \
+      dL_dimage, final_T, n_contrib, F->grad2d, F->seg_len, F->ck_table, F->ck_pool)
+  if (ppl == 2) {
+    if (canon) BGS_BWD_LAUNCH(2, true);
+    else BGS_BWD_LAUNCH(2, false);
+  } else {
+    if (canon) BGS_BWD_LAUNCH(1, true);
+    else BGS_BWD_LAUNCH(1, false);
+  }
+#undef BGS_BWD_LAUNCH
   note_launch();
   return check_launch("k_render_bwd");
 }
