@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
     float4 a_n = load_cull(id_n);
     uint32_t id_nn = load_id(2);
     bool h_c = box_hits(a_c, bx0, by0, bx1, by1);
-    float4 r1_c = none, r2_c = none;
+    float4 r1_c, r2_c;  // loaded (and read) only for a hit
     if (h_c) {
       r1_c = __ldg(record + 3 * id_c + 1);
       r2_c = __ldg(record + 3 * id_c + 2);
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
       __syncwarp();
       // (2) step s+1: hit test and its full records; (3) step s+2 cull record, s+3 id
       const bool h_n = box_hits(a_n, bx0, by0, bx1, by1);
-      float4 r1_n = none, r2_n = none;
+      float4 r1_n, r2_n;
       if (h_n) {
         r1_n = __ldg(record + 3 * id_n + 1);
         r2_n = __ldg(record + 3 * id_n + 2);

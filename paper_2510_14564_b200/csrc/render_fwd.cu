@@ -72,9 +72,9 @@ struct FwdArgs {
   uint32_t* arrive;           // segments of a split item finished so far
   float4* spec_state;         // [slot][32] {T or prod(1 - alpha), C rgb}
   uint32_t* spec_last;        // [slot][32] last | stopped << 31
-  int32_t canon;              // BGS_DEBUG_PARITY_EXP: canon_exp instead of MUFU.EX2
 };
 
+template <bool CANON>
 __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const FwdArgs a, const Cam cam) {
   __shared__ float4 s_rec[kFwdWarps][3][32];
   __shared__ uint32_t s_pos[kFwdWarps][32];
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const FwdArgs a, 
         float4 a_n = load_cull(id_n);
         uint32_t id_nn = load_id(s_lo + 2);
         bool h_c = box_hits_f(a_c, bx0, by0, bx1, by1);
-        float4 r1_c = none, r2_c = none;
+        float4 r1_c, r2_c;  // loaded (and read) only for a hit
         if (h_c) {
           r1_c = __ldg(a.record + 3 * id_c + 1);
           r2_c = __ldg(a.record + 3 * id_c + 2);
@@ -176,30 +176,31 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const FwdArgs a, 
           __syncwarp();
           // (2) step s+1 hit test and records; (3) step s+2 cull record, step s+3 id
           const bool h_n = box_hits_f(a_n, bx0, by0, bx1, by1);
-          float4 r1_n = none, r2_n = none;
+          float4 r1_n, r2_n;
           if (h_n) {
             r1_n = __ldg(a.record + 3 * id_n + 1);
             r2_n = __ldg(a.record + 3 * id_n + 2);
           }
           const float4 a_nn = load_cull(id_nn);
           const uint32_t id_nnn = load_id(s + 3);
-          // (4) walk step s
+          // (4) walk step s.  A finished pixel skips every entry through doff = -inf (power +
+          // doff < pthr), so one compare pair carries "done", R14's power > 0 guard and the
+          // exact alpha < 1/255 bound (pthr, preprocess; it skips the MUFU path)
           const int m = __popc(bal);
           int lastk = -1;
+          float doff = done ? -INFINITY : 0.0f;
           for (int k = 0; k < m; ++k) {
             const float4 r0 = sr0[k];
             const float4 r1 = sr1[k];
             const float4 r2 = sr2[k];
             const float dx = r0.x - pxf, dy = r0.y - pyf;
             const float power = fmaf(r1.x, dx * dx, fmaf(r1.z, dy * dy, r1.y * (dx * dy)));
-            // one predicate: pixel done, R14's power > 0 guard, or power below the exact
-            // alpha < 1/255 bound (pthr, preprocess) -- the last skips the MUFU path
-            if (done | (power > 0.0f) | (power < r2.w)) continue;
-            const float alpha = fminf(0.99f, r1.w * (a.canon ? canon_exp(power) : fast_exp(power)));
+            if ((power > 0.0f) | (power + doff < r2.w)) continue;
+            const float alpha = fminf(0.99f, r1.w * (CANON ? canon_exp(power) : fast_exp(power)));
             if (alpha < (1.0f / 255.0f)) continue;
             const float tT = T * (1.0f - alpha);
             if (tT < 1e-4f) {
-              done = true;
+              doff = -INFINITY;
               continue;
             }
             const float w = alpha * T;
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(kFwdWarps * 32) k_render_fwd(const FwdArgs a, 
             T = tT;
             lastk = k;
           }
+          done = doff < 0.0f;
           if (lastk >= 0) last = spos[lastk] + 1u;
           __syncwarp();
           if (__all_sync(0xffffffffu, done)) break;
@@ -448,7 +450,7 @@ static int fwd_grid() {
   static int grid = 0;
   if (!grid) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fwd, kFwdWarps * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render_fwd<false>, kFwdWarps * 32, 0);
     grid = (per_sm < 1 ? 1 : per_sm) * num_sms();
   }
   return grid;
@@ -500,8 +502,8 @@ bgs_status launch_render_fwd(Frame* F, float* image, float* final_T, uint32_t* n
   a.arrive = F->arrive;
   a.spec_state = F->spec_state;
   a.spec_last = F->spec_last;
-  a.canon = parity ? 1 : 0;
-  k_render_fwd<<<fwd_grid(), kFwdWarps * 32, 0, s>>>(a, F->cam);
+  if (parity) k_render_fwd<true><<<fwd_grid(), kFwdWarps * 32, 0, s>>>(a, F->cam);
+  else k_render_fwd<false><<<fwd_grid(), kFwdWarps * 32, 0, s>>>(a, F->cam);
   note_launch();
   F->have_cost = 1;
   return check_launch("k_render_fwd");
