@@ -75,7 +75,8 @@ __device__ __forceinline__ void put_grad(const PreBwdParams& p, int64_t e, float
 }
 
 constexpr int kBwdThreads = 64;
-constexpr int kRow = 49;  // padded row stride (floats) of the staged SH block: conflict-free
+constexpr int kRow = 52;  // padded row stride (floats) of the staged SH block: 16-byte rows,
+                          // conflict-free for 16-byte accesses (8 lanes of a phase: 20 l mod 32)
 
 // Real SH constants (R12).
 constexpr float kC0 = 0.28209479177387814f, kC1 = 0.4886025119029199f;
@@ -91,8 +92,8 @@ constexpr float kC30 = -0.5900435899266435f, kC31 = 2.890611442640554f, kC32 = -
 // per view only the camera-dependent terms are evaluated, and dL/dSigma, dL/dmu,
 // dL/dopacity and dL/dsh are summed in registers / shared memory across the views.
 __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_constant__ PreBwdParams p) {
-  __shared__ float s_sh[kBwdThreads / 32][32 * kRow];   // SH coefficients (read-only)
-  __shared__ float s_dsh[kBwdThreads / 32][32 * kRow];  // dL/dsh, summed over the views
+  __shared__ __align__(16) float s_sh[kBwdThreads / 32][32 * kRow];   // SH coefficients (read-only)
+  __shared__ __align__(16) float s_dsh[kBwdThreads / 32][32 * kRow];  // dL/dsh, summed over the views
   __shared__ int s_vis[kBwdThreads / 32][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t n = p.n;
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
   float* drow = &s_dsh[warp][lane * kRow];
   const int ncoef = (p.deg + 1) * (p.deg + 1);
   const int64_t nvalid = p.i1 - wbase < 32 ? p.i1 - wbase : 32;
-  for (int k = 0; k < 48; ++k) drow[k] = 0.f;
+  for (int k = 0; k < 12; ++k) reinterpret_cast<float4*>(drow)[k] = make_float4(0.f, 0.f, 0.f, 0.f);
   __syncwarp();
   // ---- coalesced load of the warp's SH block into shared memory
   if (p.sh_vec4) {
@@ -116,8 +117,7 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
       const int g = c / 12, e = 4 * (c % 12);
       if (!s_vis[warp][g] || e >= 3 * ncoef) continue;
       const float4 v = __ldg(src + c);
-      float* r = &s_sh[warp][g * kRow + e];
-      r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
+      *reinterpret_cast<float4*>(&s_sh[warp][g * kRow + e]) = v;
     }
   } else {
     const float* src = p.sh + 48 * wbase;
@@ -190,38 +190,67 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
         const float x = dxw * il, y = dyw * il, z = dzw * il;
         const float xx = x * x, yy = y * y, zz = z * z;
         float ddx = 0.f, ddy = 0.f, ddz = 0.f;
+        // the coefficients in groups of four (12 floats = 3 16-byte chunks of the staged row
+        // and of the gradient row): 36 shared-memory accesses per view instead of 144
+        float rv[12], dv[12];
+        auto load_group = [&](int j) {
+          const float4* r4 = reinterpret_cast<const float4*>(row) + 3 * j;
+          const float4* d4 = reinterpret_cast<const float4*>(drow) + 3 * j;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const float4 a = r4[q], b = d4[q];
+            rv[4 * q] = a.x; rv[4 * q + 1] = a.y; rv[4 * q + 2] = a.z; rv[4 * q + 3] = a.w;
+            dv[4 * q] = b.x; dv[4 * q + 1] = b.y; dv[4 * q + 2] = b.z; dv[4 * q + 3] = b.w;
+          }
+        };
+        auto store_group = [&](int j) {
+          float4* d4 = reinterpret_cast<float4*>(drow) + 3 * j;
+#pragma unroll
+          for (int q = 0; q < 3; ++q) d4[q] = make_float4(dv[4 * q], dv[4 * q + 1], dv[4 * q + 2], dv[4 * q + 3]);
+        };
         auto term = [&](int k, float Y, float dYx, float dYy, float dYz) {
-          const float shg = row[3 * k] * g_r + row[3 * k + 1] * g_g + row[3 * k + 2] * g_b;
+          const int e = 3 * (k & 3);
+          const float shg = rv[e] * g_r + rv[e + 1] * g_g + rv[e + 2] * g_b;
           ddx = fmaf(dYx, shg, ddx);
           ddy = fmaf(dYy, shg, ddy);
           ddz = fmaf(dYz, shg, ddz);
-          drow[3 * k] = fmaf(Y, g_r, drow[3 * k]);
-          drow[3 * k + 1] = fmaf(Y, g_g, drow[3 * k + 1]);
-          drow[3 * k + 2] = fmaf(Y, g_b, drow[3 * k + 2]);
+          dv[e] = fmaf(Y, g_r, dv[e]);
+          dv[e + 1] = fmaf(Y, g_g, dv[e + 1]);
+          dv[e + 2] = fmaf(Y, g_b, dv[e + 2]);
         };
+        load_group(0);
         term(0, kC0, 0.f, 0.f, 0.f);
         if (p.deg > 0) {
           term(1, -kC1 * y, 0.f, -kC1, 0.f);
           term(2, kC1 * z, 0.f, 0.f, kC1);
           term(3, -kC1 * x, -kC1, 0.f, 0.f);
-          if (p.deg > 1) {
-            term(4, kC20 * x * y, kC20 * y, kC20 * x, 0.f);
-            term(5, kC21 * y * z, 0.f, kC21 * z, kC21 * y);
-            term(6, kC22 * (2.f * zz - xx - yy), -2.f * kC22 * x, -2.f * kC22 * y, 4.f * kC22 * z);
-            term(7, kC23 * x * z, kC23 * z, 0.f, kC23 * x);
-            term(8, kC24 * (xx - yy), 2.f * kC24 * x, -2.f * kC24 * y, 0.f);
-            if (p.deg > 2) {
-              term(9, kC30 * y * (3.f * xx - yy), 6.f * kC30 * x * y, 3.f * kC30 * (xx - yy), 0.f);
-              term(10, kC31 * x * y * z, kC31 * y * z, kC31 * x * z, kC31 * x * y);
-              term(11, kC32 * y * (4.f * zz - xx - yy), -2.f * kC32 * x * y, kC32 * (4.f * zz - xx - 3.f * yy),
-                   8.f * kC32 * y * z);
-              term(12, kC33 * z * (2.f * zz - 3.f * xx - 3.f * yy), -6.f * kC33 * x * z, -6.f * kC33 * y * z,
-                   kC33 * (6.f * zz - 3.f * xx - 3.f * yy));
-              term(13, kC34 * x * (4.f * zz - xx - yy), kC34 * (4.f * zz - 3.f * xx - yy), -2.f * kC34 * x * y,
-                   8.f * kC34 * x * z);
-              term(14, kC35 * z * (xx - yy), 2.f * kC35 * x * z, -2.f * kC35 * y * z, kC35 * (xx - yy));
-              term(15, kC36 * x * (xx - 3.f * yy), 3.f * kC36 * (xx - yy), -6.f * kC36 * x * y, 0.f);
-            }
+        }
+        store_group(0);
+        if (p.deg > 1) {
+          load_group(1);
+          term(4, kC20 * x * y, kC20 * y, kC20 * x, 0.f);
+          term(5, kC21 * y * z, 0.f, kC21 * z, kC21 * y);
+          term(6, kC22 * (2.f * zz - xx - yy), -2.f * kC22 * x, -2.f * kC22 * y, 4.f * kC22 * z);
+          term(7, kC23 * x * z, kC23 * z, 0.f, kC23 * x);
+          store_group(1);
+          load_group(2);
+          term(8, kC24 * (xx - yy), 2.f * kC24 * x, -2.f * kC24 * y, 0.f);
+          if (p.deg > 2) {
+            term(9, kC30 * y * (3.f * xx - yy), 6.f * kC30 * x * y, 3.f * kC30 * (xx - yy), 0.f);
+            term(10, kC31 * x * y * z, kC31 * y * z, kC31 * x * z, kC31 * x * y);
+            term(11, kC32 * y * (4.f * zz - xx - yy), -2.f * kC32 * x * y, kC32 * (4.f * zz - xx - 3.f * yy),
+                 8.f * kC32 * y * z);
+          }
+          store_group(2);
+          if (p.deg > 2) {
+            load_group(3);
+            term(12, kC33 * z * (2.f * zz - 3.f * xx - 3.f * yy), -6.f * kC33 * x * z, -6.f * kC33 * y * z,
+                 kC33 * (6.f * zz - 3.f * xx - 3.f * yy));
+            term(13, kC34 * x * (4.f * zz - xx - yy), kC34 * (4.f * zz - 3.f * xx - yy), -2.f * kC34 * x * y,
+                 8.f * kC34 * x * z);
+            term(14, kC35 * z * (xx - yy), 2.f * kC35 * x * z, -2.f * kC35 * y * z, kC35 * (xx - yy));
+            term(15, kC36 * x * (xx - 3.f * yy), 3.f * kC36 * (xx - yy), -6.f * kC36 * x * y, 0.f);
+            store_group(3);
           }
         }
         const float dot = ddx * x + ddy * y + ddz * z;
@@ -234,10 +263,12 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
       const float t1 = V[1] * mx + V[5] * my + V[9] * mz + V[13];
       const float t2 = V[2] * mx + V[6] * my + V[10] * mz + V[14];
       const float fx = c.fx, fy = c.fy;
-      float u = t0 / t2, v = t1 / t2;
+      // MUFU reciprocals (~1 ulp): the decisions are the forward's (frozen), and the gradient
+      // tolerance (1e-3 relative) is far above the rounding of an IEEE division
+      const float itz = fast_rcp(t2), itz2 = itz * itz;
+      float u = t0 * itz, v = t1 * itz;
       if (cb & CB_JX) u = (cb & CB_JX_NEG) ? -c.limx : c.limx;
       if (cb & CB_JY) v = (cb & CB_JY_NEG) ? -c.limy : c.limy;
-      const float itz = 1.0f / t2, itz2 = itz * itz;
       const float j00 = fx * itz, j02 = -fx * u * itz, j11 = fy * itz, j12 = -fy * v * itz;
       float Tm[2][3];
 #pragma unroll
@@ -261,7 +292,8 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
         const double B = TSd[0][0] * Tm[1][0] + TSd[0][1] * Tm[1][1] + TSd[0][2] * Tm[1][2];
         const double Cc = TSd[1][0] * Tm[1][0] + TSd[1][1] * Tm[1][1] + TSd[1][2] * Tm[1][2] + 0.3;
         const double det = A * Cc - B * B;
-        const double id2 = 1.0 / (det * det);
+        const float idet = fast_rcp((float)det);  // det itself stays FP64 (it cancels)
+        const double id2 = (double)idet * (double)idet;
         const double gcx = ga4.z, gcy = ga4.w, gcz = gb4.x;
         Gp00 = (-Cc * Cc * gcx + B * Cc * gcy - B * B * gcz) * id2;
         Gp01 = 0.5 * (2.0 * B * Cc * gcx - (A * Cc + B * B) * gcy + 2.0 * A * B * gcz) * id2;
@@ -304,7 +336,7 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
         const float c0 = P[0] * mx + P[4] * my + P[8] * mz + P[12];
         const float c1 = P[1] * mx + P[5] * my + P[9] * mz + P[13];
         const float c3 = P[3] * mx + P[7] * my + P[11] * mz + P[15];
-        const float ic3 = 1.0f / c3, ic32 = ic3 * ic3;
+        const float ic3 = fast_rcp(c3), ic32 = ic3 * ic3;
         const float hx = 0.5f * (float)c.W * gx * ic32, hy = 0.5f * (float)c.H * gy * ic32;
         dmx += hx * (P[0] * c3 - P[3] * c0) + hy * (P[1] * c3 - P[3] * c1);
         dmy += hx * (P[4] * c3 - P[7] * c0) + hy * (P[5] * c3 - P[7] * c1);
@@ -383,12 +415,12 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
     for (int c = lane; c < 12 * nvalid; c += 32) {
       const int g = c / 12, e = 4 * (c % 12);
       if (!s_vis[warp][g] || e >= 3 * ncoef) continue;
-      const float* r = &s_dsh[warp][g * kRow + e];
+      const float4 r = *reinterpret_cast<const float4*>(&s_dsh[warp][g * kRow + e]);
       float4 v = dst[c];
-      v.x += r[0];
-      v.y += r[1];
-      v.z += r[2];
-      v.w += r[3];
+      v.x += r.x;
+      v.y += r.y;
+      v.z += r.z;
+      v.w += r.w;
       dst[c] = v;
     }
   } else {

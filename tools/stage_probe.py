@@ -87,6 +87,24 @@ def main():
                 res[name] = e0.elapsed_time(e1) / a.reps
             print(f"seg_len {sl:6d}: fwd {res['render_fwd']:.3f} ms  bwd {res['blend_bwd']:.3f} ms", flush=True)
         return
+    if a.views > 1:
+        # the batched stages as the bench runs them: one a2 launch and one a10 launch over
+        # --views views (their frames rendered once first)
+        vcams = [s.cameras[(a.view + 4 * j) % len(s.cameras)] for j in range(a.views)]
+        rs = [r] + [bgs.Renderer(s.n, cam.width, cam.height, max_keys=r.max_keys, device=dev) for _ in vcams[1:]]
+        fr = [rj.frame for rj in rs]
+        bcams = [bgs.camera(cj) for cj in vcams]
+
+        def pre_batch():
+            bgs.bgs_preprocess_batch(g, bcams, fr)
+
+        pre_batch()
+        for rj in rs:
+            bgs.bgs_sort(rj.frame)
+            bgs.bgs_render_fwd(rj.frame, rj.image, rj.final_T, rj.n_contrib)
+            bgs.bgs_blend_bwd(rj.frame, dl, rj.final_T, rj.n_contrib)
+        stages["preprocess_batch"] = pre_batch
+        stages["preprocess_bwd_batch"] = lambda: bgs.bgs_preprocess_bwd_batch(g, fr, grad)
     only = set(a.only.split(",")) if a.only else None
     for name, fn in stages.items():
         if only and name not in only:
