@@ -26,6 +26,11 @@
 namespace bgs {
 
 constexpr int kBwdWarpsPerCta = 4;
+// entries taken by at most this many lanes are added by per-lane REDs instead of the warp
+// reduce-scatter
+#ifndef BGS_BWD_RED_LANES
+#define BGS_BWD_RED_LANES 6
+#endif
 
 // Reduce-scatter of 9 per-lane values over the warp: each butterfly step halves the set of
 // values a lane carries (5 -> 3 -> 2 -> 1 -> 1 shuffles: 12 instead of 9 x 5 = 45).  On
@@ -339,7 +344,7 @@ __global__ void __launch_bounds__(kBwdWarpsPerCta * 32) k_render_bwd(
         }
         const uint32_t actm = __ballot_sync(0xffffffffu, any_act);
         const uint32_t id = __float_as_uint(r0.w);
-        if (__popc(actm) > 8) {
+        if (__popc(actm) > BGS_BWD_RED_LANES) {
           const float gv[9] = {g0, g1, g2, g3, g4, g5, g6, g7, g8};
           int idx;
           const float tot = warp_reduce_scatter9(gv, lane, idx);
