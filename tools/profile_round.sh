@@ -18,7 +18,7 @@ python tools/launch_shares.py $OUT/launches_$TAG.csv $OUT/launch_shares_$TAG.md 
 ncu --set full --clock-control none --import-source on -f -o /tmp/prof_$TAG \
     python tools/stage_probe.py --step 2 > $OUT/ncu_full_$TAG.log 2>&1
 python tools/ncu_summary.py /tmp/prof_$TAG.ncu-rep $OUT/ncu_summary_$TAG.md --title "$TAG, one garden view (camera 0) training step" \
-    --traffic $OUT/ncu_traffic_$TAG.json --stage 'render_fwd=^k_render_fwd$' \
+    --traffic $OUT/ncu_traffic_$TAG.json --stage 'render_fwd=^k_render_fwd' \
     --stage 'blend_bwd=^k_render_bwd<' --stage 'adam=^k_adam$' >> $OUT/ncu_full_$TAG.log 2>&1
 # the batched preprocess over 16 views, as the bench runs it (one launch)
 ncu --set full --clock-control none --import-source on -f -o /tmp/prof_pre_$TAG -k regex:k_preprocess_views -s 1 -c 1 \
