@@ -65,11 +65,13 @@ __device__ __forceinline__ void put_grad(const PreBwdParams& p, int64_t e, float
     g += p.grad[e];
     p.grad[e] = 0.0f;
   }
+  // explicit roundings (this file is built with FMA contraction; adam.cu is not): the fused
+  // update stays bit-identical to bgs_adam_step's
   float m = p.m[e], v = p.v[e];
-  m = fmaf(p.b1, m, (1.0f - p.b1) * g);
-  v = fmaf(p.b2, v, (1.0f - p.b2) * g * g);
-  const float denom = sqrtf(v) * p.inv_sqrt_bc2 + p.eps;
-  p.theta[e] = p.theta[e] - p.step_size[grp] * (m / denom);
+  m = fmaf(p.b1, m, __fmul_rn(1.0f - p.b1, g));
+  v = fmaf(p.b2, v, __fmul_rn(__fmul_rn(1.0f - p.b2, g), g));
+  const float denom = __fadd_rn(__fmul_rn(sqrtf(v), p.inv_sqrt_bc2), p.eps);
+  p.theta[e] = __fsub_rn(p.theta[e], __fmul_rn(p.step_size[grp], m / denom));
   p.m[e] = m;
   p.v[e] = v;
 }

@@ -22,7 +22,7 @@ def main():
 
     def comp(src):
         obj = os.path.join(out, os.path.basename(src).replace(".cu", ".o"))
-        r = subprocess.run([ge.NVCC, *ge.NVCC_FLAGS, *defs, "-c", src, "-o", obj], capture_output=True, text=True)
+        r = subprocess.run([ge.NVCC, *ge.flags_for(src), *defs, "-c", src, "-o", obj], capture_output=True, text=True)
         if r.returncode:
             raise RuntimeError(r.stderr)
         return obj
