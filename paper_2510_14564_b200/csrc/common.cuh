@@ -19,6 +19,12 @@ constexpr int kCkPoolSeg = 2048;
 // direct tile split (sort.cu): chunks of 2048..16384 items (a power of two chosen on the
 // device from K so that there are >= kChunkTarget chunks: one warp each); per-warp
 // shared-memory tile counters
+// keys per CTA tile of the onesweep pass (radix.cu): 256 threads x BGS_SORT_ITEMS; the
+// look-back status buffers (frame.cu) are sized by it
+#ifndef BGS_SORT_ITEMS
+#define BGS_SORT_ITEMS 16
+#endif
+constexpr int kSortTileKeys = 256 * BGS_SORT_ITEMS;
 constexpr int kChunkItemsMin = 2048, kChunkItemsMax = 16384, kChunkTarget = 2048;
 __host__ __device__ __forceinline__ uint32_t chunk_items_of(uint32_t K) {
   uint32_t c = kChunkItemsMax;

@@ -54,7 +54,7 @@ struct Layout {
 };
 
 constexpr int kScanTile = 4096;  // = kScanThreads * kScanItems of k_scan (preprocess.cu)
-constexpr int kSortTile = 4096;
+constexpr int kSortTile = kSortTileKeys;
 
 static bool make_layout(int64_t n, int32_t w, int32_t h, int64_t max_keys, Layout& L) {
   if (n < 0 || n > ((int64_t)1 << 31) - 1 || w < 1 || h < 1 || w > 16384 || h > 16384 || max_keys < 1 ||

@@ -16,9 +16,6 @@
 
 namespace bgs {
 
-#ifndef BGS_SORT_ITEMS
-#define BGS_SORT_ITEMS 16
-#endif
 #ifndef BGS_SORT_MINB
 #define BGS_SORT_MINB 3
 #endif

@@ -598,7 +598,7 @@ bgs_status launch_tile_scan(Frame* F, cudaStream_t s) {
 
 // look-back status words of a pass over at most `count` keys
 static bgs_status memset_status(Frame* F, cudaStream_t s, int64_t count = -1) {
-  const int64_t tiles = count < 0 ? F->sort_tiles_max : (count + 4095) / 4096;
+  const int64_t tiles = count < 0 ? F->sort_tiles_max : (count + kSortTileKeys - 1) / kSortTileKeys;
   if (cudaMemsetAsync(F->sort_status, 0, 4 * kRadixBins * (size_t)tiles, s) != cudaSuccess)
     return check_launch("sort status memset");
   return BGS_OK;
