@@ -148,15 +148,28 @@ __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const float* __re
   __syncthreads();
   uint32_t(*h)[kRadixBins] = s_h[threadIdx.x >> 5];
   uint32_t vis = 0;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const bool visible = tiles_touched[i] != 0;
+  auto add = [&](uint32_t tt, float d) {
+    const bool visible = tt != 0;
     if (visible || kNoCompact) {
-      const uint32_t key = visible ? __float_as_uint(depth[i]) : 0xffffffffu;
+      const uint32_t key = visible ? __float_as_uint(d) : 0xffffffffu;
       ++vis;
 #pragma unroll
       for (int p = 0; p < 4; ++p) atomicAdd(&h[p][(key >> (8 * p)) & 0xff], 1u);
     }
+  };
+  // four Gaussians per thread and iteration by 16-byte loads (the frame's arrays are
+  // 256-byte aligned), the n % 4 tail by scalar loads
+  const int64_t n4 = n >> 2;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 t4 = __ldg(reinterpret_cast<const uint4*>(tiles_touched) + i);
+    const float4 d4 = __ldg(reinterpret_cast<const float4*>(depth) + i);
+    add(t4.x, d4.x);
+    add(t4.y, d4.y);
+    add(t4.z, d4.z);
+    add(t4.w, d4.w);
   }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    add(tiles_touched[i], depth[i]);
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) vis += __shfl_xor_sync(0xffffffffu, vis, d);
   if ((threadIdx.x & 31) == 0 && vis) atomicAdd(&s_vis, vis);
@@ -342,7 +355,10 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_chunk_hist(int64_t n, cons
       if (t[q] && s0 < e0) {
         const int w = (int)rc[q].y, x0 = (int)(rc[q].x & 0xffffu), y0 = (int)(rc[q].x >> 16);
         const int ls = (int)(s0 - o[q]), le = (int)(e0 - o[q]) - 1;  // inclusive local item range
-        const int q1 = ls / w, c1 = ls - q1 * w, q2 = le / w, c2 = le - q2 * w;
+        // rows by the exact float split of k_emit_ranked (no integer divisions)
+        const float iw = 1.0f / (float)w;
+        const int q1 = (int)(((float)ls + 0.5f) * iw), c1 = ls - q1 * w;
+        const int q2 = (int)(((float)le + 0.5f) * iw), c2 = le - q2 * w;
         if (q1 == q2) {
           add_rect(x0 + c1, y0 + q1, x0 + c2 + 1, y0 + q1 + 1);
         } else {
@@ -356,19 +372,19 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_chunk_hist(int64_t n, cons
   __syncwarp();
   for (int y = lane; y <= tiles_y; y += 32) {  // prefix along rows
     int32_t run = 0;
+#pragma unroll 8
     for (int x = 0; x <= tiles_x; ++x) run = (G[y * gw + x] += run);
   }
   __syncwarp();
   for (int x = lane; x <= tiles_x; x += 32) {  // then along columns
     int32_t run = 0;
+#pragma unroll 8
     for (int y = 0; y <= tiles_y; ++y) run = (G[y * gw + x] += run);
   }
   __syncwarp();
   uint32_t* row = chunk_cnt + (size_t)c * nt;
-  for (int t = lane; t < nt; t += 32) {
-    const int y = t / tiles_x, x = t - y * tiles_x;
-    row[t] = (uint32_t)G[y * gw + x];
-  }
+  for (int y = 0; y < tiles_y; ++y)
+    for (int x = lane; x < tiles_x; x += 32) row[y * tiles_x + x] = (uint32_t)G[y * gw + x];
 }
 
 // (b) exclusive prefix over chunks of each tile's column (in place) and the tile totals.
