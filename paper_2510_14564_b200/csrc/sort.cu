@@ -137,11 +137,26 @@ constexpr bool kNoCompact = false;
 // (counters[C_VISIBLE]).  The first pass generates its (key, index) pairs from the depths
 // and tiles_touched itself (culled: key 0xffffffff, dropped), so the other three run over
 // [0, V), and the ranks [V, N) own no tiles.
+// It also zeroes, for the later kernels of the sort, the look-back status words of the
+// four passes (one region each) and the tile ranges and counts (z0 / z1 / z2, 4-byte words;
+// one launch instead of six memsets).
+__device__ __forceinline__ void zero_words(uint32_t* p, int64_t words) {
+  if (!p) return;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t w4 = words >> 2;  // 16-byte stores (the frame's buffers are 256-byte aligned)
+  for (int64_t i = t0; i < w4; i += stride) reinterpret_cast<uint4*>(p)[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int64_t i = 4 * w4 + t0; i < words; i += stride) p[i] = 0u;
+}
+
 __global__ void __launch_bounds__(256) k_depth_keys(int64_t n, const float* __restrict__ depth,
                                                     const uint32_t* __restrict__ tiles_touched,
-                                                    uint32_t* counters, uint32_t* hist) {
+                                                    uint32_t* counters, uint32_t* hist, uint32_t* z0, int64_t z0_words,
+                                                    uint32_t* z1, int64_t z1_words, uint32_t* z2, int64_t z2_words) {
   __shared__ uint32_t s_h[8][4][kRadixBins];  // one copy per warp: conflicts stay inside a warp
   __shared__ uint32_t s_vis;
+  zero_words(z0, z0_words);
+  zero_words(z1, z1_words);
+  zero_words(z2, z2_words);
   if (counters[C_OVERFLOW]) return;
   for (int k = threadIdx.x; k < 8 * 4 * kRadixBins; k += blockDim.x) (&s_h[0][0][0])[k] = 0;
   if (threadIdx.x == 0) s_vis = 0;
@@ -621,14 +636,18 @@ static bgs_status memset_status(Frame* F, cudaStream_t s, int64_t count = -1) {
 }
 
 bgs_status launch_sort(Frame* F, cudaStream_t s) {
-  if (cudaMemsetAsync(F->ranges, 0, 8 * (size_t)F->num_tiles, s) != cudaSuccess ||
-      cudaMemsetAsync(F->tile_count, 0, 4 * (size_t)F->num_tiles, s) != cudaSuccess ||
+  const bool ref64 = (F->debug_flags & (BGS_DEBUG_SORT_ONESWEEP64 | BGS_DEBUG_SKIP_SORT)) != 0;
+  // depth-first path: k_depth_keys zeroes the ranges, tile counts and the four passes' status
+  // regions when the status buffer holds four regions of the N-key pass
+  const int64_t region = (int64_t)kRadixBins * ((F->n + kSortTileKeys - 1) / kSortTileKeys);
+  const bool fused_zero = !ref64 && F->n > 0 && 4 * region <= (int64_t)kRadixBins * F->sort_tiles_max;
+  if ((!fused_zero && (cudaMemsetAsync(F->ranges, 0, 8 * (size_t)F->num_tiles, s) != cudaSuccess ||
+                       cudaMemsetAsync(F->tile_count, 0, 4 * (size_t)F->num_tiles, s) != cudaSuccess)) ||
       cudaMemsetAsync(F->sort_hist, 0, 4 * 8 * kRadixBins, s) != cudaSuccess ||
       cudaMemsetAsync(F->counters + C_SORT_TICKET, 0, 4 * 8, s) != cudaSuccess ||
       cudaMemsetAsync(F->counters + C_SORT32_TICKET, 0, 4 * 8, s) != cudaSuccess ||
       cudaMemsetAsync(F->counters + C_VISIBLE, 0, 4, s) != cudaSuccess)
     return check_launch("sort memset");
-  const bool ref64 = (F->debug_flags & (BGS_DEBUG_SORT_ONESWEEP64 | BGS_DEBUG_SKIP_SORT)) != 0;
   const int P = F->sort_passes;
   F->sort_mode = ref64 ? 1 : 0;
   F->final_buf = ref64 ? (P & 1) : ((P - 4) & 1);
@@ -655,11 +674,15 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
     return BGS_OK;
   }
   // ---- depth first: (1) stable sort of the Gaussians by depth bits
-  k_depth_keys<<<grid, 256, 0, s>>>(F->n, F->depth, F->tiles_touched, F->counters, F->sort_hist);
+  k_depth_keys<<<grid, 256, 0, s>>>(F->n, F->depth, F->tiles_touched, F->counters, F->sort_hist,
+                                    fused_zero ? F->sort_status : nullptr, 4 * region,
+                                    fused_zero ? reinterpret_cast<uint32_t*>(F->ranges) : nullptr,
+                                    2 * (int64_t)F->num_tiles, fused_zero ? F->tile_count : nullptr,
+                                    (int64_t)F->num_tiles);
   note_launch();
   if ((st = check_launch("k_depth_keys")) != BGS_OK) return st;
   for (int p = 0; p < 4; ++p) {
-    if ((st = memset_status(F, s, F->n)) != BGS_OK) return st;
+    if (!fused_zero && (st = memset_status(F, s, F->n)) != BGS_OK) return st;
     const int a = p & 1, b = (p + 1) & 1;
     // the first pass compacts the visible Gaussians; (2) the last pass also writes the
     // per-rank tile counts and packed rects (zero past V)
@@ -667,7 +690,7 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
     // the first pass reads the depths and visibility directly (keys and values generated)
     const uint32_t* kin = p ? F->dkey[a] : reinterpret_cast<const uint32_t*>(F->depth);
     st = launch_sort_pass32(kin, p ? F->dval[a] : nullptr, F->dkey[b], F->dval[b], F->sort_hist + p * kRadixBins,
-                            F->sort_status, F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, (p && !kNoCompact) ? -2 : F->n, s,
+                            F->sort_status + (fused_zero ? p * region : 0), F->counters + C_SORT32_TICKET + p, F->counters, 8 * p, (p && !kNoCompact) ? -2 : F->n, s,
                             last ? F->rect : nullptr, last ? F->rank_cnt : nullptr, last ? F->rank_rect : nullptr,
                             last ? F->rank_h : nullptr, p == 0 && !kNoCompact, last ? F->n : 0,
                             p ? nullptr : F->tiles_touched);
