@@ -458,6 +458,9 @@ __global__ void __launch_bounds__(1024) k_chunk_scan(uint32_t* chunk_cnt, int32_
 // final position of each tile's items (u32) and a per-tile item count (u8) that detects
 // two items of a 32-item batch falling into the same tile.
 constexpr int kEmitWarps = 2;
+#ifndef BGS_EMIT_PEER_LOOP
+#define BGS_EMIT_PEER_LOOP 4
+#endif
 
 __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, const uint32_t* __restrict__ item_off,
                                                                  const uint32_t* __restrict__ sigma,
@@ -550,7 +553,25 @@ __global__ void __launch_bounds__(kEmitWarps * 32) k_emit_direct(int64_t n, cons
         // depth order: each takes the tile's next position plus its rank among the tile's
         // lanes (one MATCH.ANY), and the tile's last lane advances the counter
         __syncwarp();
+#if BGS_EMIT_PEER_LOOP
+        // few contended lanes (<= BGS_EMIT_PEER_LOOP: at most half as many tiles): their peer
+        // sets by one ballot per contended tile instead of the long-latency MATCH.ANY
+        const uint32_t cm = __ballot_sync(0xffffffffu, contended);
+        uint32_t peers = 0;
+        if (__popc(cm) <= BGS_EMIT_PEER_LOOP) {
+          uint32_t todo = cm;
+          while (todo) {
+            const uint32_t lt_tile = __shfl_sync(0xffffffffu, tile, __ffs(todo) - 1);
+            const uint32_t mine = __ballot_sync(0xffffffffu, contended && tile == lt_tile);
+            if (contended && tile == lt_tile) peers = mine;
+            todo &= ~mine;
+          }
+        } else {
+          peers = __match_any_sync(0xffffffffu, contended ? tile : 0x80000000u | (uint32_t)lane);
+        }
+#else
         const uint32_t peers = __match_any_sync(0xffffffffu, contended ? tile : 0x80000000u | (uint32_t)lane);
+#endif
         uint32_t p = 0;
         if (contended) p = nxt[tile] + (uint32_t)__popc(peers & lanemask_lt());
         __syncwarp();
