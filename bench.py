@@ -89,11 +89,12 @@ def parse():
                         "full Adam on every rank; or 'overlap': the chain rule in Gaussian chunks, each chunk's "
                         "gradient all-reduced on a communication stream while the next computes (SURVEY 8(e) 1)")
     p.add_argument("--overlap-chunks", type=int, default=4, help="--update overlap: Gaussian chunks")
-    p.add_argument("--sort-streams", type=int, default=4,
+    p.add_argument("--sort-streams", type=int, default=8,
                    help="sort all of a step's views up front, round-robin over this many CUDA streams (their "
                         "latency-bound sort kernels overlap), then blend the views in order; 0 = each view's "
                         "sort inline before its forward (measured at garden: 0 -> 315.3, 2 -> 324.2, 4 -> 325.1, "
-                        "8 -> 326.1 views/s; waiting per view instead of for all sorts: no gain)")
+                        "8 -> 326.1 views/s; after the round-2 kernel work 4 -> 384.7, 8 -> 386.2; high stream "
+                        "priority for the sorts: no change; waiting per view instead of for all sorts: no gain)")
     p.add_argument("--loss", default="l1dssim", choices=["l1dssim", "l1"],
                    help="per-view loss: the 3DGS 0.8 L1 + 0.2 D-SSIM (default) or L1 alone (R19)")
     p.add_argument("--no-cpu-baseline", action="store_true")
