@@ -116,6 +116,9 @@ def parse():
                         "(step s renders views 4i + s mod 64), each view hinted by its camera's last forward")
     p.add_argument("--sort-path", default="direct", choices=["direct", "radix_split", "rowsplit", "onesweep64"],
                    help="a4-a6 implementation (default: the direct tile split; the others are bit-identical)")
+    p.add_argument("--no-assign", action="store_true",
+                   help="A/B: accumulate the chain rule into a zeroed grad and zero it in Adam (the round-2 "
+                        "default before bgs_preprocess_bwd_batch_assign)")
     p.add_argument("--no-variants", action="store_true",
                    help="skip the extra timed loops (fixed batch; rotating batch without scheduling hints)")
     p.add_argument("--pre-per-view", action="store_true",
@@ -275,6 +278,9 @@ def run_ours(args, rank, world, local_rank):
     chunk_ev = [torch.cuda.Event() for _ in range(max(1, args.overlap_chunks))]
     # one GPU, one chain-rule launch: a10 and a11 fused (no collective between them)
     fused = world == 1 and not args.one_frame and args.fuse_adam and args.views <= 16
+    # the step's single batched chain rule assigns grad, so grad is never read by it nor
+    # zeroed by Adam (bgs_preprocess_bwd_batch_assign / bgs_adam_step_keep_grad)
+    assign = not (args.one_frame or overlap or fused or args.no_assign)
     # the step's views share theta: one preprocess pass over it for all of them
     batch_pre = not args.one_frame and not args.pre_per_view
     total = 59 * n
@@ -566,7 +572,10 @@ def run_ours(args, rank, world, local_rank):
                 with torch.cuda.stream(comm_stream):
                     dp.allreduce_chunk(grad, n, b, e, world)
         elif not args.one_frame:  # a10 once over the batch's views: theta/grad cross HBM once
-            bgs.bgs_preprocess_bwd_batch(gs, frames, grad)
+            if assign:  # grad = the batch's sum: never read, never zeroed
+                bgs.bgs_preprocess_bwd_batch_assign(gs, frames, grad)
+            else:
+                bgs.bgs_preprocess_bwd_batch(gs, frames, grad)
         mark(marks)
         if fused:
             mark(marks)
@@ -580,13 +589,17 @@ def run_ours(args, rank, world, local_rank):
             g_shard = dp.reduce_scatter_grads(grad, rank, world)
             mark(marks)
             bgs.bgs_adam_step_range(theta[lo:hi], g_shard, m, v, n, lo, hi - lo, hp, step_no[0])
-            bgs.bgs_zero(grad)  # the rest of grad still holds this rank's partial sums
+            if not assign:
+                bgs.bgs_zero(grad)  # the rest of grad still holds this rank's partial sums
             mark(marks)
             dp.all_gather_params(theta, rank, world)
         else:
             dp.allreduce_grads(grad, world)  # NCCL over NVLink (one exchange per batch)
             mark(marks)
-            bgs.bgs_adam_step(theta, grad, m, v, n, hp, step_no[0])
+            if assign:
+                bgs.bgs_adam_step_keep_grad(theta, grad, m, v, n, hp, step_no[0])
+            else:
+                bgs.bgs_adam_step(theta, grad, m, v, n, hp, step_no[0])
             mark(marks)
         mark(marks)
         if args.density_every and step_no[0] % args.density_every == 0:
@@ -880,13 +893,16 @@ def run_ours(args, rank, world, local_rank):
         roof["preprocess_bwd"]["fused_with_adam"] = True
     elif args.one_frame:  # per view: theta 236 + blend grads 36 + grad RMW 472 per visible Gaussian
         frac("preprocess_bwd", 744 * V / per_launch("preprocess_bwd") / 1e9, hbm, "GB/s", "hbm")
-    else:  # batched over the rank's views: theta 236 + grad RMW 472 per Gaussian once, + per
-        # (view, visible Gaussian) the blend gradients 36 + radius 4 + clamp bits 1; radius 4 per (view, culled)
-        pb_bytes = 708 * n + (37 * V + 4 * n) * steps_views
+    else:  # batched over the rank's views: theta 236 + grad 236 written (assigned) or 472 (read-modify-
+        # written) per Gaussian once, + per (view, visible Gaussian) the blend gradients 36 + radius 4 + clamp
+        # bits 1; radius 4 per (view, culled)
+        pb_bytes = (472 if assign else 708) * n + (37 * V + 4 * n) * steps_views
         frac("preprocess_bwd", pb_bytes / max(per_step["preprocess_bwd"] / 1e3, 1e-12) / 1e9, hbm, "GB/s", "hbm")
         roof["preprocess_bwd"]["ms_per_launch"] = per_step["preprocess_bwd"] / -(-steps_views // 16)
     if not fused:
-        adam_bytes = 1888 * n / (world if sharded else 1) + (236 * n if sharded else 0)  # + zeroing grad
+        # theta, m, v read + written and grad read: 1652 B per Gaussian, + 236 with grad zeroed (not assigned)
+        adam_bytes = ((1652 if assign else 1888) * n / (world if sharded else 1)
+                      + (236 * n if sharded and not assign else 0))
         roof["adam"] = {"bound": "hbm", "achieved": adam_bytes / max(per_step["adam"] / 1e3, 1e-12) / 1e9,
                         "peak": hbm, "unit": "GB/s", "ms_per_launch": per_step["adam"]}
         roof["adam"]["frac"] = roof["adam"]["achieved"] / hbm

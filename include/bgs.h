@@ -202,6 +202,17 @@ bgs_status bgs_preprocess_bwd(const bgs_gaussians* g /*host*/, bgs_frame* f /*ho
 bgs_status bgs_preprocess_bwd_batch(const bgs_gaussians* g /*host*/, bgs_frame* const* frames /*host*/,
                                     int32_t nframes, float* grad, void* stream);
 
+/* bgs_preprocess_bwd_batch with grad ASSIGNED, not accumulated: grad[59n] = the sum over the
+ * frames of each view's chain rule, every element written (0 for a Gaussian no frame sees,
+ * and for SH coefficients above the degree).  With nframes > 16 the first launch assigns
+ * and the later ones accumulate.  grad's previous contents are never read, so a caller whose
+ * step has one chain-rule pass per rank needs no zeroing between steps (pair it with
+ * bgs_adam_step_keep_grad): theta and grad cross HBM once less.  Value-equal to
+ * bgs_preprocess_bwd_batch into a zero grad (tests/test_gpu_parity.py).  Errors as
+ * bgs_preprocess_bwd_batch. */
+bgs_status bgs_preprocess_bwd_batch_assign(const bgs_gaussians* g /*host*/, bgs_frame* const* frames /*host*/,
+                                           int32_t nframes, float* grad, void* stream);
+
 /* bgs_preprocess_bwd_batch restricted to the Gaussians [begin, begin + count): grad +=
  * their 59 elements (in each theta segment the sub-range of those Gaussians) and nothing
  * else.  Consecutive ranges covering [0, n) sum to bgs_preprocess_bwd_batch's gradient
@@ -229,6 +240,12 @@ bgs_status bgs_preprocess_bwd_batch_adam(const bgs_gaussians* g /*host*/, bgs_fr
  * sqrt), per-group learning rate, grad zeroed on exit.  step is 1-based. */
 bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
                          const bgs_adam_hparams* hp /*host*/, int64_t step, void* stream);
+
+/* bgs_adam_step leaving grad as it is (read only): the same theta / exp_avg / exp_avg_sq
+ * update, bit for bit, for a caller whose next chain rule assigns grad
+ * (bgs_preprocess_bwd_batch_assign).  Errors as bgs_adam_step. */
+bgs_status bgs_adam_step_keep_grad(float* theta, const float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
+                                   const bgs_adam_hparams* hp /*host*/, int64_t step, void* stream);
 
 /* a11 on a shard (reduce-scatter -> Adam on 1/G of theta -> all-gather):
  * the same update as bgs_adam_step restricted to theta elements [begin, begin + count) of the

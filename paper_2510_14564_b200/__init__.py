@@ -109,11 +109,14 @@ _SIGS = {
     "bgs_blend_bwd": (C.c_int, [C.POINTER(Frame), _P, _P, _P, _P]),
     "bgs_preprocess_bwd": (C.c_int, [C.POINTER(Gaussians), C.POINTER(Frame), _P, _P]),
     "bgs_preprocess_bwd_batch": (C.c_int, [C.POINTER(Gaussians), C.POINTER(C.POINTER(Frame)), C.c_int32, _P, _P]),
+    "bgs_preprocess_bwd_batch_assign": (C.c_int, [C.POINTER(Gaussians), C.POINTER(C.POINTER(Frame)), C.c_int32, _P,
+                                                 _P]),
     "bgs_preprocess_bwd_batch_range": (C.c_int, [C.POINTER(Gaussians), C.POINTER(C.POINTER(Frame)), C.c_int32, _P, C.c_int64,
                                                 C.c_int64, _P]),
     "bgs_preprocess_bwd_batch_adam": (C.c_int, [C.POINTER(Gaussians), C.POINTER(C.POINTER(Frame)), C.c_int32, _P, _P,
                                                 _P, _P, C.POINTER(AdamHParams), C.c_int64, _P]),
     "bgs_adam_step": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(AdamHParams), C.c_int64, _P]),
+    "bgs_adam_step_keep_grad": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.POINTER(AdamHParams), C.c_int64, _P]),
     "bgs_adam_step_range": (C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.POINTER(AdamHParams),
                                       C.c_int64, _P]),
     "bgs_adam_step_multimem": (C.c_int, [_P, _P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64, C.POINTER(AdamHParams),
@@ -262,6 +265,13 @@ def bgs_preprocess_bwd_batch(g: Gaussians, frames, grad, stream=None):
            "bgs_preprocess_bwd_batch")
 
 
+def bgs_preprocess_bwd_batch_assign(g: Gaussians, frames, grad, stream=None):
+    """The batched chain rule with grad assigned (= the frames' sum; every element written)."""
+    arr = (C.POINTER(Frame) * len(frames))(*[C.pointer(f) for f in frames])
+    _check(_lib.bgs_preprocess_bwd_batch_assign(C.byref(g), arr, len(frames), _ptr(grad), _stream(stream)),
+           "bgs_preprocess_bwd_batch_assign")
+
+
 def bgs_preprocess_bwd_batch_range(g: Gaussians, frames, grad, begin, count, stream=None):
     """The batched chain rule for the Gaussians [begin, begin + count) only."""
     arr = (C.POINTER(Frame) * len(frames))(*[C.pointer(f) for f in frames])
@@ -281,6 +291,12 @@ def bgs_preprocess_bwd_batch_adam(g: Gaussians, frames, theta, grad, exp_avg, ex
 def bgs_adam_step(theta, grad, exp_avg, exp_avg_sq, n, hp: AdamHParams, step: int, stream=None):
     _check(_lib.bgs_adam_step(_ptr(theta), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), n, C.byref(hp), step,
                               _stream(stream)), "bgs_adam_step")
+
+
+def bgs_adam_step_keep_grad(theta, grad, exp_avg, exp_avg_sq, n, hp: AdamHParams, step: int, stream=None):
+    """bgs_adam_step without zeroing grad (for a step whose chain rule assigns grad)."""
+    _check(_lib.bgs_adam_step_keep_grad(_ptr(theta), _ptr(grad), _ptr(exp_avg), _ptr(exp_avg_sq), n, C.byref(hp),
+                                        step, _stream(stream)), "bgs_adam_step_keep_grad")
 
 
 def bgs_adam_step_range(theta, grad, exp_avg, exp_avg_sq, n, begin, count, hp: AdamHParams, step: int,

@@ -22,6 +22,7 @@ struct AdamParams {
   float b1, b2, eps;
   float step_size[6];  // lr / bc1
   float inv_sqrt_bc2;
+  int32_t zero_grad;  // 0: grad is left as it is (the next step's chain rule assigns it)
 };
 
 __device__ __forceinline__ int adam_group(int64_t e, int64_t n) {
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(256) k_adam(AdamParams p) {
       adam_one(th.w, g.w, m.w, v.w, p.step_size[adam_group(e + 3, p.n)], p);
     }
     p.theta[i] = th;
-    p.grad[i] = g;
+    if (p.zero_grad) p.grad[i] = g;
     p.m[i] = m;
     p.v[i] = v;
   }
@@ -74,14 +75,16 @@ __global__ void k_adam_tail(float* theta, float* grad, float* m, float* v, int64
                             AdamParams p) {
   const int64_t i = start + threadIdx.x;
   if (i >= end) return;
-  adam_one(theta[i], grad[i], m[i], v[i], p.step_size[adam_group(p.base + i, n)], p);
+  float g = grad[i];
+  adam_one(theta[i], g, m[i], v[i], p.step_size[adam_group(p.base + i, n)], p);
+  if (p.zero_grad) grad[i] = g;
 }
 
 // Adam over theta elements [begin, begin + count) of the 59n layout; the pointers address
 // element `begin` (a shard of a reduce-scattered update, or begin = 0 for all of theta).
 // Elements at or past 59n (shard padding) are left untouched.
 bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, int64_t begin, int64_t count,
-                       const bgs_adam_hparams* hp, int64_t step, cudaStream_t s) {
+                       const bgs_adam_hparams* hp, int64_t step, cudaStream_t s, bool zero_grad) {
   const int64_t total = std::max<int64_t>(0, std::min<int64_t>(count, 59 * n - begin));
   if (total == 0) return BGS_OK;
   AdamParams p;
@@ -103,6 +106,7 @@ bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n,
   p.b2 = hp->beta2;
   p.eps = hp->eps;
   p.inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+  p.zero_grad = zero_grad ? 1 : 0;
   const int64_t work = p.total4 > 0 ? p.total4 : 1;
   int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)num_sms() * 8);
   k_adam<<<blocks, 256, 0, s>>>(p);
@@ -181,6 +185,7 @@ bgs_status launch_adam_multimem(float* theta, float* theta_mc, float* grad_mc, f
   p.b2 = hp->beta2;
   p.eps = hp->eps;
   p.inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+  p.zero_grad = 1;  // the multicast form zeroes every rank's shard of grad (multimem.st)
   const int64_t work = p.total4 > 0 ? p.total4 : 1;
   const int blocks = (int)std::min<int64_t>((work + 255) / 256, (int64_t)num_sms() * 8);
   k_adam_multimem<<<blocks, 256, 0, s>>>(p, grad_mc, theta_mc);

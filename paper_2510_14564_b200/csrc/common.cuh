@@ -171,11 +171,12 @@ bgs_status launch_preprocess_bwd_batch(const bgs_gaussians* g, Frame* const* fra
                                        cudaStream_t s);
 bgs_status launch_preprocess_bwd_batch_impl(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
                                             float* theta, float* m, float* v, const bgs_adam_hparams* hp,
-                                            int64_t step, cudaStream_t s, int64_t i0 = 0, int64_t i1 = -1);
+                                            int64_t step, cudaStream_t s, int64_t i0 = 0, int64_t i1 = -1,
+                                            bool assign = false);
 bgs_status launch_render_bwd(const bgs_gaussians* g, Frame* F, const float* dL_dimage, const float* final_T,
                              const uint32_t* n_contrib, float* grad, cudaStream_t s);
 bgs_status launch_adam(float* theta, float* grad, float* m, float* v, int64_t n, int64_t begin, int64_t count,
-                       const bgs_adam_hparams* hp, int64_t step, cudaStream_t s);
+                       const bgs_adam_hparams* hp, int64_t step, cudaStream_t s, bool zero_grad = true);
 bgs_status launch_l1(const float* image, const uint8_t* target, int32_t w, int32_t h, float scale, float* dl,
                      float* loss_sum, cudaStream_t s);
 size_t loss_workspace_bytes(int32_t w, int32_t h);

@@ -385,6 +385,22 @@ bgs_status bgs_preprocess_bwd_batch(const bgs_gaussians* g, bgs_frame* const* fr
   return launch_preprocess_bwd_batch(g, F, nframes, grad, (cudaStream_t)stream);
 }
 
+bgs_status bgs_preprocess_bwd_batch_assign(const bgs_gaussians* g, bgs_frame* const* frames, int32_t nframes,
+                                           float* grad, void* stream) {
+  if (!frames || nframes < 1 || nframes > 4096) return BGS_ERR_INVALID;
+  static thread_local Frame* F[4096];
+  for (int v = 0; v < nframes; ++v) {
+    if (!frame_ok(frames[v]) || !frame_of(frames[v])->cam_valid) return BGS_ERR_INVALID;
+    F[v] = frame_of(frames[v]);
+    if (F[v]->n != F[0]->n) return BGS_ERR_INVALID;
+  }
+  bgs_status st = validate_gaussians(g, F[0]);
+  if (st != BGS_OK) return st;
+  if (F[0]->n > 0 && (!grad || ((uintptr_t)grad & 3u))) return BGS_ERR_INVALID;
+  return launch_preprocess_bwd_batch_impl(g, F, nframes, grad, nullptr, nullptr, nullptr, nullptr, 0,
+                                          (cudaStream_t)stream, 0, -1, true);
+}
+
 bgs_status bgs_preprocess_bwd_batch_range(const bgs_gaussians* g, bgs_frame* const* frames, int32_t nframes,
                                           float* grad, int64_t begin, int64_t count, void* stream) {
   if (!frames || nframes < 1 || nframes > 4096 || begin < 0 || count < 0) return BGS_ERR_INVALID;
@@ -433,6 +449,18 @@ bgs_status bgs_adam_step(float* theta, float* grad, float* exp_avg, float* exp_a
   if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f && hp->beta2 >= 0.0f && hp->beta2 < 1.0f && hp->eps >= 0.0f))
     return BGS_ERR_INVALID;
   return launch_adam(theta, grad, exp_avg, exp_avg_sq, n, 0, 59 * n, hp, step, (cudaStream_t)stream);
+}
+
+bgs_status bgs_adam_step_keep_grad(float* theta, const float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,
+                                   const bgs_adam_hparams* hp, int64_t step, void* stream) {
+  if (n < 0 || !hp || step < 1) return BGS_ERR_INVALID;
+  if (n == 0) return BGS_OK;
+  if (!theta || !grad || !exp_avg || !exp_avg_sq) return BGS_ERR_INVALID;
+  if (!aligned16(theta) || !aligned16(grad) || !aligned16(exp_avg) || !aligned16(exp_avg_sq)) return BGS_ERR_INVALID;
+  if (!(hp->beta1 >= 0.0f && hp->beta1 < 1.0f && hp->beta2 >= 0.0f && hp->beta2 < 1.0f && hp->eps >= 0.0f))
+    return BGS_ERR_INVALID;
+  return launch_adam(theta, const_cast<float*>(grad), exp_avg, exp_avg_sq, n, 0, 59 * n, hp, step,
+                     (cudaStream_t)stream, false);
 }
 
 bgs_status bgs_adam_step_range(float* theta, float* grad, float* exp_avg, float* exp_avg_sq, int64_t n,

@@ -47,6 +47,7 @@ struct PreBwdParams {
   float* grad;  // theta layout (fused Adam: the partial sums of earlier launches, or null)
   // fused Adam (R21; bgs_preprocess_bwd_batch_adam): theta += Adam(sum of the gradient)
   bool adam;
+  bool assign;  // grad = (not +=) this launch's sum; unseen Gaussians get 0
   float* theta;  // writable theta (the buffer the pointers above view)
   float* m;
   float* v;
@@ -58,7 +59,8 @@ struct PreBwdParams {
 // theta[e] with g plus the partial sum of earlier launches (R21, adam.cu's arithmetic).
 __device__ __forceinline__ void put_grad(const PreBwdParams& p, int64_t e, float g, int grp) {
   if (!p.adam) {
-    p.grad[e] += g;
+    if (p.assign) p.grad[e] = g;
+    else p.grad[e] += g;
     return;
   }
   if (p.grad) {
@@ -381,6 +383,8 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
       put_grad(p, 6 * n + 4 * i + 1, d1, 2);
       put_grad(p, 6 * n + 4 * i + 2, d2, 2);
       put_grad(p, 6 * n + 4 * i + 3, d3, 2);
+    } else if (p.gq_vec4 && p.assign) {
+      reinterpret_cast<float4*>(p.grad + 6 * n)[i] = make_float4(d0, d1, d2, d3);
     } else if (p.gq_vec4) {
       float4* gq = reinterpret_cast<float4*>(p.grad + 6 * n) + i;
       float4 q4 = *gq;
@@ -397,8 +401,9 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
       gq[3] += d3;
     }
   }
-  else if (p.adam && i < p.i1) {
-    // fused Adam is dense (R26): a Gaussian no view sees still takes g = 0
+  else if ((p.adam || p.assign) && i < p.i1) {
+    // fused Adam is dense (R26): a Gaussian no view sees still takes g = 0 (and an assigning
+    // launch writes its zero gradient)
     for (int e = 0; e < 3; ++e) put_grad(p, 3 * i + e, 0.0f, 0);
     for (int e = 0; e < 3; ++e) put_grad(p, 3 * n + 3 * i + e, 0.0f, 1);
     for (int e = 0; e < 4; ++e) put_grad(p, 6 * n + 4 * i + e, 0.0f, 2);
@@ -411,6 +416,17 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
     for (int c = lane; c < 48 * nvalid; c += 32) {
       const int g = c / 48, e = c % 48;
       put_grad(p, 11 * n + 48 * wbase + c, s_dsh[warp][g * kRow + e], e < 3 ? 4 : 5);
+    }
+  } else if (p.assign) {  // every coefficient of every Gaussian (the row is zero where unseen)
+    if (p.gsh_vec4) {
+      float4* dst = reinterpret_cast<float4*>(p.grad + 11 * n) + 12 * wbase;
+      for (int c = lane; c < 12 * nvalid; c += 32) {
+        const int g = c / 12, e = 4 * (c % 12);
+        dst[c] = *reinterpret_cast<const float4*>(&s_dsh[warp][g * kRow + e]);
+      }
+    } else {
+      float* dst = p.grad + 11 * n + 48 * wbase;
+      for (int c = lane; c < 48 * nvalid; c += 32) dst[c] = s_dsh[warp][(c / 48) * kRow + c % 48];
     }
   } else if (p.gsh_vec4) {
     float4* dst = reinterpret_cast<float4*>(p.grad + 11 * n) + 12 * wbase;
@@ -452,12 +468,13 @@ __global__ void __launch_bounds__(kBwdThreads, 8) k_preprocess_bwd(const __grid_
 // null when one launch covers all views).
 bgs_status launch_preprocess_bwd_batch_impl(const bgs_gaussians* g, Frame* const* frames, int nviews, float* grad,
                                             float* theta, float* m, float* v, const bgs_adam_hparams* hp,
-                                            int64_t step, cudaStream_t s, int64_t i0, int64_t i1) {
+                                            int64_t step, cudaStream_t s, int64_t i0, int64_t i1, bool assign) {
   const int64_t n = frames[0]->n;
   if (i1 < 0) i1 = n;
   if (n == 0 || i1 <= i0) return BGS_OK;
   PreBwdParams p;
   p.adam = false;
+  p.assign = false;
   p.theta = theta;
   p.m = m;
   p.v = v;
@@ -490,6 +507,7 @@ bgs_status launch_preprocess_bwd_batch_impl(const bgs_gaussians* g, Frame* const
   for (int v0 = 0; v0 < nviews; v0 += kPreBwdMaxViews) {
     p.nviews = nviews - v0 < kPreBwdMaxViews ? nviews - v0 : kPreBwdMaxViews;
     p.adam = hp != nullptr && v0 + p.nviews >= nviews;  // the last launch applies Adam
+    p.assign = assign && v0 == 0;                        // the first launch assigns grad
     for (int v = 0; v < p.nviews; ++v) {
       const Frame* F = frames[v0 + v];
       p.view[v].cam = F->cam;

@@ -771,6 +771,42 @@ def test_fused_chain_rule_adam_equals_unfused(bgs, repeat):
         assert not grad2.any()
 
 
+@pytest.mark.parametrize("repeat", [1, 5])
+def test_chain_rule_assign_and_keep_grad_adam(bgs, repeat):
+    """bgs_preprocess_bwd_batch_assign into a NaN-filled grad == bgs_preprocess_bwd_batch into
+    a zero grad (so every element is written, 0 for Gaussians no view sees; x5 = 20 frames: the
+    second launch accumulates), and bgs_adam_step_keep_grad == bgs_adam_step on theta and the
+    moments, bit for bit, with grad left as it was."""
+    s = gen.garden(seed=4, n=20000, n_cams=4)
+    cams = s.cameras
+    dev = torch.device("cuda")
+    theta = torch.from_numpy(s.theta).to(dev)
+    rs = [bgs.Renderer(s.n, cams[0].width, cams[0].height, max_keys=1 << 22, device=dev) for _ in cams]
+    for i, (r, cam) in enumerate(zip(rs, cams)):
+        out = r.forward(theta, cam, 3)
+        dl = torch.from_numpy(gen.random_dl_dimage(70 + i, cam.width, cam.height, scale=1e-3)).to(dev)
+        bgs.bgs_blend_bwd(r.frame, dl, out["final_T"], out["n_contrib"])
+    frames = [r.frame for r in rs] * repeat
+    g = bgs.gaussians(theta, s.n, 3)
+    grad_acc = torch.zeros_like(theta)
+    bgs.bgs_preprocess_bwd_batch(g, frames, grad_acc)
+    grad_set = torch.full_like(theta, float("nan"))
+    bgs.bgs_preprocess_bwd_batch_assign(g, frames, grad_set)
+    torch.cuda.synchronize()
+    assert torch.equal(grad_set, grad_acc)
+    gen_r = np.random.default_rng(7)
+    m0 = torch.from_numpy((0.01 * gen_r.standard_normal(59 * s.n)).astype(np.float32)).to(dev)
+    v0 = torch.from_numpy((1e-4 * gen_r.random(59 * s.n)).astype(np.float32)).to(dev)
+    hp = bgs.AdamHParams()
+    th1, m1, v1, g1 = theta.clone(), m0.clone(), v0.clone(), grad_acc.clone()
+    bgs.bgs_adam_step(th1, g1, m1, v1, s.n, hp, step=2)
+    th2, m2, v2 = theta.clone(), m0.clone(), v0.clone()
+    bgs.bgs_adam_step_keep_grad(th2, grad_set, m2, v2, s.n, hp, step=2)
+    torch.cuda.synchronize()
+    assert torch.equal(th1, th2) and torch.equal(m1, m2) and torch.equal(v1, v2)
+    assert not g1.any() and torch.equal(grad_set, grad_acc)
+
+
 @pytest.mark.parametrize("name", ["tiny", "dense", "ragged", "garden20k"])
 def test_parity_mode_is_bit_exact(bgs, name):
     """R23's parity mode (BGS_DEBUG_PARITY_EXP): the GPU's canonical exponential is the
