@@ -475,7 +475,8 @@ bgs_status bgs_frame_stats(const bgs_frame* f /*host*/, const uint32_t* n_contri
 #define BGS_DEBUG_SQUARE_RECT 128
 bgs_status bgs_frame_set_debug(bgs_frame* f /*host*/, int32_t flags);
 
-/* Scheduling parameter of the blend kernels (default 4096): a (tile, 8x4 pixel block) work
+/* Scheduling parameter of the blend kernels (default 4096 for frames of >= 3000 tiles, 2048
+ * below: fewer units to balance, finer cuts): a (tile, 8x4 pixel block) work
  * item whose back-to-front walk is longer than seg_len list entries is split, in the
  * backward, into segments of seg_len entries processed independently, each starting from
  * the per-pixel {T, colour behind} the forward recorded at the segment boundary (up to 63

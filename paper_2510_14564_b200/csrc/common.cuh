@@ -14,7 +14,11 @@ constexpr int kTilePixels = kTile * kTile;
 // records each block's per-pixel state at every segment boundary b * seg_len (b = 1..kCkMax)
 // it crosses, and the backward processes the segments as independent work units.
 constexpr int kCkMax = 63;
-constexpr int kSegLenDefault = 4096;
+// default segment length by frame size: a frame with fewer tiles has fewer (tile, block)
+// units to spread over the ~3000 resident warps, so its long walks are cut finer (measured,
+// bench views/s: T&T-train 980x545, 2170 tiles: 2048 -> 1336, 4096 -> 1317; garden
+// 1237x822, 4056 tiles: 2048 -> 384, 4096 -> 391; DB-playroom 4108 tiles: equal)
+constexpr int kSegLenSmallFrame = 2048, kSegLenLargeFrame = 4096, kSegLenTilesLarge = 3000;
 constexpr int kCkPoolSeg = 2048;
 // direct tile split (sort.cu): chunks of 2048..16384 items (a power of two chosen on the
 // device from K so that there are >= kChunkTarget chunks: one warp each); per-warp

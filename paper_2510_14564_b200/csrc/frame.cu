@@ -258,7 +258,7 @@ bgs_status bgs_frame_init(bgs_frame* f, void* workspace, size_t bytes, int64_t n
   F->fwd_planned = F->bwd_planned = 0;
   F->grad2d_clean = 0;
   F->consume_g2 = 0;
-  F->seg_len = kSegLenDefault;
+  F->seg_len = L.num_tiles >= kSegLenTilesLarge ? kSegLenLargeFrame : kSegLenSmallFrame;
   F->ck_table = (uint32_t*)(base + L.ck_table);
   F->ck_pool = (float4*)(base + L.ck_pool);
   F->ck_cap = L.ck_cap;
