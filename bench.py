@@ -116,6 +116,10 @@ def parse():
                         "(step s renders views 4i + s mod 64), each view hinted by its camera's last forward")
     p.add_argument("--sort-path", default="direct", choices=["direct", "radix_split", "rowsplit", "onesweep64"],
                    help="a4-a6 implementation (default: the direct tile split; the others are bit-identical)")
+    p.add_argument("--hints", default="none", choices=["none", "camera"],
+                   help="forward scheduling hint of the rotating batch: none (work ordered by the tile list "
+                        "lengths) or the camera's last forward (bgs_frame_save_hint / load_hint; round 1's "
+                        "default: 264 vs 249 views/s then, 391.0 vs 393.4 after round 2's kernel work)")
     p.add_argument("--no-assign", action="store_true",
                    help="A/B: accumulate the chain rule into a zeroed grad and zero it in Adam (the round-2 "
                         "default before bgs_preprocess_bwd_batch_assign)")
@@ -659,7 +663,7 @@ def run_ours(args, rank, world, local_rank):
     launches0 = bgs.launch_count()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    hint_mode = "slot" if args.fixed_batch else "camera"
+    hint_mode = "slot" if args.fixed_batch else args.hints
     with ClockSampler(_device_index(local_rank)) as clk:
         torch.cuda.nvtx.range_push("bench_timed")  # ncu --nvtx --nvtx-include "bench_timed/"
         t0.record(stream)
@@ -746,7 +750,8 @@ def run_ours(args, rank, world, local_rank):
     variants = None
     if not args.no_variants and not args.one_frame and not args.density_every:
         variants = {}
-        runs = [("unhinted", "none", args.fixed_batch)]
+        runs = [("hinted" if args.hints == "none" else "unhinted", "camera" if args.hints == "none" else "none",
+                 args.fixed_batch)]
         if not args.fixed_batch:
             runs.insert(0, ("fixed_batch", "slot", True))
         for name, mode, fixed in runs:
@@ -952,7 +957,8 @@ def run_ours(args, rank, world, local_rank):
         "schedule": {"batch": "views 4i mod 64 every step" if args.fixed_batch else
                      "rotating: step s renders views 4i + s mod 64 (each camera every 4 steps)",
                      "scheduling_hint": "each frame's previous forward (same camera)" if args.fixed_batch else
-                     "each view hinted by its camera's last forward (bgs_frame_save_hint / load_hint)",
+                     ("each view hinted by its camera's last forward (bgs_frame_save_hint / load_hint)"
+                      if args.hints == "camera" else "none: each forward's work ordered by its tile list lengths"),
                      "sort_path": args.sort_path,
                      "sorts": (f"all views' a4-a6 first, over {args.sort_streams} streams" if args.sort_streams > 0
                                and not args.one_frame else "each view's a4-a6 inline before its forward"),
