@@ -116,6 +116,8 @@ def parse():
                         "(step s renders views 4i + s mod 64), each view hinted by its camera's last forward")
     p.add_argument("--sort-path", default="direct", choices=["direct", "radix_split", "rowsplit", "onesweep64"],
                    help="a4-a6 implementation (default: the direct tile split; the others are bit-identical)")
+    p.add_argument("--seg-len", type=int, default=0,
+                   help="blend work-unit segment length (bgs_frame_set_seg_len); 0 = the library's default")
     p.add_argument("--hints", default="none", choices=["none", "camera"],
                    help="forward scheduling hint of the rotating batch: none (work ordered by the tile list "
                         "lengths) or the camera's last forward (bgs_frame_save_hint / load_hint; round 1's "
@@ -389,6 +391,9 @@ def run_ours(args, rank, world, local_rank):
         if not args.one_frame and not args.no_consume:  # the batched chain rule zeroes what it reads
             for f in S["frames"]:
                 bgs.bgs_frame_set_consume(f, True)
+        if args.seg_len:
+            for f in S["frames"]:
+                bgs.bgs_frame_set_seg_len(f, args.seg_len)
 
     derive()
     del theta, grad, m, v, rends
