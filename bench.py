@@ -118,10 +118,12 @@ def parse():
                    help="a4-a6 implementation (default: the direct tile split; the others are bit-identical)")
     p.add_argument("--seg-len", type=int, default=0,
                    help="blend work-unit segment length (bgs_frame_set_seg_len); 0 = the library's default")
-    p.add_argument("--hints", default="none", choices=["none", "camera"],
-                   help="forward scheduling hint of the rotating batch: none (work ordered by the tile list "
-                        "lengths) or the camera's last forward (bgs_frame_save_hint / load_hint; round 1's "
-                        "default: 264 vs 249 views/s then, 391.0 vs 393.4 after round 2's kernel work)")
+    p.add_argument("--hints", default="camera", choices=["none", "camera"],
+                   help="forward scheduling hint of the rotating batch: the camera's last forward "
+                        "(bgs_frame_save_hint / load_hint: heavy-first order and speculative splits of walks "
+                        "longer than 4 segments) or none (work ordered by the tile list lengths, no splits: "
+                        "as fast in the overlapped step, 394.9 vs 393.5 views/s, but each forward alone "
+                        "0.87 instead of 0.68 ms at garden)")
     p.add_argument("--no-assign", action="store_true",
                    help="A/B: accumulate the chain rule into a zeroed grad and zero it in Adam (the round-2 "
                         "default before bgs_preprocess_bwd_batch_assign)")

@@ -42,6 +42,11 @@ namespace bgs {
 #define BGS_FWD_CULL 0
 #endif
 constexpr int kFwdWarps = 4;
+// a hinted forward splits a walk into speculative segments when its hinted length exceeds
+// this many segment lengths
+#ifndef BGS_FWD_SPLIT_MUL
+#define BGS_FWD_SPLIT_MUL 4
+#endif
 // The forward keeps a one-CTA planner: it places a tile's eight blocks next to each other
 // inside their cost bucket, and the tile list they share stays hot in L2 (a grid-wide
 // planner with atomics per bucket scattered them: forward 13.6 -> 14.0 ms per step).
@@ -377,7 +382,7 @@ __global__ void __launch_bounds__(kFwdPlanThreads) k_fwd_plan(const uint32_t* __
       if (t >= n_items) continue;
       const uint32_t h = hq[q];
       uint32_t ns = 1, base = 0;
-      if (hinted && h > 2u * (uint32_t)seg_len) {
+      if (hinted && h > (uint32_t)BGS_FWD_SPLIT_MUL * (uint32_t)seg_len) {
         ns = min((h + (uint32_t)seg_len - 1u) / (uint32_t)seg_len, (uint32_t)kCkMax + 1u);
         base = atomicAdd(&s_bump, ns);
         if (base + ns > cap) ns = 1;
