@@ -323,7 +323,9 @@ __device__ __forceinline__ int64_t rank_of_item(const uint32_t* __restrict__ ite
   return lo;
 }
 
-// (a) per-(chunk, tile) item counts.  Grid cells: (tiles_y + 1) x (tiles_x + 1) ints per warp.
+// (a) per-(chunk, tile) item counts.  Grid cells: (tiles_y + 1) x (tiles_x + 1) ints per
+// chunk; the kChunkWarps warps of a CTA share one chunk's grid (a warp per chunk held 17 KB
+// of shared memory per warp: 12 warps per SM, latency-bound at 86 us per garden view).
 __global__ void __launch_bounds__(kChunkWarps * 32) k_chunk_hist(int64_t n, const uint32_t* __restrict__ item_off,
                                                                  const uint32_t* __restrict__ rank_cnt,
                                                                  const uint2* __restrict__ rank_rect, int32_t tiles_x,
@@ -331,15 +333,16 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_chunk_hist(int64_t n, cons
                                                                  uint32_t* chunk_cnt) {
   extern __shared__ int32_t s_grid[];
   if (counters[C_OVERFLOW]) return;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+  constexpr int T = kChunkWarps * 32;
   const int gw = tiles_x + 1, cells = gw * (tiles_y + 1), nt = tiles_x * tiles_y;
-  int32_t* G = s_grid + warp * cells;
+  int32_t* G = s_grid;
   const uint32_t K = counters[C_SCAN_TOTAL];
   const uint32_t CI = chunk_items_of(K), n_chunks = (K + CI - 1) / CI;
-  const uint32_t c = blockIdx.x * kChunkWarps + warp;
+  const uint32_t c = blockIdx.x;
   if (c >= n_chunks) return;
-  for (int k = lane; k < cells; k += 32) G[k] = 0;
-  __syncwarp();
+  for (int k = tid; k < cells; k += T) G[k] = 0;
+  __syncthreads();
   const uint32_t a = c * CI, b = min(K, a + CI);
   auto add_rect = [&](int x0, int y0, int x1, int y1) {  // [x0, x1) x [y0, y1), non-empty
     atomicAdd(&G[y0 * gw + x0], 1);
@@ -347,9 +350,10 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_chunk_hist(int64_t n, cons
     atomicAdd(&G[y1 * gw + x0], -1);
     atomicAdd(&G[y1 * gw + x1], 1);
   };
-  // the chunk's ranks [r0, r1]: independent loads, 4 windows of 32 per round
+  // the chunk's ranks [r0, r1] (each warp searches; the loads hit L1/L2): per warp and
+  // round, 4 windows of 32 ranks, their loads independent
   const int64_t r0 = rank_of_item(item_off, n, a, lane), r1 = rank_of_item(item_off, n, b - 1, lane);
-  for (int64_t rb = r0; rb <= r1; rb += 128) {
+  for (int64_t rb = r0 + 128 * warp; rb <= r1; rb += 128 * kChunkWarps) {
     uint32_t o[4], t[4];
     uint2 rc[4];
 #pragma unroll
@@ -384,21 +388,21 @@ __global__ void __launch_bounds__(kChunkWarps * 32) k_chunk_hist(int64_t n, cons
       }
     }
   }
-  __syncwarp();
-  for (int y = lane; y <= tiles_y; y += 32) {  // prefix along rows
+  __syncthreads();
+  for (int y = tid; y <= tiles_y; y += T) {  // prefix along rows
     int32_t run = 0;
 #pragma unroll 8
     for (int x = 0; x <= tiles_x; ++x) run = (G[y * gw + x] += run);
   }
-  __syncwarp();
-  for (int x = lane; x <= tiles_x; x += 32) {  // then along columns
+  __syncthreads();
+  for (int x = tid; x <= tiles_x; x += T) {  // then along columns
     int32_t run = 0;
 #pragma unroll 8
     for (int y = 0; y <= tiles_y; ++y) run = (G[y * gw + x] += run);
   }
-  __syncwarp();
+  __syncthreads();
   uint32_t* row = chunk_cnt + (size_t)c * nt;
-  for (int y = 0; y < tiles_y; ++y)
+  for (int y = warp; y < tiles_y; y += kChunkWarps)
     for (int x = lane; x < tiles_x; x += 32) row[y * tiles_x + x] = (uint32_t)G[y * gw + x];
 }
 
@@ -732,14 +736,13 @@ bgs_status launch_sort(Frame* F, cudaStream_t s) {
     F->final_buf = 0;
     const int gw = F->tiles_x + 1, cells = gw * (F->tiles_y + 1), nt = F->num_tiles;
     const int64_t max_chunks = (F->max_keys + kChunkItemsMin - 1) / kChunkItemsMin;  // device picks the size
-    const int blocks = (int)((max_chunks + kChunkWarps - 1) / kChunkWarps);
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_chunk_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       cudaFuncSetAttribute(k_emit_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
       attr = true;
     }
-    k_chunk_hist<<<blocks, kChunkWarps * 32, (size_t)kChunkWarps * cells * 4, s>>>(
+    k_chunk_hist<<<(int)max_chunks, kChunkWarps * 32, (size_t)cells * 4, s>>>(
         F->n, F->item_off, F->rank_cnt, F->rank_rect, F->tiles_x, F->tiles_y, F->counters, F->chunk_cnt);
     note_launch();
     if ((st = check_launch("k_chunk_hist")) != BGS_OK) return st;
