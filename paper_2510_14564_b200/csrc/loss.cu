@@ -26,6 +26,7 @@ namespace bgs {
 constexpr int kLTx = 32, kLTy = 32, kLR = 5, kLWin = 2 * kLR + 1;
 constexpr int kLHx = kLTx + 2 * kLR, kLHy = kLTy + 2 * kLR;  // tile + halo (42 x 42)
 constexpr int kLThreads = 256;
+constexpr int kLStage = (kLHy * kLHx + kLThreads - 1) / kLThreads;  // staging rounds per thread
 // register blocking: the row pass gives each thread 4 consecutive outputs of one halo row
 // (14 inputs per map instead of 44), the column pass 4 consecutive outputs of one column
 constexpr int kLRun = 4, kLSegs = kLTx / kLRun, kLRowItems = kLHy * kLSegs, kLColRuns = kLTy / kLRun;
@@ -70,15 +71,27 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_fwd(const float* __restrict_
   const size_t plane = (size_t)W * H;
   const float* xc = img + ch * plane;
   const uint8_t* yc = tgt + ch * plane;
-  for (int i = threadIdx.x; i < kLHy * kLHx; i += kLThreads) {
-    const int r = i / kLHx, c = i - r * kLHx;
-    const int gx = x0 + c - kLR, gy = y0 + r - kLR;
-    float xv = 0.f, yv = 0.f;
-    if (gx >= 0 && gx < W && gy >= 0 && gy < H) {
-      xv = xc[(size_t)gy * W + gx];
-      yv = (float)yc[(size_t)gy * W + gx] * (1.0f / 255.0f);
+  {
+    // the tile + halo in one batch of independent loads per thread (kLStage rounds unrolled:
+    // every load in flight before the first store)
+    float xv[kLStage], yv[kLStage];
+#pragma unroll
+    for (int q = 0; q < kLStage; ++q) {
+      const int i = threadIdx.x + q * kLThreads;
+      const int r = i / kLHx, c = i - r * kLHx;
+      const int gx = x0 + c - kLR, gy = y0 + r - kLR;
+      xv[q] = 0.f;
+      yv[q] = 0.f;
+      if (i < kLHy * kLHx && gx >= 0 && gx < W && gy >= 0 && gy < H) {
+        xv[q] = __ldg(xc + (size_t)gy * W + gx);
+        yv[q] = (float)__ldg(yc + (size_t)gy * W + gx) * (1.0f / 255.0f);
+      }
     }
-    s_xy[r][c] = make_float2(xv, yv);
+#pragma unroll
+    for (int q = 0; q < kLStage; ++q) {
+      const int i = threadIdx.x + q * kLThreads;
+      if (i < kLHy * kLHx) s_xy[i / kLHx][i % kLHx] = make_float2(xv[q], yv[q]);
+    }
   }
   __syncthreads();
   // rows: the 11-tap pass along x of the five moment maps, 4 outputs per thread; (x, y) and
@@ -216,14 +229,27 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_bwd(const float* __restrict_
       atomicAdd(loss_sum, (float)(scale * ((1.0 - lam) * l1 / n + lam * (1.0 - ss / n))));
     }
   }
-  for (int i = threadIdx.x; i < kLHy * kLHx; i += kLThreads) {
-    const int r = i / kLHx, c = i - r * kLHx;
-    const int gx = x0 + c - kLR, gy = y0 + r - kLR;
-    const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;
-    const size_t p = (size_t)gy * W + gx;
-    sg01[r][c] = in ? make_float2(part[(0 * 3 + ch) * plane + p], part[(1 * 3 + ch) * plane + p])
-                    : make_float2(0.f, 0.f);
-    sg2[r][c] = in ? part[(2 * 3 + ch) * plane + p] : 0.f;
+  {
+    float a0[kLStage], a1[kLStage], a2[kLStage];  // all loads in flight before the stores
+#pragma unroll
+    for (int q = 0; q < kLStage; ++q) {
+      const int i = threadIdx.x + q * kLThreads;
+      const int r = i / kLHx, c = i - r * kLHx;
+      const int gx = x0 + c - kLR, gy = y0 + r - kLR;
+      const bool in = i < kLHy * kLHx && gx >= 0 && gx < W && gy >= 0 && gy < H;
+      const size_t p = (size_t)gy * W + gx;
+      a0[q] = in ? __ldg(part + (0 * 3 + ch) * plane + p) : 0.f;
+      a1[q] = in ? __ldg(part + (1 * 3 + ch) * plane + p) : 0.f;
+      a2[q] = in ? __ldg(part + (2 * 3 + ch) * plane + p) : 0.f;
+    }
+#pragma unroll
+    for (int q = 0; q < kLStage; ++q) {
+      const int i = threadIdx.x + q * kLThreads;
+      if (i < kLHy * kLHx) {
+        sg01[i / kLHx][i % kLHx] = make_float2(a0[q], a1[q]);
+        sg2[i / kLHx][i % kLHx] = a2[q];
+      }
+    }
   }
   __syncthreads();
   for (int it = threadIdx.x; it < kLRowItems; it += kLThreads) {
