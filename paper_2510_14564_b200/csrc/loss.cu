@@ -229,6 +229,17 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_bwd(const float* __restrict_
       atomicAdd(loss_sum, (float)(scale * ((1.0 - lam) * l1 / n + lam * (1.0 - ss / n))));
     }
   }
+  // this thread's output pixels' image and target values, loaded now (used after the passes)
+  const int oc = threadIdx.x % kLTx, or0 = (threadIdx.x / kLTx) * kLRun;
+  float pxv[kLRun], pyv[kLRun];
+#pragma unroll
+  for (int j = 0; j < kLRun; ++j) {
+    const int gx = x0 + oc, gy = y0 + or0 + j;
+    const bool in = gx < W && gy < H;
+    const size_t p = (size_t)gy * W + gx;
+    pxv[j] = in ? __ldg(img + ch * plane + p) : 0.f;
+    pyv[j] = in ? (float)__ldg(tgt + ch * plane + p) * (1.0f / 255.0f) : 0.f;
+  }
   {
     float a0[kLStage], a1[kLStage], a2[kLStage];  // all loads in flight before the stores
 #pragma unroll
@@ -292,7 +303,7 @@ __global__ void __launch_bounds__(kLThreads) k_ssim_bwd(const float* __restrict_
     const int gy = y0 + r0 + j;
     if (gx >= W || gy >= H) continue;
     const size_t p = (size_t)gy * W + gx;
-    const float xv = img[ch * plane + p], yv = (float)tgt[ch * plane + p] * (1.0f / 255.0f);
+    const float xv = pxv[j], yv = pyv[j];
     const float d = xv - yv;
     const float sgn = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
     const float dssim = m[0][j] + 2.f * xv * m[1][j] + yv * m[2][j];
