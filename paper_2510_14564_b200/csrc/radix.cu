@@ -205,6 +205,39 @@ __global__ void __launch_bounds__(kSortThreads, BGS_SORT_MINB) k_sort_pass(const
     }
     __syncthreads();
     const int tvalid = (int)S.tile_valid;
+    if (rank_rect) {
+      // the depth sort's last pass: per-rank tile count and packed rect, the rect gathers of
+      // four keys per thread in flight together
+      constexpr int B = 4;
+      for (int j0 = tid; j0 < tvalid; j0 += B * kSortThreads) {
+        uint32_t gq[B], vq[B];
+        uint2 rq[B];
+        bool ok[B];
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+          const int j = j0 + q * kSortThreads;
+          ok[q] = j < tvalid;
+          const KT k2 = ok[q] ? S.keys[j] : (KT)~(KT)0;
+          const uint32_t d = (uint32_t)((k2 >> shift) & 0xff);
+          gq[q] = ok[q] ? S.global_base[d] + (uint32_t)j - S.tile_start[d] : 0u;
+          vq[q] = ok[q] ? S.vals[j] : 0u;
+          rq[q] = make_uint2(0u, 0u);
+          if (ok[q]) {
+            kout[gq[q]] = k2;
+            if ((uint32_t)k2 != 0xffffffffu) rq[q] = __ldg(rect + vq[q]);  // visible: the preprocess's rect
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < B; ++q) {
+          if (!ok[q]) continue;
+          vout[gq[q]] = vq[q];
+          const uint32_t w = rq[q].y & 0xffffu, hh = rq[q].y >> 16;
+          rank_cnt[gq[q]] = w * hh;
+          rank_rect[gq[q]] = make_uint2(rq[q].x, w);
+          rank_h[gq[q]] = hh;
+        }
+      }
+    } else
     for (int j = tid; j < tvalid; j += kSortThreads) {
       const KT k2 = S.keys[j];
       const uint32_t d = (uint32_t)((k2 >> shift) & 0xff);
@@ -212,20 +245,6 @@ __global__ void __launch_bounds__(kSortThreads, BGS_SORT_MINB) k_sort_pass(const
       const uint32_t v = S.vals[j];
       kout[g] = k2;
       vout[g] = v;
-      if (rank_rect) {  // the depth sort's last pass: per-rank tile count and packed rect
-        uint32_t t = 0, hh = 0;
-        uint2 packed = make_uint2(0u, 0u);
-        if ((uint32_t)k2 != 0xffffffffu) {  // visible: the preprocess's rect (R11)
-          const uint2 q = rect[v];
-          const uint32_t w = q.y & 0xffffu;
-          hh = q.y >> 16;
-          t = w * hh;
-          packed = make_uint2(q.x, w);
-        }
-        rank_cnt[g] = t;
-        rank_rect[g] = packed;
-        rank_h[g] = hh;
-      }
     }
     __syncthreads();
   }
